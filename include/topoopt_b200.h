@@ -1,0 +1,166 @@
+/*
+ * topoopt_b200 — C ABI of the B200-native ADMM topology solver.
+ *
+ * Drop-in boundary for the hot path of the reference library `topoopt`
+ * (arXiv 2512.07536, /root/reference/proj). The reference exposes a C++ API
+ * (no FFI); every entry point below replaces one reference function, cited as
+ * file:line under proj/. The reference-compatible C++ API
+ * (include/topoopt/ headers, namespace topoopt) is a thin host layer over these.
+ *
+ * Conventions
+ *  - plain pointers and sizes, caller-owned HOST buffers; device memory is
+ *    owned by the library (or by a tp_solver handle);
+ *  - every function returns a status code mirroring the reference exception
+ *    taxonomy (proj/include/topoopt/errors.hpp): TP_OK, or one of TP_ERR_*;
+ *    tp_last_error_message() holds the reference's message text;
+ *  - edges are (i, j) int32 pairs with i < j, lexicographically sorted
+ *    (Topology invariants, proj/include/topoopt/topology.hpp:16-28); packed
+ *    edge vectors follow edge_index (proj/src/topology.cpp:78-84);
+ *  - state vectors use the reference block layout (proj/src/admm.cpp:24-44):
+ *    [g (m) | lambda | S (n*n, column-major) | y (n) | T (n*n) | z (m) | nu (m)];
+ *  - all arithmetic is FP64 on the GPU (sm_100a); there is no CPU fallback:
+ *    without a CUDA device every call returns TP_ERR_CUDA.
+ *  - thread safety: one tp_solver per host thread; stateless calls are safe.
+ */
+#ifndef TOPOOPT_B200_H
+#define TOPOOPT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TP_OK 0
+#define TP_ERR_INVALID_ARGUMENT 1  /* std::invalid_argument */
+#define TP_ERR_INFEASIBLE 2        /* InfeasibleError */
+#define TP_ERR_LINEAR_SOLVE 3      /* LinearSolveError */
+#define TP_ERR_DEGENERATE 4        /* DegenerateSolutionError */
+#define TP_ERR_PIVOT 5             /* PivotError (never raised: no factorisation) */
+#define TP_ERR_INTERNAL 6
+#define TP_ERR_CUDA 7
+
+/* SolverConfig (proj/include/topoopt/admm.hpp:15-25) plus device options. */
+typedef struct tp_config {
+    double rho;            /* 1.0 */
+    double epsilon;        /* 1e-6: stop when sum (x-y)^2 <= epsilon */
+    int32_t max_iter;      /* 20000 */
+    double alpha;          /* 2.0 */
+    double weight_floor;   /* 1e-6 */
+    uint64_t seed;         /* 0: warm-start annealer seed */
+    double linear_tol;     /* 1e-10 (accepted; the x-step is solved exactly) */
+    int32_t trace_stride;  /* 1: acf_iterate every iteration, as the reference */
+    int32_t chunk;         /* 0: auto; iterations per CUDA graph launch */
+} tp_config;
+
+/* Solution scalars (proj/include/topoopt/admm.hpp:38-53). */
+typedef struct tp_result {
+    int32_t iterations;
+    int32_t converged;
+    int32_t connected;
+    int32_t repaired;
+    int32_t n_edges;
+    int32_t best_iter;
+    double residual;
+    double lambda_tilde;
+    double acf;
+    double lambda2;
+    double lambda_n;
+} tp_result;
+
+void tp_config_default(tp_config* cfg);
+/* SolverConfig::validate (proj/src/admm.cpp:186-195). */
+int tp_config_validate(const tp_config* cfg);
+const char* tp_last_error_message(void);
+int tp_version(void);
+int tp_set_device(int device);
+
+/* ---------------------------------------------------------------- solves */
+
+/* topoopt::solve (proj/src/admm.cpp:356-428). warm_edges may be NULL
+ * (n_warm < 0): the balanced-degree annealed start default_warm_start
+ * (proj/src/admm.cpp:337-354) is generated on the host. Outputs: result,
+ * up to r edges (2 ints each) and weights, trace rows (iterations x 3:
+ * residual, lambda_tilde, acf_iterate) when trace != NULL (capacity
+ * max_iter rows), the note string. */
+int tp_solve(int32_t n, int32_t r, const tp_config* cfg, const int32_t* warm_edges, int32_t n_warm,
+             tp_result* out, int32_t* edges, double* weights, double* trace, char* note,
+             int32_t note_cap);
+
+/* topoopt::solve_het on node_level_constraints(n, degrees)
+ * (proj/src/admm_het.cpp:231-369, proj/src/bandwidth.cpp:116-146). */
+int tp_solve_het_node(int32_t n, const int32_t* degrees, const tp_config* cfg,
+                      const int32_t* warm_edges, int32_t n_warm, tp_result* out, int32_t* edges,
+                      double* weights, double* trace, char* note, int32_t note_cap);
+
+/* Warm starts (host): anneal_degree_topology (proj/src/anneal.cpp:245-273) and
+ * default_warm_start (proj/src/admm.cpp:337-354); edges capacity sum(degrees)/2
+ * resp. r pairs. */
+int tp_anneal_degree(int32_t n, const int32_t* degrees, double t0, double cooling, int32_t steps,
+                     int32_t moves_per_temp, uint64_t seed, int32_t* edges, int32_t* n_edges);
+int tp_default_warm_start(int32_t n, int32_t r, uint64_t seed, int32_t* edges, int32_t* n_edges);
+
+/* ------------------------------------------------ batched solver handle */
+/* Independent solves of one n in lockstep (edge-budget sweeps, bandwidth
+ * scenarios, restarts). r[batch] (hom) or degrees[batch*n] (node-level het). */
+typedef struct tp_solver tp_solver;
+int tp_solver_create(int32_t n, int32_t batch, const int32_t* r, const int32_t* degrees,
+                     const tp_config* cfg, tp_solver** out);
+int tp_solver_destroy(tp_solver* s);
+int tp_solver_set_warm(tp_solver* s, int32_t b, const int32_t* edges, int32_t n_edges);
+int tp_solver_start(tp_solver* s);                  /* feasible start (admm.cpp:143-173) */
+int tp_solver_iterate(tp_solver* s, int32_t k);     /* enqueue k ADMM iterations, async */
+int tp_solver_sync(tp_solver* s, int32_t* all_done);
+int tp_solver_run(tp_solver* s);                    /* iterate until every solve stops */
+int tp_solver_finish(tp_solver* s);                 /* extraction + spectral report */
+int tp_solver_result(tp_solver* s, int32_t b, tp_result* out, int32_t* edges, double* weights,
+                     double* trace, char* note, int32_t note_cap);
+void* tp_solver_stream(tp_solver* s);               /* cudaStream_t of the main stream */
+/* {n, m, nx, neq, off_s, off_y, off_t, lambda_ix, off_z, off_nu, batch, het} */
+int tp_solver_dims(tp_solver* s, int32_t* dims);
+/* Device pointers of the state (X, Y, D), each batch*nx doubles. */
+int tp_solver_state(tp_solver* s, double** x, double** y, double** d);
+
+/* ---------------------------------------------------------------- substeps */
+/* project_Y (proj/src/admm.cpp:268-277); x, d, y of length nx. */
+int tp_project_Y(int32_t n, int32_t r, double alpha, double rho, const double* x, const double* d,
+                 double* y);
+/* project_Y_het (proj/src/admm_het.cpp:156-171), node-level system. */
+int tp_project_Y_het_node(int32_t n, const int32_t* degrees, double alpha, double rho,
+                          const double* x, const double* d, double* y);
+/* update_X (proj/src/admm.cpp:279-293): kkt_out = [x (nx) ; mu (neq)], the
+ * exact solution of the delta-regularised KKT system the reference solves
+ * with BiCGSTAB. */
+int tp_update_X(int32_t n, int32_t r, double alpha, double rho, const double* y, const double* d,
+                double* kkt_out);
+int tp_update_X_het_node(int32_t n, const int32_t* degrees, double alpha, double rho,
+                         const double* y, const double* d, double* kkt_out);
+/* update_duals (proj/src/admm.cpp:295-297): d += rho (x - y). */
+int tp_update_duals(int64_t nx, double rho, const double* x, const double* y, double* d);
+/* project_binary_z (proj/src/admm_het.cpp:116-123). */
+int tp_project_binary_z(const double* v, int64_t m, int32_t r, double* z);
+/* extract_topology (proj/src/admm.cpp:299-335); edges/weights capacity r. */
+int tp_extract_topology(int32_t n, int32_t r, const double* g, double weight_floor,
+                        int32_t* edges, double* weights, int32_t* n_edges);
+/* allocate_edge_capacity (proj/src/bandwidth.cpp:28-89); caps may be NULL. */
+int tp_allocate(const double* b, const int32_t* caps, int32_t n, int32_t r, double* b_unit,
+                int32_t* e);
+/* P independent allocations of n nodes (b: P*n, caps: P*n or NULL, r: P);
+ * status[p] = TP_OK / TP_ERR_INVALID_ARGUMENT / TP_ERR_INFEASIBLE. */
+int tp_allocate_batch(const double* b, const int32_t* caps, int32_t n, const int32_t* r, int32_t P,
+                      double* b_unit, int32_t* e, int32_t* status);
+/* spectral_report (proj/src/topology.cpp:125-144) of a dense row-major W;
+ * out = {acf, lambda2, lambda_n, connected}. */
+int tp_spectral_report(int32_t n, const double* w, double* out4);
+/* spectral_report(gossip_matrix(t)) for a topology given as edges/weights. */
+int tp_spectral_edges(int32_t n, const int32_t* edges, const double* weights, int32_t k,
+                      double* out4);
+/* project_psd / project_nsd (proj/src/eig.cpp:174-176), row-major n x n. */
+int tp_project_psd(int32_t n, const double* a, double* out);
+int tp_project_nsd(int32_t n, const double* a, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TOPOOPT_B200_H */

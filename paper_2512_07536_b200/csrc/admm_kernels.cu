@@ -1,0 +1,657 @@
+// ADMM iteration kernels: projection prep, closed-form x-step, dual update,
+// residual and bookkeeping. All HBM-bound; tiles of 32 x 32 node pairs so the
+// column-major S/T blocks are read once per orientation with coalesced rows.
+//
+// Reference mapping (all in /root/reference/proj):
+//   prep            <- project_Y / project_Y_het first half (src/admm.cpp:268-277,
+//                      src/admm_het.cpp:156-171): v = x + d/rho, clamps.
+//   xstep a/node/b/diag <- update_X: kkt_rhs + bicgstab on [[I,A^T],[A,-1e-8 I]]
+//                      (src/admm.cpp:175-182, 279-293; src/admm_het.cpp:270-280),
+//                      solved here in closed form.
+//   diag (tail)     <- update_duals + residual + trace + best iterate + stop test
+//                      (src/admm.cpp:388-405, src/admm_het.cpp:281-300).
+#include "admm_kernels.cuh"
+
+namespace tpb {
+
+namespace {
+
+constexpr int TB = 32;  // tile edge
+constexpr int TY = 8;   // threads in y
+
+__device__ inline void tile_of(int t, int& bi, int& bj) {
+    int b = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while ((b + 1) * (b + 2) / 2 <= t) ++b;
+    while (b * (b + 1) / 2 > t) --b;
+    bj = b;
+    bi = t - b * (b + 1) / 2;
+}
+
+__device__ inline bool solve_done(const Dev& d, int b) { return d.ictl[b * 8 + kDone] != 0; }
+
+}  // namespace
+
+XConst make_xconst(int n, double alpha, double rho) {
+    XConst c{};
+    const double delta = kKktShift;
+    const double s = 1.0 / (1.0 + delta);
+    c.rho = rho;
+    c.inv_rho = 1.0 / rho;
+    c.alpha = alpha;
+    c.alpha_over_n = alpha / n;
+    c.delta = delta;
+    c.s = s;
+    c.lam_den = 1.0 + 2.0 * n * s;
+    // homogeneous H_gg = a I + b K, f(k) = 1/(a + b k)
+    const double a = 1.0 + 4.0 * s, b = 3.0 * s;
+    const double qp = n - 2.0, q1 = 2.0 * n - 2.0;
+    c.f0 = 1.0 / a;
+    c.c1 = -b / (a * (a + b * qp));
+    c.c2 = -b / (a * (a + b * q1));
+    // heterogeneous node-level
+    const double a1 = 1.0 + 5.0 * s, b1 = 3.0 * s, a2 = 1.0 + s;
+    auto det = [&](double k) { return (a1 + b1 * k) * a2 - s * s; };
+    const double d0 = det(0), dp = det(qp), d1 = det(q1);
+    c.g11_0 = a2 / d0;
+    c.g12_0 = s / d0;
+    c.g22_0 = a1 / d0;
+    c.c1_11 = -b1 * a2 * a2 / (dp * d0);
+    c.c2_11 = -b1 * a2 * a2 / (d1 * d0);
+    c.c1_12 = -b1 * s * a2 / (dp * d0);
+    c.c2_12 = -b1 * s * a2 / (d1 * d0);
+    c.c1_22 = -b1 * s * s / (dp * d0);
+    c.c2_22 = -b1 * s * s / (d1 * d0);
+    c.g12_p = s / dp;
+    c.g22_p = (a1 + b1 * qp) / dp;
+    c.g12_1 = s / d1;
+    c.g22_1 = (a1 + b1 * q1) / d1;
+    c.mu_den_p = qp * c.g22_p + delta;
+    c.mu_den_1 = q1 * c.g22_1 + delta;
+    return c;
+}
+
+// ---------------------------------------------------------------- prep
+// Block (bi <= bj) of node pairs. Writes A_S/A_T = sym(v) in both triangles of
+// the ld-padded buffers, clamps the packed edge blocks for pairs in the tile,
+// and the per-node blocks (lambda, y) from tile 0.
+__global__ void __launch_bounds__(TB* TY) prep_kernel(Dev d, XConst c) {
+    const int b = blockIdx.y;
+    if (solve_done(d, b)) return;
+    int bi, bj;
+    tile_of(blockIdx.x, bi, bj);
+    const Layout& lo = d.lo;
+    const int n = lo.n;
+    const double* X = d.X + (long long)b * d.nx;
+    const double* D = d.D + (long long)b * d.nx;
+    double* Y = d.Y + (long long)b * d.nx;
+    const long long ld2 = (long long)d.ld * d.ld;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int i0 = bi * TB, j0 = bj * TB;
+    __shared__ double red[TB * TY / 32];
+    double fro[2] = {0.0, 0.0};
+
+    for (int which = 0; which < 2; ++which) {
+        const int off = which == 0 ? lo.off_s : lo.off_t;
+        double* A = d.A + ((long long)b * 2 + which) * ld2;
+        __shared__ double Vs[TB][TB + 1];  // Vs[jl][il] = v(i0+il, j0+jl)
+        // orientation 1: entries (i, j), column-major (r=i, c=j) at j*n + i
+        for (int cc = ty; cc < TB; cc += TY) {
+            const int i = i0 + tx, j = j0 + cc;
+            double v = 0.0;
+            if (i < n && j < n) {
+                const long long p = off + (long long)j * n + i;
+                v = X[p] + D[p] / c.rho;
+            }
+            Vs[cc][tx] = v;
+        }
+        __syncthreads();
+        // orientation 2: entries (j, i) at i*n + j; symmetrize with (i, j)
+        for (int cc = ty; cc < TB; cc += TY) {
+            const int j = j0 + tx, i = i0 + cc;  // entry (row j, col i)
+            if (i < n && j < n) {
+                const long long p = off + (long long)i * n + j;
+                const double vji = X[p] + D[p] / c.rho;
+                const double vij = Vs[tx][cc];
+                const double a = 0.5 * (vij + vji);  // symmetrize (proj/src/eig.cpp:157)
+                // A is symmetric; write (j, i) here (row-major j*ld + i)
+                A[(long long)j * d.ld + i] = a;
+                Vs[tx][cc] = a;  // hand (i, j) to the transposed write below
+                const double w = (bi == bj) ? (i == j ? 1.0 : (j > i ? 2.0 : 0.0)) : 2.0;
+                fro[which] += w * a * a;
+            }
+        }
+        __syncthreads();
+        if (bi != bj) {
+            for (int cc = ty; cc < TB; cc += TY) {
+                const int i = i0 + tx, j = j0 + cc;
+                if (i < n && j < n) A[(long long)i * d.ld + j] = Vs[cc][tx];
+            }
+        }
+        __syncthreads();
+    }
+    // packed edge blocks for pairs (i, j), i < j, i in block bi, j in block bj
+    for (int il = ty; il < TB; il += TY) {
+        const int i = i0 + il, j = j0 + tx;
+        if (i >= n || j >= n || j <= i) continue;
+        const long long l = edge_idx(n, i, j);
+        const double vg = X[l] + D[l] / c.rho;
+        Y[l] = (0.0 < vg) ? vg : 0.0;  // std::max(0.0, v) (proj/src/admm.cpp:273)
+        if (d.het) {
+            const long long lz = lo.off_z + l, lv = lo.off_nu + l;
+            Y[lz] = X[lz] + D[lz] / c.rho;  // z-score; binary projection follows
+            const double vn = X[lv] + D[lv] / c.rho;
+            Y[lv] = (0.0 < vn) ? vn : 0.0;
+        }
+    }
+    if (blockIdx.x == 0) {
+        const int t = ty * TB + tx;
+        if (t == 0) {
+            const double vl = X[lo.lambda_ix] + D[lo.lambda_ix] / c.rho;
+            Y[lo.lambda_ix] = (0.0 < vl) ? vl : 0.0;
+        }
+        for (int i = t; i < n; i += TB * TY) {
+            const double vy = X[lo.off_y + i] + D[lo.off_y + i] / c.rho;
+            Y[lo.off_y + i] = (0.0 < vy) ? vy : 0.0;
+        }
+    }
+    // deterministic per-tile Frobenius partials
+    for (int which = 0; which < 2; ++which) {
+        double* part = d.frob_part + ((long long)b * 2 + which) * d.ntile;
+        // block sum over 2D block: flatten thread id
+        double v = fro[which];
+        const int lane = (ty * TB + tx) & 31, wid = (ty * TB + tx) >> 5;
+        v = warp_sum(v);
+        __syncthreads();
+        if (lane == 0) red[wid] = v;
+        __syncthreads();
+        if (ty == 0 && tx == 0) {
+            double s = 0.0;
+            for (int w = 0; w < TB * TY / 32; ++w) s += red[w];
+            part[blockIdx.x] = s;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void frob_finalize_kernel(Dev d) {
+    const int b = blockIdx.x;
+    if (solve_done(d, b)) return;
+    __shared__ double scratch[32];
+    for (int which = 0; which < 2; ++which) {
+        const double* part = d.frob_part + ((long long)b * 2 + which) * d.ntile;
+        double v = 0.0;
+        for (int t = threadIdx.x; t < d.ntile; t += blockDim.x) v += part[t];
+        v = block_sum(v, scratch);
+        if (threadIdx.x == 0) {
+            const double f = sqrt(v);
+            d.inv_scale[b * 2 + which] = f > 0.0 ? 1.0 / f : 0.0;
+        }
+    }
+}
+
+void launch_prep(const Dev& d, const XConst& c, cudaStream_t st) {
+    dim3 grid(d.ntile, d.B), block(TB, TY);
+    prep_kernel<<<grid, block, 0, st>>>(d, c);
+    TPB_CHECK_LAUNCH();
+}
+
+void launch_frob_finalize(const Dev& d, cudaStream_t st) {
+    frob_finalize_kernel<<<d.B, 256, 0, st>>>(d);
+    TPB_CHECK_LAUNCH();
+}
+
+// ---------------------------------------------------------------- x-step A
+// h_g(i,j) = r_g + s (4 - R_ii - R_jj + R_ij + R_ji + v2_i + v2_j) [- s r_nu]
+// with r = Y - (D + c)/rho, R = r_S + r_T, v2 = 1 - r_y.
+__global__ void __launch_bounds__(TB* TY) xstep_a_kernel(Dev d, XConst c) {
+    const int b = blockIdx.y;
+    if (solve_done(d, b)) return;
+    int bi, bj;
+    tile_of(blockIdx.x, bi, bj);
+    const Layout& lo = d.lo;
+    const int n = lo.n;
+    const double* Y = d.Y + (long long)b * d.nx;
+    const double* D = d.D + (long long)b * d.nx;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int i0 = bi * TB, j0 = bj * TB;
+    __shared__ double Rs[TB][TB + 1];  // Rs[il][jl] = R(i,j) + R(j,i)
+    __shared__ double Hs[TB][TB + 1];  // Hs[il][jl] = h(i,j) (valid for pairs)
+    __shared__ double Zs[TB][TB + 1];  // het: h_z'(i,j)
+    __shared__ double rd_i[TB], rd_j[TB], v2_i[TB], v2_j[TB];
+
+    auto rS = [&](long long p) { return Y[lo.off_s + p] - D[lo.off_s + p] / c.rho; };
+    auto rT = [&](long long p) { return Y[lo.off_t + p] - D[lo.off_t + p] / c.rho; };
+    // orientation 1: R(i, j) at j*n + i
+    for (int cc = ty; cc < TB; cc += TY) {
+        const int i = i0 + tx, j = j0 + cc;
+        double v = 0.0;
+        if (i < n && j < n) {
+            const long long p = (long long)j * n + i;
+            v = rS(p) + rT(p);
+        }
+        Rs[tx][cc] = v;
+    }
+    // diagonals and v2 for both node blocks
+    if (ty == 0) {
+        const int i = i0 + tx, j = j0 + tx;
+        if (i < n) {
+            const long long p = (long long)i * n + i;
+            rd_i[tx] = rS(p) + rT(p);
+            v2_i[tx] = 1.0 - (Y[lo.off_y + i] - D[lo.off_y + i] / c.rho);
+        }
+        if (j < n) {
+            const long long p = (long long)j * n + j;
+            rd_j[tx] = rS(p) + rT(p);
+            v2_j[tx] = 1.0 - (Y[lo.off_y + j] - D[lo.off_y + j] / c.rho);
+        }
+    }
+    __syncthreads();
+    // orientation 2: R(j, i) at i*n + j
+    for (int cc = ty; cc < TB; cc += TY) {
+        const int j = j0 + tx, i = i0 + cc;
+        if (i < n && j < n) {
+            const long long p = (long long)i * n + j;
+            Rs[cc][tx] += rS(p) + rT(p);
+        }
+    }
+    __syncthreads();
+    // h over pairs of the tile (packed index contiguous in j)
+    for (int il = ty; il < TB; il += TY) {
+        const int i = i0 + il, jl = tx, j = j0 + jl;
+        double hv = 0.0, hz = 0.0;
+        if (i < n && j < n && j > i) {
+            const long long l = edge_idx(n, i, j);
+            const double rg = Y[l] - D[l] / c.rho;
+            hv = rg + c.s * (4.0 - rd_i[il] - rd_j[jl] + Rs[il][jl] + v2_i[il] + v2_j[jl]);
+            if (d.het) {
+                const long long lz = lo.off_z + l, lv = lo.off_nu + l;
+                const double rnu = Y[lv] - D[lv] / c.rho;
+                const double rz = Y[lz] - D[lz] / c.rho;
+                hv -= c.s * rnu;
+                hz = rz + c.s * rnu;
+            }
+            d.h[(long long)b * lo.m + l] = hv;
+        }
+        Hs[il][jl] = hv;
+        if (d.het) Zs[il][jl] = hz;
+    }
+    __syncthreads();
+    // node partials: PU[bj][i] (rows of block bi) and PU[bi][j] (cols of block bj)
+    const int t = ty * TB + tx;
+    double* PU = d.PU + (long long)b * d.nb * n;
+    double* PZ = d.PZ + (long long)b * d.nb * n;
+    if (t < TB) {
+        const int il = t, i = i0 + il;
+        if (i < n) {
+            double su = 0.0, sz = 0.0;
+            for (int jl = 0; jl < TB; ++jl) {
+                if (bi == bj) {
+                    if (jl == il) continue;
+                    const int a = jl > il ? il : jl, bb = jl > il ? jl : il;
+                    su += Hs[a][bb];
+                    if (d.het) sz += Zs[a][bb];
+                } else {
+                    su += Hs[il][jl];
+                    if (d.het) sz += Zs[il][jl];
+                }
+            }
+            PU[(long long)bj * n + i] = su;
+            if (d.het) PZ[(long long)bj * n + i] = sz;
+        }
+    } else if (t < 2 * TB && bi != bj) {
+        const int jl = t - TB, j = j0 + jl;
+        if (j < n) {
+            double su = 0.0, sz = 0.0;
+            for (int il = 0; il < TB; ++il) {
+                su += Hs[il][jl];
+                if (d.het) sz += Zs[il][jl];
+            }
+            PU[(long long)bi * n + j] = su;
+            if (d.het) PZ[(long long)bi * n + j] = sz;
+        }
+    }
+}
+
+void launch_xstep_a(const Dev& d, const XConst& c, cudaStream_t st) {
+    dim3 grid(d.ntile, d.B), block(TB, TY);
+    xstep_a_kernel<<<grid, block, 0, st>>>(d, c);
+    TPB_CHECK_LAUNCH();
+}
+
+// ---------------------------------------------------------------- node solve
+// One CTA per solve: node sums u = D h, lambda, and the node-space vectors of
+// the closed form. node[0..n) = t (hom) / t_g (het); node[n..2n) = t_z;
+// node[2n..3n) = mu_d. scal[kLambda] = lambda.
+__global__ void xstep_node_kernel(Dev d, XConst c) {
+    const int b = blockIdx.x;
+    if (solve_done(d, b)) return;
+    const Layout& lo = d.lo;
+    const int n = lo.n;
+    const double* Y = d.Y + (long long)b * d.nx;
+    const double* D = d.D + (long long)b * d.nx;
+    const double* PU = d.PU + (long long)b * d.nb * n;
+    const double* PZ = d.PZ + (long long)b * d.nb * n;
+    double* node = d.node + (long long)b * 4 * n;
+    __shared__ double scratch[32];
+    extern __shared__ double sh[];  // 3n doubles: ug, uz, tmp
+    double* ug = sh;
+    double* uz = sh + n;
+    double* tmp = sh + 2 * n;
+
+    // traces of r_S, r_T for lambda
+    double trS = 0.0, trT = 0.0, su = 0.0, sz = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const long long p = (long long)i * n + i;
+        trS += Y[lo.off_s + p] - D[lo.off_s + p] / c.rho;
+        trT += Y[lo.off_t + p] - D[lo.off_t + p] / c.rho;
+        double u = 0.0, z = 0.0;
+        for (int k = 0; k < d.nb; ++k) {
+            u += PU[(long long)k * n + i];
+            if (d.het) z += PZ[(long long)k * n + i];
+        }
+        ug[i] = u;
+        uz[i] = z;
+        su += u;
+        sz += z;
+    }
+    trS = block_sum(trS, scratch);
+    trT = block_sum(trT, scratch);
+    su = block_sum(su, scratch);
+    sz = block_sum(sz, scratch);
+    if (threadIdx.x == 0) {
+        const double rl = Y[lo.lambda_ix] - D[lo.lambda_ix] / c.rho + c.inv_rho;  // +1/rho: c = -1 at lambda
+        const double hl = rl + c.s * (c.alpha + trS + 2.0 * n - trT);
+        d.scal[b * 8 + kLambda] = hl / c.lam_den;
+    }
+    const double ubar = su / n;
+    if (!d.het) {
+        for (int i = threadIdx.x; i < n; i += blockDim.x)
+            node[i] = c.c1 * (ug[i] - ubar) + c.c2 * ubar;
+        return;
+    }
+    // het: rhs_d = G21(Q) u_g + G22(Q) u_z - e ; Q = (n-2) I + J
+    const double zbar = sz / n;
+    double srhs = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double rhs = c.g12_p * (ug[i] - ubar) + c.g12_1 * ubar + c.g22_p * (uz[i] - zbar) +
+                           c.g22_1 * zbar - d.deg[(long long)b * n + i];
+        tmp[i] = rhs;
+        srhs += rhs;
+    }
+    srhs = block_sum(srhs, scratch);
+    const double rbar = srhs / n;
+    double smu = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double mu = (tmp[i] - rbar) / c.mu_den_p + rbar / c.mu_den_1;
+        tmp[i] = mu;
+        node[2 * n + i] = mu;
+        smu += mu;
+    }
+    smu = block_sum(smu, scratch);
+    // u_z'' = u_z - Q mu = u_z - (n-2) mu - (sum mu) 1
+    double sz2 = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double v = uz[i] - (n - 2.0) * tmp[i] - smu;
+        uz[i] = v;
+        sz2 += v;
+    }
+    sz2 = block_sum(sz2, scratch);
+    const double z2bar = sz2 / n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double pg = ug[i] - ubar, pz = uz[i] - z2bar;
+        node[i] = c.c1_11 * pg + c.c2_11 * ubar + c.c1_12 * pz + c.c2_12 * z2bar;
+        node[n + i] = c.c1_12 * pg + c.c2_12 * ubar + c.c1_22 * pz + c.c2_22 * z2bar;
+    }
+}
+
+void launch_xstep_node(const Dev& d, const XConst& c, cudaStream_t st) {
+    const int threads = 256;
+    xstep_node_kernel<<<d.B, threads, 3 * d.lo.n * sizeof(double), st>>>(d, c);
+    TPB_CHECK_LAUNCH();
+}
+
+// ---------------------------------------------------------------- x-step B
+__global__ void __launch_bounds__(TB* TY) xstep_b_kernel(Dev d, XConst c) {
+    const int b = blockIdx.y;
+    if (solve_done(d, b)) return;
+    int bi, bj;
+    tile_of(blockIdx.x, bi, bj);
+    const Layout& lo = d.lo;
+    const int n = lo.n;
+    const double* Y = d.Y + (long long)b * d.nx;
+    double* X = d.X + (long long)b * d.nx;
+    double* D = d.D + (long long)b * d.nx;
+    const double* node = d.node + (long long)b * 4 * n;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int i0 = bi * TB, j0 = bj * TB;
+    __shared__ double Gs[TB][TB + 1];  // g(i, j) of the tile's pairs
+    __shared__ double red[TB * TY / 32];
+    double res = 0.0;
+
+    // edge blocks
+    for (int il = ty; il < TB; il += TY) {
+        const int i = i0 + il, jl = tx, j = j0 + jl;
+        double g = 0.0;
+        if (i < n && j < n && j > i) {
+            const long long l = edge_idx(n, i, j);
+            const double hv = d.h[(long long)b * lo.m + l];
+            if (!d.het) {
+                g = c.f0 * hv + node[i] + node[j];
+            } else {
+                const long long lz = lo.off_z + l, lv = lo.off_nu + l;
+                const double rz = Y[lz] - D[lz] / c.rho;
+                const double rnu = Y[lv] - D[lv] / c.rho;
+                const double hz2 = rz + c.s * rnu - node[2 * n + i] - node[2 * n + j];
+                g = c.g11_0 * hv + c.g12_0 * hz2 + node[i] + node[j];
+                const double z = c.g12_0 * hv + c.g22_0 * hz2 + node[n + i] + node[n + j];
+                // nu = s (delta r_nu - (g - z))   (slack of g - z + nu = 0)
+                const double nu = c.s * (c.delta * rnu - (g - z));
+                const double dz = z - Y[lz], dnu = nu - Y[lv];
+                X[lz] = z;
+                X[lv] = nu;
+                if (d.upd_duals) {
+                    D[lz] += c.rho * dz;
+                    D[lv] += c.rho * dnu;
+                }
+                res += dz * dz + dnu * dnu;
+            }
+            const double dg = g - Y[l];
+            X[l] = g;
+            if (d.upd_duals) D[l] += c.rho * dg;
+            res += dg * dg;
+        }
+        Gs[il][jl] = g;
+    }
+    __syncthreads();
+    // off-diagonal S/T entries: L_ij = -g, so
+    //   S_ij = s (delta r_S,ij - alpha/n + g),  T_ij = s (delta r_T,ij + g)
+    auto upd = [&](long long p, double g) {
+        const long long ps = lo.off_s + p, pt = lo.off_t + p;
+        const double ys = Y[ps], yt = Y[pt];
+        const double rs = ys - D[ps] / c.rho, rt = yt - D[pt] / c.rho;
+        const double xs = c.s * (c.delta * rs - c.alpha_over_n + g);
+        const double xt = c.s * (c.delta * rt + g);
+        X[ps] = xs;
+        X[pt] = xt;
+        if (d.upd_duals) {
+            D[ps] += c.rho * (xs - ys);
+            D[pt] += c.rho * (xt - yt);
+        }
+        res += (xs - ys) * (xs - ys) + (xt - yt) * (xt - yt);
+    };
+    // orientation 1: entries (i, j), address j*n + i
+    for (int cc = ty; cc < TB; cc += TY) {
+        const int i = i0 + tx, j = j0 + cc;
+        if (i >= n || j >= n || i == j) continue;
+        if (bi == bj) {
+            // diagonal tile: entry (i, j) with either order
+            const double g = i < j ? Gs[tx][cc] : Gs[cc][tx];
+            upd((long long)j * n + i, g);
+        } else {
+            upd((long long)j * n + i, Gs[tx][cc]);
+        }
+    }
+    if (bi != bj) {
+        // orientation 2: entries (j, i), address i*n + j
+        for (int cc = ty; cc < TB; cc += TY) {
+            const int j = j0 + tx, i = i0 + cc;
+            if (i >= n || j >= n) continue;
+            upd((long long)i * n + j, Gs[cc][tx]);
+        }
+    }
+    // node partials of g (deg = L_ii)
+    const int t = ty * TB + tx;
+    double* PG = d.PG + (long long)b * d.nb * n;
+    if (t < TB) {
+        const int il = t, i = i0 + il;
+        if (i < n) {
+            double s = 0.0;
+            for (int jl = 0; jl < TB; ++jl) {
+                if (bi == bj) {
+                    if (jl == il) continue;
+                    s += jl > il ? Gs[il][jl] : Gs[jl][il];
+                } else {
+                    s += Gs[il][jl];
+                }
+            }
+            PG[(long long)bj * n + i] = s;
+        }
+    } else if (t < 2 * TB && bi != bj) {
+        const int jl = t - TB, j = j0 + jl;
+        if (j < n) {
+            double s = 0.0;
+            for (int il = 0; il < TB; ++il) s += Gs[il][jl];
+            PG[(long long)bi * n + j] = s;
+        }
+    }
+    // residual partial of this tile
+    {
+        const int lane = t & 31, wid = t >> 5;
+        double v = warp_sum(res);
+        __syncthreads();
+        if (lane == 0) red[wid] = v;
+        __syncthreads();
+        if (t == 0) {
+            double s = 0.0;
+            for (int w = 0; w < TB * TY / 32; ++w) s += red[w];
+            d.res_part[(long long)b * d.ntile + blockIdx.x] = s;
+        }
+    }
+}
+
+void launch_xstep_b(const Dev& d, const XConst& c, cudaStream_t st) {
+    dim3 grid(d.ntile, d.B), block(TB, TY);
+    xstep_b_kernel<<<grid, block, 0, st>>>(d, c);
+    TPB_CHECK_LAUNCH();
+}
+
+// ---------------------------------------------------------------- diag + tail
+// deg_i = L_ii = sum of node partials of g. Diagonal entries:
+//   S_ii = s (delta r_S,ii - alpha/n - deg_i + lambda)
+//   T_ii = s (delta r_T,ii + 2 - deg_i - lambda)
+//   y_i  = s (delta r_y,i + 1 - deg_i)
+// then residual, trace row, best iterate flag and the stop test.
+__global__ void xstep_diag_kernel(Dev d, XConst c) {
+    const int b = blockIdx.x;
+    int* ctl = d.ictl + b * 8;
+    if (ctl[kDone]) return;
+    const Layout& lo = d.lo;
+    const int n = lo.n;
+    const double* Y = d.Y + (long long)b * d.nx;
+    double* X = d.X + (long long)b * d.nx;
+    double* D = d.D + (long long)b * d.nx;
+    const double* PG = d.PG + (long long)b * d.nb * n;
+    const double lam = d.scal[b * 8 + kLambda];
+    __shared__ double scratch[32];
+    double res = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double deg = 0.0;
+        for (int k = 0; k < d.nb; ++k) deg += PG[(long long)k * n + i];
+        const long long p = (long long)i * n + i;
+        const long long ps = lo.off_s + p, pt = lo.off_t + p, py = lo.off_y + i;
+        const double ys = Y[ps], yt = Y[pt], yy = Y[py];
+        const double rs = ys - D[ps] / c.rho, rt = yt - D[pt] / c.rho, ry = yy - D[py] / c.rho;
+        const double xs = c.s * (c.delta * rs - c.alpha_over_n - deg + lam);
+        const double xt = c.s * (c.delta * rt + 2.0 - deg - lam);
+        const double xy = c.s * (c.delta * ry + 1.0 - deg);
+        X[ps] = xs;
+        X[pt] = xt;
+        X[py] = xy;
+        if (d.upd_duals) {
+            D[ps] += c.rho * (xs - ys);
+            D[pt] += c.rho * (xt - yt);
+            D[py] += c.rho * (xy - yy);
+        }
+        res += (xs - ys) * (xs - ys) + (xt - yt) * (xt - yt) + (xy - yy) * (xy - yy);
+    }
+    // tile partials in fixed order
+    for (int t = threadIdx.x; t < d.ntile; t += blockDim.x) res += d.res_part[(long long)b * d.ntile + t];
+    res = block_sum(res, scratch);
+    if (threadIdx.x == 0 && !d.upd_duals) X[lo.lambda_ix] = lam;
+    if (threadIdx.x == 0 && d.upd_duals) {
+        const double yl = Y[lo.lambda_ix];
+        X[lo.lambda_ix] = lam;
+        D[lo.lambda_ix] += c.rho * (lam - yl);
+        res += (lam - yl) * (lam - yl);
+        const int it = ctl[kIter];  // 0-based index of this iteration
+        d.tr_res[(long long)b * d.max_iter + it] = res;
+        d.tr_lam[(long long)b * d.max_iter + it] = yl;
+        d.scal[b * 8 + kRes] = res;
+        ctl[kIter] = it + 1;
+        if (d.track_best && res < d.scal[b * 8 + kBestRes]) {
+            d.scal[b * 8 + kBestRes] = res;
+            ctl[kBestIter] = it + 1;
+            ctl[kImproved] = 1;
+        }
+        if (res <= d.epsilon) {
+            ctl[kDone] = 1;
+            ctl[4] = 1;  // converged
+        } else if (it + 1 >= d.max_iter) {
+            ctl[kDone] = 1;
+        }
+    }
+}
+
+void launch_xstep_diag(const Dev& d, const XConst& c, cudaStream_t st) {
+    xstep_diag_kernel<<<d.B, 256, 0, st>>>(d, c);
+    TPB_CHECK_LAUNCH();
+}
+
+// ---------------------------------------------------------------- best copy
+__global__ void best_copy_kernel(Dev d, XConst c) {
+    const int b = blockIdx.y;
+    int* ctl = d.ictl + b * 8;
+    if (!ctl[kImproved]) return;
+    const double* Y = d.Y + (long long)b * d.nx;
+    double* bY = d.bestY + (long long)b * d.nx;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < d.nx; k += stride)
+        bY[k] = Y[k];
+    if (d.het) {
+        const Layout& lo = d.lo;
+        const double* X = d.X + (long long)b * d.nx;
+        const double* D = d.D + (long long)b * d.nx;
+        double* sc = d.bestScore + (long long)b * lo.m;
+        for (long long l = (long long)blockIdx.x * blockDim.x + threadIdx.x; l < lo.m; l += stride)
+            sc[l] = X[lo.off_z + l] + D[lo.off_z + l] / c.rho;  // proj/src/admm_het.cpp:293-294
+    }
+}
+
+__global__ void clear_improved_kernel(Dev d) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < d.B) d.ictl[b * 8 + kImproved] = 0;
+}
+
+void launch_best_copy(const Dev& d, const XConst& c, cudaStream_t st) {
+    const int blocks = (int)std::min<long long>((d.nx + 255) / 256, 512);
+    best_copy_kernel<<<dim3(blocks, d.B), 256, 0, st>>>(d, c);
+    TPB_CHECK_LAUNCH();
+    clear_improved_kernel<<<(d.B + 127) / 128, 128, 0, st>>>(d);
+    TPB_CHECK_LAUNCH();
+}
+
+void init_attrs_admm() {
+    set_max_dyn_smem(xstep_node_kernel);
+}
+
+}  // namespace tpb

@@ -1,0 +1,77 @@
+// Kernel interfaces of the ADMM iteration (projection prep, closed-form
+// x-step passes, dual update, residual, bookkeeping). See DESIGN.md §3.
+#pragma once
+
+#include "common.cuh"
+
+namespace tpb {
+
+// Scalars of the closed-form x-step. All derived on the host
+// in FP64 from rho, alpha, n and the KKT shift delta = 1e-8.
+struct XConst {
+    double rho, inv_rho, alpha, alpha_over_n, delta, s;  // s = 1/(1+delta)
+    // homogeneous: g = f(K) h, f(k) = 1/(a + b k), K = D^T D
+    double f0, c1, c2, lam_den;                           // lam_den = 1 + 2 n s
+    // heterogeneous (node-level): 2x2 block G(k) of [[a1+b1 k, -s], [-s, a2]]^-1
+    double g11_0, g12_0, g22_0;                           // G(0)
+    double c1_11, c2_11, c1_12, c2_12, c1_22, c2_22;      // (G(q)-G(0))/q at q=n-2, 2n-2
+    double g12_p, g22_p, g12_1, g22_1;                    // G12/G22 at n-2 and 2n-2
+    double mu_den_p, mu_den_1;                            // (n-2)G22(n-2)+delta, (2n-2)G22(2n-2)+delta
+};
+
+XConst make_xconst(int n, double alpha, double rho);
+
+// Per-batch device views (every array has a leading batch dimension).
+struct Dev {
+    Layout lo;
+    int B = 1;       // solves in lockstep
+    int het = 0;
+    int nb = 0;      // 32-wide node blocks
+    int ntile = 0;   // nb (nb+1) / 2 upper block pairs
+    int ld = 0;      // padded projection dimension
+    long long nx = 0;
+    // state
+    double *X, *Y, *D, *bestY, *bestScore;
+    // projection
+    double* A;         // B x 2 x ld x ld  (S, T inputs, symmetrized)
+    double* frob_part; // B x 2 x ntile
+    double* inv_scale; // B x 2   (1/||A||_F)
+    // x-step scratch
+    double* h;         // B x m
+    double* PU;        // B x nb x n  (row partials of h)
+    double* PZ;        // B x nb x n  (het: row partials of h_z')
+    double* PG;        // B x nb x n  (row partials of g)
+    double* node;      // B x 4 x n   (hom: t; het: t_g, t_z, mu_d)
+    double* res_part;  // B x ntile
+    double* scal;      // B x 8 : [lambda, res, best_res, ...]
+    int* ictl;         // B x 8 : [iter, done, best_iter, improved, active]
+    const int* r;      // B     edge budgets
+    const double* deg; // B x n (het degree targets as doubles)
+    // traces (B x max_iter): residual, lambda, acf
+    double *tr_res, *tr_lam, *tr_acf;
+    int max_iter;
+    double epsilon;
+    int track_best;
+    int upd_duals;   // 0: x-step only (substep API), no dual update / bookkeeping
+};
+
+enum Ctl { kIter = 0, kDone = 1, kBestIter = 2, kImproved = 3 };
+enum Scal { kLambda = 0, kRes = 1, kBestRes = 2 };
+
+// v = X + D/rho; symmetrized S/T into A (ld-padded), clamps of g, lambda, y,
+// nu; z-scores into Y_z. Frobenius partials per tile.
+void launch_prep(const Dev& d, const XConst& c, cudaStream_t st);
+// 1/||A||_F per matrix.
+void launch_frob_finalize(const Dev& d, cudaStream_t st);
+// x-step pass A: h (packed) and node partials.
+void launch_xstep_a(const Dev& d, const XConst& c, cudaStream_t st);
+// node-space solve (lambda, t, mu_d).
+void launch_xstep_node(const Dev& d, const XConst& c, cudaStream_t st);
+// x-step pass B: g (z, nu), off-diagonal S/T, dual update, residual partials.
+void launch_xstep_b(const Dev& d, const XConst& c, cudaStream_t st);
+// diagonal entries, y, lambda, residual, trace, best/done flags.
+void launch_xstep_diag(const Dev& d, const XConst& c, cudaStream_t st);
+// best_y <- Y (and best_score) where the last iteration improved.
+void launch_best_copy(const Dev& d, const XConst& c, cudaStream_t st);
+
+}  // namespace tpb

@@ -1,0 +1,326 @@
+// C ABI (include/topoopt_b200.h): host entry points over the device solver.
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/topoopt_b200.h"
+#include "host_anneal.hpp"
+#include "solver.cuh"
+
+using namespace tpb;
+
+namespace {
+
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return TP_OK;
+    } catch (const Error& e) {
+        last_error_ref() = e.what();
+        return e.status;
+    } catch (const std::bad_alloc& e) {
+        last_error_ref() = std::string("out of memory: ") + e.what();
+        return TP_ERR_INTERNAL;
+    } catch (const std::exception& e) {
+        last_error_ref() = e.what();
+        return TP_ERR_INTERNAL;
+    }
+}
+
+Config to_cfg(const tp_config* c) {
+    Config k;
+    if (c) {
+        k.rho = c->rho;
+        k.epsilon = c->epsilon;
+        k.max_iter = c->max_iter;
+        k.alpha = c->alpha;
+        k.weight_floor = c->weight_floor;
+        k.linear_tol = c->linear_tol;
+        k.trace_stride = c->trace_stride;
+        k.chunk = c->chunk;
+    }
+    return k;
+}
+
+void require_device() {
+    int count = 0;
+    const cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        throw Error(kCuda, "no CUDA device: the B200 solver has no CPU fallback");
+}
+
+// Topology::normalize_and_validate (proj/src/topology.cpp:19-51) on an edge
+// list, returned as ascending packed indices.
+std::vector<int> packed_edges(int n, const int32_t* edges, int k) {
+    std::vector<long long> idx(k);
+    for (int e = 0; e < k; ++e) {
+        const int i = edges[2 * e], j = edges[2 * e + 1];
+        if (i < 0 || j < 0 || i >= n || j >= n)
+            throw Error(kInvalidArgument, "topology: edge endpoint out of range");
+        if (i >= j) throw Error(kInvalidArgument, "topology: edge endpoints must satisfy i < j");
+        idx[e] = edge_idx(n, i, j);
+    }
+    std::sort(idx.begin(), idx.end());
+    for (int e = 1; e < k; ++e)
+        if (idx[e] == idx[e - 1])
+            throw Error(kInvalidArgument, "topology: edges must be sorted without duplicates");
+    return std::vector<int>(idx.begin(), idx.end());
+}
+
+void fill_result(const SolveResult& R, tp_result* out, int32_t* edges, double* weights,
+                 double* trace, char* note, int note_cap) {
+    if (out) {
+        out->iterations = R.iterations;
+        out->converged = R.converged;
+        out->connected = R.connected;
+        out->repaired = R.repaired;
+        out->n_edges = (int32_t)R.w.size();
+        out->best_iter = R.best_iter;
+        out->residual = R.residual;
+        out->lambda_tilde = R.lambda_tilde;
+        out->acf = R.acf;
+        out->lambda2 = R.lambda2;
+        out->lambda_n = R.lambda_n;
+    }
+    if (edges)
+        for (size_t k = 0; k < R.w.size(); ++k) {
+            edges[2 * k] = R.ei[k];
+            edges[2 * k + 1] = R.ej[k];
+        }
+    if (weights) std::copy(R.w.begin(), R.w.end(), weights);
+    if (trace)
+        for (int k = 0; k < R.iterations; ++k) {
+            trace[3 * k] = R.tr_res[k];
+            trace[3 * k + 1] = R.tr_lam[k];
+            trace[3 * k + 2] = R.tr_acf[k];
+        }
+    if (note && note_cap > 0) {
+        const size_t len = std::min<size_t>(R.note.size(), note_cap - 1);
+        std::memcpy(note, R.note.data(), len);
+        note[len] = 0;
+    }
+}
+
+// default warm start through the host annealer + device Alg. 1
+std::vector<int> default_warm(int n, int r, uint64_t seed);
+
+}  // namespace
+
+namespace tpb {
+std::string& last_error_ref() {
+    thread_local std::string msg;
+    return msg;
+}
+}  // namespace tpb
+
+struct tp_solver {
+    std::unique_ptr<Solver> s;
+};
+
+extern "C" {
+
+void tp_config_default(tp_config* c) {
+    c->rho = 1.0;
+    c->epsilon = 1e-6;
+    c->max_iter = 20000;
+    c->alpha = 2.0;
+    c->weight_floor = 1e-6;
+    c->seed = 0;
+    c->linear_tol = 1e-10;
+    c->trace_stride = 1;
+    c->chunk = 0;
+}
+
+int tp_config_validate(const tp_config* c) {
+    return guarded([&] { validate(to_cfg(c)); });
+}
+
+const char* tp_last_error_message(void) { return last_error_ref().c_str(); }
+int tp_version(void) { return 1; }
+
+int tp_set_device(int device) {
+    return guarded([&] { TPB_CUDA(cudaSetDevice(device)); });
+}
+
+int tp_solver_create(int32_t n, int32_t batch, const int32_t* r, const int32_t* degrees,
+                     const tp_config* cfg, tp_solver** out) {
+    return guarded([&] {
+        require_device();
+        std::vector<int> rv, dg;
+        if (r) rv.assign(r, r + batch);
+        if (degrees) dg.assign(degrees, degrees + (size_t)batch * n);
+        auto h = std::make_unique<tp_solver>();
+        h->s = std::make_unique<Solver>(n, batch, degrees != nullptr, rv, dg, to_cfg(cfg));
+        *out = h.release();
+    });
+}
+
+int tp_solver_destroy(tp_solver* s) {
+    return guarded([&] { delete s; });
+}
+
+int tp_solver_set_warm(tp_solver* s, int32_t b, const int32_t* edges, int32_t k) {
+    return guarded([&] { s->s->set_warm(b, packed_edges(s->s->n(), edges, k)); });
+}
+
+int tp_solver_start(tp_solver* s) {
+    return guarded([&] { s->s->start(); });
+}
+
+int tp_solver_iterate(tp_solver* s, int32_t k) {
+    return guarded([&] { s->s->iterate_async(k); });
+}
+
+int tp_solver_sync(tp_solver* s, int32_t* all_done) {
+    return guarded([&] {
+        const bool d = s->s->all_done();
+        if (all_done) *all_done = d ? 1 : 0;
+    });
+}
+
+int tp_solver_run(tp_solver* s) {
+    return guarded([&] { s->s->run_to_completion(); });
+}
+
+int tp_solver_finish(tp_solver* s) {
+    return guarded([&] { s->s->finish(); });
+}
+
+int tp_solver_result(tp_solver* s, int32_t b, tp_result* out, int32_t* edges, double* weights,
+                     double* trace, char* note, int32_t note_cap) {
+    return guarded([&] { fill_result(s->s->result(b), out, edges, weights, trace, note, note_cap); });
+}
+
+void* tp_solver_stream(tp_solver* s) { return (void*)s->s->stream(); }
+
+int tp_solver_dims(tp_solver* s, int32_t* d) {
+    return guarded([&] {
+        const Layout& lo = s->s->layout();
+        const int32_t v[12] = {lo.n, lo.m, lo.nx, lo.neq, lo.off_s, lo.off_y, lo.off_t,
+                               lo.lambda_ix, lo.off_z, lo.off_nu, s->s->batch(), lo.off_z >= 0};
+        std::copy(v, v + 12, d);
+    });
+}
+
+int tp_solver_state(tp_solver* s, double** x, double** y, double** d) {
+    return guarded([&] {
+        Dev& dv = s->s->dev();
+        if (x) *x = dv.X;
+        if (y) *y = dv.Y;
+        if (d) *d = dv.D;
+    });
+}
+
+int tp_solve(int32_t n, int32_t r, const tp_config* cfg, const int32_t* warm_edges, int32_t n_warm,
+             tp_result* out, int32_t* edges, double* weights, double* trace, char* note,
+             int32_t note_cap) {
+    return guarded([&] {
+        require_device();
+        const Config c = to_cfg(cfg);
+        validate(c);
+        Solver s(n, 1, false, std::vector<int>{r}, {}, c);
+        std::vector<int> warm;
+        if (warm_edges && n_warm >= 0) warm = packed_edges(n, warm_edges, n_warm);
+        else warm = default_warm(n, r, cfg ? cfg->seed : 0);
+        s.set_warm(0, warm);
+        s.start();
+        s.run_to_completion();
+        s.finish();
+        const SolveResult R = s.result(0);
+        if (R.w.empty()) throw Error(kDegenerate, "every edge weight is at or below the floor");
+        fill_result(R, out, edges, weights, trace, note, note_cap);
+    });
+}
+
+int tp_solve_het_node(int32_t n, const int32_t* degrees, const tp_config* cfg,
+                      const int32_t* warm_edges, int32_t n_warm, tp_result* out, int32_t* edges,
+                      double* weights, double* trace, char* note, int32_t note_cap) {
+    return guarded([&] {
+        require_device();
+        const Config c = to_cfg(cfg);
+        validate(c);
+        std::vector<int> dg(degrees, degrees + n);
+        Solver s(n, 1, true, {}, dg, c);
+        std::vector<int> warm;
+        if (warm_edges && n_warm >= 0) {
+            warm = packed_edges(n, warm_edges, n_warm);
+        } else {
+            // anneal_topology -> anneal_degree_topology (proj/src/anneal.cpp:393-407)
+            AnnealParams ap;
+            ap.seed = cfg ? cfg->seed : 0;
+            warm = anneal_degree_packed(dg, ap);
+        }
+        s.set_warm(0, warm);
+        s.start();
+        s.run_to_completion();
+        s.finish();
+        fill_result(s.result(0), out, edges, weights, trace, note, note_cap);
+    });
+}
+
+int tp_anneal_degree(int32_t n, const int32_t* degrees, double t0, double cooling, int32_t steps,
+                     int32_t moves_per_temp, uint64_t seed, int32_t* edges, int32_t* n_edges) {
+    return guarded([&] {
+        AnnealParams ap;
+        ap.t0 = t0;
+        ap.cooling = cooling;
+        ap.steps = steps;
+        ap.moves_per_temp = moves_per_temp;
+        ap.seed = seed;
+        const auto es = anneal_degree_edges(std::vector<int>(degrees, degrees + n), ap);
+        for (size_t k = 0; k < es.size(); ++k) {
+            edges[2 * k] = es[k].first;
+            edges[2 * k + 1] = es[k].second;
+        }
+        *n_edges = (int32_t)es.size();
+    });
+}
+
+int tp_default_warm_start(int32_t n, int32_t r, uint64_t seed, int32_t* edges, int32_t* n_edges) {
+    return guarded([&] {
+        if (n < 2) throw Error(kInvalidArgument, "enumerate_edges: need at least two nodes");
+        const auto packed = default_warm(n, r, seed);
+        for (size_t k = 0; k < packed.size(); ++k) {
+            // invert the packed index on the host
+            long long l = packed[k];
+            int i = 0;
+            while (edge_base(n, i + 1) <= l && i < n - 2) ++i;
+            edges[2 * k] = i;
+            edges[2 * k + 1] = (int)(l - edge_base(n, i)) + i + 1;
+        }
+        *n_edges = (int32_t)packed.size();
+    });
+}
+
+}  // extern "C"
+
+namespace {
+
+std::vector<int> default_warm(int n, int r, uint64_t seed) {
+    // proj/src/admm.cpp:337-354: Alg. 1 with unit bandwidths, then the
+    // balanced-degree anneal; r < n-1 falls back to a chain of r edges.
+    std::vector<double> b(n, 1.0);
+    std::vector<int32_t> e(n);
+    double bu = 0.0;
+    const int st = tp_allocate(b.data(), nullptr, n, r, &bu, e.data());
+    if (st == TP_OK) {
+        try {
+            AnnealParams ap;
+            ap.seed = seed;
+            return anneal_degree_packed(std::vector<int>(e.begin(), e.end()), ap);
+        } catch (const Error& err) {
+            if (err.status != kInfeasible) throw;
+        }
+    } else if (st != TP_ERR_INFEASIBLE) {
+        throw Error(st, last_error_ref());
+    }
+    std::vector<int> chain;
+    for (int i = 0; i < r; ++i) chain.push_back((int)edge_idx(n, i, i + 1));
+    return chain;
+}
+
+}  // namespace

@@ -1,0 +1,369 @@
+// PSD / NSD cone projections of the n x n slack blocks on the FP64 tensor
+// pipe (DMMA, mma.sync.m8n8k4.f64). Replaces the reference's per-iteration
+// eigen-clamps project_nsd(S) / project_psd(T) (proj/src/admm.cpp:96-112 ->
+// clamp_spectrum, proj/src/eig.cpp:131-176: Householder tridiagonalisation +
+// implicit QL + rank-1 rebuild, O(n^3) scalar code).
+//
+// tcgen05 has no FP64 kind; B200's FP64 tensor path is DMMA,
+// measured at ~37 TFLOP/s (tools/microbench/fp64_peak.cu). The projection is
+// a polynomial sign iteration (cone_kernels.cuh) whose every product is of
+// commuting symmetric matrices, so only lower-triangular 64x64 tiles are
+// computed (half the flops) and mirrored on store (exact symmetry, as the
+// reference's symmetrize() gives).
+#include "cone_kernels.cuh"
+
+namespace tpb {
+
+namespace {
+
+constexpr int BM = 64;        // tile edge
+constexpr int BK = 16;        // k per stage
+constexpr int PAD = BK + 4;   // smem row stride (doubles): conflict-free fragments
+constexpr int STAGES = 3;
+constexpr int GT = 128;       // 4 warps, 2 x 2 warp tiles of 32 x 32
+
+__device__ inline void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+__device__ inline void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ inline void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ inline void cp_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ inline void lower_tile(int t, int& bi, int& bj) {
+    // t enumerates (bi >= bj): t = bi (bi+1)/2 + bj
+    int b = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while ((b + 1) * (b + 2) / 2 <= t) ++b;
+    while (b * (b + 1) / 2 > t) --b;
+    bi = b;
+    bj = t - b * (b + 1) / 2;
+}
+
+__device__ inline double powi(double s, int p) { return p == 0 ? 1.0 : (p == 1 ? s : s * s); }
+
+}  // namespace
+
+__global__ void __launch_bounds__(GT) sym_gemm_kernel(GemmArgs g) {
+    const int mat = blockIdx.y;
+    if (g.ictl && g.ictl[(mat >> 1) * 8 + 1]) return;
+    int bi, bj;
+    lower_tile(blockIdx.x, bi, bj);
+    const int i0 = bi * BM, j0 = bj * BM;
+    const int ld = g.ld;
+    const double* A = g.A + (long long)mat * g.mstride;
+    const double* B = g.B + (long long)mat * g.mstride;
+    extern __shared__ __align__(16) double smem[];
+    double* As = smem;                          // STAGES x BM x PAD
+    double* Bs = smem + STAGES * BM * PAD;      // STAGES x BM x PAD
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wr = (warp >> 1) * 32, wc = (warp & 1) * 32;
+
+    auto load_stage = [&](int slot, int kt) {
+        const int k0 = kt * BK;
+        double* as = As + slot * BM * PAD;
+        double* bs = Bs + slot * BM * PAD;
+        // 64 rows x 8 chunks of 16 B per panel
+#pragma unroll
+        for (int c = tid; c < BM * (BK / 2); c += GT) {
+            const int r = c >> 3, q = (c & 7) * 2;
+            cp_async16(as + r * PAD + q, A + (long long)(i0 + r) * ld + k0 + q);
+            cp_async16(bs + r * PAD + q, B + (long long)(j0 + r) * ld + k0 + q);
+        }
+    };
+
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+    const int KT = ld / BK;
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < KT) load_stage(s, s);
+        cp_commit();
+    }
+    for (int kt = 0; kt < KT; ++kt) {
+        cp_wait<STAGES - 2>();
+        __syncthreads();
+        const int nk = kt + STAGES - 1;
+        if (nk < KT) load_stage(nk % STAGES, nk);
+        cp_commit();
+        const double* as = As + (kt % STAGES) * BM * PAD;
+        const double* bs = Bs + (kt % STAGES) * BM * PAD;
+#pragma unroll
+        for (int ks = 0; ks < BK / 4; ++ks) {
+            double af[4], bf[4];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+                af[mi] = as[(wr + mi * 8 + (lane >> 2)) * PAD + ks * 4 + (lane & 3)];
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni)
+                bf[ni] = bs[(wc + ni * 8 + (lane >> 2)) * PAD + ks * 4 + (lane & 3)];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+        }
+    }
+    cp_wait<0>();
+    __syncthreads();
+
+    // epilogue: C = alpha acc + beta E, staged through smem for the mirror store
+    const double s = g.scale ? g.scale[mat] : 1.0;
+    double alpha = g.alpha_c * powi(s, g.pa);
+    const double beta = g.beta_c * powi(s, g.pb);
+    if (g.sign_mode && (mat & 1) == 0) alpha = -alpha;
+    const double* E = g.E ? g.E + (long long)mat * g.mstride : nullptr;
+    double* Cs = smem;  // BM x (BM + 1)
+    constexpr int CP = BM + 1;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+            const int r = wr + mi * 8 + (lane >> 2);
+            const int c = wc + ni * 8 + (lane & 3) * 2;
+            double v0 = alpha * acc[mi][ni][0], v1 = alpha * acc[mi][ni][1];
+            if (E) {
+                const double* e = E + (long long)(i0 + r) * ld + j0 + c;
+                v0 += beta * e[0];
+                v1 += beta * e[1];
+            }
+            Cs[r * CP + c] = v0;
+            Cs[r * CP + c + 1] = v1;
+        }
+    __syncthreads();
+    double* C = g.C + (long long)(mat >> 1) * g.c_stride_b + (long long)(mat & 1) * g.c_stride_w;
+    const int nv = g.nvalid;
+    for (int idx = tid; idx < BM * BM; idx += GT) {
+        const int r = idx / BM, c = idx % BM;
+        const int i = i0 + r, j = j0 + c;
+        if (i < nv && j < nv) {
+            // diagonal tiles: take the lower-triangle value for exact symmetry
+            const double v = (bi == bj && c > r) ? Cs[c * CP + r] : Cs[r * CP + c];
+            C[(long long)i * g.ldc + j] = v;
+        }
+    }
+    if (bi != bj) {
+        for (int idx = tid; idx < BM * BM; idx += GT) {
+            const int r = idx / BM, c = idx % BM;  // write (j0 + r, i0 + c) = Cs[c][r]
+            const int i = j0 + r, j = i0 + c;
+            if (i < nv && j < nv) C[(long long)i * g.ldc + j] = Cs[c * CP + r];
+        }
+    }
+}
+
+void launch_sym_gemm(const GemmArgs& g, int nmat, cudaStream_t st) {
+    const int nt = g.ld / BM;
+    const int tiles = nt * (nt + 1) / 2;
+    const int smem = 2 * STAGES * BM * PAD * sizeof(double);
+    sym_gemm_kernel<<<dim3(tiles, nmat), GT, smem, st>>>(g);
+    TPB_CHECK_LAUNCH();
+}
+
+void enqueue_cone_tiled(const double* A, double* w0, double* w1, double* w2, int ld, int n,
+                        const double* scale, double* C, long long c_stride_b,
+                        long long c_stride_w, const int* ictl, int nmat, const SignSchedule& sch,
+                        cudaStream_t st) {
+    const long long ms = (long long)ld * ld;
+    GemmArgs g{};
+    g.mstride = ms;
+    g.ld = ld;
+    g.scale = scale;
+    g.ictl = ictl;
+    g.ldc = ld;
+    g.nvalid = ld;
+    g.c_stride_b = 2 * ms;
+    g.c_stride_w = ms;
+    auto step = [&](const double* a, const double* b, const double* e, double* c, double al,
+                    double be, int pa, int pb) {
+        g.A = a;
+        g.B = b;
+        g.E = e;
+        g.C = c;
+        g.alpha_c = al;
+        g.beta_c = be;
+        g.pa = pa;
+        g.pb = pb;
+        launch_sym_gemm(g, nmat, st);
+    };
+    // X lives in one work buffer (or is A before the first step); each step
+    // takes the two buffers X does not occupy.
+    const double* X = A;  // X0 = s A: the scale is folded into alpha/beta powers
+    double* bufs[3] = {w0, w1, w2};
+    auto free_pair = [&](double*& f0, double*& f1) {
+        int k = 0;
+        double* fr[3];
+        for (int q = 0; q < 3; ++q)
+            if (bufs[q] != X) fr[k++] = bufs[q];
+        f0 = fr[0];
+        f1 = fr[1];
+    };
+    int first = 1;
+    for (int it = 0; it < sch.k1; ++it) {
+        double *Y, *Z;
+        free_pair(Y, Z);
+        step(X, X, nullptr, Y, 1.0, 0.0, first ? 2 : 0, 0);             // Y = X^2
+        step(Y, Y, Y, Z, sch.qc, sch.qb, 0, 0);                          // Z = c Y^2 + b Y
+        step(X, Z, X, Y, 1.0, sch.qa, first ? 1 : 0, first ? 1 : 0);     // X' = X Z + a X (into Y)
+        X = Y;
+        first = 0;
+    }
+    for (int it = 0; it < sch.k2; ++it) {
+        double *Y, *Xn;
+        free_pair(Y, Xn);
+        step(X, X, nullptr, Y, 1.0, 0.0, first ? 2 : 0, 0);              // Y = X^2
+        step(X, Y, X, Xn, -0.5, 1.5, first ? 1 : 0, first ? 1 : 0);      // X' = 1.5 X - 0.5 X Y
+        X = Xn;
+        first = 0;
+    }
+    // P = 0.5 A -/+ 0.5 A X into the state (column-major n x n == row-major by symmetry)
+    g.ldc = n;
+    g.nvalid = n;
+    g.c_stride_b = c_stride_b;
+    g.c_stride_w = c_stride_w;
+    g.sign_mode = 1;
+    step(A, X, A, C, 0.5, 0.5, 0, 0);
+}
+
+// ---------------------------------------------------------------- small n
+// One CTA per matrix; all iterates in shared memory (npad <= 64).
+namespace {
+constexpr int ST = 256;  // 8 warps
+}
+
+__global__ void __launch_bounds__(ST) cone_small_kernel(const double* Ag, long long mstride, int ld, int n,
+                                                       double* Cg, long long c_stride_b,
+                                                       long long c_stride_w, const int* ictl,
+                                                       SignSchedule sch) {
+    const int mat = blockIdx.x;
+    if (ictl && ictl[(mat >> 1) * 8 + 1]) return;
+    const int np = (n + 7) & ~7;
+    const int P = np + 4;  // padded stride
+    extern __shared__ __align__(16) double sm[];
+    double* A = sm;
+    double* X = A + np * P;
+    double* Y = X + np * P;
+    double* Z = Y + np * P;
+    double* T = Z + np * P;
+    __shared__ double scratch[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const double* src = Ag + (long long)mat * mstride;
+    double fro = 0.0;
+    for (int idx = tid; idx < np * np; idx += ST) {
+        const int r = idx / np, c = idx % np;
+        const double v = (r < n && c < n) ? src[(long long)r * ld + c] : 0.0;
+        A[r * P + c] = v;
+        fro += v * v;
+    }
+    fro = block_sum(fro, scratch);
+    const double s = fro > 0.0 ? 1.0 / sqrt(fro) : 0.0;
+    const int nf = np / 8;
+    const int nfr = nf * (nf + 1) / 2;  // lower 8x8 fragments
+
+    // dst = alpha * (a . b) + beta * e ; lower frags computed, mirrored
+    auto gemm = [&](const double* a, const double* b, const double* e, double* dst, double alpha,
+                    double beta) {
+        for (int f = warp; f < nfr; f += ST / 32) {
+            int fi = (int)((sqrt(8.0 * f + 1.0) - 1.0) * 0.5);
+            while ((fi + 1) * (fi + 2) / 2 <= f) ++fi;
+            while (fi * (fi + 1) / 2 > f) --fi;
+            const int fj = f - fi * (fi + 1) / 2;
+            double d0 = 0.0, d1 = 0.0;
+            for (int k = 0; k < np; k += 4) {
+                const double av = a[(fi * 8 + (lane >> 2)) * P + k + (lane & 3)];
+                const double bv = b[(fj * 8 + (lane >> 2)) * P + k + (lane & 3)];
+                dmma(d0, d1, av, bv);
+            }
+            const int r = fi * 8 + (lane >> 2);
+            const int c = fj * 8 + (lane & 3) * 2;
+            double v0 = alpha * d0, v1 = alpha * d1;
+            if (e) {
+                v0 += beta * e[r * P + c];
+                v1 += beta * e[r * P + c + 1];
+            }
+            if (fi == fj) {
+                // keep lower entries (c <= r) and mirror them
+                if (c <= r) {
+                    dst[r * P + c] = v0;
+                    dst[c * P + r] = v0;
+                }
+                if (c + 1 <= r) {
+                    dst[r * P + c + 1] = v1;
+                    dst[(c + 1) * P + r] = v1;
+                }
+            } else {
+                dst[r * P + c] = v0;
+                dst[c * P + r] = v0;
+                dst[r * P + c + 1] = v1;
+                dst[(c + 1) * P + r] = v1;
+            }
+        }
+        __syncthreads();
+    };
+
+    // first quintic step from X0 = s A (scale folded into the coefficients)
+    const double* Xc = A;
+    double xs = s;  // pending scale of Xc
+    double* bufs[4] = {X, Y, Z, T};
+    auto free3 = [&](double*& f0, double*& f1, double*& f2) {
+        double* fr[4];
+        int k = 0;
+        for (int q = 0; q < 4; ++q)
+            if (bufs[q] != Xc) fr[k++] = bufs[q];
+        f0 = fr[0];
+        f1 = fr[1];
+        f2 = fr[2];
+    };
+    for (int it = 0; it < sch.k1; ++it) {
+        double *Yb, *Zb, *Xn;
+        free3(Yb, Zb, Xn);
+        gemm(Xc, Xc, nullptr, Yb, xs * xs, 0.0);
+        gemm(Yb, Yb, Yb, Zb, sch.qc, sch.qb);
+        gemm(Xc, Zb, Xc, Xn, xs, sch.qa * xs);
+        xs = 1.0;
+        Xc = Xn;
+    }
+    for (int it = 0; it < sch.k2; ++it) {
+        double *Yb, *Xn, *unused;
+        free3(Yb, Xn, unused);
+        gemm(Xc, Xc, nullptr, Yb, xs * xs, 0.0);
+        gemm(Xc, Yb, Xc, Xn, -0.5 * xs, 1.5 * xs);
+        xs = 1.0;
+        Xc = Xn;
+    }
+    // P = 0.5 A -/+ 0.5 A X
+    double *out, *u1, *u2;
+    free3(out, u1, u2);
+    const double sg = (mat & 1) == 0 ? -0.5 : 0.5;  // S -> NSD, T -> PSD
+    gemm(A, Xc, A, out, sg * xs, 0.5);
+    double* C = Cg + (long long)(mat >> 1) * c_stride_b + (long long)(mat & 1) * c_stride_w;
+    for (int idx = tid; idx < n * n; idx += ST) {
+        const int r = idx / n, c = idx % n;
+        C[(long long)c * n + r] = out[r * P + c];
+    }
+}
+
+void launch_cone_small(const double* A, long long mstride, int ld, int n, double* C,
+                       long long c_stride_b, long long c_stride_w, const int* ictl, int nmat,
+                       const SignSchedule& sch, cudaStream_t st) {
+    const int np = (n + 7) & ~7;
+    const int smem = 5 * np * (np + 4) * sizeof(double);
+    cone_small_kernel<<<nmat, ST, smem, st>>>(A, mstride, ld, n, C, c_stride_b, c_stride_w, ictl, sch);
+    TPB_CHECK_LAUNCH();
+}
+
+void init_attrs_cone() {
+    set_max_dyn_smem(sym_gemm_kernel);
+    set_max_dyn_smem(cone_small_kernel);
+}
+
+}  // namespace tpb

@@ -1,0 +1,40 @@
+#pragma once
+
+#include "common.cuh"
+
+namespace tpb {
+
+// SLEM (second-largest eigenvalue modulus) of W = I - L(g) for the weights g
+// of the listed edges; spectral_report semantics (proj/src/topology.cpp:125-144).
+struct SlemArgs {
+    int n;
+    long long m;
+    const double* g;       // packed weights, per solve at g + b*stride
+    long long stride;
+    const int* list;       // ascending nonzero edge indices, per solve at list + b*list_cap
+    const int* count;
+    int list_cap;
+    // scratch (global, per solve)
+    int* e_i;              // list_cap
+    int* e_j;
+    double* e_w;
+    int* col_idx;          // list_cap
+    double* basis;         // kmax x n (full reorthogonalisation), or null
+    int kmax;
+    double tol;
+    // outputs: out[b*8 + {0:acf, 1:lambda2, 2:lambda_n, 3:connected, 4:steps, 5:converged}]
+    double* out;
+    // trace mode: acf -> tr_acf[b*max_iter + ictl[b*8]] ; skipped when done
+    double* tr_acf;
+    const int* ictl;
+    int max_iter;
+};
+
+void launch_slem(const SlemArgs& a, int B, cudaStream_t st);
+
+// Dense symmetric W (row-major n x n), full spectrum Lanczos with full
+// reorthogonalisation; out[0..4) = {acf, lambda2, lambda_n, connected}.
+// deflate=1 when W 1 = 1 (gossip matrix): the Krylov space is built on 1-perp.
+void launch_slem_dense(const double* w, int n, double* basis, double* out, int deflate, cudaStream_t st);
+
+}  // namespace tpb

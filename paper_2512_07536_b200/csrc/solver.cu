@@ -1,0 +1,633 @@
+// Device-resident batched ADMM driver. Mirrors the control flow of
+// topoopt::solve / topoopt::solve_het (proj/src/admm.cpp:356-428,
+// proj/src/admm_het.cpp:231-369): feasible start, Y-X-D iterations with the
+// residual stop test and best-iterate bookkeeping, then extraction and the
+// final spectral report. Each iteration is one CUDA-graph segment with three
+// streams: cone projections (s0) || top-r selection (s1) -> trace SLEM (s2).
+#include "solver.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+
+namespace tpb {
+
+void validate(const Config& c) {
+    // proj/src/admm.cpp:186-195
+    if (!(c.rho > 0.0)) throw Error(kInvalidArgument, "SolverConfig: rho must be positive");
+    if (!(c.epsilon > 0.0)) throw Error(kInvalidArgument, "SolverConfig: epsilon must be positive");
+    if (c.max_iter < 1) throw Error(kInvalidArgument, "SolverConfig: max_iter must be >= 1");
+    if (!(c.alpha > 0.0)) throw Error(kInvalidArgument, "SolverConfig: alpha must be positive");
+    if (c.weight_floor < 0.0) throw Error(kInvalidArgument, "SolverConfig: weight_floor must be >= 0");
+    if (!(c.linear_tol > 0.0)) throw Error(kInvalidArgument, "SolverConfig: linear_tol must be positive");
+    if (c.trace_stride < 1) throw Error(kInvalidArgument, "SolverConfig: trace_stride must be >= 1");
+}
+
+namespace {
+
+template <typename T>
+T* dalloc(std::vector<void*>& pool, size_t count) {
+    void* p = nullptr;
+    if (count == 0) count = 1;
+    TPB_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    pool.push_back(p);
+    return static_cast<T*>(p);
+}
+
+}  // namespace
+
+Solver::Solver(int n, int B, bool het, const std::vector<int>& r, const std::vector<int>& degrees,
+               const Config& cfg)
+    : B_(B), het_(het), cfg_(cfg) {
+    validate(cfg);
+    if (n < 2) throw Error(kInvalidArgument, "assemble: need at least 2 nodes");
+    if (B < 1) throw Error(kInvalidArgument, "batch must be >= 1");
+    lo_ = het ? het_layout(n, n) : hom_layout(n);
+    const int m = lo_.m;
+    r_host_.resize(B);
+    if (het) {
+        if ((int)degrees.size() != B * n)
+            throw Error(kInvalidArgument, "node_level_constraints: degree list size mismatch");
+        for (int b = 0; b < B; ++b) {
+            long long sum = 0;
+            for (int i = 0; i < n; ++i) {
+                const int dgi = degrees[(size_t)b * n + i];
+                if (dgi < 0 || dgi > n - 1)
+                    throw Error(kInvalidArgument, "node_level_constraints: degree of node " +
+                                                      std::to_string(i) + " outside [0, n-1]");
+                sum += dgi;
+            }
+            if (sum % 2) throw Error(kInfeasible, "degree sum " + std::to_string(sum) + " is odd");
+            const int total = (int)(sum / 2);
+            if (!r.empty() && r[b] >= 0 && r[b] != total)
+                throw Error(kInvalidArgument, "edge total conflicts with the degree rows");
+            if (total < 1 || total > m)
+                throw Error(kInvalidArgument, "assemble_het: edge total outside [1, |E|]");
+            r_host_[b] = total;
+        }
+    } else {
+        if ((int)r.size() != B) throw Error(kInvalidArgument, "one edge budget per solve expected");
+        for (int b = 0; b < B; ++b) {
+            if (r[b] < 1 || r[b] > m) throw Error(kInvalidArgument, "assemble: r outside [1, n(n-1)/2]");
+            r_host_[b] = r[b];
+        }
+    }
+    c_ = make_xconst(n, cfg.alpha, cfg.rho);
+    small_ = n <= 64;
+    ld_ = small_ ? ((n + 7) & ~7) : ((n + 63) / 64) * 64;
+    list_cap_ = het ? m : *std::max_element(r_host_.begin(), r_host_.end());
+    int chunk = cfg.chunk > 0 ? cfg.chunk : (n <= 64 ? 32 : (n <= 256 ? 16 : 8));
+    chunk = ((chunk + cfg.trace_stride - 1) / cfg.trace_stride) * cfg.trace_stride;
+    chunk_ = chunk;
+    init_attrs();
+    TPB_CUDA(cudaStreamCreateWithFlags(&s0_, cudaStreamNonBlocking));
+    TPB_CUDA(cudaStreamCreateWithFlags(&s1_, cudaStreamNonBlocking));
+    TPB_CUDA(cudaStreamCreateWithFlags(&s2_, cudaStreamNonBlocking));
+    TPB_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+    TPB_CUDA(cudaEventCreateWithFlags(&ev_sel_, cudaEventDisableTiming));
+    TPB_CUDA(cudaEventCreateWithFlags(&ev_slem_, cudaEventDisableTiming));
+    alloc();
+    if (het) {
+        std::vector<double> dg(degrees.begin(), degrees.end());
+        TPB_CUDA(cudaMemcpy(d_deg_, dg.data(), dg.size() * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    TPB_CUDA(cudaMemcpy(d_r_, r_host_.data(), B * sizeof(int), cudaMemcpyHostToDevice));
+    warm_.assign(B, {});
+    res_.assign(B, {});
+}
+
+Solver::~Solver() {
+    if (g_chunk_) cudaGraphExecDestroy(g_chunk_);
+    if (g_one_) cudaGraphExecDestroy(g_one_);
+    for (void* p : allocs_) cudaFree(p);
+    if (h_ctl_) cudaFreeHost(h_ctl_);
+    if (ev_fork_) cudaEventDestroy(ev_fork_);
+    if (ev_sel_) cudaEventDestroy(ev_sel_);
+    if (ev_slem_) cudaEventDestroy(ev_slem_);
+    if (s0_) cudaStreamDestroy(s0_);
+    if (s1_) cudaStreamDestroy(s1_);
+    if (s2_) cudaStreamDestroy(s2_);
+}
+
+void Solver::alloc() {
+    const int n = lo_.n;
+    const long long m = lo_.m, nx = lo_.nx;
+    const int B = B_;
+    d_.lo = lo_;
+    d_.B = B;
+    d_.het = het_ ? 1 : 0;
+    d_.nb = (n + 31) / 32;
+    d_.ntile = d_.nb * (d_.nb + 1) / 2;
+    d_.ld = ld_;
+    d_.nx = nx;
+    d_.max_iter = cfg_.max_iter;
+    d_.epsilon = cfg_.epsilon;
+    d_.track_best = 1;
+    d_.upd_duals = 1;
+    const long long ld2 = (long long)ld_ * ld_;
+    d_.X = dalloc<double>(allocs_, B * nx);
+    d_.Y = dalloc<double>(allocs_, B * nx);
+    d_.D = dalloc<double>(allocs_, B * nx);
+    d_.bestY = dalloc<double>(allocs_, B * nx);
+    d_.bestScore = dalloc<double>(allocs_, het_ ? B * m : 1);
+    d_.A = dalloc<double>(allocs_, (size_t)B * 2 * ld2);
+    TPB_CUDA(cudaMemset(d_.A, 0, (size_t)B * 2 * ld2 * sizeof(double)));
+    d_.frob_part = dalloc<double>(allocs_, (size_t)B * 2 * d_.ntile);
+    d_.inv_scale = dalloc<double>(allocs_, (size_t)B * 2);
+    d_.h = dalloc<double>(allocs_, B * m);
+    d_.PU = dalloc<double>(allocs_, (size_t)B * d_.nb * n);
+    d_.PZ = dalloc<double>(allocs_, (size_t)B * d_.nb * n);
+    d_.PG = dalloc<double>(allocs_, (size_t)B * d_.nb * n);
+    d_.node = dalloc<double>(allocs_, (size_t)B * 4 * n);
+    d_.res_part = dalloc<double>(allocs_, (size_t)B * d_.ntile);
+    d_.scal = dalloc<double>(allocs_, (size_t)B * 8);
+    d_.ictl = dalloc<int>(allocs_, (size_t)B * 8);
+    d_r_ = dalloc<int>(allocs_, B);
+    d_.r = d_r_;
+    d_deg_ = dalloc<double>(allocs_, het_ ? (size_t)B * n : 1);
+    d_.deg = d_deg_;
+    d_.tr_res = dalloc<double>(allocs_, (size_t)B * cfg_.max_iter);
+    d_.tr_lam = dalloc<double>(allocs_, (size_t)B * cfg_.max_iter);
+    d_.tr_acf = dalloc<double>(allocs_, (size_t)B * cfg_.max_iter);
+    if (!small_) {
+        w0_ = dalloc<double>(allocs_, (size_t)B * 2 * ld2);
+        w1_ = dalloc<double>(allocs_, (size_t)B * 2 * ld2);
+        w2_ = dalloc<double>(allocs_, (size_t)B * 2 * ld2);
+        TPB_CUDA(cudaMemset(w0_, 0, (size_t)B * 2 * ld2 * sizeof(double)));
+        TPB_CUDA(cudaMemset(w1_, 0, (size_t)B * 2 * ld2 * sizeof(double)));
+        TPB_CUDA(cudaMemset(w2_, 0, (size_t)B * 2 * ld2 * sizeof(double)));
+    }
+    list_ = dalloc<int>(allocs_, (size_t)B * list_cap_);
+    list_count_ = dalloc<int>(allocs_, B);
+    e_i_ = dalloc<int>(allocs_, (size_t)B * list_cap_);
+    e_j_ = dalloc<int>(allocs_, (size_t)B * list_cap_);
+    col_idx_ = dalloc<int>(allocs_, (size_t)B * list_cap_);
+    e_w_ = dalloc<double>(allocs_, (size_t)B * list_cap_);
+    if (n <= 256) {
+        trace_kmax_ = n - 1;
+        basis_ = dalloc<double>(allocs_, (size_t)B * std::max(1, n - 1) * n);
+    } else {
+        trace_kmax_ = std::min(2048, 2 * n);
+        basis_ = nullptr;
+    }
+    basis_final_ = dalloc<double>(allocs_, (size_t)B * std::max(1, n - 1) * n);
+    slem_out_ = dalloc<double>(allocs_, (size_t)B * 8);
+    tmp_m_ = dalloc<double>(allocs_, (size_t)B * m);
+    tmp_m2_ = dalloc<double>(allocs_, (size_t)B * m);
+    worst_ = dalloc<double>(allocs_, B);
+    fs_scal_ = dalloc<double>(allocs_, (size_t)B * 2);
+    TPB_CUDA(cudaMallocHost(&h_ctl_, (size_t)B * 8 * sizeof(int)));
+    TPB_CUDA(cudaMemset(d_.ictl, 0, (size_t)B * 8 * sizeof(int)));
+}
+
+void Solver::set_warm(int b, const std::vector<int>& packed) {
+    if (b < 0 || b >= B_) throw Error(kInvalidArgument, "set_warm: solve index out of range");
+    if ((int)packed.size() > r_host_[b])
+        throw Error(kInvalidArgument, het_ ? "solve_het: warm start has more than r edges"
+                                           : "solve: warm start has more than r edges");
+    warm_[b] = packed;
+}
+
+void Solver::start() {
+    const int B = B_;
+    const long long nx = lo_.nx;
+    TPB_CUDA(cudaMemsetAsync(d_.X, 0, B * nx * sizeof(double), s0_));
+    TPB_CUDA(cudaMemsetAsync(d_.D, 0, B * nx * sizeof(double), s0_));
+    TPB_CUDA(cudaMemsetAsync(d_.ictl, 0, (size_t)B * 8 * sizeof(int), s0_));
+    if (het_) TPB_CUDA(cudaMemsetAsync(d_.bestScore, 0, (size_t)B * lo_.m * sizeof(double), s0_));
+    {
+        std::vector<double> sc((size_t)B * 8, 0.0);
+        for (int b = 0; b < B; ++b) sc[(size_t)b * 8 + kBestRes] = std::numeric_limits<double>::infinity();
+        TPB_CUDA(cudaMemcpyAsync(d_.scal, sc.data(), sc.size() * sizeof(double), cudaMemcpyHostToDevice, s0_));
+        std::vector<double> nanv((size_t)B * cfg_.max_iter, std::numeric_limits<double>::quiet_NaN());
+        TPB_CUDA(cudaMemcpyAsync(d_.tr_acf, nanv.data(), nanv.size() * sizeof(double), cudaMemcpyHostToDevice, s0_));
+        // warm lists
+        std::vector<int> lists((size_t)B * list_cap_, 0), counts(B, 0);
+        for (int b = 0; b < B; ++b) {
+            counts[b] = (int)warm_[b].size();
+            std::copy(warm_[b].begin(), warm_[b].end(), lists.begin() + (size_t)b * list_cap_);
+        }
+        TPB_CUDA(cudaMemcpyAsync(list_, lists.data(), lists.size() * sizeof(int), cudaMemcpyHostToDevice, s0_));
+        TPB_CUDA(cudaMemcpyAsync(list_count_, counts.data(), B * sizeof(int), cudaMemcpyHostToDevice, s0_));
+        launch_feasible_a(d_, list_, list_count_, list_cap_, fs_scal_, s0_);
+        final_slem(d_.X, list_, list_count_, slem_out_);  // SLEM of the warm start, stride nx
+        launch_feasible_b(d_, c_, slem_out_, fs_scal_, s0_);
+        TPB_CUDA(cudaStreamSynchronize(s0_));  // host vectors above go out of scope
+    }
+    TPB_CUDA(cudaMemcpyAsync(d_.Y, d_.X, B * nx * sizeof(double), cudaMemcpyDeviceToDevice, s0_));
+    TPB_CUDA(cudaMemcpyAsync(d_.bestY, d_.X, B * nx * sizeof(double), cudaMemcpyDeviceToDevice, s0_));
+    TPB_CUDA(cudaStreamSynchronize(s0_));
+    if (!g_chunk_) build_graphs();
+    it_enqueued_ = 0;
+}
+
+void Solver::final_slem(const double* packed, const int* list, const int* count, double* out) {
+    SlemArgs a{};
+    a.n = lo_.n;
+    a.m = lo_.m;
+    a.g = packed;
+    a.stride = packed == d_.X ? lo_.nx : lo_.m;
+    a.list = list;
+    a.count = count;
+    a.list_cap = list_cap_;
+    a.e_i = e_i_;
+    a.e_j = e_j_;
+    a.e_w = e_w_;
+    a.col_idx = col_idx_;
+    a.basis = basis_final_;
+    a.kmax = std::max(1, lo_.n - 1);
+    a.tol = 1e-14;
+    a.out = out;
+    a.tr_acf = nullptr;
+    a.ictl = nullptr;
+    launch_slem(a, B_, s0_);
+}
+
+void Solver::enqueue_select(cudaStream_t st) {
+    SelectArgs a{};
+    a.stride = lo_.nx;
+    a.m = lo_.m;
+    a.r = d_r_;
+    a.list = list_;
+    a.list_count = list_count_;
+    a.list_cap = list_cap_;
+    a.done = d_.ictl;
+    if (het_) {
+        a.base = d_.Y + lo_.off_z;
+        a.gbase = d_.Y;
+        a.binary = 1;
+    } else {
+        a.base = d_.Y;
+        a.gbase = nullptr;
+        a.binary = 0;
+    }
+    launch_topr(a, B_, st);
+}
+
+void Solver::enqueue_slem_trace(cudaStream_t st) {
+    SlemArgs a{};
+    a.n = lo_.n;
+    a.m = lo_.m;
+    a.g = d_.Y;
+    a.stride = lo_.nx;
+    a.list = list_;
+    a.count = list_count_;
+    a.list_cap = list_cap_;
+    a.e_i = e_i_;
+    a.e_j = e_j_;
+    a.e_w = e_w_;
+    a.col_idx = col_idx_;
+    a.basis = basis_;
+    a.kmax = trace_kmax_;
+    a.tol = cfg_.slem_tol;
+    a.out = nullptr;
+    a.tr_acf = d_.tr_acf;
+    a.ictl = d_.ictl;
+    a.max_iter = cfg_.max_iter;
+    launch_slem(a, B_, st);
+}
+
+void Solver::enqueue_projection() {
+    const long long cb = lo_.nx, cw = lo_.off_t - lo_.off_s;
+    if (small_) {
+        launch_cone_small(d_.A, (long long)ld_ * ld_, ld_, lo_.n, d_.Y + lo_.off_s, cb, cw, d_.ictl,
+                          2 * B_, sch_, s0_);
+    } else {
+        enqueue_cone_tiled(d_.A, w0_, w1_, w2_, ld_, lo_.n, d_.inv_scale, d_.Y + lo_.off_s, cb, cw,
+                           d_.ictl, 2 * B_, sch_, s0_);
+    }
+}
+
+void Solver::enqueue_iteration(bool with_slem) {
+    launch_prep(d_, c_, s0_);
+    if (!small_) launch_frob_finalize(d_, s0_);
+    TPB_CUDA(cudaEventRecord(ev_fork_, s0_));
+    TPB_CUDA(cudaStreamWaitEvent(s1_, ev_fork_, 0));
+    enqueue_select(s1_);
+    TPB_CUDA(cudaEventRecord(ev_sel_, s1_));
+    if (with_slem) {
+        TPB_CUDA(cudaStreamWaitEvent(s2_, ev_sel_, 0));
+        enqueue_slem_trace(s2_);
+        TPB_CUDA(cudaEventRecord(ev_slem_, s2_));
+    }
+    enqueue_projection();
+    TPB_CUDA(cudaStreamWaitEvent(s0_, ev_sel_, 0));
+    launch_xstep_a(d_, c_, s0_);
+    launch_xstep_node(d_, c_, s0_);
+    launch_xstep_b(d_, c_, s0_);
+    if (with_slem) TPB_CUDA(cudaStreamWaitEvent(s0_, ev_slem_, 0));
+    launch_xstep_diag(d_, c_, s0_);
+    launch_best_copy(d_, c_, s0_);
+}
+
+void Solver::build_graphs() {
+    auto capture = [&](int iters, bool stride_aligned) {
+        cudaGraph_t g;
+        TPB_CUDA(cudaStreamBeginCapture(s0_, cudaStreamCaptureModeThreadLocal));
+        for (int j = 0; j < iters; ++j) {
+            const bool slem = stride_aligned ? (j % cfg_.trace_stride == 0) : (cfg_.trace_stride == 1);
+            enqueue_iteration(slem);
+        }
+        TPB_CUDA(cudaStreamEndCapture(s0_, &g));
+        cudaGraphExec_t ex;
+        TPB_CUDA(cudaGraphInstantiate(&ex, g, 0));
+        TPB_CUDA(cudaGraphDestroy(g));
+        return ex;
+    };
+    g_chunk_ = capture(chunk_, true);
+    g_one_ = capture(1, false);
+}
+
+void Solver::iterate_async(int k) {
+    while (k >= chunk_) {
+        TPB_CUDA(cudaGraphLaunch(g_chunk_, s0_));
+        k -= chunk_;
+        it_enqueued_ += chunk_;
+    }
+    while (k-- > 0) {
+        TPB_CUDA(cudaGraphLaunch(g_one_, s0_));
+        ++it_enqueued_;
+    }
+}
+
+bool Solver::all_done() {
+    TPB_CUDA(cudaMemcpyAsync(h_ctl_, d_.ictl, (size_t)B_ * 8 * sizeof(int), cudaMemcpyDeviceToHost, s0_));
+    TPB_CUDA(cudaStreamSynchronize(s0_));
+    for (int b = 0; b < B_; ++b)
+        if (!h_ctl_[b * 8 + kDone]) return false;
+    return true;
+}
+
+void Solver::run_to_completion() {
+    while (!all_done()) iterate_async(chunk_);
+}
+
+void Solver::finish() {
+    TPB_CUDA(cudaStreamSynchronize(s0_));
+    all_done();
+    std::vector<double> scal((size_t)B_ * 8);
+    TPB_CUDA(cudaMemcpy(scal.data(), d_.scal, scal.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    for (int b = 0; b < B_; ++b) {
+        SolveResult& R = res_[b];
+        R = SolveResult{};
+        R.iterations = h_ctl_[b * 8 + kIter];
+        R.converged = h_ctl_[b * 8 + 4] != 0;
+        R.best_iter = h_ctl_[b * 8 + kBestIter];
+        R.residual = R.converged ? scal[(size_t)b * 8 + kRes] : scal[(size_t)b * 8 + kBestRes];
+        if (!R.converged)
+            R.note = "stopped at max_iter; best iterate from iteration " + std::to_string(R.best_iter);
+        const int it = R.iterations;
+        R.tr_res.resize(it);
+        R.tr_lam.resize(it);
+        R.tr_acf.resize(it);
+        const size_t off = (size_t)b * cfg_.max_iter;
+        TPB_CUDA(cudaMemcpy(R.tr_res.data(), d_.tr_res + off, it * sizeof(double), cudaMemcpyDeviceToHost));
+        TPB_CUDA(cudaMemcpy(R.tr_lam.data(), d_.tr_lam + off, it * sizeof(double), cudaMemcpyDeviceToHost));
+        TPB_CUDA(cudaMemcpy(R.tr_acf.data(), d_.tr_acf + off, it * sizeof(double), cudaMemcpyDeviceToHost));
+        const double* pick = (R.converged ? d_.Y : d_.bestY) + (size_t)b * lo_.nx;
+        TPB_CUDA(cudaMemcpy(&R.lambda_tilde, pick + lo_.lambda_ix, sizeof(double), cudaMemcpyDeviceToHost));
+    }
+    if (het_) epilogue_het();
+    else epilogue_hom();
+}
+
+void Solver::epilogue_hom() {
+    const long long m = lo_.m, nx = lo_.nx;
+    for (int b = 0; b < B_; ++b) {
+        const double* pick = (res_[b].converged ? d_.Y : d_.bestY) + (size_t)b * nx;
+        TPB_CUDA(cudaMemcpyAsync(tmp_m_ + (size_t)b * m, pick, m * sizeof(double), cudaMemcpyDeviceToDevice, s0_));
+    }
+    launch_floor_mask(tmp_m_, m, m, cfg_.weight_floor, tmp_m2_, B_, s0_);
+    SelectArgs a{};
+    a.base = tmp_m2_;
+    a.stride = m;
+    a.m = m;
+    a.r = d_r_;
+    a.binary = 0;
+    a.list = list_;
+    a.list_count = list_count_;
+    a.list_cap = list_cap_;
+    a.done = nullptr;
+    launch_topr(a, B_, s0_);
+    TPB_CUDA(cudaMemsetAsync(tmp_m_, 0, (size_t)B_ * m * sizeof(double), s0_));
+    launch_extract(lo_.n, m, tmp_m2_, m, list_, list_count_, list_cap_, e_i_, e_j_, e_w_, tmp_m_, worst_,
+                   col_idx_, B_, s0_);
+    std::vector<int> counts(B_);
+    TPB_CUDA(cudaMemcpyAsync(counts.data(), list_count_, B_ * sizeof(int), cudaMemcpyDeviceToHost, s0_));
+    TPB_CUDA(cudaStreamSynchronize(s0_));
+    std::vector<int> ei((size_t)B_ * list_cap_), ej((size_t)B_ * list_cap_);
+    std::vector<double> ew((size_t)B_ * list_cap_);
+    TPB_CUDA(cudaMemcpy(ei.data(), e_i_, ei.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    TPB_CUDA(cudaMemcpy(ej.data(), e_j_, ej.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    TPB_CUDA(cudaMemcpy(ew.data(), e_w_, ew.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    final_slem(tmp_m_, list_, list_count_, slem_out_);
+    std::vector<double> so((size_t)B_ * 8);
+    TPB_CUDA(cudaMemcpyAsync(so.data(), slem_out_, so.size() * sizeof(double), cudaMemcpyDeviceToHost, s0_));
+    TPB_CUDA(cudaStreamSynchronize(s0_));
+    for (int b = 0; b < B_; ++b) {
+        SolveResult& R = res_[b];
+        const int k = std::min(counts[b], list_cap_);
+        R.ei.assign(ei.begin() + (size_t)b * list_cap_, ei.begin() + (size_t)b * list_cap_ + k);
+        R.ej.assign(ej.begin() + (size_t)b * list_cap_, ej.begin() + (size_t)b * list_cap_ + k);
+        R.w.assign(ew.begin() + (size_t)b * list_cap_, ew.begin() + (size_t)b * list_cap_ + k);
+        R.acf = so[(size_t)b * 8 + 0];
+        R.lambda2 = so[(size_t)b * 8 + 1];
+        R.lambda_n = so[(size_t)b * 8 + 2];
+        R.connected = so[(size_t)b * 8 + 3] != 0.0;
+    }
+}
+
+namespace {
+
+// proj/src/admm_het.cpp:179-227 (sequential greedy; runs once per solve).
+bool repair_selection(int n, const std::vector<int>& target, std::vector<char>& sel,
+                      const std::vector<double>& w, const std::vector<double>& score, bool* changed) {
+    const long long m = (long long)n * (n - 1) / 2;
+    std::vector<int> pi(m), pj(m);
+    {
+        long long l = 0;
+        for (int i = 0; i < n; ++i)
+            for (int j = i + 1; j < n; ++j, ++l) {
+                pi[l] = i;
+                pj[l] = j;
+            }
+    }
+    std::vector<int> deg(n, 0);
+    for (long long l = 0; l < m; ++l)
+        if (sel[l]) {
+            ++deg[pi[l]];
+            ++deg[pj[l]];
+        }
+    *changed = false;
+    for (;;) {
+        int node = -1;
+        for (int i = 0; i < n; ++i)
+            if (deg[i] > target[i] && (node < 0 || deg[i] - target[i] > deg[node] - target[node])) node = i;
+        if (node < 0) break;
+        long long drop = -1;
+        for (long long l = 0; l < m; ++l) {
+            if (!sel[l] || (pi[l] != node && pj[l] != node)) continue;
+            if (drop < 0 || w[l] < w[drop]) drop = l;
+        }
+        if (drop < 0) return false;
+        sel[drop] = 0;
+        --deg[pi[drop]];
+        --deg[pj[drop]];
+        *changed = true;
+    }
+    for (;;) {
+        bool deficit = false;
+        for (int i = 0; i < n; ++i) deficit = deficit || deg[i] < target[i];
+        if (!deficit) break;
+        long long add = -1;
+        for (long long l = 0; l < m; ++l) {
+            if (sel[l]) continue;
+            if (deg[pi[l]] >= target[pi[l]] || deg[pj[l]] >= target[pj[l]]) continue;
+            if (add < 0 || score[l] > score[add]) add = l;
+        }
+        if (add < 0) return false;
+        sel[add] = 1;
+        ++deg[pi[add]];
+        ++deg[pj[add]];
+        *changed = true;
+    }
+    return true;
+}
+
+}  // namespace
+
+void Solver::epilogue_het() {
+    const int n = lo_.n;
+    const long long m = lo_.m, nx = lo_.nx;
+    std::vector<double> degd((size_t)B_ * n);
+    TPB_CUDA(cudaMemcpy(degd.data(), d_deg_, degd.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    std::vector<int> lists((size_t)B_ * list_cap_, 0), counts(B_, 0);
+    std::vector<double> packed((size_t)B_ * m, 0.0);
+    for (int b = 0; b < B_; ++b) {
+        SolveResult& R = res_[b];
+        const double* pick = (R.converged ? d_.Y : d_.bestY) + (size_t)b * nx;
+        std::vector<double> pg(m), pz(m), score(m);
+        TPB_CUDA(cudaMemcpy(pg.data(), pick, m * sizeof(double), cudaMemcpyDeviceToHost));
+        TPB_CUDA(cudaMemcpy(pz.data(), pick + lo_.off_z, m * sizeof(double), cudaMemcpyDeviceToHost));
+        if (R.converged) {
+            std::vector<double> xz(m), dz(m);
+            TPB_CUDA(cudaMemcpy(xz.data(), d_.X + (size_t)b * nx + lo_.off_z, m * sizeof(double), cudaMemcpyDeviceToHost));
+            TPB_CUDA(cudaMemcpy(dz.data(), d_.D + (size_t)b * nx + lo_.off_z, m * sizeof(double), cudaMemcpyDeviceToHost));
+            for (long long l = 0; l < m; ++l) score[l] = xz[l] + dz[l] / cfg_.rho;
+        } else {
+            TPB_CUDA(cudaMemcpy(score.data(), d_.bestScore + (size_t)b * m, m * sizeof(double), cudaMemcpyDeviceToHost));
+        }
+        // proj/src/admm_het.cpp:315-358
+        std::vector<char> sel(m);
+        std::vector<double> w(m);
+        for (long long l = 0; l < m; ++l) {
+            sel[l] = pz[l] > 0.5 ? 1 : 0;
+            w[l] = std::max(0.0, pg[l]);
+        }
+        std::vector<int> target(n);
+        for (int i = 0; i < n; ++i) target[i] = (int)degd[(size_t)b * n + i];
+        bool changed = false;
+        if (!repair_selection(n, target, sel, w, score, &changed)) {
+            if (!R.note.empty()) R.note += "; ";
+            R.note += "degree repair incomplete";
+        }
+        if (changed) {
+            R.repaired = true;
+            if (R.note.find("degree repair incomplete") == std::string::npos) {
+                if (!R.note.empty()) R.note += "; ";
+                R.note += "degree rows restored by edge swap";
+            }
+        }
+        int count = 0;
+        for (long long l = 0; l < m; ++l) count += sel[l];
+        if (count == 0) throw Error(kDegenerate, "no edge selected");
+        if (count < r_host_[b]) {
+            if (!R.note.empty()) R.note += "; ";
+            R.note += "capacity limits stopped selection at " + std::to_string(count) + " of " +
+                      std::to_string(r_host_[b]) + " edges";
+        }
+        std::vector<double> node_sum(n, 0.0);
+        std::vector<int> pi, pj;
+        std::vector<long long> ls;
+        {
+            long long l = 0;
+            for (int i = 0; i < n; ++i)
+                for (int j = i + 1; j < n; ++j, ++l)
+                    if (sel[l]) {
+                        node_sum[i] += w[l];
+                        node_sum[j] += w[l];
+                        pi.push_back(i);
+                        pj.push_back(j);
+                        ls.push_back(l);
+                    }
+        }
+        const double worst = *std::max_element(node_sum.begin(), node_sum.end());
+        const double scale = worst > 1.0 ? 1.0 / worst : 1.0;
+        R.ei = pi;
+        R.ej = pj;
+        R.w.resize(ls.size());
+        for (size_t k = 0; k < ls.size(); ++k) {
+            R.w[k] = w[ls[k]] * scale;
+            packed[(size_t)b * m + ls[k]] = R.w[k];
+            if ((int)k < list_cap_) lists[(size_t)b * list_cap_ + k] = (int)ls[k];
+        }
+        counts[b] = (int)ls.size();
+    }
+    TPB_CUDA(cudaMemcpy(tmp_m_, packed.data(), packed.size() * sizeof(double), cudaMemcpyHostToDevice));
+    TPB_CUDA(cudaMemcpy(list_, lists.data(), lists.size() * sizeof(int), cudaMemcpyHostToDevice));
+    TPB_CUDA(cudaMemcpy(list_count_, counts.data(), counts.size() * sizeof(int), cudaMemcpyHostToDevice));
+    final_slem(tmp_m_, list_, list_count_, slem_out_);
+    std::vector<double> so((size_t)B_ * 8);
+    TPB_CUDA(cudaMemcpyAsync(so.data(), slem_out_, so.size() * sizeof(double), cudaMemcpyDeviceToHost, s0_));
+    TPB_CUDA(cudaStreamSynchronize(s0_));
+    for (int b = 0; b < B_; ++b) {
+        SolveResult& R = res_[b];
+        R.acf = so[(size_t)b * 8 + 0];
+        R.lambda2 = so[(size_t)b * 8 + 1];
+        R.lambda_n = so[(size_t)b * 8 + 2];
+        R.connected = so[(size_t)b * 8 + 3] != 0.0;
+    }
+}
+
+SolveResult Solver::result(int b) const { return res_.at(b); }
+
+void Solver::upload(const double* X, const double* Y, const double* D) {
+    const size_t bytes = (size_t)B_ * lo_.nx * sizeof(double);
+    if (X) TPB_CUDA(cudaMemcpy(d_.X, X, bytes, cudaMemcpyHostToDevice));
+    if (Y) TPB_CUDA(cudaMemcpy(d_.Y, Y, bytes, cudaMemcpyHostToDevice));
+    if (D) TPB_CUDA(cudaMemcpy(d_.D, D, bytes, cudaMemcpyHostToDevice));
+}
+
+void Solver::download(double* X, double* Y, double* D) {
+    TPB_CUDA(cudaStreamSynchronize(s0_));
+    const size_t bytes = (size_t)B_ * lo_.nx * sizeof(double);
+    if (X) TPB_CUDA(cudaMemcpy(X, d_.X, bytes, cudaMemcpyDeviceToHost));
+    if (Y) TPB_CUDA(cudaMemcpy(Y, d_.Y, bytes, cudaMemcpyDeviceToHost));
+    if (D) TPB_CUDA(cudaMemcpy(D, d_.D, bytes, cudaMemcpyDeviceToHost));
+}
+
+void Solver::project_only() {
+    TPB_CUDA(cudaMemsetAsync(d_.ictl, 0, (size_t)B_ * 8 * sizeof(int), s0_));
+    launch_prep(d_, c_, s0_);
+    if (!small_) launch_frob_finalize(d_, s0_);
+    enqueue_select(s0_);
+    enqueue_projection();
+    TPB_CUDA(cudaStreamSynchronize(s0_));
+}
+
+void Solver::xstep_only(bool update_duals) {
+    TPB_CUDA(cudaMemsetAsync(d_.ictl, 0, (size_t)B_ * 8 * sizeof(int), s0_));
+    Dev d = d_;
+    d.upd_duals = update_duals ? 1 : 0;
+    d.track_best = 0;
+    launch_xstep_a(d, c_, s0_);
+    launch_xstep_node(d, c_, s0_);
+    launch_xstep_b(d, c_, s0_);
+    launch_xstep_diag(d, c_, s0_);
+    TPB_CUDA(cudaStreamSynchronize(s0_));
+    TPB_CUDA(cudaMemsetAsync(d_.ictl, 0, (size_t)B_ * 8 * sizeof(int), s0_));
+    TPB_CUDA(cudaStreamSynchronize(s0_));
+}
+
+}  // namespace tpb

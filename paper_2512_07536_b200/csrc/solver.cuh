@@ -1,0 +1,126 @@
+// Device-resident batched ADMM solver (one or many independent solves of the
+// same n in lockstep). Host orchestration of the kernels; no CPU fallback.
+#pragma once
+
+#include <vector>
+
+#include "admm_kernels.cuh"
+#include "cone_kernels.cuh"
+#include "misc_kernels.cuh"
+#include "select_kernels.cuh"
+#include "slem_kernels.cuh"
+
+namespace tpb {
+
+struct Config {
+    double rho = 1.0;
+    double epsilon = 1e-6;
+    int max_iter = 20000;
+    double alpha = 2.0;
+    double weight_floor = 1e-6;
+    double linear_tol = 1e-10;  // accepted for API parity; the x-step is exact
+    int trace_stride = 1;       // acf_iterate every k-th iteration (reference: 1)
+    double slem_tol = 1e-12;    // Lanczos residual tolerance (relative)
+    int chunk = 0;              // iterations per CUDA graph (0: auto)
+};
+
+void validate(const Config& c);
+
+struct SolveResult {
+    int iterations = 0;
+    bool converged = false;
+    bool connected = false;
+    bool repaired = false;
+    int best_iter = 0;
+    double residual = 0.0;
+    double lambda_tilde = 0.0;
+    double acf = 1.0, lambda2 = 1.0, lambda_n = 0.0;
+    std::vector<int> ei, ej;
+    std::vector<double> w;
+    std::vector<double> tr_res, tr_lam, tr_acf;
+    std::string note;
+};
+
+class Solver {
+   public:
+    // r: per-solve edge budget (hom) ; degrees: B x n targets (het node-level).
+    Solver(int n, int B, bool het, const std::vector<int>& r, const std::vector<int>& degrees,
+           const Config& cfg);
+    ~Solver();
+    Solver(const Solver&) = delete;
+    Solver& operator=(const Solver&) = delete;
+
+    int n() const { return lo_.n; }
+    int batch() const { return B_; }
+    const Layout& layout() const { return lo_; }
+    cudaStream_t stream() const { return s0_; }
+    Dev& dev() { return d_; }
+    const XConst& xconst() const { return c_; }
+
+    // warm topology of solve b: ascending packed edge indices
+    void set_warm(int b, const std::vector<int>& packed);
+    void start();                    // feasible start of every solve
+    void iterate_async(int k);       // enqueue k iterations (graphs)
+    bool all_done();                 // sync + read flags
+    void run_to_completion();        // chunks until every solve stops
+    void finish();                   // extraction + final SLEM (hom) / het epilogue
+    SolveResult result(int b) const;
+
+    // single-step entry points for the substep API
+    void upload(const double* X, const double* Y, const double* D);  // host, each B*nx or null
+    void download(double* X, double* Y, double* D);
+    void project_only();             // Y <- project_Y(X, D)
+    void xstep_only(bool update_duals);  // X <- update_X(Y, D) [, D += rho (X - Y)]
+    const double* node_dev() const { return d_.node; }
+
+   private:
+    void alloc();
+    void enqueue_iteration(bool with_slem);
+    void enqueue_projection();
+    void enqueue_select(cudaStream_t st);
+    void enqueue_slem_trace(cudaStream_t st);
+    void build_graphs();
+    void epilogue_hom();
+    void epilogue_het();
+    void final_slem(const double* packed, const int* list, const int* count, double* out);
+
+    Layout lo_;
+    int B_;
+    bool het_;
+    Config cfg_;
+    XConst c_;
+    SignSchedule sch_;
+    Dev d_{};
+    bool small_;
+    int ld_;
+    int list_cap_;
+    int chunk_;
+    std::vector<int> r_host_;
+    std::vector<std::vector<int>> warm_;
+    // device buffers
+    std::vector<void*> allocs_;
+    int* d_r_ = nullptr;
+    double* d_deg_ = nullptr;
+    double *w0_ = nullptr, *w1_ = nullptr, *w2_ = nullptr;
+    int *list_ = nullptr, *list_count_ = nullptr;
+    int *e_i_ = nullptr, *e_j_ = nullptr, *col_idx_ = nullptr;
+    double* e_w_ = nullptr;
+    double* basis_ = nullptr;        // trace Lanczos (full reorth when n small)
+    int trace_kmax_ = 0;
+    double* basis_final_ = nullptr;  // final report
+    double* slem_out_ = nullptr;     // B x 8
+    double* tmp_m_ = nullptr;        // B x m
+    double* tmp_m2_ = nullptr;       // B x m
+    double* worst_ = nullptr;        // B
+    double* fs_scal_ = nullptr;      // B x 2
+    int* h_ctl_ = nullptr;           // pinned B x 8
+    // streams / graphs
+    cudaStream_t s0_ = nullptr, s1_ = nullptr, s2_ = nullptr;
+    cudaEvent_t ev_fork_ = nullptr, ev_sel_ = nullptr, ev_slem_ = nullptr;
+    cudaGraphExec_t g_chunk_ = nullptr, g_one_ = nullptr;
+    int it_enqueued_ = 0;
+    // results
+    std::vector<SolveResult> res_;
+};
+
+}  // namespace tpb

@@ -1,0 +1,492 @@
+"""Python mirror of the reference C++ API (namespace ``topoopt``) for the ADMM
+hot path, backed by the B200 kernels through the C ABI.
+
+Names, argument meaning and error behaviour follow the reference headers
+(/root/reference/proj/include/topoopt/admm.hpp, admm_het.hpp, bandwidth.hpp,
+topology.hpp, errors.hpp); exceptions mirror proj/include/topoopt/errors.hpp.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import tp_config, tp_result
+
+
+# ---------------------------------------------------------------- errors
+class InfeasibleError(RuntimeError):
+    """proj/include/topoopt/errors.hpp:9-12"""
+
+
+class PivotError(RuntimeError):
+    """proj/include/topoopt/errors.hpp:14-18"""
+
+
+class LinearSolveError(RuntimeError):
+    """proj/include/topoopt/errors.hpp:20-23"""
+
+
+class DegenerateSolutionError(RuntimeError):
+    """proj/include/topoopt/errors.hpp:24-27"""
+
+
+class CudaError(RuntimeError):
+    """No device / CUDA failure (the solver has no CPU fallback)."""
+
+
+_EXC = {
+    _lib.TP_ERR_INVALID_ARGUMENT: ValueError,
+    _lib.TP_ERR_INFEASIBLE: InfeasibleError,
+    _lib.TP_ERR_LINEAR_SOLVE: LinearSolveError,
+    _lib.TP_ERR_DEGENERATE: DegenerateSolutionError,
+    _lib.TP_ERR_PIVOT: PivotError,
+    _lib.TP_ERR_INTERNAL: RuntimeError,
+    _lib.TP_ERR_CUDA: CudaError,
+}
+
+
+def _check(status: int):
+    if status != _lib.TP_OK:
+        msg = _lib.load().tp_last_error_message().decode(errors="replace")
+        raise _EXC.get(status, RuntimeError)(msg)
+
+
+def _dp(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _ip(a):
+    return a.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+def _f64(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def _i32(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+
+
+# ---------------------------------------------------------------- config
+@dataclass
+class SolverConfig:
+    """proj/include/topoopt/admm.hpp:15-25 (+ device options)."""
+    rho: float = 1.0
+    epsilon: float = 1e-6
+    max_iter: int = 20000
+    alpha: float = 2.0
+    weight_floor: float = 1e-6
+    seed: int = 0
+    linear_tol: float = 1e-10
+    trace_stride: int = 1
+    chunk: int = 0
+
+    def to_c(self) -> tp_config:
+        return tp_config(self.rho, self.epsilon, int(self.max_iter), self.alpha,
+                         self.weight_floor, int(self.seed), self.linear_tol,
+                         int(self.trace_stride), int(self.chunk))
+
+    def validate(self):
+        c = self.to_c()
+        _check(_lib.load().tp_config_validate(C.byref(c)))
+
+
+def _config(cfg: SolverConfig | None, kw) -> SolverConfig:
+    cfg = SolverConfig(**kw) if cfg is None else cfg
+    return cfg
+
+
+# ---------------------------------------------------------------- topology
+def enumerate_edges(n: int) -> np.ndarray:
+    """Lexicographic pairs (proj/src/topology.cpp:69-76)."""
+    if n < 2:
+        raise ValueError("enumerate_edges: need at least two nodes")
+    i, j = np.triu_indices(n, 1)
+    return np.stack([i, j], 1).astype(np.int32)
+
+
+def edge_index(n: int, i: int, j: int) -> int:
+    """proj/src/topology.cpp:78-84"""
+    if i == j:
+        raise ValueError("edge_index: self loop")
+    if i > j:
+        i, j = j, i
+    if i < 0 or j >= n:
+        raise ValueError("edge_index: endpoint out of range")
+    return i * n - i * (i + 1) // 2 + (j - i - 1)
+
+
+def gossip_matrix(n: int, edges, weights) -> np.ndarray:
+    """W = I - L (proj/src/topology.cpp:96-123), output formatting of a result."""
+    lap = np.zeros((n, n))
+    for (i, j), w in zip(np.asarray(edges).reshape(-1, 2), np.asarray(weights)):
+        lap[i, i] += w
+        lap[j, j] += w
+        lap[i, j] -= w
+        lap[j, i] -= w
+    if n and np.any(np.diag(lap) > 1.0 + 1e-12):
+        raise ValueError("gossip_matrix: weighted degree exceeds 1")
+    return np.eye(n) - lap
+
+
+def spectral_report(w) -> dict:
+    """proj/src/topology.cpp:125-144, on the GPU (Lanczos)."""
+    w = _f64(w)
+    n = w.shape[0]
+    out = np.zeros(4)
+    _check(_lib.load().tp_spectral_report(n, _dp(w), _dp(out)))
+    return {"acf": out[0], "lambda2": out[1], "lambda_n": out[2], "connected": bool(out[3])}
+
+
+def spectral_edges(n: int, edges, weights) -> dict:
+    """spectral_report(gossip_matrix(topology)) without forming W."""
+    e = _i32(np.asarray(edges).reshape(-1, 2))
+    w = _f64(weights)
+    out = np.zeros(4)
+    _check(_lib.load().tp_spectral_edges(n, _ip(e), _dp(w), len(w), _dp(out)))
+    return {"acf": out[0], "lambda2": out[1], "lambda_n": out[2], "connected": bool(out[3])}
+
+
+def acf(w) -> float:
+    return spectral_report(w)["acf"]
+
+
+def project_psd(a) -> np.ndarray:
+    """proj/src/eig.cpp:176"""
+    a = _f64(a)
+    out = np.zeros_like(a)
+    _check(_lib.load().tp_project_psd(a.shape[0], _dp(a), _dp(out)))
+    return out
+
+
+def project_nsd(a) -> np.ndarray:
+    """proj/src/eig.cpp:174"""
+    a = _f64(a)
+    out = np.zeros_like(a)
+    _check(_lib.load().tp_project_nsd(a.shape[0], _dp(a), _dp(out)))
+    return out
+
+
+# ---------------------------------------------------------------- bandwidth
+def allocate_edge_capacity(bandwidths, r: int, edge_caps=None):
+    """Alg. 1 (proj/src/bandwidth.cpp:28-89) -> (b_unit, edges_per_node)."""
+    b = _f64(bandwidths)
+    n = len(b)
+    e = np.zeros(max(n, 1), np.int32)
+    bu = C.c_double(0.0)
+    caps = None if edge_caps is None or len(edge_caps) == 0 else _i32(edge_caps)
+    if caps is not None and len(caps) != n:
+        raise ValueError("allocate_edge_capacity: edge_caps size mismatch")
+    _check(_lib.load().tp_allocate(_dp(b), _ip(caps) if caps is not None else None, n, int(r),
+                                   C.byref(bu), _ip(e)))
+    return bu.value, e[:n].copy()
+
+
+def allocate_batch(bandwidths, r, edge_caps=None):
+    """P independent allocations on the GPU (one warp each). bandwidths: (P, n)."""
+    b = _f64(bandwidths)
+    P, n = b.shape
+    r = _i32(r)
+    caps = None if edge_caps is None else _i32(edge_caps)
+    bu = np.zeros(P)
+    e = np.zeros((P, n), np.int32)
+    st = np.zeros(P, np.int32)
+    _check(_lib.load().tp_allocate_batch(_dp(b), _ip(caps) if caps is not None else None, n,
+                                         _ip(r), P, _dp(bu), _ip(e), _ip(st)))
+    return bu, e, st
+
+
+def node_level_constraints(n: int, degrees) -> np.ndarray:
+    """proj/src/bandwidth.cpp:116-146: the node-level system is fully
+    described by its degree targets (one row per node over incident pairs)."""
+    d = np.asarray(degrees, np.int64)
+    if n < 2:
+        raise ValueError("node_level_constraints: need at least 2 nodes")
+    if len(d) != n:
+        raise ValueError("node_level_constraints: degree list size mismatch")
+    if np.any(d < 0) or np.any(d > n - 1):
+        raise ValueError("node_level_constraints: degree outside [0, n-1]")
+    if d.sum() % 2:
+        raise InfeasibleError(f"degree sum {int(d.sum())} is odd")
+    return d.astype(np.int32)
+
+
+# ---------------------------------------------------------------- warm starts
+def anneal_degree_topology(degrees, t0=1.0, cooling=0.995, steps=200, moves_per_temp=0, seed=0):
+    """proj/src/anneal.cpp:245-273 (host) -> edges (k, 2)."""
+    d = _i32(degrees)
+    n = len(d)
+    e = np.zeros((max(int(d.sum()) // 2, 1), 2), np.int32)
+    k = C.c_int32(0)
+    _check(_lib.load().tp_anneal_degree(n, _ip(d), t0, cooling, steps, moves_per_temp, seed,
+                                        _ip(e), C.byref(k)))
+    return e[: k.value].copy()
+
+
+def default_warm_start(n: int, r: int, seed: int = 0):
+    """proj/src/admm.cpp:337-354 -> edges (k, 2)."""
+    e = np.zeros((max(r, 1), 2), np.int32)
+    k = C.c_int32(0)
+    _check(_lib.load().tp_default_warm_start(n, r, seed, _ip(e), C.byref(k)))
+    return e[: k.value].copy()
+
+
+# ---------------------------------------------------------------- solutions
+@dataclass
+class Solution:
+    """proj/include/topoopt/admm.hpp:38-53"""
+    edges: np.ndarray
+    weights: np.ndarray
+    w: np.ndarray
+    lambda_tilde: float
+    acf_value: float
+    converged: bool
+    connected: bool
+    repaired: bool
+    residual: float
+    iterations: int
+    note: str
+    trace: np.ndarray = field(repr=False)  # rows: iter, residual, lambda_tilde, acf_iterate
+    lambda2: float = 1.0
+    lambda_n: float = 0.0
+    best_iter: int = 0
+
+    def trace_csv(self) -> str:
+        """proj/src/admm.cpp:223-236"""
+        out = ["iter,residual,lambda_tilde,acf_iterate"]
+        for row in self.trace:
+            out.append(f"{int(row[0])},{row[1]:.17g},{row[2]:.17g},{row[3]:.17g}")
+        return "\n".join(out) + "\n"
+
+
+def _solution(n, res: tp_result, edges, weights, trace, note) -> Solution:
+    k = res.n_edges
+    e = edges[:k].copy()
+    w = weights[:k].copy()
+    it = res.iterations
+    tr = np.column_stack([np.arange(1, it + 1), trace[:it]]) if it else np.zeros((0, 4))
+    return Solution(e, w, gossip_matrix(n, e, w), res.lambda_tilde, res.acf, bool(res.converged),
+                    bool(res.connected), bool(res.repaired), res.residual, it,
+                    note.value.decode(), tr, res.lambda2, res.lambda_n, res.best_iter)
+
+
+def _warm_arg(warm_start):
+    if warm_start is None:
+        return None, -1
+    we = _i32(np.asarray(warm_start, dtype=np.int32).reshape(-1, 2))
+    return we, len(we)
+
+
+def solve(n: int, r: int, cfg: SolverConfig | None = None, warm_start=None, **kw) -> Solution:
+    """topoopt::solve (proj/src/admm.cpp:356-428)."""
+    cfg = _config(cfg, kw)
+    c = cfg.to_c()
+    res = tp_result()
+    edges = np.zeros((max(r, 1), 2), np.int32)
+    weights = np.zeros(max(r, 1))
+    trace = np.zeros((cfg.max_iter, 3))
+    note = C.create_string_buffer(512)
+    we, nw = _warm_arg(warm_start)
+    _check(_lib.load().tp_solve(n, r, C.byref(c), _ip(we) if we is not None else None, nw,
+                                C.byref(res), _ip(edges), _dp(weights), _dp(trace), note, 512))
+    return _solution(n, res, edges, weights, trace, note)
+
+
+def solve_het(degrees, cfg: SolverConfig | None = None, warm_start=None, r=None, **kw) -> Solution:
+    """topoopt::solve_het on node_level_constraints (proj/src/admm_het.cpp:231-369)."""
+    cfg = _config(cfg, kw)
+    d = _i32(degrees)
+    n = len(d)
+    total = int(d.sum()) // 2
+    if r is not None and int(d.sum()) % 2 == 0 and r != total:
+        raise ValueError("edge total conflicts with the degree rows")
+    c = cfg.to_c()
+    res = tp_result()
+    m = n * (n - 1) // 2
+    edges = np.zeros((max(m, 1), 2), np.int32)
+    weights = np.zeros(max(m, 1))
+    trace = np.zeros((cfg.max_iter, 3))
+    note = C.create_string_buffer(512)
+    we, nw = _warm_arg(warm_start)
+    _check(_lib.load().tp_solve_het_node(n, _ip(d), C.byref(c), _ip(we) if we is not None else None,
+                                         nw, C.byref(res), _ip(edges), _dp(weights), _dp(trace),
+                                         note, 512))
+    return _solution(n, res, edges, weights, trace, note)
+
+
+# ---------------------------------------------------------------- layout / substeps
+@dataclass
+class Layout:
+    """proj/src/admm.cpp:24-44"""
+    n: int
+    m: int
+    lambda_ix: int
+    off_s: int
+    off_y: int
+    off_t: int
+    nx: int
+    neq: int
+    off_z: int = -1
+    off_nu: int = -1
+
+
+def hom_layout(n: int) -> Layout:
+    m = n * (n - 1) // 2
+    off_s = m + 1
+    off_y = off_s + n * n
+    off_t = off_y + n
+    return Layout(n, m, m, off_s, off_y, off_t, off_t + n * n, 2 * n * n + n)
+
+
+def het_layout(n: int, q: int) -> Layout:
+    lo = hom_layout(n)
+    lo.off_z = lo.nx
+    lo.off_nu = lo.off_z + lo.m
+    lo.nx = lo.off_nu + lo.m
+    lo.neq += q + lo.m
+    return lo
+
+
+def project_Y(n, r, x, d, alpha=2.0, rho=1.0) -> np.ndarray:
+    """proj/src/admm.cpp:268-277"""
+    x, d = _f64(x), _f64(d)
+    y = np.zeros_like(x)
+    _check(_lib.load().tp_project_Y(n, r, alpha, rho, _dp(x), _dp(d), _dp(y)))
+    return y
+
+
+def project_Y_het(degrees, x, d, alpha=2.0, rho=1.0) -> np.ndarray:
+    """proj/src/admm_het.cpp:156-171 (node-level system)."""
+    deg = _i32(degrees)
+    x, d = _f64(x), _f64(d)
+    y = np.zeros_like(x)
+    _check(_lib.load().tp_project_Y_het_node(len(deg), _ip(deg), alpha, rho, _dp(x), _dp(d), _dp(y)))
+    return y
+
+
+def update_X(n, r, y, d, alpha=2.0, rho=1.0) -> tuple[np.ndarray, np.ndarray]:
+    """proj/src/admm.cpp:279-293 -> (x, kkt = [x; mu])."""
+    lo = hom_layout(n)
+    y, d = _f64(y), _f64(d)
+    kkt = np.zeros(lo.nx + lo.neq)
+    _check(_lib.load().tp_update_X(n, r, alpha, rho, _dp(y), _dp(d), _dp(kkt)))
+    return kkt[: lo.nx].copy(), kkt
+
+
+def update_X_het(degrees, y, d, alpha=2.0, rho=1.0) -> tuple[np.ndarray, np.ndarray]:
+    deg = _i32(degrees)
+    n = len(deg)
+    lo = het_layout(n, n)
+    y, d = _f64(y), _f64(d)
+    kkt = np.zeros(lo.nx + lo.neq)
+    _check(_lib.load().tp_update_X_het_node(n, _ip(deg), alpha, rho, _dp(y), _dp(d), _dp(kkt)))
+    return kkt[: lo.nx].copy(), kkt
+
+
+def update_duals(x, y, d, rho) -> np.ndarray:
+    """proj/src/admm.cpp:295-297 (returns the updated duals)."""
+    x, y = _f64(x), _f64(y)
+    d = _f64(d).copy()
+    _check(_lib.load().tp_update_duals(len(d), rho, _dp(x), _dp(y), _dp(d)))
+    return d
+
+
+def project_binary_z(v, r: int) -> np.ndarray:
+    """proj/src/admm_het.cpp:116-123"""
+    v = _f64(v)
+    z = np.zeros_like(v)
+    _check(_lib.load().tp_project_binary_z(_dp(v), len(v), int(r), _dp(z)))
+    return z
+
+
+def extract_topology(n: int, r: int, g, weight_floor: float = 1e-6):
+    """proj/src/admm.cpp:299-335 -> (edges, weights, W)."""
+    g = _f64(g)
+    m = n * (n - 1) // 2
+    if len(g) < m:
+        raise ValueError("extract_topology: weight vector shorter than |E|")
+    cap = max(min(r, m), 1)
+    e = np.zeros((cap, 2), np.int32)
+    w = np.zeros(cap)
+    k = C.c_int32(0)
+    _check(_lib.load().tp_extract_topology(n, r, _dp(g), weight_floor, _ip(e), _dp(w), C.byref(k)))
+    e, w = e[: k.value].copy(), w[: k.value].copy()
+    return e, w, gossip_matrix(n, e, w)
+
+
+# ---------------------------------------------------------------- batched handle
+class BatchSolver:
+    """Independent solves of one n in lockstep on the current device
+    (tp_solver_*): edge-budget sweeps, bandwidth scenarios, restarts."""
+
+    def __init__(self, n: int, r=None, degrees=None, cfg: SolverConfig | None = None, **kw):
+        self.cfg = _config(cfg, kw)
+        self.n = n
+        L = _lib.load()
+        c = self.cfg.to_c()
+        h = C.c_void_p()
+        if degrees is not None:
+            deg = _i32(np.asarray(degrees).reshape(-1, n))
+            self.batch = deg.shape[0]
+            self.r = deg.sum(1) // 2
+            _check(L.tp_solver_create(n, self.batch, None, _ip(deg), C.byref(c), C.byref(h)))
+        else:
+            rr = _i32(np.atleast_1d(r))
+            self.batch = len(rr)
+            self.r = rr
+            _check(L.tp_solver_create(n, self.batch, _ip(rr), None, C.byref(c), C.byref(h)))
+        self.h = h
+        dims = np.zeros(12, np.int32)
+        _check(L.tp_solver_dims(self.h, _ip(dims)))
+        self.dims = dims
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.load().tp_solver_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def set_warm(self, b: int, edges):
+        e = _i32(np.asarray(edges, np.int32).reshape(-1, 2))
+        _check(_lib.load().tp_solver_set_warm(self.h, b, _ip(e), len(e)))
+
+    def start(self):
+        _check(_lib.load().tp_solver_start(self.h))
+
+    def iterate(self, k: int):
+        _check(_lib.load().tp_solver_iterate(self.h, k))
+
+    def sync(self) -> bool:
+        done = C.c_int32(0)
+        _check(_lib.load().tp_solver_sync(self.h, C.byref(done)))
+        return bool(done.value)
+
+    def run(self):
+        _check(_lib.load().tp_solver_run(self.h))
+
+    def finish(self):
+        _check(_lib.load().tp_solver_finish(self.h))
+
+    @property
+    def stream(self) -> int:
+        return _lib.load().tp_solver_stream(self.h)
+
+    def state_pointers(self):
+        x, y, d = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        _check(_lib.load().tp_solver_state(self.h, C.byref(x), C.byref(y), C.byref(d)))
+        return x.value, y.value, d.value
+
+    def result(self, b: int) -> Solution:
+        m = self.n * (self.n - 1) // 2
+        res = tp_result()
+        edges = np.zeros((max(m, 1), 2), np.int32)
+        weights = np.zeros(max(m, 1))
+        trace = np.zeros((self.cfg.max_iter, 3))
+        note = C.create_string_buffer(512)
+        _check(_lib.load().tp_solver_result(self.h, b, C.byref(res), _ip(edges), _dp(weights),
+                                            _dp(trace), note, 512))
+        return _solution(self.n, res, edges, weights, trace, note)
