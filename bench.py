@@ -1,0 +1,318 @@
+"""Benchmark of the B200 ADMM topology solver (BASELINE.json metric:
+"ADMM iter/s & time-to-topology at n=1024; batched solves/s at 1/2/4/8 GPUs").
+
+Default workload (N=1): one n=1024 candidate-complete instance (m = 523,776
+edge variables), r = 4096, rho = 10, epsilon = 1e-8 — SURVEY §8(d) config 4.
+A step is one ADMM iteration (project_Y, update_X, update_duals, residual,
+trace SLEM) over the device-resident state. With --gpus N every rank runs an
+independent restart (warm-start seed = rank): weak scaling, no collective on
+the data path; the barrier and the max-over-ranks timing use torch.distributed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload n1024|sweep]
+
+`--impl reference` times the reference's own CPU implementation (compiled
+from /root/reference into oracle/_ref) on the host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+N_NODES, R_EDGES = 1024, 4096
+CFG = dict(rho=10.0, epsilon=1e-8)
+
+
+def peaks():
+    try:
+        with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+FP64_DMMA_TFLOPS = 37.1  # tools/microbench/fp64_peak.cu on this pool's B200 (DMMA m8n8k4)
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[2 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------- helpers
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def warm_start(T, n, r, seed):
+    bu, e = T.allocate_edge_capacity([1.0] * n, r)
+    return T.anneal_degree_topology(e, steps=1, moves_per_temp=1, seed=seed)
+
+
+def cpu_reference_sample(n, r, warm):
+    """One reference ADMM iteration at (n, r), per-substep seconds (1 core each,
+    run concurrently to bound wall time) — see oracle/ref_shim.cpp."""
+    from oracle import ref
+    t = time.time()
+    s = ref.iteration_sample(n, r, warm, rho=CFG["rho"], chunk=10)
+    wall = time.time() - t
+    per_iter = s["project_nsd_s"] + s["project_psd_s"] + s["xstep_s"] + s["acf_s"]
+    return per_iter, s, wall
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return
+    from oracle import ref
+    if not ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    sys.path.insert(0, HERE)
+    # warm start from the reference's own annealer (steps=1, moves=1), SURVEY §8(d)
+    bu, e = ref.allocate([1.0] * N_NODES, R_EDGES)
+    warm = ref.anneal_degree(e, steps=1, moves_per_temp=1, seed=0)
+    samples, details = [], []
+    t_start = time.time()
+    budget_s = 150.0
+    for k in range(max(1, args.steps)):
+        per_iter, s, wall = cpu_reference_sample(N_NODES, R_EDGES, warm)
+        samples.append(per_iter)
+        details.append(s)
+        if time.time() - t_start > budget_s:
+            break
+    per = statistics.median(samples)
+    value = 1.0 / per
+    cores = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": "admm_iter_per_s_n1024", "value": value, "unit": "iter/s",
+        "n_gpus": args.gpus, "steps": len(samples), "warmup": 0, "ms_per_step": per * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": "n1024_single_instance", "n": N_NODES, "r": R_EDGES, **CFG},
+        "cpu_baseline": {"value": value, "unit": "iter/s", "cores": 1, "kind": "reference",
+                         "host_cores": cores,
+                         "sample": f"{len(samples)} reference ADMM iteration(s) at n=1024: project_nsd, "
+                                   "project_psd, kkt_rhs+BiCGSTAB/ILU (restarted every 10), acf_of_g; "
+                                   "substeps timed concurrently on separate cores, summed per iteration",
+                         "substeps_s": details[-1]},
+        "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as tdist
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    from paper_2512_07536_b200 import topoopt as T
+    from paper_2512_07536_b200 import _lib
+
+    _lib.load().tp_set_device(local)
+
+    def barrier():
+        if ws > 1:
+            tdist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if ws == 1:
+            return x
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        return float(t.item())
+
+    n, r = N_NODES, R_EDGES
+    K, W = args.steps, args.warmup
+    warm = warm_start(T, n, r, seed=rank)
+    max_iter = W + K + 8
+    bs = T.BatchSolver(n, r=[r], max_iter=max_iter, **CFG)
+    bs.set_warm(0, warm)
+    bs.start()
+    stream = torch.cuda.ExternalStream(bs.stream)
+    bs.iterate(W)
+    bs.sync()
+    launches_per_iter = bs.launches_per_iteration()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        bs.iterate(K)
+        e1.record(stream)
+        e1.synchronize()
+    barrier()
+    dt = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+    value = ws * K / dt
+    done = bs.sync()
+
+    # live per-phase timing on the solver stream (state is discarded after)
+    def phase(ph, reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        bs.bench_phase(ph, 1)
+        torch.cuda.synchronize()
+        a.record(stream)
+        per = bs.bench_phase(ph, reps)
+        b.record(stream)
+        b.synchronize()
+        return a.elapsed_time(b) / 1e3 / reps, per
+
+    t_cone, gemms = phase(0, 3)
+    t_x, _ = phase(1, 10)
+    t_sel, _ = phase(2, 5)
+    t_slem, _ = phase(3, 3)
+    t_prep, _ = phase(4, 10)
+    bs.close()
+
+    # roofline of the dominant kernel: the symmetric FP64 DMMA GEMM
+    gemm_flops = 2 * 2.0 * n * (n * (n + 1) / 2)  # 2 matrices x lower triangle x 2n flops
+    gemm_avg = t_cone / gemms
+    achieved = gemm_flops / gemm_avg / 1e12
+    # x-step algorithmic bytes: passes a+b read Y,D (S,T blocks, edges), write X,D
+    m = n * (n - 1) // 2
+    xbytes = 8.0 * (4 * n * n + 2 * m + m) + 8.0 * (4 * n * n + m + 2 * m + 4 * n * n + 2 * m)
+
+    # e2e: the C-ABI solve with host buffers (warm edges in, solution out)
+    barrier()
+    t0 = time.time()
+    sol = T.solve(n, r, warm_start=warm, max_iter=K, **CFG)
+    e2e_s = time.time() - t0
+    e2e_s = max_over_ranks(e2e_s)
+    e2e = ws * K / e2e_s
+    h2d = warm.nbytes + 64
+    d2h = sol.edges.nbytes + sol.weights.nbytes + K * 3 * 8 + 96
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle import ref
+            if ref.available():
+                per_iter, s, wall = cpu_reference_sample(n, r, warm)
+                cpu = {"value": 1.0 / per_iter, "unit": "iter/s", "cores": 1, "kind": "reference",
+                       "sample": "one reference ADMM iteration at n=1024 (project_nsd, project_psd, "
+                                 "restarted BiCGSTAB x-step, acf_of_g), substeps timed concurrently, "
+                                 f"summed: {per_iter:.2f} s/iter (wall {wall:.1f} s)",
+                       "substeps_s": s}
+        except Exception as exc:  # the baseline is reported, not required
+            cpu = {"value": None, "unit": "iter/s", "cores": 1, "kind": "reference",
+                   "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        pk = peaks()
+        line = {
+            "metric": "admm_iter_per_s_n1024", "value": value, "unit": "iter/s", "n_gpus": ws,
+            "steps": K, "warmup": W, "ms_per_step": dt / K * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "n1024_single_instance_per_gpu", "n": n, "r": r,
+                       "m_edge_vars": m, **CFG,
+                       "warm_start": "anneal_degree_topology(Alg.1 unit bandwidth, steps=1, moves=1, seed=rank)",
+                       "l2": "state+work buffers ~170 MB > 126 MB L2 per iteration"},
+            "roofline": {"bound": "tensor", "kernel": "sym_gemm_kernel (FP64 DMMA)",
+                         "achieved": achieved, "peak": FP64_DMMA_TFLOPS, "unit": "TFLOP/s",
+                         "frac": achieved / FP64_DMMA_TFLOPS, "traffic": None,
+                         "peak_source": "measured FP64 DMMA microbenchmark (tools/microbench/fp64_peak.cu); "
+                                        "MEASURED_PEAKS.json has no FP64 entry",
+                         "gemms_per_iteration": gemms, "gemm_avg_ms": gemm_avg * 1e3},
+            "phases_ms": {"cone_projection": t_cone * 1e3, "xstep": t_x * 1e3, "topr": t_sel * 1e3,
+                          "trace_slem": t_slem * 1e3, "prep": t_prep * 1e3},
+            "xstep_roofline": {"bound": "hbm", "achieved": xbytes / t_x / 1e9,
+                               "peak": pk.get("hbm_gbs", 6538.9), "unit": "GB/s",
+                               "frac": xbytes / t_x / 1e9 / pk.get("hbm_gbs", 6538.9),
+                               "bytes_per_launch_set": xbytes},
+            "e2e": {"value": e2e, "unit": "iter/s", "h2d_bytes_per_step": h2d / K,
+                    "d2h_bytes_per_step": d2h / K,
+                    "note": "tp_solve through the C ABI with host warm-start edges in and the host "
+                            "Solution out (setup, feasible start, K iterations, extraction, final SLEM)"},
+            "gpu_launches": launches_per_iter * K,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        tdist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="n1024", choices=["n1024"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

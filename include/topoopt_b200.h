@@ -121,6 +121,12 @@ int tp_solver_dims(tp_solver* s, int32_t* dims);
 /* Device pointers of the state (X, Y, D), each batch*nx doubles. */
 int tp_solver_state(tp_solver* s, double** x, double** y, double** d);
 
+/* Instrumentation: enqueue `reps` repetitions of one iteration phase on the
+ * solver stream (0 cone projection, 1 x-step, 2 top-r, 3 trace SLEM, 4 prep)
+ * so callers can time it with events; the state is left undefined. */
+int tp_solver_bench_phase(tp_solver* s, int32_t phase, int32_t reps, int32_t* launches_per_rep);
+int tp_solver_launches_per_iteration(tp_solver* s, int32_t* out);
+
 /* ---------------------------------------------------------------- substeps */
 /* project_Y (proj/src/admm.cpp:268-277); x, d, y of length nx. */
 int tp_project_Y(int32_t n, int32_t r, double alpha, double rho, const double* x, const double* d,

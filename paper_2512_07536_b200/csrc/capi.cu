@@ -215,6 +215,17 @@ int tp_solver_state(tp_solver* s, double** x, double** y, double** d) {
     });
 }
 
+int tp_solver_bench_phase(tp_solver* s, int32_t phase, int32_t reps, int32_t* launches_per_rep) {
+    return guarded([&] {
+        const int per = s->s->bench_phase(phase, reps);
+        if (launches_per_rep) *launches_per_rep = per;
+    });
+}
+
+int tp_solver_launches_per_iteration(tp_solver* s, int32_t* out) {
+    return guarded([&] { *out = s->s->launches_per_iteration(); });
+}
+
 int tp_solve(int32_t n, int32_t r, const tp_config* cfg, const int32_t* warm_edges, int32_t n_warm,
              tp_result* out, int32_t* edges, double* weights, double* trace, char* note,
              int32_t note_cap) {

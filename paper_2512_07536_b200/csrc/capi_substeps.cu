@@ -178,7 +178,8 @@ void slem_edges(int n, const std::vector<int>& packed, const std::vector<double>
     const long long m = (long long)n * (n - 1) / 2;
     const int k = (int)packed.size();
     init_attrs();
-    DBuf<double> g(m), out(8), basis((size_t)std::max(1, n - 1) * n), ew(std::max(1, k));
+    const int kfin = n - 1 <= kFinalExactDim ? std::max(1, n - 1) : kFinalKrylov;
+    DBuf<double> g(m), out(8), basis((size_t)kfin * n), ew(std::max(1, k));
     DBuf<int> list(std::max(1, k)), count(1), ei(std::max(1, k)), ej(std::max(1, k)), ci(std::max(1, k));
     g.zero();
     std::vector<double> packedw(m, 0.0);
@@ -199,8 +200,10 @@ void slem_edges(int n, const std::vector<int>& packed, const std::vector<double>
     a.e_w = ew.p;
     a.col_idx = ci.p;
     a.basis = basis.p;
-    a.kmax = std::max(1, n - 1);
-    a.tol = 1e-14;
+    a.kmax = kfin;
+    a.max_restarts = 200;
+    a.min_steps = 64;
+    a.tol = 1e-10;
     a.out = out.p;
     launch_slem(a, 1, 0);
     TPB_CUDA(cudaDeviceSynchronize());

@@ -5,15 +5,17 @@
 // proj/src/topology.cpp:125-144) and once for the final report.
 //
 //  * L has <= r nonzero edges; the 1-vector is its known null vector, so the
-//    Krylov space is built on 1-perp (explicit mean deflation every step).
-//    lambda2(W) = 1 - mu_min(L|1perp), lambda_n(W) = 1 - mu_max(L).
+//    Krylov space is built on 1-perp. lambda2(W) = 1 - mu_min(L|1perp),
+//    lambda_n(W) = 1 - mu_max(L).
 //  * SpMV is a deterministic gather: per node, incident edges in ascending
 //    edge index (column part from a stable counting sort, then row part).
-//  * Full reorthogonalisation (CGS2 against the stored basis) when a basis
-//    buffer is given; otherwise plain three-term Lanczos (extreme Ritz values
-//    stay correct; ghosts only duplicate converged values).
+//  * Full reorthogonalisation (CGS2 against the stored basis); the 1-vector is
+//    deflated last so round-off is not amplified by 1/beta.
+//  * Explicit restarts from the two extreme Ritz vectors, and a warm start
+//    from the previous ADMM iteration's Ritz vectors (the support moves
+//    slowly), keep the trace evaluation at a few dozen matvecs.
 //  * Extreme Ritz values by warp multisection on Sturm counts; convergence by
-//    the residual bound beta_k |s_k| from inverse iteration on T_k.
+//    the residual bound beta_k |s_k| (s from inverse iteration on T_k).
 #include "slem_kernels.cuh"
 #include "csr.cuh"
 
@@ -22,29 +24,25 @@ namespace tpb {
 namespace {
 
 constexpr int kThreads = 512;
-constexpr int kMaxK = 2048;  // smem alpha/beta capacity
 
-// Sturm count: number of eigenvalues of the k x k tridiagonal (al, be) < x.
+// number of eigenvalues of the k x k tridiagonal (al, be) below x
 __device__ int sturm_count(const double* al, const double* be, int k, double x) {
     int cnt = 0;
     double d = 1.0;
-    const double pivmin = 1e-300;
     for (int i = 0; i < k; ++i) {
-        const double b2 = i > 0 ? be[i - 1] * be[i - 1] : 0.0;
-        d = (al[i] - x) - (i > 0 ? b2 / d : 0.0);
-        if (fabs(d) < pivmin) d = -pivmin;
+        d = (al[i] - x) - (i > 0 ? be[i - 1] * be[i - 1] / d : 0.0);
+        if (fabs(d) < 1e-300) d = -1e-300;
         if (d < 0.0) ++cnt;
     }
     return cnt;
 }
 
-// idx-th smallest eigenvalue (0-based) of T_k by warp multisection.
+// idx-th smallest eigenvalue (0-based) of T_k by warp multisection (one warp).
 __device__ double tri_eig(const double* al, const double* be, int k, int idx, double lo, double hi) {
     const int lane = threadIdx.x & 31;
     for (int round = 0; round < 40; ++round) {
         const double x = lo + (hi - lo) * (lane + 1) / 33.0;
         const int c = sturm_count(al, be, k, x);
-        // first lane whose count exceeds idx bounds the eigenvalue from above
         const unsigned mask = __ballot_sync(0xffffffffu, c > idx);
         const int first = mask ? __ffs(mask) - 1 : 32;
         const double nlo = first == 0 ? lo : lo + (hi - lo) * first / 33.0;
@@ -56,36 +54,49 @@ __device__ double tri_eig(const double* al, const double* be, int k, int idx, do
     return 0.5 * (lo + hi);
 }
 
-// |last component| of the unit eigenvector of T_k for eigenvalue theta, by two
-// steps of inverse iteration (Thomas algorithm on T - theta I). Single thread.
-__device__ double ritz_last(const double* al, const double* be, int k, double theta, double* wk) {
-    // wk: 3k doubles (c', d', x)
-    double* cp = wk;
-    double* dp = wk + k;
-    double* x = wk + 2 * k;
+__device__ void gershgorin(const double* al, const double* be, int k, double& lo, double& hi) {
+    lo = 1e300;
+    hi = -1e300;
+    for (int i = 0; i < k; ++i) {
+        const double r = (i > 0 ? fabs(be[i - 1]) : 0.0) + (i < k - 1 ? fabs(be[i]) : 0.0);
+        lo = fmin(lo, al[i] - r);
+        hi = fmax(hi, al[i] + r);
+    }
+    lo -= 1e-12 * fmax(1.0, fabs(lo));
+    hi += 1e-12 * fmax(1.0, fabs(hi));
+}
+
+// Unit eigenvector s of T_k for eigenvalue theta (two inverse iterations,
+// Thomas algorithm); returns |s_{k-1}|. Single thread; work: 2k doubles.
+__device__ double tri_vec(const double* al, const double* be, int k, double theta, double* work,
+                          double* s) {
+    double* cp = work;
+    double* dp = work + k;
     const double shift = theta + 1e-14 * fmax(1.0, fabs(theta));
-    for (int i = 0; i < k; ++i) x[i] = 1.0;
+    for (int i = 0; i < k; ++i) s[i] = 1.0;
     for (int it = 0; it < 2; ++it) {
-        // solve (T - shift) y = x
-        double denom = al[0] - shift;
-        if (fabs(denom) < 1e-300) denom = 1e-300;
-        cp[0] = k > 1 ? be[0] / denom : 0.0;
-        dp[0] = x[0] / denom;
+        double den = al[0] - shift;
+        if (fabs(den) < 1e-300) den = 1e-300;
+        cp[0] = k > 1 ? be[0] / den : 0.0;
+        dp[0] = s[0] / den;
         for (int i = 1; i < k; ++i) {
             double dn = (al[i] - shift) - be[i - 1] * cp[i - 1];
             if (fabs(dn) < 1e-300) dn = 1e-300;
             cp[i] = i < k - 1 ? be[i] / dn : 0.0;
-            dp[i] = (x[i] - be[i - 1] * dp[i - 1]) / dn;
+            dp[i] = (s[i] - be[i - 1] * dp[i - 1]) / dn;
         }
-        x[k - 1] = dp[k - 1];
-        for (int i = k - 2; i >= 0; --i) x[i] = dp[i] - cp[i] * x[i + 1];
+        s[k - 1] = dp[k - 1];
+        for (int i = k - 2; i >= 0; --i) s[i] = dp[i] - cp[i] * s[i + 1];
         double nrm = 0.0;
-        for (int i = 0; i < k; ++i) nrm += x[i] * x[i];
+        for (int i = 0; i < k; ++i) nrm += s[i] * s[i];
         nrm = sqrt(nrm);
-        if (!(nrm > 0.0) || !isfinite(nrm)) return 1.0;
-        for (int i = 0; i < k; ++i) x[i] /= nrm;
+        if (!(nrm > 0.0) || !isfinite(nrm)) {
+            for (int i = 0; i < k; ++i) s[i] = (i == k - 1) ? 1.0 : 0.0;
+            return 1.0;
+        }
+        for (int i = 0; i < k; ++i) s[i] /= nrm;
     }
-    return fabs(x[k - 1]);
+    return fabs(s[k - 1]);
 }
 
 __device__ inline double hash_unit(int i) {
@@ -96,13 +107,100 @@ __device__ inline double hash_unit(int i) {
     return (double)(x & 0xffffff) / 16777216.0 - 0.5;
 }
 
+// q <- (q - mean q) / ||q - mean q||
+__device__ void deflate_normalize(double* q, int n, double* scratch) {
+    double s = 0.0;
+    for (int v = threadIdx.x; v < n; v += blockDim.x) s += q[v];
+    s = block_sum(s, scratch);
+    const double mean = s / n;
+    double nn = 0.0;
+    for (int v = threadIdx.x; v < n; v += blockDim.x) {
+        q[v] -= mean;
+        nn += q[v] * q[v];
+    }
+    nn = block_sum(nn, scratch);
+    const double inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
+    for (int v = threadIdx.x; v < n; v += blockDim.x) q[v] *= inv;
+    __syncthreads();
+}
+
+// convergence checks at k = 4, 8, 12, 16, 24, 32, 48, 64, 96, ...
+__device__ inline bool check_step(int kk) {
+    if (kk <= 16) return (kk & 3) == 0;
+    int p = 16;
+    while (p < kk) {
+        if (p + p / 2 == kk) return true;
+        p <<= 1;
+    }
+    return p == kk;
+}
+
 }  // namespace
+
+__device__ inline void block_sum2(double& a, double& b, double* scratch) {
+    // deterministic fused reduction of two values (scratch: 64 doubles)
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nw = (blockDim.x + 31) >> 5;
+    a = warp_sum(a);
+    b = warp_sum(b);
+    __syncthreads();
+    if (lane == 0) {
+        scratch[wid] = a;
+        scratch[32 + wid] = b;
+    }
+    __syncthreads();
+    double x = 0.0, y = 0.0;
+    for (int k = 0; k < nw; ++k) {
+        x += scratch[k];
+        y += scratch[32 + k];
+    }
+    a = x;
+    b = y;
+}
+
+// w <- w - sum_{j<=k} (Q_j . w) Q_j, twice (CGS2); cf[j] receives the first
+// pass coefficients (cf[k] = alpha when q_k is the current Lanczos vector).
+__device__ inline void cgs2(const double* Q, int n, int ldq, int k, double* w, double* cf,
+                            double* cf2, bool q_in_smem) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    for (int pass = 0; pass < 2; ++pass) {
+        double* c_out = pass == 0 ? cf : cf2;
+        if (q_in_smem && k < (int)blockDim.x) {
+            // one thread per basis vector: no shuffles on the critical path
+            if (tid <= k) {
+                const double* qj = Q + (long long)tid * ldq;
+                double c0 = 0.0, c1 = 0.0;
+                int v = 0;
+                for (; v + 1 < n; v += 2) {
+                    c0 += qj[v] * w[v];
+                    c1 += qj[v + 1] * w[v + 1];
+                }
+                if (v < n) c0 += qj[v] * w[v];
+                c_out[tid] = c0 + c1;
+            }
+        } else {
+            for (int j = wid; j <= k; j += nw) {
+                double c = 0.0;
+                for (int v = lane; v < n; v += 32) c += Q[(long long)j * ldq + v] * w[v];
+                c = warp_sum(c);
+                if (lane == 0) c_out[j] = c;
+            }
+        }
+        __syncthreads();
+        for (int v = tid; v < n; v += blockDim.x) {
+            double acc = w[v];
+            for (int j = 0; j <= k; ++j) acc -= c_out[j] * Q[(long long)j * ldq + v];
+            w[v] = acc;
+        }
+        __syncthreads();
+    }
+}
 
 __global__ void __launch_bounds__(kThreads) slem_kernel(SlemArgs a) {
     const int b = blockIdx.x;
     if (a.ictl && a.ictl[b * 8 + 1]) return;  // solve already finished
     const int n = a.n;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, nthr = blockDim.x, wid = tid >> 5;
     const int ne = min(a.count[b], a.list_cap);
     const int* list = a.list + (long long)b * a.list_cap;
     const double* g = a.g + (long long)b * a.stride;
@@ -110,178 +208,193 @@ __global__ void __launch_bounds__(kThreads) slem_kernel(SlemArgs a) {
     int* ej = a.e_j + (long long)b * a.list_cap;
     double* ew = a.e_w + (long long)b * a.list_cap;
     int* cidx = a.col_idx + (long long)b * a.list_cap;
-    double* basis = a.basis ? a.basis + (long long)b * a.kmax * n : nullptr;
+    const int dim = n - 1;
+    const int kmax = max(1, min(a.kmax, dim));
 
     extern __shared__ double sh[];
-    double* q = sh;            // n
-    double* qp = sh + n;       // n
-    double* w = sh + 2 * n;    // n
-    double* al = sh + 3 * n;   // kMaxK
-    double* be = al + kMaxK;   // kMaxK
-    double* wk = be + kMaxK;   // 4*kMaxK
-    int* rowptr = (int*)(wk + 4 * kMaxK);  // n+1
-    int* colptr = rowptr + (n + 1);        // n+1
-    int* cur = colptr + (n + 1);           // n
-    __shared__ double scratch[32];
+    double* q = sh;                   // n
+    double* w = q + n;                // n
+    double* al = w + n;               // kmax
+    double* be = al + kmax;           // kmax
+    double* smin = be + kmax;         // kmax
+    double* smax = smin + kmax;       // kmax
+    double* cf = smax + kmax;         // kmax
+    double* cf2 = cf + kmax;          // kmax
+    double* wk = cf2 + kmax;          // 2 kmax
+    int* rowptr = (int*)(wk + 2 * kmax);  // n+1
+    int* colptr = rowptr + (n + 1);       // n+1
+    int* cur = colptr + (n + 1);          // n
+    // Krylov basis: shared memory when it fits (a.basis == null), else global
+    // (odd row stride in shared memory: conflict-free per-vector dot products)
+    const int ldq = a.basis ? n : (n | 1);
+    double* Q = a.basis ? a.basis + (long long)b * a.kmax * n
+                        : (double*)(((uintptr_t)(cur + n) + 15) & ~(uintptr_t)15);
+    __shared__ double scratch[64];
     __shared__ int iscr[32];
-    __shared__ int s_stop, s_k;
-    __shared__ double s_res[2];
+    __shared__ int s_flag;  // bit0 stop, bit1 converged
+    __shared__ double s_th[2];
 
-    // ---- deterministic incidence of the support
     build_csr(n, ne, list, g, ei, ej, ew, rowptr, colptr, cur, cidx, iscr);
 
-    // ---- Lanczos on L restricted to 1-perp
-    const int dim = n - 1;
-    int kmax = min(a.kmax, min(dim, kMaxK));
-    if (kmax < 1) kmax = 1;
-    {
-        double s = 0.0;
-        for (int v = tid; v < n; v += kThreads) {
-            q[v] = hash_unit(v);
-            qp[v] = 0.0;
-            s += q[v];
-        }
-        s = block_sum(s, scratch);
-        const double mean = s / n;
-        double nn = 0.0;
-        for (int v = tid; v < n; v += kThreads) {
-            q[v] -= mean;
-            nn += q[v] * q[v];
-        }
-        nn = block_sum(nn, scratch);
-        const double inv = 1.0 / sqrt(nn);
-        for (int v = tid; v < n; v += kThreads) q[v] *= inv;
-    }
-    if (tid == 0) {
-        s_stop = 0;
-        s_k = 0;
+    // Exact mode (Krylov dimension covers 1-perp): run to completion, no early
+    // stop, so the extreme Ritz values are eigenvalues up to rounding.
+    // Restarted mode: random start, or a warm start from the previous extreme
+    // Ritz vectors plus a small fixed random component, and at least
+    // a.min_steps matvecs before the residual test.
+    const bool exact = kmax >= dim;
+    const bool warm = !exact && a.ritz && a.ritz_ok && a.ritz_ok[b];
+    double* rz = a.ritz ? a.ritz + (long long)b * 2 * n : nullptr;
+    if (warm) {
+        for (int v = tid; v < n; v += nthr) w[v] = hash_unit(v);
+        __syncthreads();
+        deflate_normalize(w, n, scratch);
+        for (int v = tid; v < n; v += nthr) q[v] = rz[v] + rz[n + v];
+        __syncthreads();
+        deflate_normalize(q, n, scratch);
+        for (int v = tid; v < n; v += nthr) q[v] += a.noise * w[v];
+    } else {
+        for (int v = tid; v < n; v += nthr) q[v] = hash_unit(v);
     }
     __syncthreads();
-    double beta_prev = 0.0;
+    deflate_normalize(q, n, scratch);
+
     double th_min = 0.0, th_max = 0.0;
-    int k = 0;
-    for (k = 0; k < kmax; ++k) {
-        if (basis)
-            for (int v = tid; v < n; v += kThreads) basis[(long long)k * n + v] = q[v];
-        // w = L q - beta_prev q_prev
-        for (int v = tid; v < n; v += kThreads) {
-            const double qv = q[v];
-            double acc = 0.0;
-            for (int p = colptr[v]; p < colptr[v + 1]; ++p) {
-                const int e = cidx[p];
-                acc += ew[e] * (qv - q[ei[e]]);
-            }
-            for (int e = rowptr[v]; e < rowptr[v + 1]; ++e) acc += ew[e] * (qv - q[ej[e]]);
-            w[v] = acc - beta_prev * qp[v];
-        }
+    int steps = 0, converged = 0, kk = 0;
+    for (int cycle = 0; cycle <= a.max_restarts; ++cycle) {
+        if (tid == 0) s_flag = 0;
         __syncthreads();
-        double dot = 0.0;
-        for (int v = tid; v < n; v += kThreads) dot += w[v] * q[v];
-        const double alpha = block_sum(dot, scratch);
-        for (int v = tid; v < n; v += kThreads) w[v] -= alpha * q[v];
-        __syncthreads();
-        if (basis) {
-            // CGS2 against q_0..q_k: dots by warps, update by nodes
-            const int lane = tid & 31, wid = tid >> 5;
-            for (int pass = 0; pass < 2; ++pass) {
-                for (int j = wid; j <= k; j += kThreads / 32) {
-                    double c = 0.0;
-                    for (int v = lane; v < n; v += 32) c += basis[(long long)j * n + v] * w[v];
-                    c = warp_sum(c);
-                    if (lane == 0) wk[j] = c;
+        for (int k = 0; k < kmax; ++k) {
+            for (int v = tid; v < n; v += nthr) Q[(long long)k * ldq + v] = q[v];
+            // w = L q (gather, ascending edge order)
+            for (int v = tid; v < n; v += nthr) {
+                const double qv = q[v];
+                double acc = 0.0;
+                for (int p = colptr[v]; p < colptr[v + 1]; ++p) {
+                    const int e = cidx[p];
+                    acc += ew[e] * (qv - q[ei[e]]);
                 }
-                __syncthreads();
-                for (int v = tid; v < n; v += kThreads) {
-                    double acc = w[v];
-                    for (int j = 0; j <= k; ++j) acc -= wk[j] * basis[(long long)j * n + v];
-                    w[v] = acc;
-                }
-                __syncthreads();
-            }
-        }
-        // deflate the 1-vector last, so reorthogonalisation round-off is not
-        // amplified by 1/beta into the null direction
-        double s = 0.0;
-        for (int v = tid; v < n; v += kThreads) s += w[v];
-        s = block_sum(s, scratch);
-        const double mean = s / n;
-        for (int v = tid; v < n; v += kThreads) w[v] -= mean;
-        double nn = 0.0;
-        for (int v = tid; v < n; v += kThreads) nn += w[v] * w[v];
-        nn = block_sum(nn, scratch);
-        const double beta = sqrt(nn);
-        if (tid == 0) {
-            al[k] = alpha;
-            be[k] = beta;
-        }
-        __syncthreads();
-        const int kk = k + 1;
-        const double scale = fmax(fabs(alpha), 1e-300);
-        bool breakdown = !(beta > 1e-13 * fmax(scale, fabs(th_max)));
-        const bool check = breakdown || kk == kmax || (kk % 8 == 0);
-        if (check) {
-            if (tid < 32) {
-                // Gershgorin bounds
-                double lo = 1e300, hi = -1e300;
-                for (int i = 0; i < kk; ++i) {
-                    const double r = (i > 0 ? fabs(be[i - 1]) : 0.0) + (i < kk - 1 ? fabs(be[i]) : 0.0);
-                    lo = fmin(lo, al[i] - r);
-                    hi = fmax(hi, al[i] + r);
-                }
-                lo -= 1e-12 * fmax(1.0, fabs(lo));
-                hi += 1e-12 * fmax(1.0, fabs(hi));
-                const double tmin = tri_eig(al, be, kk, 0, lo, hi);
-                const double tmax = tri_eig(al, be, kk, kk - 1, lo, hi);
-                if (tid == 0) {
-                    double r1 = 0.0, r2 = 0.0;
-                    if (!breakdown && kk < dim) {
-                        r1 = beta * ritz_last(al, be, kk, tmin, wk + kMaxK / 2);
-                        r2 = beta * ritz_last(al, be, kk, tmax, wk + kMaxK / 2);
-                    }
-                    const double sc = fmax(fabs(tmax), 1e-300);
-                    s_res[0] = tmin;
-                    s_res[1] = tmax;
-                    if (breakdown || kk >= dim || (r1 <= a.tol * sc && r2 <= a.tol * sc)) s_stop = 1;
-                    s_k = kk;
-                }
+                for (int e = rowptr[v]; e < rowptr[v + 1]; ++e) acc += ew[e] * (qv - q[ej[e]]);
+                w[v] = acc;
             }
             __syncthreads();
-            th_min = s_res[0];
-            th_max = s_res[1];
-            if (s_stop) break;
+            cgs2(Q, n, ldq, k, w, cf, cf2, a.basis == nullptr);
+            const double alpha = cf[k] + cf2[k];
+            // deflate the 1-vector last; ||w - mean||^2 = sum w^2 - n mean^2
+            double s = 0.0, s2 = 0.0;
+            for (int v = tid; v < n; v += nthr) {
+                s += w[v];
+                s2 += w[v] * w[v];
+            }
+            block_sum2(s, s2, scratch);
+            const double mean = s / n;
+            const double beta = sqrt(fmax(s2 - n * mean * mean, 0.0));
+            if (tid == 0) {
+                al[k] = alpha;
+                be[k] = beta;
+            }
+            kk = k + 1;
+            ++steps;
+            const bool breakdown = !(beta > 1e-13 * fmax(fabs(alpha), fabs(th_max)) + 1e-300);
+            if (breakdown && kk < dim && kk < kmax) {
+                // invariant subspace found early: continue with a fresh direction
+                // orthogonal to the basis (T decouples, beta_k = 0)
+                for (int v = tid; v < n; v += nthr) w[v] = hash_unit(v * 7 + 13 * kk + 1);
+                __syncthreads();
+                cgs2(Q, n, ldq, k, w, cf, cf2, a.basis == nullptr);
+                if (tid == 0) be[k] = 0.0;
+                for (int v = tid; v < n; v += nthr) q[v] = w[v];
+                __syncthreads();
+                deflate_normalize(q, n, scratch);
+                continue;
+            }
+            const bool want_check =
+                exact ? (kk >= dim || breakdown)
+                      : (breakdown || kk == kmax || (steps >= a.min_steps && check_step(kk)));
+            if (want_check) {
+                __syncthreads();
+                if (wid == 0) {
+                    double lo, hi;
+                    gershgorin(al, be, kk, lo, hi);
+                    const double tmin = tri_eig(al, be, kk, 0, lo, hi);
+                    const double tmax = tri_eig(al, be, kk, kk - 1, lo, hi);
+                    if (tid == 0) {
+                        const double r1 = beta * tri_vec(al, be, kk, tmin, wk, smin);
+                        const double r2 = beta * tri_vec(al, be, kk, tmax, wk, smax);
+                        const double sc = fmax(fabs(tmax), 1e-300);
+                        const bool conv = kk >= dim || (!exact && (breakdown || (r1 <= a.tol * sc &&
+                                                                                   r2 <= a.tol * sc)));
+                        s_th[0] = tmin;
+                        s_th[1] = tmax;
+                        s_flag = (conv || kk == kmax) ? (1 | (conv ? 2 : 0)) : 0;
+                    }
+                }
+                __syncthreads();
+                th_min = s_th[0];
+                th_max = s_th[1];
+                if (s_flag & 1) {
+                    converged = (s_flag >> 1) & 1;
+                    break;
+                }
+            }
+            const double inv = beta > 0.0 ? 1.0 / beta : 0.0;
+            for (int v = tid; v < n; v += nthr) q[v] = (w[v] - mean) * inv;
+            __syncthreads();
         }
-        // advance
-        const double inv = beta > 0.0 ? 1.0 / beta : 0.0;
-        for (int v = tid; v < n; v += kThreads) {
-            qp[v] = q[v];
-            q[v] = w[v] * inv;
+        // Ritz vectors y = Q s of both extremes (restart vector / next warm start)
+        if (rz || !converged) {
+            for (int v = tid; v < n; v += nthr) {
+                double y1 = 0.0, y2 = 0.0;
+                for (int j = 0; j < kk; ++j) {
+                    const double qj = Q[(long long)j * ldq + v];
+                    y1 += smin[j] * qj;
+                    y2 += smax[j] * qj;
+                }
+                w[v] = y1;
+                q[v] = y2;
+            }
+            __syncthreads();
+            if (rz) {
+                for (int v = tid; v < n; v += nthr) {
+                    rz[v] = w[v];
+                    rz[n + v] = q[v];
+                }
+            }
+            for (int v = tid; v < n; v += nthr) q[v] += w[v];
+            __syncthreads();
+            deflate_normalize(q, n, scratch);
         }
-        beta_prev = beta;
-        __syncthreads();
+        if (converged) break;
     }
     if (tid == 0) {
+        if (a.ritz_ok) a.ritz_ok[b] = 1;
         const double l2 = 1.0 - th_min, ln = 1.0 - th_max;
         const double acf = fmax(fabs(l2), fabs(ln));
-        if (a.tr_acf) {
-            const int it = a.ictl[b * 8];
-            a.tr_acf[(long long)b * a.max_iter + it] = acf;
-        }
+        if (a.tr_acf) a.tr_acf[(long long)b * a.max_iter + a.ictl[b * 8]] = acf;
         if (a.out) {
             double* o = a.out + b * 8;
-            o[0] = n == 1 ? 0.0 : acf;
+            o[0] = acf;
             o[1] = l2;
             o[2] = ln;
             o[3] = (l2 < 1.0 - 1e-8) ? 1.0 : 0.0;
-            o[4] = s_k;
-            o[5] = s_stop;
+            o[4] = steps;
+            o[5] = converged;
         }
     }
 }
 
+size_t slem_smem_bytes(int n, int kmax, bool basis_in_smem) {
+    kmax = std::max(1, std::min(kmax, n - 1));
+    size_t bytes = (2 * (size_t)n + 8 * (size_t)kmax) * sizeof(double) + (3 * (size_t)n + 2) * sizeof(int);
+    if (basis_in_smem) bytes = ((bytes + 15) & ~(size_t)15) + (size_t)kmax * (n | 1) * sizeof(double);
+    return bytes;
+}
+
 void launch_slem(const SlemArgs& a, int B, cudaStream_t st) {
     const int n = a.n;
-    const size_t smem = (3 * (size_t)n + 6 * kMaxK) * sizeof(double) + (3 * (size_t)n + 2) * sizeof(int);
-    slem_kernel<<<B, kThreads, smem, st>>>(a);
+    const size_t smem = slem_smem_bytes(n, a.kmax, a.basis == nullptr);
+    // one thread per node up to 512; small graphs use fewer warps (cheaper barriers)
+    const int threads = std::min(kThreads, std::max(128, ((n + 31) / 32) * 32));
+    slem_kernel<<<B, threads, smem, st>>>(a);
     TPB_CHECK_LAUNCH();
 }
 
@@ -291,35 +404,32 @@ void launch_slem(const SlemArgs& a, int B, cudaStream_t st) {
 __global__ void __launch_bounds__(kThreads) slem_dense_kernel(const double* W, int n, double* basis,
                                                              double* out, int deflate) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int kmax = deflate ? max(1, n - 1) : n;
     extern __shared__ double sh[];
     double* q = sh;
-    double* w = sh + n;
-    double* al = sh + 2 * n;
-    double* be = al + kMaxK;
-    double* cf = be + kMaxK;
+    double* w = q + n;
+    double* al = w + n;
+    double* be = al + kmax;
+    double* cf = be + kmax;
     __shared__ double scratch[32];
     __shared__ int s_stop;
-    double s = 0.0;
-    for (int v = tid; v < n; v += kThreads) {
-        q[v] = hash_unit(v) + (deflate ? 0.0 : 1.0);
-        s += q[v];
+    for (int v = tid; v < n; v += kThreads) q[v] = hash_unit(v) + (deflate ? 0.0 : 1.0);
+    __syncthreads();
+    if (deflate) {
+        deflate_normalize(q, n, scratch);
+    } else {
+        double nn = 0.0;
+        for (int v = tid; v < n; v += kThreads) nn += q[v] * q[v];
+        nn = block_sum(nn, scratch);
+        for (int v = tid; v < n; v += kThreads) q[v] /= sqrt(nn);
+        __syncthreads();
     }
-    s = block_sum(s, scratch);
-    double nn0 = 0.0;
-    for (int v = tid; v < n; v += kThreads) {
-        if (deflate) q[v] -= s / n;
-        nn0 += q[v] * q[v];
-    }
-    nn0 = block_sum(nn0, scratch);
-    for (int v = tid; v < n; v += kThreads) q[v] /= sqrt(nn0);
     if (tid == 0) s_stop = 0;
     __syncthreads();
-    const int kmax = min(deflate ? n - 1 : n, kMaxK);
     int kk = 0;
     for (int k = 0; k < kmax; ++k) {
         for (int v = tid; v < n; v += kThreads) basis[(long long)k * n + v] = q[v];
-        // w = W q (row-major; one warp per row)
-        for (int r = wid; r < n; r += kThreads / 32) {
+        for (int r = wid; r < n; r += kThreads / 32) {  // w = W q, one warp per row
             double acc = 0.0;
             for (int c = lane; c < n; c += 32) acc += W[(long long)r * n + c] * q[c];
             acc = warp_sum(acc);
@@ -344,7 +454,7 @@ __global__ void __launch_bounds__(kThreads) slem_dense_kernel(const double* W, i
             }
             __syncthreads();
         }
-        if (deflate) {  // last, see slem_kernel
+        if (deflate) {  // last, so reorthogonalisation round-off is not amplified
             double sm = 0.0;
             for (int v = tid; v < n; v += kThreads) sm += w[v];
             sm = block_sum(sm, scratch);
@@ -366,15 +476,9 @@ __global__ void __launch_bounds__(kThreads) slem_dense_kernel(const double* W, i
         for (int v = tid; v < n; v += kThreads) q[v] = w[v] / beta;
         __syncthreads();
     }
-    if (tid < 32) {
-        double lo = 1e300, hi = -1e300;
-        for (int i = 0; i < kk; ++i) {
-            const double r = (i > 0 ? fabs(be[i - 1]) : 0.0) + (i < kk - 1 ? fabs(be[i]) : 0.0);
-            lo = fmin(lo, al[i] - r);
-            hi = fmax(hi, al[i] + r);
-        }
-        lo -= 1e-12 * fmax(1.0, fabs(lo));
-        hi += 1e-12 * fmax(1.0, fabs(hi));
+    if (wid == 0) {
+        double lo, hi;
+        gershgorin(al, be, kk, lo, hi);
         const double lmin = tri_eig(al, be, kk, 0, lo, hi);
         double l2;
         if (deflate) {
@@ -386,7 +490,7 @@ __global__ void __launch_bounds__(kThreads) slem_dense_kernel(const double* W, i
             l2 = kk >= 2 ? tri_eig(al, be, kk, kk - 2, lo, hi) : lmin;
         }
         const double lminall = deflate ? fmin(lmin, 1.0) : lmin;
-        if (tid == 0) {
+        if (lane == 0) {
             out[0] = n == 1 ? 0.0 : fmax(fabs(l2), fabs(lminall));
             out[1] = n == 1 ? 0.0 : l2;
             out[2] = lminall;
@@ -396,7 +500,8 @@ __global__ void __launch_bounds__(kThreads) slem_dense_kernel(const double* W, i
 }
 
 void launch_slem_dense(const double* w, int n, double* basis, double* out, int deflate, cudaStream_t st) {
-    const size_t smem = (2 * (size_t)n + 3 * kMaxK) * sizeof(double);
+    const int kmax = deflate ? std::max(1, n - 1) : n;
+    const size_t smem = (2 * (size_t)n + 3 * (size_t)kmax) * sizeof(double);
     slem_dense_kernel<<<1, kThreads, smem, st>>>(w, n, basis, out, deflate);
     TPB_CHECK_LAUNCH();
 }

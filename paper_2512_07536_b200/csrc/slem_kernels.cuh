@@ -19,9 +19,15 @@ struct SlemArgs {
     int* e_j;
     double* e_w;
     int* col_idx;          // list_cap
-    double* basis;         // kmax x n (full reorthogonalisation), or null
-    int kmax;
-    double tol;
+    double* basis;         // kmax x n per solve in global memory, or null: shared memory
+    int kmax;              // Krylov dimension per cycle (<= n-1); >= n-1: exact mode
+    int max_restarts;      // explicit restarts from the extreme Ritz vectors
+    int min_steps;         // restarted mode: matvecs before the first residual test
+    double noise;          // warm start: weight of the fixed random component
+    double tol;            // residual tolerance relative to the spectral scale
+    // optional warm start: ritz[b*2n ..] = previous (v_min, v_max); ritz_ok[b]
+    double* ritz;
+    int* ritz_ok;
     // outputs: out[b*8 + {0:acf, 1:lambda2, 2:lambda_n, 3:connected, 4:steps, 5:converged}]
     double* out;
     // trace mode: acf -> tr_acf[b*max_iter + ictl[b*8]] ; skipped when done
@@ -31,6 +37,8 @@ struct SlemArgs {
 };
 
 void launch_slem(const SlemArgs& a, int B, cudaStream_t st);
+// dynamic shared memory of launch_slem (basis_in_smem: a.basis == null)
+size_t slem_smem_bytes(int n, int kmax, bool basis_in_smem);
 
 // Dense symmetric W (row-major n x n), full spectrum Lanczos with full
 // reorthogonalisation; out[0..4) = {acf, lambda2, lambda_n, connected}.

@@ -164,14 +164,20 @@ void Solver::alloc() {
     e_j_ = dalloc<int>(allocs_, (size_t)B * list_cap_);
     col_idx_ = dalloc<int>(allocs_, (size_t)B * list_cap_);
     e_w_ = dalloc<double>(allocs_, (size_t)B * list_cap_);
-    if (n <= 256) {
-        trace_kmax_ = n - 1;
-        basis_ = dalloc<double>(allocs_, (size_t)B * std::max(1, n - 1) * n);
-    } else {
-        trace_kmax_ = std::min(2048, 2 * n);
-        basis_ = nullptr;
+    // trace Lanczos: exact for n <= 97, else restarted and warm-started from
+    // the previous Ritz vectors; basis in shared memory when it fits
+    trace_kmax_ = std::max(1, std::min(n - 1, 96));
+    {
+        int dev = 0, optin = 0;
+        TPB_CUDA(cudaGetDevice(&dev));
+        TPB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        if (slem_smem_bytes(n, trace_kmax_, true) + 2048 <= (size_t)optin) basis_ = nullptr;
+        else basis_ = dalloc<double>(allocs_, (size_t)B * trace_kmax_ * n);
     }
-    basis_final_ = dalloc<double>(allocs_, (size_t)B * std::max(1, n - 1) * n);
+    ritz_ = dalloc<double>(allocs_, (size_t)B * 2 * n);
+    ritz_ok_ = dalloc<int>(allocs_, B);
+    const int kfin = n - 1 <= kFinalExactDim ? std::max(1, n - 1) : kFinalKrylov;
+    basis_final_ = dalloc<double>(allocs_, (size_t)B * kfin * n);
     slem_out_ = dalloc<double>(allocs_, (size_t)B * 8);
     tmp_m_ = dalloc<double>(allocs_, (size_t)B * m);
     tmp_m2_ = dalloc<double>(allocs_, (size_t)B * m);
@@ -195,6 +201,7 @@ void Solver::start() {
     TPB_CUDA(cudaMemsetAsync(d_.X, 0, B * nx * sizeof(double), s0_));
     TPB_CUDA(cudaMemsetAsync(d_.D, 0, B * nx * sizeof(double), s0_));
     TPB_CUDA(cudaMemsetAsync(d_.ictl, 0, (size_t)B * 8 * sizeof(int), s0_));
+    TPB_CUDA(cudaMemsetAsync(ritz_ok_, 0, (size_t)B * sizeof(int), s0_));
     if (het_) TPB_CUDA(cudaMemsetAsync(d_.bestScore, 0, (size_t)B * lo_.m * sizeof(double), s0_));
     {
         std::vector<double> sc((size_t)B * 8, 0.0);
@@ -235,9 +242,13 @@ void Solver::final_slem(const double* packed, const int* list, const int* count,
     a.e_j = e_j_;
     a.e_w = e_w_;
     a.col_idx = col_idx_;
+    // exact (complete Krylov space) up to n = 257, restarted beyond
+    const int n = lo_.n;
     a.basis = basis_final_;
-    a.kmax = std::max(1, lo_.n - 1);
-    a.tol = 1e-14;
+    a.kmax = n - 1 <= kFinalExactDim ? std::max(1, n - 1) : kFinalKrylov;
+    a.max_restarts = 200;
+    a.min_steps = 64;
+    a.tol = 1e-10;
     a.out = out;
     a.tr_acf = nullptr;
     a.ictl = nullptr;
@@ -278,8 +289,13 @@ void Solver::enqueue_slem_trace(cudaStream_t st) {
     a.e_j = e_j_;
     a.e_w = e_w_;
     a.col_idx = col_idx_;
-    a.basis = basis_;
+    a.basis = basis_;  // null: Krylov basis in shared memory
     a.kmax = trace_kmax_;
+    a.max_restarts = 40;
+    a.min_steps = 8;
+    a.noise = 0.0;
+    a.ritz = ritz_;
+    a.ritz_ok = ritz_ok_;
     a.tol = cfg_.slem_tol;
     a.out = nullptr;
     a.tr_acf = d_.tr_acf;
@@ -628,6 +644,49 @@ void Solver::xstep_only(bool update_duals) {
     TPB_CUDA(cudaStreamSynchronize(s0_));
     TPB_CUDA(cudaMemsetAsync(d_.ictl, 0, (size_t)B_ * 8 * sizeof(int), s0_));
     TPB_CUDA(cudaStreamSynchronize(s0_));
+}
+
+int Solver::launches_per_iteration() const {
+    const int cone = small_ ? 1 : sch_.gemms();
+    return 1 + (small_ ? 0 : 1) + 1 + 1 + cone + 4 + 2;
+}
+
+int Solver::bench_phase(int phase, int reps) {
+    int per = 0;
+    for (int k = 0; k < reps; ++k) {
+        switch (phase) {
+            case 0:
+                enqueue_projection();
+                per = small_ ? 1 : sch_.gemms();
+                break;
+            case 1: {
+                Dev d = d_;
+                d.upd_duals = 0;
+                d.track_best = 0;
+                launch_xstep_a(d, c_, s0_);
+                launch_xstep_node(d, c_, s0_);
+                launch_xstep_b(d, c_, s0_);
+                launch_xstep_diag(d, c_, s0_);
+                per = 4;
+                break;
+            }
+            case 2:
+                enqueue_select(s0_);
+                per = 1;
+                break;
+            case 3:
+                enqueue_slem_trace(s0_);
+                per = 1;
+                break;
+            case 4:
+                launch_prep(d_, c_, s0_);
+                per = 1;
+                break;
+            default:
+                throw Error(kInvalidArgument, "bench_phase: unknown phase");
+        }
+    }
+    return per;
 }
 
 }  // namespace tpb

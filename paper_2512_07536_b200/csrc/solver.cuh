@@ -20,11 +20,16 @@ struct Config {
     double weight_floor = 1e-6;
     double linear_tol = 1e-10;  // accepted for API parity; the x-step is exact
     int trace_stride = 1;       // acf_iterate every k-th iteration (reference: 1)
-    double slem_tol = 1e-12;    // Lanczos residual tolerance (relative)
+    double slem_tol = 1e-7;     // trace Lanczos residual tolerance (eigenvalue error <= tol^2/gap)
     int chunk = 0;              // iterations per CUDA graph (0: auto)
 };
 
 void validate(const Config& c);
+
+// One-off spectral reports (feasible start, final topology): complete Krylov
+// space up to this dimension, restarted Lanczos with this basis beyond.
+constexpr int kFinalExactDim = 256;
+constexpr int kFinalKrylov = 128;
 
 struct SolveResult {
     int iterations = 0;
@@ -72,6 +77,12 @@ class Solver {
     void project_only();             // Y <- project_Y(X, D)
     void xstep_only(bool update_duals);  // X <- update_X(Y, D) [, D += rho (X - Y)]
     const double* node_dev() const { return d_.node; }
+    // Enqueue `reps` repetitions of one phase of the iteration on the main
+    // stream (for live per-kernel timing): 0 projection (cone GEMMs),
+    // 1 x-step, 2 top-r selection, 3 trace SLEM, 4 prep. Returns the number
+    // of kernel launches per repetition.
+    int bench_phase(int phase, int reps);
+    int launches_per_iteration() const;
 
    private:
     void alloc();
@@ -105,8 +116,10 @@ class Solver {
     int *list_ = nullptr, *list_count_ = nullptr;
     int *e_i_ = nullptr, *e_j_ = nullptr, *col_idx_ = nullptr;
     double* e_w_ = nullptr;
-    double* basis_ = nullptr;        // trace Lanczos (full reorth when n small)
+    double* basis_ = nullptr;        // trace Lanczos basis (B x kmax x n)
     int trace_kmax_ = 0;
+    double* ritz_ = nullptr;         // B x 2n extreme Ritz vectors (warm start)
+    int* ritz_ok_ = nullptr;
     double* basis_final_ = nullptr;  // final report
     double* slem_out_ = nullptr;     // B x 8
     double* tmp_m_ = nullptr;        // B x m

@@ -480,6 +480,16 @@ class BatchSolver:
         _check(_lib.load().tp_solver_state(self.h, C.byref(x), C.byref(y), C.byref(d)))
         return x.value, y.value, d.value
 
+    def bench_phase(self, phase: int, reps: int) -> int:
+        per = C.c_int32(0)
+        _check(_lib.load().tp_solver_bench_phase(self.h, phase, reps, C.byref(per)))
+        return per.value
+
+    def launches_per_iteration(self) -> int:
+        out = C.c_int32(0)
+        _check(_lib.load().tp_solver_launches_per_iteration(self.h, C.byref(out)))
+        return out.value
+
     def result(self, b: int) -> Solution:
         m = self.n * (self.n - 1) // 2
         res = tp_result()

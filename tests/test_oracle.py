@@ -1,0 +1,142 @@
+"""CPU: the numpy oracle (oracle/topoopt_oracle.py) pinned against the
+reference's golden fixtures (tests/golden/, generated from the compiled
+reference by tests/golden/make_golden.py) and, when oracle/_ref is built,
+against the reference itself."""
+import numpy as np
+import pytest
+
+from conftest import rel
+
+
+def test_layout_dimensions(O):
+    # proj/tests/test_admm.cpp:15-34 and test_admm_het.cpp:80-108
+    lo = O.hom_layout(2)
+    assert (lo.m, lo.nx, lo.neq) == (1, 12, 10)
+    lo = O.hom_layout(16)
+    assert (lo.m, lo.nx, lo.neq) == (120, 649, 528)
+    assert O.hom_layout(4).nx + O.hom_layout(4).neq == 43 + 36
+    het = O.het_layout(3, 3)
+    assert (het.nx, het.neq) == (31, 27)
+    pd = O.assemble_het_node([2, 2, 2])
+    assert list(pd.beq[21:24]) == [2.0, 2.0, 2.0] and list(pd.beq[24:27]) == [0.0, 0.0, 0.0]
+    with pytest.raises(ValueError):
+        O.assemble(4, 0)
+    with pytest.raises(ValueError):
+        O.assemble(4, 7)
+
+
+def test_edge_index_roundtrip(O):
+    for n in (2, 3, 7, 64):
+        e = O.enumerate_edges(n)
+        for l, (i, j) in enumerate(e):
+            assert O.edge_index(n, i, j) == l == O.edge_index(n, j, i)
+
+
+def test_allocation_bit_exact_vs_reference(O, golden):
+    for c in golden("allocation.json"):
+        if c["status"] == 0:
+            bu, e = O.allocate_edge_capacity(c["b"], c["r"], c["caps"])
+            assert bu == c["b_unit"]  # bitwise
+            assert e.tolist() == c["e"]
+        elif c["status"] == 2:
+            with pytest.raises(O.InfeasibleError):
+                O.allocate_edge_capacity(c["b"], c["r"], c["caps"])
+        else:
+            with pytest.raises(ValueError):
+                O.allocate_edge_capacity(c["b"], c["r"], c["caps"])
+
+
+def test_two_tier_allocation_goldens(O):
+    # proj/tests/test_bandwidth.cpp:38-52
+    b = [9.76] * 8 + [3.25] * 8
+    bu, e = O.allocate_edge_capacity(b, 16)
+    assert bu == pytest.approx(3.25) and e.tolist() == [3] * 8 + [1] * 8
+    bu, e = O.allocate_edge_capacity(b, 32)
+    assert bu == pytest.approx(1.625) and e.tolist() == [6] * 8 + [2] * 8
+
+
+def test_substeps_vs_reference(O, golden):
+    for c in golden("substeps.json"):
+        if c["kind"] == "hom":
+            pd = O.assemble(c["n"], c["r"], 2.0, 1.0)
+            y = O.project_Y(pd, np.array(c["x"]), np.array(c["d"]))
+        else:
+            pd = O.assemble_het_node(c["degrees"], 2.0, 1.0)
+            y = O.project_Y_het(pd, np.array(c["x"]), np.array(c["d"]))
+        assert np.max(np.abs(y - np.array(c["y"]))) < 1e-12
+        x, kkt = O.update_X(pd, np.array(c["y"]), np.array(c["d"]))
+        # the reference solves to 1e-13 relative with BiCGSTAB; same system
+        assert np.max(np.abs(x - np.array(c["xstep"]))) < 1e-9
+
+
+def test_spectral_vs_reference(O, golden):
+    for c in golden("spectral.json"):
+        W = O.gossip_matrix(c["n"], c["edges"], c["weights"])
+        rep = O.spectral_report(W)
+        assert rep["acf"] == pytest.approx(c["acf"], rel=1e-12, abs=1e-14)
+        assert rep["lambda2"] == pytest.approx(c["lambda2"], rel=1e-12, abs=1e-14)
+        assert rep["connected"] == c["connected"]
+
+
+def test_exponential_closed_form(O):
+    # proj/tests/test_topology.cpp:305-314: exponential graph ACF (m-1)/(m+1)
+    e, w = O.generate_benchmark("exponential", 256)
+    rep = O.spectral_report(O.gossip_matrix(256, e, w))
+    assert rep["acf"] == pytest.approx(7.0 / 9.0, abs=1e-12)
+
+
+def test_config1_full_solve_vs_reference(O, golden):
+    g = golden("config1.json")
+    s = O.solve(16, 32, g["warm"], **g["cfg"])
+    ref = g["solution"]
+    assert s.iterations == ref["iterations"] and s.converged
+    assert s.edges.tolist() == ref["edges"]
+    assert rel(s.weights, ref["weights"]) < 1e-6
+    assert s.acf == pytest.approx(ref["acf"], rel=1e-9)
+    tr = np.array(ref["trace"])
+    assert np.max(np.abs(s.trace[:, 3] - tr[:, 3])) < 1e-6
+
+
+def test_small_solves_vs_reference(O, golden):
+    for c in golden("small_solves.json"):
+        ref = c["solution"]
+        if c["kind"] == "hom":
+            s = O.solve(c["n"], c["r"], c["warm"], **c["cfg"])
+        else:
+            s = O.solve_het_node(c["degrees"], c["warm"], **c["cfg"])
+        assert s.iterations == ref["iterations"], c
+        assert s.converged == ref["converged"]
+        assert s.edges.tolist() == ref["edges"]
+        assert np.max(np.abs(s.weights - np.array(ref["weights"]))) < 1e-6
+        assert s.acf == pytest.approx(ref["acf"], rel=1e-6, abs=1e-9)
+
+
+@pytest.mark.slow
+def test_config2_het_vs_reference(O, golden):
+    import os
+    from conftest import GOLDEN
+    if not os.path.exists(os.path.join(GOLDEN, "config2.json")):
+        pytest.skip("config2 fixture not generated")
+    g = golden("config2.json")
+    s = O.solve_het_node(g["degrees"], g["warm"], **g["cfg"])
+    ref = g["solution"]
+    assert s.iterations == ref["iterations"]
+    assert s.edges.tolist() == ref["edges"]
+    assert s.acf == pytest.approx(ref["acf"], rel=1e-6)
+
+
+def test_oracle_against_live_reference():
+    from oracle import ref, topoopt_oracle as O
+    if not ref.available():
+        pytest.skip("oracle/_ref not built (run make -C oracle)")
+    rng = np.random.default_rng(7)
+    for n, r in [(5, 4), (7, 9), (10, 20)]:
+        p = ref.Problem(n, r, 2.0, 3.0)
+        pd = O.assemble(n, r, 2.0, 3.0)
+        x = rng.standard_normal(p.nx)
+        d = rng.standard_normal(p.nx)
+        assert np.max(np.abs(p.project_Y(x, d) - O.project_Y(pd, x, d))) < 1e-12
+        assert np.array_equal(p.beq, pd.beq)
+        fs = p.feasible_start(ref.default_warm_start(n, r, 1))
+        fo = O.feasible_start(pd.lo, ref.default_warm_start(n, r, 1), 2.0)
+        assert np.max(np.abs(fs - fo)) < 1e-12
