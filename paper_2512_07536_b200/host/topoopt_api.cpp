@@ -1,0 +1,653 @@
+// Reference-compatible C++ API (include/topoopt/topoopt_b200.hpp) over the C
+// ABI (include/topoopt_b200.h). Host value types and formatting live here; the
+// numerical work of every hot-path call runs on the GPU behind the ABI.
+#include "topoopt/topoopt_b200.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <numeric>
+#include <set>
+
+#include "topoopt_b200.h"
+
+namespace topoopt {
+
+namespace {
+
+// ABI status -> the reference's exception taxonomy
+void raise(int status) {
+    if (status == TP_OK) return;
+    const std::string msg = tp_last_error_message();
+    switch (status) {
+        case TP_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+        case TP_ERR_INFEASIBLE: throw InfeasibleError(msg);
+        case TP_ERR_LINEAR_SOLVE: throw LinearSolveError(msg);
+        case TP_ERR_DEGENERATE: throw DegenerateSolutionError(msg);
+        case TP_ERR_PIVOT: throw PivotError(msg, -1);
+        default: throw std::runtime_error(msg);
+    }
+}
+
+tp_config to_c(const SolverConfig& c) {
+    tp_config k;
+    tp_config_default(&k);
+    k.rho = c.rho;
+    k.epsilon = c.epsilon;
+    k.max_iter = c.max_iter;
+    k.alpha = c.alpha;
+    k.weight_floor = c.weight_floor;
+    k.seed = c.seed;
+    k.linear_tol = c.linear_tol;
+    return k;
+}
+
+std::vector<int32_t> flat_edges(const Topology& t) {
+    std::vector<int32_t> e;
+    e.reserve(2 * t.edges.size());
+    for (const auto& p : t.edges) {
+        e.push_back(p.first);
+        e.push_back(p.second);
+    }
+    return e;
+}
+
+Topology from_flat(int n, const int32_t* e, const double* w, int k) {
+    Topology t;
+    t.n = n;
+    for (int i = 0; i < k; ++i) {
+        t.edges.push_back({e[2 * i], e[2 * i + 1]});
+        t.weights.push_back(w ? w[i] : 0.0);
+    }
+    return t;
+}
+
+Solution collect(int n, const tp_result& res, const std::vector<int32_t>& edges,
+                 const std::vector<double>& weights, const std::vector<double>& trace,
+                 const char* note) {
+    Solution sol;
+    sol.topology = from_flat(n, edges.data(), weights.data(), res.n_edges);
+    sol.topology.validate();
+    sol.w = gossip_matrix(sol.topology);
+    sol.lambda_tilde = res.lambda_tilde;
+    sol.acf_value = res.acf;
+    sol.converged = res.converged != 0;
+    sol.connected = res.connected != 0;
+    sol.repaired = res.repaired != 0;
+    sol.residual = res.residual;
+    sol.iterations = res.iterations;
+    sol.note = note;
+    sol.trace.resize(res.iterations);
+    for (int k = 0; k < res.iterations; ++k)
+        sol.trace[k] = {k + 1, trace[3 * k], trace[3 * k + 1], trace[3 * k + 2]};
+    return sol;
+}
+
+// node-level system: equality rows, row i = pairs incident to node i
+bool node_level_degrees(const CapacitySystem& sys, std::vector<int32_t>& degrees) {
+    if (!sys.equality || (int)sys.rows.size() != sys.n) return false;
+    const auto pairs = enumerate_edges(sys.n);
+    for (int i = 0; i < sys.n; ++i) {
+        std::vector<int> want;
+        for (int c = 0; c < (int)pairs.size(); ++c)
+            if (pairs[c].first == i || pairs[c].second == i) want.push_back(c);
+        std::vector<int> have = sys.rows[i].edge_cols;
+        std::sort(have.begin(), have.end());
+        if (have != want) return false;
+    }
+    for (char a : sys.allowed)
+        if (!a) return false;
+    degrees.resize(sys.n);
+    for (int i = 0; i < sys.n; ++i) degrees[i] = sys.rows[i].capacity;
+    return true;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ dense
+Matrix Matrix::identity(int n) {
+    Matrix m(n, n, 0.0);
+    for (int i = 0; i < n; ++i) m(i, i) = 1.0;
+    return m;
+}
+
+Matrix matmul(const Matrix& a, const Matrix& b) {
+    if (a.cols() != b.rows()) throw std::invalid_argument("matmul: shape mismatch");
+    Matrix c(a.rows(), b.cols(), 0.0);
+    for (int i = 0; i < a.rows(); ++i)
+        for (int k = 0; k < a.cols(); ++k) {
+            const double x = a(i, k);
+            for (int j = 0; j < b.cols(); ++j) c(i, j) += x * b(k, j);
+        }
+    return c;
+}
+
+Matrix transpose(const Matrix& a) {
+    Matrix t(a.cols(), a.rows());
+    for (int i = 0; i < a.rows(); ++i)
+        for (int j = 0; j < a.cols(); ++j) t(j, i) = a(i, j);
+    return t;
+}
+
+double max_abs_diff(const Matrix& a, const Matrix& b) {
+    if (a.rows() != b.rows() || a.cols() != b.cols())
+        throw std::invalid_argument("max_abs_diff: shape mismatch");
+    double m = 0.0;
+    for (size_t k = 0; k < a.data().size(); ++k) m = std::max(m, std::abs(a.data()[k] - b.data()[k]));
+    return m;
+}
+
+double frobenius_norm(const Matrix& a) {
+    double s = 0.0;
+    for (double v : a.data()) s += v * v;
+    return std::sqrt(s);
+}
+
+bool is_symmetric(const Matrix& a, double tol) {
+    if (a.rows() != a.cols()) return false;
+    for (int i = 0; i < a.rows(); ++i)
+        for (int j = i + 1; j < a.cols(); ++j)
+            if (std::abs(a(i, j) - a(j, i)) > tol) return false;
+    return true;
+}
+
+Matrix symmetrize(const Matrix& a) {
+    Matrix s(a.rows(), a.cols());
+    for (int i = 0; i < a.rows(); ++i)
+        for (int j = 0; j < a.cols(); ++j) s(i, j) = 0.5 * (a(i, j) + a(j, i));
+    return s;
+}
+
+double dot(const Vec& a, const Vec& b) {
+    double s = 0.0;
+    for (size_t k = 0; k < a.size(); ++k) s += a[k] * b[k];
+    return s;
+}
+
+double norm2(const Vec& a) { return std::sqrt(dot(a, a)); }
+
+void axpy(double alpha, const Vec& x, Vec& y) {
+    for (size_t k = 0; k < x.size(); ++k) y[k] += alpha * x[k];
+}
+
+// ------------------------------------------------------------------ topology
+void Topology::validate() const {
+    if (n < 1) throw std::invalid_argument("topology: n must be positive");
+    if (weights.size() != edges.size())
+        throw std::invalid_argument("topology: weights length differs from edge count");
+    for (size_t k = 0; k < edges.size(); ++k) {
+        const int i = edges[k].first, j = edges[k].second;
+        if (i < 0 || j < 0 || i >= n || j >= n)
+            throw std::invalid_argument("topology: edge endpoint out of range");
+        if (i >= j) throw std::invalid_argument("topology: edge endpoints must satisfy i < j");
+        if (k > 0 && !(edges[k - 1] < edges[k]))
+            throw std::invalid_argument("topology: edges must be sorted without duplicates");
+        if (!(weights[k] >= 0.0)) throw std::invalid_argument("topology: negative or NaN weight");
+    }
+}
+
+void Topology::normalize_and_validate() {
+    if (weights.size() != edges.size())
+        throw std::invalid_argument("topology: weights length differs from edge count");
+    std::vector<size_t> ord(edges.size());
+    std::iota(ord.begin(), ord.end(), 0);
+    std::sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return edges[a] < edges[b]; });
+    std::vector<Edge> e2;
+    std::vector<double> w2;
+    for (size_t k : ord) {
+        e2.push_back(edges[k]);
+        w2.push_back(weights[k]);
+    }
+    edges.swap(e2);
+    weights.swap(w2);
+    validate();
+}
+
+std::vector<int> Topology::degrees() const {
+    std::vector<int> d(n, 0);
+    for (const auto& e : edges) {
+        ++d[e.first];
+        ++d[e.second];
+    }
+    return d;
+}
+
+bool Topology::has_uniform_weights(double tol) const {
+    for (double w : weights)
+        if (std::abs(w - weights.front()) > tol) return false;
+    return true;
+}
+
+std::vector<Edge> enumerate_edges(int n) {
+    if (n < 2) throw std::invalid_argument("enumerate_edges: need at least two nodes");
+    std::vector<Edge> out;
+    out.reserve(static_cast<size_t>(n) * (n - 1) / 2);
+    for (int i = 0; i + 1 < n; ++i)
+        for (int j = i + 1; j < n; ++j) out.push_back({i, j});
+    return out;
+}
+
+int edge_index(int n, int i, int j) {
+    if (i == j) throw std::invalid_argument("edge_index: self loop");
+    if (i > j) std::swap(i, j);
+    if (i < 0 || j >= n) throw std::invalid_argument("edge_index: endpoint out of range");
+    return i * n - i * (i + 1) / 2 + (j - i - 1);
+}
+
+Matrix laplacian(const Topology& t) {
+    t.validate();
+    Matrix l(t.n, t.n, 0.0);
+    for (size_t k = 0; k < t.edges.size(); ++k) {
+        const int i = t.edges[k].first, j = t.edges[k].second;
+        const double w = t.weights[k];
+        l(i, i) += w;
+        l(j, j) += w;
+        l(i, j) -= w;
+        l(j, i) -= w;
+    }
+    return l;
+}
+
+Matrix gossip_matrix(const Topology& t) {
+    Matrix l = laplacian(t);
+    for (int i = 0; i < t.n; ++i)
+        if (l(i, i) > 1.0 + 1e-12)
+            throw std::invalid_argument("gossip_matrix: weighted degree " + std::to_string(l(i, i)) +
+                                        " at node " + std::to_string(i) + " exceeds 1");
+    Matrix w = Matrix::identity(t.n);
+    for (size_t k = 0; k < w.data().size(); ++k) w.data()[k] -= l.data()[k];
+    return w;
+}
+
+SpectralReport spectral_report(const Matrix& w) {
+    if (w.rows() != w.cols()) throw std::invalid_argument("spectral_report: matrix not square");
+    double out[4];
+    raise(tp_spectral_report(w.rows(), w.data().data(), out));
+    return SpectralReport{out[0], out[1], out[2], out[3] != 0.0};
+}
+
+double acf(const Matrix& w) { return spectral_report(w).acf; }
+
+void validate_gossip(const Matrix& w) {
+    const int n = w.rows();
+    if (n < 1 || w.cols() != n) throw std::invalid_argument("gossip matrix must be square");
+    for (int i = 0; i < n; ++i) {
+        double s = 0.0;
+        for (int j = 0; j < n; ++j) {
+            if (std::abs(w(i, j) - w(j, i)) > 1e-8)
+                throw std::invalid_argument("gossip matrix asymmetric beyond 1e-8");
+            if (w(i, j) < -1e-8) throw std::invalid_argument("gossip matrix has an entry below -1e-8");
+            s += w(i, j);
+        }
+        if (std::abs(s - 1.0) > 1e-8)
+            throw std::invalid_argument("gossip matrix row " + std::to_string(i) + " does not sum to 1");
+    }
+}
+
+BenchmarkKind benchmark_kind_from_string(const std::string& name) {
+    if (name == "ring") return BenchmarkKind::ring;
+    if (name == "grid2d") return BenchmarkKind::grid2d;
+    if (name == "torus2d") return BenchmarkKind::torus2d;
+    if (name == "exponential") return BenchmarkKind::exponential;
+    throw std::invalid_argument("unknown benchmark kind: " + name);
+}
+
+Topology generate_benchmark(BenchmarkKind kind, int n) {
+    // baselines of proj/src/topology.cpp:227-281 (uniform 1/(d_max+1), or
+    // 1/(2 (hops+1)) for the exponential graph)
+    if (n < 2) throw std::invalid_argument("generate_benchmark: need at least two nodes");
+    std::set<Edge> es;
+    auto add = [&](int a, int b) {
+        if (a != b) es.insert({std::min(a, b), std::max(a, b)});
+    };
+    double weight = 0.0;
+    if (kind == BenchmarkKind::ring) {
+        if (n < 3) throw std::invalid_argument("generate_benchmark: ring needs n >= 3");
+        for (int i = 0; i < n; ++i) add(i, (i + 1) % n);
+        weight = 1.0 / 3.0;
+    } else if (kind == BenchmarkKind::exponential) {
+        int hops = 0;
+        for (int h = 1; h <= n - 1; h *= 2, ++hops)
+            for (int i = 0; i < n; ++i) add(i, (i + h) % n);
+        weight = 1.0 / (2.0 * (hops + 1));
+    } else {
+        const int s = (int)std::lround(std::sqrt((double)n));
+        if (s * s != n || s < 2)
+            throw std::invalid_argument("generate_benchmark: grid/torus needs a perfect square n >= 4");
+        const bool torus = kind == BenchmarkKind::torus2d;
+        for (int r = 0; r < s; ++r)
+            for (int c = 0; c < s; ++c) {
+                const int u = r * s + c;
+                if (torus) {
+                    add(u, r * s + (c + 1) % s);
+                    add(u, ((r + 1) % s) * s + c);
+                } else {
+                    if (c + 1 < s) add(u, u + 1);
+                    if (r + 1 < s) add(u, u + s);
+                }
+            }
+        weight = 1.0 / ((s >= 3 ? 4 : 2) + 1);
+    }
+    Topology t;
+    t.n = n;
+    t.edges.assign(es.begin(), es.end());
+    t.weights.assign(t.edges.size(), weight);
+    t.normalize_and_validate();
+    return t;
+}
+
+// ------------------------------------------------------------------ eig
+static Matrix cone(const Matrix& s, bool psd) {
+    if (s.rows() != s.cols()) throw std::invalid_argument("sym_eig: matrix not square");
+    Matrix out(s.rows(), s.cols());
+    raise(psd ? tp_project_psd(s.rows(), s.data().data(), out.data().data())
+              : tp_project_nsd(s.rows(), s.data().data(), out.data().data()));
+    return out;
+}
+Matrix project_nsd(const Matrix& s) { return cone(s, false); }
+Matrix project_psd(const Matrix& s) { return cone(s, true); }
+
+// ------------------------------------------------------------------ bandwidth
+Allocation allocate_edge_capacity(const BandwidthProfile& p, int r) {
+    const int n = (int)p.bandwidths.size();
+    if (!p.edge_caps.empty() && (int)p.edge_caps.size() != n)
+        throw std::invalid_argument("allocate_edge_capacity: edge_caps size mismatch");
+    Allocation a;
+    a.edges_per_node.assign(std::max(n, 1), 0);
+    std::vector<int32_t> e(std::max(n, 1));
+    std::vector<int32_t> caps(p.edge_caps.begin(), p.edge_caps.end());
+    raise(tp_allocate(p.bandwidths.data(), caps.empty() ? nullptr : caps.data(), n, r, &a.b_unit,
+                      e.data()));
+    a.edges_per_node.assign(e.begin(), e.begin() + n);
+    return a;
+}
+
+std::vector<int> CapacitySystem::loads(const std::vector<char>& selected) const {
+    if ((int)selected.size() != num_edges)
+        throw std::invalid_argument("CapacitySystem::loads: selection size mismatch");
+    std::vector<int> out(rows.size(), 0);
+    for (size_t k = 0; k < rows.size(); ++k)
+        for (int c : rows[k].edge_cols) out[k] += selected[c] ? 1 : 0;
+    return out;
+}
+
+int CapacitySystem::implied_edge_total() const {
+    long long s = 0;
+    for (const auto& row : rows) s += row.capacity;
+    if (s % 2) throw std::invalid_argument("CapacitySystem: capacity sum is odd, no edge total");
+    return (int)(s / 2);
+}
+
+CapacitySystem node_level_constraints(int n, const std::vector<int>& degrees) {
+    if (n < 2) throw std::invalid_argument("node_level_constraints: need at least 2 nodes");
+    if ((int)degrees.size() != n)
+        throw std::invalid_argument("node_level_constraints: degree list size mismatch");
+    long long sum = 0;
+    for (int i = 0; i < n; ++i) {
+        if (degrees[i] < 0 || degrees[i] > n - 1)
+            throw std::invalid_argument("node_level_constraints: degree of node " + std::to_string(i) +
+                                        " outside [0, n-1]");
+        sum += degrees[i];
+    }
+    if (sum % 2) throw InfeasibleError("degree sum " + std::to_string(sum) + " is odd");
+    CapacitySystem sys;
+    sys.n = n;
+    sys.num_edges = n * (n - 1) / 2;
+    sys.equality = true;
+    sys.allowed.assign(sys.num_edges, 1);
+    sys.rows.resize(n);
+    int col = 0;
+    for (int i = 0; i < n; ++i) {
+        sys.rows[i].label = "node" + std::to_string(i);
+        sys.rows[i].capacity = degrees[i];
+    }
+    for (int i = 0; i + 1 < n; ++i)
+        for (int j = i + 1; j < n; ++j, ++col) {
+            sys.rows[i].edge_cols.push_back(col);
+            sys.rows[j].edge_cols.push_back(col);
+        }
+    for (auto& row : sys.rows) std::sort(row.edge_cols.begin(), row.edge_cols.end());
+    return sys;
+}
+
+// ------------------------------------------------------------------ anneal
+void AnnealConfig::validate() const {
+    if (!(t0 > 0.0)) throw std::invalid_argument("AnnealConfig: t0 must be positive");
+    if (!(cooling > 0.0 && cooling < 1.0))
+        throw std::invalid_argument("AnnealConfig: cooling must lie in (0, 1)");
+    if (steps < 1) throw std::invalid_argument("AnnealConfig: steps must be >= 1");
+    if (moves_per_temp < 0) throw std::invalid_argument("AnnealConfig: moves_per_temp must be >= 0");
+}
+
+Topology anneal_degree_topology(const std::vector<int>& degrees, const AnnealConfig& cfg) {
+    cfg.validate();
+    const int n = (int)degrees.size();
+    long long sum = 0;
+    for (int d : degrees) sum += d;
+    std::vector<int32_t> e(2 * std::max<long long>(sum / 2, 1));
+    int32_t k = 0;
+    std::vector<int32_t> deg(degrees.begin(), degrees.end());
+    raise(tp_anneal_degree(n, deg.data(), cfg.t0, cfg.cooling, cfg.steps, cfg.moves_per_temp, cfg.seed,
+                           e.data(), &k));
+    Topology t = from_flat(n, e.data(), nullptr, k);
+    int dmax = 0;
+    for (int d : t.degrees()) dmax = std::max(dmax, d);
+    t.weights.assign(k, 1.0 / (dmax + 1));
+    t.validate();
+    return t;
+}
+
+Topology anneal_topology(const CapacitySystem& sys, std::optional<int> r, const AnnealConfig& cfg) {
+    std::vector<int32_t> deg;
+    if (!node_level_degrees(sys, deg))
+        throw std::invalid_argument("anneal_topology: only node-level equality systems are supported");
+    if (r && *r != sys.implied_edge_total())
+        throw std::invalid_argument("anneal_topology: r conflicts with the degree sum");
+    return anneal_degree_topology(std::vector<int>(deg.begin(), deg.end()), cfg);
+}
+
+// ------------------------------------------------------------------ admm
+void SolverConfig::validate() const {
+    const tp_config c = to_c(*this);
+    raise(tp_config_validate(&c));
+}
+
+std::string Solution::trace_csv() const {
+    std::string out = "iter,residual,lambda_tilde,acf_iterate\n";
+    char buf[128];
+    for (const auto& row : trace) {
+        std::snprintf(buf, sizeof buf, "%d,%.17g,%.17g,%.17g\n", row.iter, row.residual,
+                      row.lambda_tilde, row.acf_iterate);
+        out += buf;
+    }
+    return out;
+}
+
+ProblemData assemble(int n, int r, double alpha, double rho) {
+    if (n < 2) throw std::invalid_argument("assemble: need at least 2 nodes");
+    const int m = n * (n - 1) / 2;
+    if (r < 1 || r > m) throw std::invalid_argument("assemble: r outside [1, n(n-1)/2]");
+    if (!(alpha > 0.0)) throw std::invalid_argument("assemble: alpha must be positive");
+    if (!(rho > 0.0)) throw std::invalid_argument("assemble: rho must be positive");
+    ProblemData pd;
+    pd.n = n;
+    pd.m = m;
+    pd.r = r;
+    pd.alpha = alpha;
+    pd.rho = rho;
+    pd.lambda_ix = m;
+    pd.off_s = m + 1;
+    pd.off_y = pd.off_s + n * n;
+    pd.off_t = pd.off_y + n;
+    pd.nx = pd.off_t + n * n;
+    pd.neq = 2 * n * n + n;
+    pd.pairs = enumerate_edges(n);
+    pd.beq.assign(n * n, -alpha / n);
+    for (int c = 0; c < n; ++c)
+        for (int rr = 0; rr < n; ++rr) pd.beq.push_back(rr == c ? 2.0 : 0.0);
+    pd.beq.insert(pd.beq.end(), n, 1.0);
+    return pd;
+}
+
+Vec project_Y(const ProblemData& pd, const Vec& x, const Vec& d) {
+    if ((int)x.size() != pd.nx || (int)d.size() != pd.nx)
+        throw std::invalid_argument("project_Y: state length differs from nx");
+    Vec y(pd.nx);
+    raise(tp_project_Y(pd.n, pd.r, pd.alpha, pd.rho, x.data(), d.data(), y.data()));
+    return y;
+}
+
+Vec update_X(const ProblemData& pd, const Vec& y, const Vec& d, Vec& kkt_warm, double) {
+    if ((int)y.size() != pd.nx || (int)d.size() != pd.nx)
+        throw std::invalid_argument("update_X: state length differs from nx");
+    kkt_warm.resize(pd.nx + pd.neq);
+    raise(tp_update_X(pd.n, pd.r, pd.alpha, pd.rho, y.data(), d.data(), kkt_warm.data()));
+    return Vec(kkt_warm.begin(), kkt_warm.begin() + pd.nx);
+}
+
+void update_duals(const ProblemData& pd, const Vec& x, const Vec& y, Vec& d) {
+    raise(tp_update_duals(pd.nx, pd.rho, x.data(), y.data(), d.data()));
+}
+
+Extraction extract_topology(int n, int r, const Vec& g, double weight_floor) {
+    if (n < 2) throw std::invalid_argument("enumerate_edges: need at least two nodes");
+    const int m = n * (n - 1) / 2;
+    if ((int)g.size() < m) throw std::invalid_argument("extract_topology: weight vector shorter than |E|");
+    const int cap = std::max(1, std::min(r, m));
+    std::vector<int32_t> e(2 * cap);
+    std::vector<double> w(cap);
+    int32_t k = 0;
+    raise(tp_extract_topology(n, r, g.data(), weight_floor, e.data(), w.data(), &k));
+    Extraction ex;
+    ex.topology = from_flat(n, e.data(), w.data(), k);
+    ex.topology.validate();
+    ex.w = gossip_matrix(ex.topology);
+    return ex;
+}
+
+Topology default_warm_start(int n, int r, std::uint64_t seed) {
+    std::vector<int32_t> e(2 * std::max(r, 1));
+    int32_t k = 0;
+    raise(tp_default_warm_start(n, r, seed, e.data(), &k));
+    Topology t = from_flat(n, e.data(), nullptr, k);
+    if (k > 0) {
+        int dmax = 0;
+        for (int d : t.degrees()) dmax = std::max(dmax, d);
+        // annealed starts carry 1/(d_max+1); the chain fallback carries 1/3
+        const bool chain = k == r && k < n - 1;
+        t.weights.assign(k, chain ? 1.0 / 3.0 : 1.0 / (dmax + 1));
+    }
+    t.validate();
+    return t;
+}
+
+Solution solve(int n, int r, const SolverConfig& cfg, const std::optional<Topology>& warm) {
+    const auto t0 = std::chrono::steady_clock::now();
+    cfg.validate();
+    const tp_config c = to_c(cfg);
+    tp_result res{};
+    const int cap = std::max(1, r);
+    std::vector<int32_t> edges(2 * cap);
+    std::vector<double> weights(cap), trace(3 * (size_t)cfg.max_iter);
+    char note[512] = {0};
+    if (warm) {
+        warm->validate();
+        if (warm->n != n) throw std::invalid_argument("solve: warm start node count mismatch");
+        const auto we = flat_edges(*warm);
+        raise(tp_solve(n, r, &c, we.data(), (int32_t)warm->edges.size(), &res, edges.data(),
+                       weights.data(), trace.data(), note, sizeof note));
+    } else {
+        raise(tp_solve(n, r, &c, nullptr, -1, &res, edges.data(), weights.data(), trace.data(), note,
+                       sizeof note));
+    }
+    Solution sol = collect(n, res, edges, weights, trace, note);
+    sol.wall_time_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return sol;
+}
+
+// ------------------------------------------------------------------ admm_het
+ProblemDataHet assemble_het(const CapacitySystem& sys, std::optional<int> r, double alpha, double rho) {
+    std::vector<int32_t> deg;
+    if (!node_level_degrees(sys, deg))
+        throw std::invalid_argument("assemble_het: only node-level equality systems are supported");
+    if (!(alpha > 0.0)) throw std::invalid_argument("assemble_het: alpha must be positive");
+    if (!(rho > 0.0)) throw std::invalid_argument("assemble_het: rho must be positive");
+    long long total = 0;
+    for (int d : deg) total += d;
+    if (total % 2) throw InfeasibleError("degree sum " + std::to_string(total) + " is odd");
+    if (r && *r != total / 2) throw std::invalid_argument("edge total conflicts with the degree rows");
+    const ProblemData base = assemble(sys.n, std::max(1, (int)(total / 2)), alpha, rho);
+    ProblemDataHet pd;
+    pd.n = base.n;
+    pd.m = base.m;
+    pd.r = (int)(total / 2);
+    pd.alpha = alpha;
+    pd.rho = rho;
+    pd.q = sys.n;
+    pd.lambda_ix = base.lambda_ix;
+    pd.off_s = base.off_s;
+    pd.off_y = base.off_y;
+    pd.off_t = base.off_t;
+    pd.off_z = base.nx;
+    pd.off_nu = base.nx + base.m;
+    pd.nx = base.nx + 2 * base.m;
+    pd.neq = base.neq + pd.q + base.m;
+    pd.pairs = base.pairs;
+    pd.sys = sys;
+    pd.beq = base.beq;
+    for (int d : deg) pd.beq.push_back((double)d);
+    pd.beq.insert(pd.beq.end(), base.m, 0.0);
+    return pd;
+}
+
+Vec project_binary_z(const Vec& v, int r) {
+    Vec z(v.size());
+    raise(tp_project_binary_z(v.data(), (int64_t)v.size(), r, z.data()));
+    return z;
+}
+
+Vec project_Y_het(const ProblemDataHet& pd, const Vec& x, const Vec& d) {
+    std::vector<int32_t> deg;
+    if (!node_level_degrees(pd.sys, deg))
+        throw std::invalid_argument("project_Y_het: only node-level equality systems are supported");
+    Vec y(pd.nx);
+    raise(tp_project_Y_het_node(pd.n, deg.data(), pd.alpha, pd.rho, x.data(), d.data(), y.data()));
+    return y;
+}
+
+Solution solve_het(const CapacitySystem& sys, std::optional<int> r, const SolverConfig& cfg,
+                   const std::optional<Topology>& warm) {
+    const auto t0 = std::chrono::steady_clock::now();
+    cfg.validate();
+    std::vector<int32_t> deg;
+    if (!node_level_degrees(sys, deg))
+        throw std::invalid_argument("solve_het: only node-level equality systems are supported");
+    long long total = 0;
+    for (int d : deg) total += d;
+    if (total % 2 == 0 && r && *r != total / 2)
+        throw std::invalid_argument("edge total conflicts with the degree rows");
+    const tp_config c = to_c(cfg);
+    tp_result res{};
+    const int m = sys.n * (sys.n - 1) / 2;
+    std::vector<int32_t> edges(2 * std::max(m, 1));
+    std::vector<double> weights(std::max(m, 1)), trace(3 * (size_t)cfg.max_iter);
+    char note[512] = {0};
+    if (warm) {
+        warm->validate();
+        if (warm->n != sys.n) throw std::invalid_argument("solve_het: warm start node count mismatch");
+        const auto we = flat_edges(*warm);
+        raise(tp_solve_het_node(sys.n, deg.data(), &c, we.data(), (int32_t)warm->edges.size(), &res,
+                                edges.data(), weights.data(), trace.data(), note, sizeof note));
+    } else {
+        raise(tp_solve_het_node(sys.n, deg.data(), &c, nullptr, -1, &res, edges.data(), weights.data(),
+                                trace.data(), note, sizeof note));
+    }
+    Solution sol = collect(sys.n, res, edges, weights, trace, note);
+    sol.wall_time_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return sol;
+}
+
+}  // namespace topoopt
