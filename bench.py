@@ -297,19 +297,74 @@ def run_ours(args):
         tdist.destroy_process_group()
 
 
+def run_sweep(args):
+    """Config 5: n=256 x 64 budgets x 4 bandwidth scenarios = 256 independent
+    solves, sharded round-robin across ranks (no data-path collective)."""
+    import torch
+    import torch.distributed as tdist
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    from paper_2512_07536_b200 import _lib
+    from paper_2512_07536_b200.sweep import gather, partition, run_jobs, sweep_jobs
+
+    _lib.load().tp_set_device(local)
+    jobs = sweep_jobs(n=256, n_budgets=args.sweep_budgets, dr=32 * (64 // args.sweep_budgets))
+    mine = partition(jobs, ws, rank)
+    if ws > 1:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        rows, dev_s = run_jobs(mine, 256, rank=rank, rho=10.0, epsilon=1e-8, max_iter=args.sweep_max_iter)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+    if ws > 1:
+        t = torch.tensor([wall], device="cuda", dtype=torch.float64)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        wall = float(t.item())
+    allrows = gather(rows)
+    if rank == 0:
+        ok = [r for r in allrows if r.status == "ok"]
+        line = {
+            "metric": "batched_solves_per_s_n256_sweep", "value": len(jobs) / wall, "unit": "solves/s",
+            "n_gpus": ws, "steps": len(jobs), "warmup": 0, "ms_per_step": wall / len(jobs) * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": "sweep_n256_budgets_x_scenarios", "n": 256,
+                       "budgets": sorted({j.r for j in jobs}), "scenarios": list({j.scenario for j in jobs}),
+                       "rho": 10.0, "epsilon": 1e-8, "max_iter": args.sweep_max_iter,
+                       "warm_start": "anneal_degree_topology(Alg.1, steps=1, moves=1)"},
+            "solved": len(ok), "infeasible": len(allrows) - len(ok),
+            "converged": sum(r.converged for r in ok),
+            "iterations_total": sum(r.iterations for r in ok),
+            "iterations_max": max((r.iterations for r in ok), default=0),
+            "wall_s": wall, "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        tdist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="n1024", choices=["n1024"])
+    ap.add_argument("--workload", default="n1024", choices=["n1024", "sweep"])
+    ap.add_argument("--sweep-budgets", type=int, default=64)
+    ap.add_argument("--sweep-max-iter", type=int, default=40000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "sweep":
+        run_sweep(args)
     else:
         run_ours(args)
 

@@ -11,6 +11,7 @@
 // 0 ok, 1 invalid_argument, 2 InfeasibleError, 3 LinearSolveError,
 // 4 DegenerateSolutionError, 5 PivotError, 6 other.
 #include <algorithm>
+#include <cmath>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -456,7 +457,10 @@ int ref_iteration_sample(int n, int r, const int* warm_edges, int n_warm, double
                 s(rr, c) = x[pd.off_s + c * n + rr];
                 t(rr, c) = x[pd.off_t + c * n + rr];
             }
-        Vec y = x;  // x-step input: the feasible start itself
+        // x-step input: the feasible start moved off the constraint set (as the
+        // cone projection does), so BiCGSTAB works as in a real iteration
+        Vec y = x;
+        for (size_t k = 0; k < y.size(); ++k) y[k] += 1e-3 * std::sin(0.7 * (double)k);
         Vec warm_kkt(pd.nx + pd.neq, 0.0);
         std::copy(x.begin(), x.end(), warm_kkt.begin());
         double tn = 0, tp = 0, tx = 0, ta = 0;
