@@ -389,8 +389,125 @@ size_t slem_smem_bytes(int n, int kmax, bool basis_in_smem) {
     return bytes;
 }
 
+// ---------------------------------------------------------------- small n
+// n <= kSmallDense: dense W = I - L(g) in shared memory, Householder
+// tridiagonalisation in FP64, then the two eigenvalues spectral_report reads
+// (values[n-2], values[0]) by Sturm multisection. Exact up to rounding like
+// the reference's Householder + QL (eig.cpp:18-129), without iterating.
+__global__ void __launch_bounds__(256) slem_small_kernel(SlemArgs a) {
+    const int b = blockIdx.x;
+    if (a.ictl && a.ictl[b * 8 + 1]) return;
+    const int n = a.n, ld = n + 1;
+    const int tid = threadIdx.x, nthr = blockDim.x, wid = tid >> 5;
+    const int ne = min(a.count[b], a.list_cap);
+    const int* list = a.list + (long long)b * a.list_cap;
+    const double* g = a.g + (long long)b * a.stride;
+    extern __shared__ double sh[];
+    double* A = sh;              // n x ld
+    double* v = A + n * ld;      // n
+    double* p = v + n;           // n
+    double* d = p + n;           // n
+    double* e = d + n;           // n
+    __shared__ double scratch[32];
+    __shared__ int s_it;
+    if (tid == 0 && a.ictl) s_it = a.ictl[b * 8];
+    // W: off-diagonals +g, diagonal 1 - (sum of incident g, ascending edges)
+    for (int k = tid; k < n * ld; k += nthr) A[k] = 0.0;
+    __syncthreads();
+    for (int t = tid; t < ne; t += nthr) {
+        int i, j;
+        edge_pair(n, list[t], i, j);
+        const double w = g[list[t]];
+        A[i * ld + j] = w;
+        A[j * ld + i] = w;
+    }
+    __syncthreads();
+    for (int i = tid; i < n; i += nthr) {
+        double s = 0.0;
+        for (int j = 0; j < n; ++j)
+            if (j != i) s += A[i * ld + j];
+        A[i * ld + i] = 1.0 - s;
+    }
+    __syncthreads();
+    for (int k = 0; k + 2 < n; ++k) {
+        const int m0 = k + 1, len = n - m0;
+        double nn = 0.0;
+        for (int i = m0 + tid; i < n; i += nthr) nn += A[i * ld + k] * A[i * ld + k];
+        nn = block_sum(nn, scratch);
+        const double a0 = A[m0 * ld + k];
+        if (nn == 0.0) {
+            if (tid == 0) {
+                d[k] = A[k * ld + k];
+                e[k] = 0.0;
+            }
+            __syncthreads();
+            continue;
+        }
+        const double s = sqrt(nn);
+        const double sg = a0 >= 0.0 ? 1.0 : -1.0;
+        const double beta = 1.0 / (s * (s + fabs(a0)));
+        for (int i = m0 + tid; i < n; i += nthr) v[i] = A[i * ld + k] + (i == m0 ? sg * s : 0.0);
+        __syncthreads();
+        // p = beta A[m0:, m0:] v
+        for (int i = m0 + tid; i < n; i += nthr) {
+            double acc = 0.0;
+            for (int j = m0; j < n; ++j) acc += A[i * ld + j] * v[j];
+            p[i] = beta * acc;
+        }
+        __syncthreads();
+        double pv = 0.0;
+        for (int i = m0 + tid; i < n; i += nthr) pv += p[i] * v[i];
+        pv = block_sum(pv, scratch);
+        const double K = 0.5 * beta * pv;
+        for (int i = m0 + tid; i < n; i += nthr) p[i] -= K * v[i];  // w
+        __syncthreads();
+        for (int idx = tid; idx < len * len; idx += nthr) {
+            const int i = m0 + idx / len, j = m0 + idx % len;
+            A[i * ld + j] -= v[i] * p[j] + p[i] * v[j];
+        }
+        if (tid == 0) {
+            d[k] = A[k * ld + k];
+            e[k] = -sg * s;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        if (n >= 2) {
+            d[n - 2] = A[(n - 2) * ld + n - 2];
+            e[n - 2] = A[(n - 1) * ld + n - 2];
+        }
+        d[n - 1] = A[(n - 1) * ld + n - 1];
+    }
+    __syncthreads();
+    if (wid == 0) {
+        double lo, hi;
+        gershgorin(d, e, n, lo, hi);
+        const double ln = tri_eig(d, e, n, 0, lo, hi);
+        const double l2 = n >= 2 ? tri_eig(d, e, n, n - 2, lo, hi) : ln;
+        if (tid == 0) {
+            const double acf = n == 1 ? 0.0 : fmax(fabs(l2), fabs(ln));
+            if (a.tr_acf) a.tr_acf[(long long)b * a.max_iter + s_it] = acf;
+            if (a.out) {
+                double* o = a.out + b * 8;
+                o[0] = acf;
+                o[1] = l2;
+                o[2] = ln;
+                o[3] = (l2 < 1.0 - 1e-8) ? 1.0 : 0.0;
+                o[4] = n;
+                o[5] = 1.0;
+            }
+        }
+    }
+}
+
 void launch_slem(const SlemArgs& a, int B, cudaStream_t st) {
     const int n = a.n;
+    if (n <= kSmallDense) {
+        const size_t smem = ((size_t)n * (n + 1) + 4 * (size_t)n) * sizeof(double);
+        slem_small_kernel<<<B, 256, smem, st>>>(a);
+        TPB_CHECK_LAUNCH();
+        return;
+    }
     const size_t smem = slem_smem_bytes(n, a.kmax, a.basis == nullptr);
     // one thread per node up to 512; small graphs use fewer warps (cheaper barriers)
     const int threads = std::min(kThreads, std::max(128, ((n + 31) / 32) * 32));
@@ -509,6 +626,7 @@ void launch_slem_dense(const double* w, int n, double* basis, double* out, int d
 void init_attrs_slem() {
     set_max_dyn_smem(slem_kernel);
     set_max_dyn_smem(slem_dense_kernel);
+    set_max_dyn_smem(slem_small_kernel);
 }
 
 }  // namespace tpb

@@ -36,6 +36,9 @@ struct SlemArgs {
     int max_iter;
 };
 
+// n <= kSmallDense: dense Householder tridiagonalisation in shared memory
+// (exact, no iteration); larger n: Lanczos (exact or restarted, see SlemArgs).
+constexpr int kSmallDense = 128;
 void launch_slem(const SlemArgs& a, int B, cudaStream_t st);
 // dynamic shared memory of launch_slem (basis_in_smem: a.basis == null)
 size_t slem_smem_bytes(int n, int kmax, bool basis_in_smem);

@@ -166,14 +166,10 @@ void Solver::alloc() {
     e_w_ = dalloc<double>(allocs_, (size_t)B * list_cap_);
     // trace Lanczos: exact for n <= 97, else restarted and warm-started from
     // the previous Ritz vectors; basis in shared memory when it fits
+    // Krylov basis in global memory: a shared-memory basis (~200 KB at n=256)
+    // would pin one SLEM CTA per SM and starve the concurrent cone GEMMs.
     trace_kmax_ = std::max(1, std::min(n - 1, 96));
-    {
-        int dev = 0, optin = 0;
-        TPB_CUDA(cudaGetDevice(&dev));
-        TPB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-        if (slem_smem_bytes(n, trace_kmax_, true) + 2048 <= (size_t)optin) basis_ = nullptr;
-        else basis_ = dalloc<double>(allocs_, (size_t)B * trace_kmax_ * n);
-    }
+    basis_ = dalloc<double>(allocs_, (size_t)B * trace_kmax_ * n);
     ritz_ = dalloc<double>(allocs_, (size_t)B * 2 * n);
     ritz_ok_ = dalloc<int>(allocs_, B);
     const int kfin = n - 1 <= kFinalExactDim ? std::max(1, n - 1) : kFinalKrylov;
