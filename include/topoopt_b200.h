@@ -127,6 +127,12 @@ int tp_solver_state(tp_solver* s, double** x, double** y, double** d);
 int tp_solver_bench_phase(tp_solver* s, int32_t phase, int32_t reps, int32_t* launches_per_rep);
 int tp_solver_launches_per_iteration(tp_solver* s, int32_t* out);
 
+/* Tuning hooks of the FP64 DMMA GEMM behind the cone projections:
+ * variant 0 = production; tp_bench_gemm times one GEMM step on nmat
+ * matrices of order n (event-timed, ms per launch). */
+int tp_set_gemm_variant(int32_t variant);
+int tp_bench_gemm(int32_t n, int32_t nmat, int32_t variant, int32_t reps, double* ms_per_launch);
+
 /* ---------------------------------------------------------------- substeps */
 /* project_Y (proj/src/admm.cpp:268-277); x, d, y of length nx. */
 int tp_project_Y(int32_t n, int32_t r, double alpha, double rho, const double* x, const double* d,

@@ -82,6 +82,8 @@ SIGNATURES = {
     "tp_solver_state": (_I, [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P)]),
     "tp_solver_bench_phase": (_I, [_P, _I, _I, _ip]),
     "tp_solver_launches_per_iteration": (_I, [_P, _ip]),
+    "tp_set_gemm_variant": (_I, [_I]),
+    "tp_bench_gemm": (_I, [_I, _I, _I, _I, _dp]),
     "tp_project_Y": (_I, [_I, _I, _D, _D, _dp, _dp, _dp]),
     "tp_project_Y_het_node": (_I, [_I, _ip, _D, _D, _dp, _dp, _dp]),
     "tp_update_X": (_I, [_I, _I, _D, _D, _dp, _dp, _dp]),

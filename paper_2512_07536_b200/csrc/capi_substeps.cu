@@ -431,4 +431,61 @@ int tp_project_nsd(int32_t n, const double* a, double* out) {
     return guarded([&] { cone_dense(n, a, out, false); });
 }
 
+int tp_set_gemm_variant(int32_t variant) {
+    return guarded([&] {
+        if (variant < 0 || variant >= sym_gemm_variants())
+            throw Error(kInvalidArgument, "gemm variant out of range");
+        set_sym_gemm_variant(variant);
+    });
+}
+
+// Times one symmetric DMMA GEMM step (C = A.B + E over nmat ld x ld matrices)
+// for the given variant: ms per launch averaged over `reps` launches.
+int tp_bench_gemm(int32_t n, int32_t nmat, int32_t variant, int32_t reps, double* ms_per_launch) {
+    return guarded([&] {
+        require_device();
+        init_attrs();
+        const int ld = ((n + 63) / 64) * 64;
+        const size_t sz = (size_t)nmat * ld * ld;
+        DBuf<double> A(sz), B(sz), C(sz);
+        std::vector<double> h(sz);
+        for (size_t k = 0; k < sz; ++k) {
+            const size_t r = (k / ld) % ld, c = k % ld;
+            h[k] = r < (size_t)n && c < (size_t)n ? 1.0 / (1.0 + (double)((r * 7 + c * 7) % 97)) : 0.0;
+        }
+        A.up(h.data(), sz);
+        B.up(h.data(), sz);
+        C.zero();
+        const int old = get_sym_gemm_variant();
+        set_sym_gemm_variant(variant);
+        GemmArgs g{};
+        g.A = A.p;
+        g.B = B.p;
+        g.E = A.p;
+        g.mstride = (long long)ld * ld;
+        g.C = C.p;
+        g.c_stride_b = 2LL * ld * ld;
+        g.c_stride_w = (long long)ld * ld;
+        g.ldc = ld;
+        g.nvalid = ld;
+        g.ld = ld;
+        g.alpha_c = 1.0;
+        g.beta_c = 0.5;
+        cudaEvent_t e0, e1;
+        TPB_CUDA(cudaEventCreate(&e0));
+        TPB_CUDA(cudaEventCreate(&e1));
+        launch_sym_gemm(g, nmat, 0);
+        TPB_CUDA(cudaEventRecord(e0, 0));
+        for (int k = 0; k < reps; ++k) launch_sym_gemm(g, nmat, 0);
+        TPB_CUDA(cudaEventRecord(e1, 0));
+        TPB_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        TPB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        set_sym_gemm_variant(old);
+        *ms_per_launch = ms / reps;
+    });
+}
+
 }  // extern "C"

@@ -17,10 +17,6 @@ namespace tpb {
 namespace {
 
 constexpr int BM = 64;        // tile edge
-constexpr int BK = 16;        // k per stage
-constexpr int PAD = BK + 4;   // smem row stride (doubles): conflict-free fragments
-constexpr int STAGES = 3;
-constexpr int GT = 128;       // 4 warps, 2 x 2 warp tiles of 32 x 32
 
 __device__ inline void dmma(double& d0, double& d1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -51,7 +47,13 @@ __device__ inline double powi(double s, int p) { return p == 0 ? 1.0 : (p == 1 ?
 
 }  // namespace
 
-__global__ void __launch_bounds__(GT) sym_gemm_kernel(GemmArgs g) {
+// 64x64 lower tile per CTA; WM x WN warps, each an (64/WM) x (64/WN) block of
+// 8x8 DMMA fragments; BK-deep k stages, STG-stage cp.async pipeline.
+template <int BK, int STG, int WM, int WN>
+__global__ void __launch_bounds__(WM* WN * 32) sym_gemm_kernel(GemmArgs g) {
+    constexpr int GT = WM * WN * 32;
+    constexpr int PAD = BK + 4;  // smem row stride (doubles): conflict-free fragments
+    constexpr int MI = 64 / WM / 8, NI = 64 / WN / 8;
     const int mat = blockIdx.y;
     if (g.ictl && g.ictl[(mat >> 1) * 8 + 1]) return;
     int bi, bj;
@@ -61,57 +63,57 @@ __global__ void __launch_bounds__(GT) sym_gemm_kernel(GemmArgs g) {
     const double* A = g.A + (long long)mat * g.mstride;
     const double* B = g.B + (long long)mat * g.mstride;
     extern __shared__ __align__(16) double smem[];
-    double* As = smem;                          // STAGES x BM x PAD
-    double* Bs = smem + STAGES * BM * PAD;      // STAGES x BM x PAD
+    double* As = smem;                       // STG x BM x PAD
+    double* Bs = smem + STG * BM * PAD;      // STG x BM x PAD
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wr = (warp >> 1) * 32, wc = (warp & 1) * 32;
+    const int wr = (warp / WN) * (64 / WM), wc = (warp % WN) * (64 / WN);
 
     auto load_stage = [&](int slot, int kt) {
         const int k0 = kt * BK;
         double* as = As + slot * BM * PAD;
         double* bs = Bs + slot * BM * PAD;
-        // 64 rows x 8 chunks of 16 B per panel
+        // 64 rows x BK/2 chunks of 16 B per panel
 #pragma unroll
         for (int c = tid; c < BM * (BK / 2); c += GT) {
-            const int r = c >> 3, q = (c & 7) * 2;
+            const int r = c / (BK / 2), q = (c % (BK / 2)) * 2;
             cp_async16(as + r * PAD + q, A + (long long)(i0 + r) * ld + k0 + q);
             cp_async16(bs + r * PAD + q, B + (long long)(j0 + r) * ld + k0 + q);
         }
     };
 
-    double acc[4][4][2];
+    double acc[MI][NI][2];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < MI; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+        for (int b = 0; b < NI; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
     const int KT = ld / BK;
 #pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) {
+    for (int s = 0; s < STG - 1; ++s) {
         if (s < KT) load_stage(s, s);
         cp_commit();
     }
     for (int kt = 0; kt < KT; ++kt) {
-        cp_wait<STAGES - 2>();
+        cp_wait<STG - 2>();
         __syncthreads();
-        const int nk = kt + STAGES - 1;
-        if (nk < KT) load_stage(nk % STAGES, nk);
+        const int nk = kt + STG - 1;
+        if (nk < KT) load_stage(nk % STG, nk);
         cp_commit();
-        const double* as = As + (kt % STAGES) * BM * PAD;
-        const double* bs = Bs + (kt % STAGES) * BM * PAD;
+        const double* as = As + (kt % STG) * BM * PAD;
+        const double* bs = Bs + (kt % STG) * BM * PAD;
 #pragma unroll
         for (int ks = 0; ks < BK / 4; ++ks) {
-            double af[4], bf[4];
+            double af[MI], bf[NI];
 #pragma unroll
-            for (int mi = 0; mi < 4; ++mi)
+            for (int mi = 0; mi < MI; ++mi)
                 af[mi] = as[(wr + mi * 8 + (lane >> 2)) * PAD + ks * 4 + (lane & 3)];
 #pragma unroll
-            for (int ni = 0; ni < 4; ++ni)
+            for (int ni = 0; ni < NI; ++ni)
                 bf[ni] = bs[(wc + ni * 8 + (lane >> 2)) * PAD + ks * 4 + (lane & 3)];
 #pragma unroll
-            for (int mi = 0; mi < 4; ++mi)
+            for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-                for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+                for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
         }
     }
     cp_wait<0>();
@@ -126,9 +128,9 @@ __global__ void __launch_bounds__(GT) sym_gemm_kernel(GemmArgs g) {
     double* Cs = smem;  // BM x (BM + 1)
     constexpr int CP = BM + 1;
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
+    for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) {
+        for (int ni = 0; ni < NI; ++ni) {
             const int r = wr + mi * 8 + (lane >> 2);
             const int c = wc + ni * 8 + (lane & 3) * 2;
             double v0 = alpha * acc[mi][ni][0], v1 = alpha * acc[mi][ni][1];
@@ -161,12 +163,32 @@ __global__ void __launch_bounds__(GT) sym_gemm_kernel(GemmArgs g) {
     }
 }
 
-void launch_sym_gemm(const GemmArgs& g, int nmat, cudaStream_t st) {
+namespace {
+
+template <int BK, int STG, int WM, int WN>
+void launch_variant(const GemmArgs& g, int nmat, cudaStream_t st) {
     const int nt = g.ld / BM;
     const int tiles = nt * (nt + 1) / 2;
-    const int smem = 2 * STAGES * BM * PAD * sizeof(double);
-    sym_gemm_kernel<<<dim3(tiles, nmat), GT, smem, st>>>(g);
+    const int smem = 2 * STG * BM * (BK + 4) * sizeof(double);
+    sym_gemm_kernel<BK, STG, WM, WN><<<dim3(tiles, nmat), WM * WN * 32, smem, st>>>(g);
     TPB_CHECK_LAUNCH();
+}
+
+int g_gemm_variant = 0;  // production default (profiles/)
+
+}  // namespace
+
+int sym_gemm_variants() { return 4; }
+void set_sym_gemm_variant(int v) { g_gemm_variant = v; }
+int get_sym_gemm_variant() { return g_gemm_variant; }
+
+void launch_sym_gemm(const GemmArgs& g, int nmat, cudaStream_t st) {
+    switch (g_gemm_variant) {
+        case 1: launch_variant<32, 3, 2, 2>(g, nmat, st); break;   // 4 warps, BK 32
+        case 2: launch_variant<16, 3, 2, 4>(g, nmat, st); break;   // 8 warps (32x16), BK 16
+        case 3: launch_variant<32, 3, 2, 4>(g, nmat, st); break;   // 8 warps, BK 32
+        default: launch_variant<16, 3, 2, 2>(g, nmat, st); break;  // 4 warps (32x32), BK 16
+    }
 }
 
 void enqueue_cone_tiled(const double* A, double* w0, double* w1, double* w2, int ld, int n,
@@ -362,7 +384,10 @@ void launch_cone_small(const double* A, long long mstride, int ld, int n, double
 }
 
 void init_attrs_cone() {
-    set_max_dyn_smem(sym_gemm_kernel);
+    set_max_dyn_smem(sym_gemm_kernel<16, 3, 2, 2>);
+    set_max_dyn_smem(sym_gemm_kernel<32, 3, 2, 2>);
+    set_max_dyn_smem(sym_gemm_kernel<16, 3, 2, 4>);
+    set_max_dyn_smem(sym_gemm_kernel<32, 3, 2, 4>);
     set_max_dyn_smem(cone_small_kernel);
 }
 

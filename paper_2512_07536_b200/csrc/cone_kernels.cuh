@@ -39,6 +39,10 @@ struct GemmArgs {
 };
 
 void launch_sym_gemm(const GemmArgs& g, int nmat, cudaStream_t st);
+// tile/pipeline variants of the DMMA GEMM (for tuning; 0 = production)
+int sym_gemm_variants();
+void set_sym_gemm_variant(int v);
+int get_sym_gemm_variant();
 
 // Fused small-n projection: one CTA per matrix, whole iteration in shared
 // memory (npad <= 64). A at A + mat*mstride (ld-padded, symmetric); output to

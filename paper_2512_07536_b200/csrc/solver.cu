@@ -7,7 +7,10 @@
 #include "solver.cuh"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 
@@ -24,13 +27,38 @@ void validate(const Config& c) {
     if (c.trace_stride < 1) throw Error(kInvalidArgument, "SolverConfig: trace_stride must be >= 1");
 }
 
+// TPB_TIMING=1: device-synchronised phase timings on stderr (setup overheads)
+void phase_mark(const char* what) {
+    static const bool on = std::getenv("TPB_TIMING") != nullptr;
+    if (!on) return;
+    static auto last = std::chrono::steady_clock::now();
+    cudaDeviceSynchronize();
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[tpb] %-24s %9.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - last).count());
+    last = now;
+}
+
 namespace {
 
+// Stream-ordered allocation from the device's default memory pool, whose
+// release threshold is raised so that freed blocks stay reserved: repeated
+// solves (tp_solve per call) neither map nor unmap device memory.
 template <typename T>
-T* dalloc(std::vector<void*>& pool, size_t count) {
+T* dalloc(cudaStream_t st, std::vector<void*>& pool, size_t count) {
+    static bool pool_ready[64] = {};
+    int dev = 0;
+    TPB_CUDA(cudaGetDevice(&dev));
+    if (dev < 64 && !pool_ready[dev]) {
+        cudaMemPool_t mp;
+        TPB_CUDA(cudaDeviceGetDefaultMemPool(&mp, dev));
+        uint64_t thr = UINT64_MAX;
+        TPB_CUDA(cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr));
+        pool_ready[dev] = true;
+    }
     void* p = nullptr;
     if (count == 0) count = 1;
-    TPB_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    TPB_CUDA(cudaMallocAsync(&p, count * sizeof(T), st));
     pool.push_back(p);
     return static_cast<T*>(p);
 }
@@ -95,12 +123,18 @@ Solver::Solver(int n, int B, bool het, const std::vector<int>& r, const std::vec
     TPB_CUDA(cudaMemcpy(d_r_, r_host_.data(), B * sizeof(int), cudaMemcpyHostToDevice));
     warm_.assign(B, {});
     res_.assign(B, {});
+    phase_mark("solver alloc");
 }
 
 Solver::~Solver() {
+    phase_mark("(before teardown)");
     if (g_chunk_) cudaGraphExecDestroy(g_chunk_);
     if (g_one_) cudaGraphExecDestroy(g_one_);
-    for (void* p : allocs_) cudaFree(p);
+    phase_mark("graph destroy");
+    // stream-ordered frees return the blocks to the device pool (no unmap)
+    for (void* p : allocs_) cudaFreeAsync(p, s0_);
+    cudaStreamSynchronize(s0_);
+    phase_mark("free");
     if (h_ctl_) cudaFreeHost(h_ctl_);
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_sel_) cudaEventDestroy(ev_sel_);
@@ -126,61 +160,64 @@ void Solver::alloc() {
     d_.track_best = 1;
     d_.upd_duals = 1;
     const long long ld2 = (long long)ld_ * ld_;
-    d_.X = dalloc<double>(allocs_, B * nx);
-    d_.Y = dalloc<double>(allocs_, B * nx);
-    d_.D = dalloc<double>(allocs_, B * nx);
-    d_.bestY = dalloc<double>(allocs_, B * nx);
-    d_.bestScore = dalloc<double>(allocs_, het_ ? B * m : 1);
-    d_.A = dalloc<double>(allocs_, (size_t)B * 2 * ld2);
-    TPB_CUDA(cudaMemset(d_.A, 0, (size_t)B * 2 * ld2 * sizeof(double)));
-    d_.frob_part = dalloc<double>(allocs_, (size_t)B * 2 * d_.ntile);
-    d_.inv_scale = dalloc<double>(allocs_, (size_t)B * 2);
-    d_.h = dalloc<double>(allocs_, B * m);
-    d_.PU = dalloc<double>(allocs_, (size_t)B * d_.nb * n);
-    d_.PZ = dalloc<double>(allocs_, (size_t)B * d_.nb * n);
-    d_.PG = dalloc<double>(allocs_, (size_t)B * d_.nb * n);
-    d_.node = dalloc<double>(allocs_, (size_t)B * 4 * n);
-    d_.res_part = dalloc<double>(allocs_, (size_t)B * d_.ntile);
-    d_.scal = dalloc<double>(allocs_, (size_t)B * 8);
-    d_.ictl = dalloc<int>(allocs_, (size_t)B * 8);
-    d_r_ = dalloc<int>(allocs_, B);
+    d_.X = dalloc<double>(s0_, allocs_,B * nx);
+    d_.Y = dalloc<double>(s0_, allocs_,B * nx);
+    d_.D = dalloc<double>(s0_, allocs_,B * nx);
+    d_.bestY = dalloc<double>(s0_, allocs_,B * nx);
+    d_.bestScore = dalloc<double>(s0_, allocs_,het_ ? B * m : 1);
+    d_.A = dalloc<double>(s0_, allocs_,(size_t)B * 2 * ld2);
+    TPB_CUDA(cudaMemsetAsync(d_.A, 0, (size_t)B * 2 * ld2 * sizeof(double), s0_));
+    d_.frob_part = dalloc<double>(s0_, allocs_,(size_t)B * 2 * d_.ntile);
+    d_.inv_scale = dalloc<double>(s0_, allocs_,(size_t)B * 2);
+    d_.h = dalloc<double>(s0_, allocs_,B * m);
+    d_.PU = dalloc<double>(s0_, allocs_,(size_t)B * d_.nb * n);
+    d_.PZ = dalloc<double>(s0_, allocs_,(size_t)B * d_.nb * n);
+    d_.PG = dalloc<double>(s0_, allocs_,(size_t)B * d_.nb * n);
+    d_.node = dalloc<double>(s0_, allocs_,(size_t)B * 4 * n);
+    d_.res_part = dalloc<double>(s0_, allocs_,(size_t)B * d_.ntile);
+    d_.scal = dalloc<double>(s0_, allocs_,(size_t)B * 8);
+    d_.ictl = dalloc<int>(s0_, allocs_,(size_t)B * 8);
+    d_r_ = dalloc<int>(s0_, allocs_,B);
     d_.r = d_r_;
-    d_deg_ = dalloc<double>(allocs_, het_ ? (size_t)B * n : 1);
+    d_deg_ = dalloc<double>(s0_, allocs_,het_ ? (size_t)B * n : 1);
     d_.deg = d_deg_;
-    d_.tr_res = dalloc<double>(allocs_, (size_t)B * cfg_.max_iter);
-    d_.tr_lam = dalloc<double>(allocs_, (size_t)B * cfg_.max_iter);
-    d_.tr_acf = dalloc<double>(allocs_, (size_t)B * cfg_.max_iter);
+    d_.tr_res = dalloc<double>(s0_, allocs_,(size_t)B * cfg_.max_iter);
+    d_.tr_lam = dalloc<double>(s0_, allocs_,(size_t)B * cfg_.max_iter);
+    d_.tr_acf = dalloc<double>(s0_, allocs_,(size_t)B * cfg_.max_iter);
     if (!small_) {
-        w0_ = dalloc<double>(allocs_, (size_t)B * 2 * ld2);
-        w1_ = dalloc<double>(allocs_, (size_t)B * 2 * ld2);
-        w2_ = dalloc<double>(allocs_, (size_t)B * 2 * ld2);
-        TPB_CUDA(cudaMemset(w0_, 0, (size_t)B * 2 * ld2 * sizeof(double)));
-        TPB_CUDA(cudaMemset(w1_, 0, (size_t)B * 2 * ld2 * sizeof(double)));
-        TPB_CUDA(cudaMemset(w2_, 0, (size_t)B * 2 * ld2 * sizeof(double)));
+        w0_ = dalloc<double>(s0_, allocs_,(size_t)B * 2 * ld2);
+        w1_ = dalloc<double>(s0_, allocs_,(size_t)B * 2 * ld2);
+        w2_ = dalloc<double>(s0_, allocs_,(size_t)B * 2 * ld2);
+        TPB_CUDA(cudaMemsetAsync(w0_, 0, (size_t)B * 2 * ld2 * sizeof(double), s0_));
+        TPB_CUDA(cudaMemsetAsync(w1_, 0, (size_t)B * 2 * ld2 * sizeof(double), s0_));
+        TPB_CUDA(cudaMemsetAsync(w2_, 0, (size_t)B * 2 * ld2 * sizeof(double), s0_));
     }
-    list_ = dalloc<int>(allocs_, (size_t)B * list_cap_);
-    list_count_ = dalloc<int>(allocs_, B);
-    e_i_ = dalloc<int>(allocs_, (size_t)B * list_cap_);
-    e_j_ = dalloc<int>(allocs_, (size_t)B * list_cap_);
-    col_idx_ = dalloc<int>(allocs_, (size_t)B * list_cap_);
-    e_w_ = dalloc<double>(allocs_, (size_t)B * list_cap_);
+    list_ = dalloc<int>(s0_, allocs_,(size_t)B * list_cap_);
+    list_count_ = dalloc<int>(s0_, allocs_,B);
+    e_i_ = dalloc<int>(s0_, allocs_,(size_t)B * list_cap_);
+    e_j_ = dalloc<int>(s0_, allocs_,(size_t)B * list_cap_);
+    col_idx_ = dalloc<int>(s0_, allocs_,(size_t)B * list_cap_);
+    e_w_ = dalloc<double>(s0_, allocs_,(size_t)B * list_cap_);
     // trace Lanczos: exact for n <= 97, else restarted and warm-started from
     // the previous Ritz vectors; basis in shared memory when it fits
     // Krylov basis in global memory: a shared-memory basis (~200 KB at n=256)
     // would pin one SLEM CTA per SM and starve the concurrent cone GEMMs.
     trace_kmax_ = std::max(1, std::min(n - 1, 96));
-    basis_ = dalloc<double>(allocs_, (size_t)B * trace_kmax_ * n);
-    ritz_ = dalloc<double>(allocs_, (size_t)B * 2 * n);
-    ritz_ok_ = dalloc<int>(allocs_, B);
+    basis_ = dalloc<double>(s0_, allocs_,(size_t)B * trace_kmax_ * n);
+    ritz_ = dalloc<double>(s0_, allocs_,(size_t)B * 2 * n);
+    ritz_ok_ = dalloc<int>(s0_, allocs_,B);
     const int kfin = n - 1 <= kFinalExactDim ? std::max(1, n - 1) : kFinalKrylov;
-    basis_final_ = dalloc<double>(allocs_, (size_t)B * kfin * n);
-    slem_out_ = dalloc<double>(allocs_, (size_t)B * 8);
-    tmp_m_ = dalloc<double>(allocs_, (size_t)B * m);
-    tmp_m2_ = dalloc<double>(allocs_, (size_t)B * m);
-    worst_ = dalloc<double>(allocs_, B);
-    fs_scal_ = dalloc<double>(allocs_, (size_t)B * 2);
+    basis_final_ = dalloc<double>(s0_, allocs_,(size_t)B * kfin * n);
+    slem_out_ = dalloc<double>(s0_, allocs_,(size_t)B * 8);
+    tmp_m_ = dalloc<double>(s0_, allocs_,(size_t)B * m);
+    tmp_m2_ = dalloc<double>(s0_, allocs_,(size_t)B * m);
+    worst_ = dalloc<double>(s0_, allocs_,B);
+    fs_scal_ = dalloc<double>(s0_, allocs_,(size_t)B * 2);
     TPB_CUDA(cudaMallocHost(&h_ctl_, (size_t)B * 8 * sizeof(int)));
-    TPB_CUDA(cudaMemset(d_.ictl, 0, (size_t)B * 8 * sizeof(int)));
+    TPB_CUDA(cudaMemsetAsync(d_.ictl, 0, (size_t)B * 8 * sizeof(int), s0_));
+    // allocations are ordered on s0_; later work also runs on s1_/s2_ and the
+    // legacy stream, so complete them here
+    TPB_CUDA(cudaStreamSynchronize(s0_));
 }
 
 void Solver::set_warm(int b, const std::vector<int>& packed) {
@@ -215,13 +252,16 @@ void Solver::start() {
         TPB_CUDA(cudaMemcpyAsync(list_count_, counts.data(), B * sizeof(int), cudaMemcpyHostToDevice, s0_));
         launch_feasible_a(d_, list_, list_count_, list_cap_, fs_scal_, s0_);
         final_slem(d_.X, list_, list_count_, slem_out_);  // SLEM of the warm start, stride nx
+        phase_mark("feasible start (pre-SLEM)");
         launch_feasible_b(d_, c_, slem_out_, fs_scal_, s0_);
+        phase_mark("feasible SLEM + fill");
         TPB_CUDA(cudaStreamSynchronize(s0_));  // host vectors above go out of scope
     }
     TPB_CUDA(cudaMemcpyAsync(d_.Y, d_.X, B * nx * sizeof(double), cudaMemcpyDeviceToDevice, s0_));
     TPB_CUDA(cudaMemcpyAsync(d_.bestY, d_.X, B * nx * sizeof(double), cudaMemcpyDeviceToDevice, s0_));
     TPB_CUDA(cudaStreamSynchronize(s0_));
     if (!g_chunk_) build_graphs();
+    phase_mark("graph capture");
     it_enqueued_ = 0;
 }
 
@@ -400,8 +440,10 @@ void Solver::finish() {
         const double* pick = (R.converged ? d_.Y : d_.bestY) + (size_t)b * lo_.nx;
         TPB_CUDA(cudaMemcpy(&R.lambda_tilde, pick + lo_.lambda_ix, sizeof(double), cudaMemcpyDeviceToHost));
     }
+    phase_mark("iterations");
     if (het_) epilogue_het();
     else epilogue_hom();
+    phase_mark("extraction + final SLEM");
 }
 
 void Solver::epilogue_hom() {

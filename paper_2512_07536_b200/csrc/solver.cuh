@@ -25,6 +25,7 @@ struct Config {
 };
 
 void validate(const Config& c);
+void phase_mark(const char* what);
 
 // One-off spectral reports (feasible start, final topology): complete Krylov
 // space up to this dimension, restarted Lanczos with this basis beyond.
