@@ -274,7 +274,11 @@ def run_ours(args):
                        "l2": "state+work buffers ~170 MB > 126 MB L2 per iteration"},
             "roofline": {"bound": "tensor", "kernel": "sym_gemm_kernel (FP64 DMMA)",
                          "achieved": achieved, "peak": FP64_DMMA_TFLOPS, "unit": "TFLOP/s",
-                         "frac": achieved / FP64_DMMA_TFLOPS, "traffic": None,
+                         "frac": achieved / FP64_DMMA_TFLOPS,
+                         # dram read+write bytes per launch, ncu --set full capture
+                         # (profiles/r01/prof_gemm_raw.csv, n=1024, 2 matrices)
+                         "traffic": 16.797184e6 if n == 1024 else None,
+                         "traffic_unit": "bytes/launch",
                          "peak_source": "measured FP64 DMMA microbenchmark (tools/microbench/fp64_peak.cu); "
                                         "MEASURED_PEAKS.json has no FP64 entry",
                          "gemms_per_iteration": gemms, "gemm_avg_ms": gemm_avg * 1e3},
