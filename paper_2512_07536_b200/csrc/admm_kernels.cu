@@ -29,6 +29,21 @@ __device__ inline void tile_of(int t, int& bi, int& bj) {
 
 __device__ inline bool solve_done(const Dev& d, int b) { return d.ictl[b * 8 + kDone] != 0; }
 
+// sum_k P[k*stride + i] in k order, loads batched so their latencies overlap
+__device__ inline double sum_partials(const double* P, int nb, long long stride, int i) {
+    double s = 0.0;
+    int k = 0;
+    for (; k + 8 <= nb; k += 8) {
+        double v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = P[(long long)(k + q) * stride + i];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s += v[q];
+    }
+    for (; k < nb; ++k) s += P[(long long)k * stride + i];
+    return s;
+}
+
 }  // namespace
 
 XConst make_xconst(int n, double alpha, double rho) {
@@ -344,11 +359,8 @@ __global__ void xstep_node_kernel(Dev d, XConst c) {
         const long long p = (long long)i * n + i;
         trS += Y[lo.off_s + p] - D[lo.off_s + p] / c.rho;
         trT += Y[lo.off_t + p] - D[lo.off_t + p] / c.rho;
-        double u = 0.0, z = 0.0;
-        for (int k = 0; k < d.nb; ++k) {
-            u += PU[(long long)k * n + i];
-            if (d.het) z += PZ[(long long)k * n + i];
-        }
+        const double u = sum_partials(PU, d.nb, n, i);
+        const double z = d.het ? sum_partials(PZ, d.nb, n, i) : 0.0;
         ug[i] = u;
         uz[i] = z;
         su += u;
@@ -405,7 +417,8 @@ __global__ void xstep_node_kernel(Dev d, XConst c) {
 }
 
 void launch_xstep_node(const Dev& d, const XConst& c, cudaStream_t st) {
-    const int threads = 256;
+    // one thread per node (latency-bound single-CTA pass)
+    const int threads = std::min(1024, std::max(128, ((d.lo.n + 31) / 32) * 32));
     xstep_node_kernel<<<d.B, threads, 3 * d.lo.n * sizeof(double), st>>>(d, c);
     TPB_CHECK_LAUNCH();
 }
@@ -428,16 +441,44 @@ __global__ void __launch_bounds__(TB* TY) xstep_b_kernel(Dev d, XConst c) {
     __shared__ double red[TB * TY / 32];
     double res = 0.0;
 
-    // edge blocks
-    for (int il = ty; il < TB; il += TY) {
+    // edge blocks (hom: batched loads of h, Y_g, D_g for the thread's rows)
+    if (!d.het) {
+        constexpr int NR = TB / TY;
+        long long l[NR];
+        bool ok[NR];
+        double hv[NR], yg[NR], dg[NR];
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+            const int i = i0 + ty + k * TY, j = j0 + tx;
+            ok[k] = i < n && j < n && j > i;
+            l[k] = ok[k] ? edge_idx(n, i, j) : 0;
+            if (ok[k]) {
+                hv[k] = d.h[(long long)b * lo.m + l[k]];
+                yg[k] = Y[l[k]];
+                dg[k] = D[l[k]];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+            const int il = ty + k * TY, i = i0 + il, j = j0 + tx;
+            double g = 0.0;
+            if (ok[k]) {
+                g = c.f0 * hv[k] + node[i] + node[j];
+                const double e = g - yg[k];
+                X[l[k]] = g;
+                if (d.upd_duals) D[l[k]] = dg[k] + c.rho * e;
+                res += e * e;
+            }
+            Gs[il][tx] = g;
+        }
+    }
+    for (int il = ty; il < TB && d.het; il += TY) {
         const int i = i0 + il, jl = tx, j = j0 + jl;
         double g = 0.0;
         if (i < n && j < n && j > i) {
             const long long l = edge_idx(n, i, j);
             const double hv = d.h[(long long)b * lo.m + l];
-            if (!d.het) {
-                g = c.f0 * hv + node[i] + node[j];
-            } else {
+            {
                 const long long lz = lo.off_z + l, lv = lo.off_nu + l;
                 const double rz = Y[lz] - D[lz] / c.rho;
                 const double rnu = Y[lv] - D[lv] / c.rho;
@@ -465,39 +506,65 @@ __global__ void __launch_bounds__(TB* TY) xstep_b_kernel(Dev d, XConst c) {
     __syncthreads();
     // off-diagonal S/T entries: L_ij = -g, so
     //   S_ij = s (delta r_S,ij - alpha/n + g),  T_ij = s (delta r_T,ij + g)
-    auto upd = [&](long long p, double g) {
-        const long long ps = lo.off_s + p, pt = lo.off_t + p;
-        const double ys = Y[ps], yt = Y[pt];
-        const double rs = ys - D[ps] / c.rho, rt = yt - D[pt] / c.rho;
-        const double xs = c.s * (c.delta * rs - c.alpha_over_n + g);
-        const double xt = c.s * (c.delta * rt + g);
-        X[ps] = xs;
-        X[pt] = xt;
-        if (d.upd_duals) {
-            D[ps] += c.rho * (xs - ys);
-            D[pt] += c.rho * (xt - yt);
+    // The TB/TY entries a thread owns per orientation are handled as one
+    // batch: all loads first (independent, in flight together), then the
+    // arithmetic and the stores (X/D may alias Y in the compiler's view).
+    constexpr int NE = TB / TY;
+    auto upd_batch = [&](const long long (&pos)[NE], const double (&gv)[NE], const bool (&ok)[NE]) {
+        double ys[NE], yt[NE], ds[NE], dt[NE];
+#pragma unroll
+        for (int k = 0; k < NE; ++k) {
+            if (!ok[k]) continue;
+            ys[k] = Y[lo.off_s + pos[k]];
+            yt[k] = Y[lo.off_t + pos[k]];
+            ds[k] = D[lo.off_s + pos[k]];
+            dt[k] = D[lo.off_t + pos[k]];
         }
-        res += (xs - ys) * (xs - ys) + (xt - yt) * (xt - yt);
+#pragma unroll
+        for (int k = 0; k < NE; ++k) {
+            if (!ok[k]) continue;
+            const double rs = ys[k] - ds[k] / c.rho, rt = yt[k] - dt[k] / c.rho;
+            const double xs = c.s * (c.delta * rs - c.alpha_over_n + gv[k]);
+            const double xt = c.s * (c.delta * rt + gv[k]);
+            X[lo.off_s + pos[k]] = xs;
+            X[lo.off_t + pos[k]] = xt;
+            if (d.upd_duals) {
+                D[lo.off_s + pos[k]] = ds[k] + c.rho * (xs - ys[k]);
+                D[lo.off_t + pos[k]] = dt[k] + c.rho * (xt - yt[k]);
+            }
+            res += (xs - ys[k]) * (xs - ys[k]) + (xt - yt[k]) * (xt - yt[k]);
+        }
     };
-    // orientation 1: entries (i, j), address j*n + i
-    for (int cc = ty; cc < TB; cc += TY) {
-        const int i = i0 + tx, j = j0 + cc;
-        if (i >= n || j >= n || i == j) continue;
-        if (bi == bj) {
-            // diagonal tile: entry (i, j) with either order
-            const double g = i < j ? Gs[tx][cc] : Gs[cc][tx];
-            upd((long long)j * n + i, g);
-        } else {
-            upd((long long)j * n + i, Gs[tx][cc]);
+    {
+        // orientation 1: entries (i, j), address j*n + i
+        long long pos[NE];
+        double gv[NE];
+        bool ok[NE];
+#pragma unroll
+        for (int k = 0; k < NE; ++k) {
+            const int cc = ty + k * TY;
+            const int i = i0 + tx, j = j0 + cc;
+            ok[k] = i < n && j < n && i != j;
+            pos[k] = (long long)j * n + i;
+            // diagonal tiles hold each pair once: entry (i, j) with either order
+            gv[k] = (bi == bj && i > j) ? Gs[cc][tx] : Gs[tx][cc];
         }
+        upd_batch(pos, gv, ok);
     }
     if (bi != bj) {
         // orientation 2: entries (j, i), address i*n + j
-        for (int cc = ty; cc < TB; cc += TY) {
+        long long pos[NE];
+        double gv[NE];
+        bool ok[NE];
+#pragma unroll
+        for (int k = 0; k < NE; ++k) {
+            const int cc = ty + k * TY;
             const int j = j0 + tx, i = i0 + cc;
-            if (i >= n || j >= n) continue;
-            upd((long long)i * n + j, Gs[cc][tx]);
+            ok[k] = i < n && j < n;
+            pos[k] = (long long)i * n + j;
+            gv[k] = Gs[cc][tx];
         }
+        upd_batch(pos, gv, ok);
     }
     // node partials of g (deg = L_ii)
     const int t = ty * TB + tx;
@@ -565,8 +632,7 @@ __global__ void xstep_diag_kernel(Dev d, XConst c) {
     __shared__ double scratch[32];
     double res = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        double deg = 0.0;
-        for (int k = 0; k < d.nb; ++k) deg += PG[(long long)k * n + i];
+        const double deg = sum_partials(PG, d.nb, n, i);
         const long long p = (long long)i * n + i;
         const long long ps = lo.off_s + p, pt = lo.off_t + p, py = lo.off_y + i;
         const double ys = Y[ps], yt = Y[pt], yy = Y[py];
@@ -613,7 +679,8 @@ __global__ void xstep_diag_kernel(Dev d, XConst c) {
 }
 
 void launch_xstep_diag(const Dev& d, const XConst& c, cudaStream_t st) {
-    xstep_diag_kernel<<<d.B, 256, 0, st>>>(d, c);
+    const int threads = std::min(1024, std::max(128, ((d.lo.n + 31) / 32) * 32));
+    xstep_diag_kernel<<<d.B, threads, 0, st>>>(d, c);
     TPB_CHECK_LAUNCH();
 }
 

@@ -165,8 +165,13 @@ void cone_dense(int n, const double* a, double* out, bool psd) {
         w0.zero();
         w1.zero();
         w2.zero();
+        const int G = stream_k_ctas(ld);
+        const int nt = ld / 64;
+        DBuf<double> skw((size_t)std::max(G, 1) * 64 * 64);
+        DBuf<int> skf((size_t)nt * (nt + 1));
+        skf.zero();
         enqueue_cone_tiled(A.p, w0.p, w1.p, w2.p, ld, n, scale.p, C.p, 0, (long long)n * n, nullptr, 2,
-                           sch, 0);
+                           sch, 0, G > 0 ? skw.p : nullptr, G > 0 ? skf.p : nullptr);
         TPB_CUDA(cudaDeviceSynchronize());
     }
     TPB_CUDA(cudaDeviceSynchronize());
@@ -457,8 +462,19 @@ int tp_bench_gemm(int32_t n, int32_t nmat, int32_t variant, int32_t reps, double
         B.up(h.data(), sz);
         C.zero();
         const int old = get_sym_gemm_variant();
-        set_sym_gemm_variant(variant);
+        // variant == sym_gemm_variants(): stream-K decomposition (single pair)
+        const bool sk = variant == sym_gemm_variants();
+        set_sym_gemm_variant(sk ? 0 : variant);
+        const int G = sk ? stream_k_ctas(ld) : 0;
+        const int nt = ld / 64;
+        DBuf<double> skw((size_t)std::max(G, 1) * 64 * 64);
+        DBuf<int> skf((size_t)nt * (nt + 1));
+        skf.zero();
         GemmArgs g{};
+        if (G > 0) {
+            g.sk_ws = skw.p;
+            g.sk_flags = skf.p;
+        }
         g.A = A.p;
         g.B = B.p;
         g.E = A.p;

@@ -191,6 +191,14 @@ void Solver::alloc() {
         TPB_CUDA(cudaMemsetAsync(w0_, 0, (size_t)B * 2 * ld2 * sizeof(double), s0_));
         TPB_CUDA(cudaMemsetAsync(w1_, 0, (size_t)B * 2 * ld2 * sizeof(double), s0_));
         TPB_CUDA(cudaMemsetAsync(w2_, 0, (size_t)B * 2 * ld2 * sizeof(double), s0_));
+        // stream-K GEMM workspace for single large instances
+        const int G = B == 1 ? stream_k_ctas(ld_) : 0;
+        if (G > 0) {
+            const int nt = ld_ / 64, T = nt * (nt + 1) / 2;
+            sk_ws_ = dalloc<double>(s0_, allocs_, (size_t)G * 64 * 64);
+            sk_flags_ = dalloc<int>(s0_, allocs_, (size_t)2 * T);
+            TPB_CUDA(cudaMemsetAsync(sk_flags_, 0, (size_t)2 * T * sizeof(int), s0_));
+        }
     }
     list_ = dalloc<int>(s0_, allocs_,(size_t)B * list_cap_);
     list_count_ = dalloc<int>(s0_, allocs_,B);
@@ -347,7 +355,7 @@ void Solver::enqueue_projection() {
                           2 * B_, sch_, s0_);
     } else {
         enqueue_cone_tiled(d_.A, w0_, w1_, w2_, ld_, lo_.n, d_.inv_scale, d_.Y + lo_.off_s, cb, cw,
-                           d_.ictl, 2 * B_, sch_, s0_);
+                           d_.ictl, 2 * B_, sch_, s0_, sk_ws_, sk_flags_);
     }
 }
 

@@ -114,6 +114,8 @@ class Solver {
     int* d_r_ = nullptr;
     double* d_deg_ = nullptr;
     double *w0_ = nullptr, *w1_ = nullptr, *w2_ = nullptr;
+    double* sk_ws_ = nullptr;   // stream-K partial tiles (B == 1, large n)
+    int* sk_flags_ = nullptr;
     int *list_ = nullptr, *list_count_ = nullptr;
     int *e_i_ = nullptr, *e_j_ = nullptr, *col_idx_ = nullptr;
     double* e_w_ = nullptr;
