@@ -132,6 +132,20 @@ int tp_solver_launches_per_iteration(tp_solver* s, int32_t* out);
  * matrices of order n (event-timed, ms per launch). */
 int tp_set_gemm_variant(int32_t variant);
 int tp_bench_gemm(int32_t n, int32_t nmat, int32_t variant, int32_t reps, double* ms_per_launch);
+/* One Ozaki-scheme GEMM on the int8 tensor cores (tcgen05 kind::i8) over nmat
+ * symmetric ld x ld host matrices (ld % 128 == 0): C = alpha A.B + beta E
+ * (E = A if use_e), operands split into 8 digit planes with exponents ea, eb;
+ * optional digit planes of C (exponent ec, nmat x 8 x ld x ld int8). reps > 0
+ * re-runs the GEMM and returns the event-timed ms per launch. */
+int tp_oz_gemm(int32_t ld, int32_t nmat, const double* a, int32_t ea, const double* b, int32_t eb,
+               int32_t use_e, double alpha, double beta, double* c, int8_t* cd, int32_t ec,
+               int32_t reps, double* ms);
+/* Instrumented variant: mode bit 0 skips the MMAs, bit 1 the TMA loads;
+ * stamps (4 globaltimer ns values per CTA: start, setup, accumulators
+ * ready, end) if non-null. */
+int tp_oz_gemm_dbg(int32_t ld, int32_t nmat, const double* a, int32_t ea, const double* b, int32_t eb,
+                   int32_t use_e, double alpha, double beta, double* c, int8_t* cd, int32_t ec,
+                   int32_t reps, double* ms, int32_t mode, long long* stamps);
 
 /* ---------------------------------------------------------------- substeps */
 /* project_Y (proj/src/admm.cpp:268-277); x, d, y of length nx. */

@@ -84,6 +84,9 @@ SIGNATURES = {
     "tp_solver_launches_per_iteration": (_I, [_P, _ip]),
     "tp_set_gemm_variant": (_I, [_I]),
     "tp_bench_gemm": (_I, [_I, _I, _I, _I, _dp]),
+    "tp_oz_gemm": (_I, [_I, _I, _dp, _I, _dp, _I, _I, C.c_double, C.c_double, _dp, C.c_void_p, _I, _I, _dp]),
+    "tp_oz_gemm_dbg": (_I, [_I, _I, _dp, _I, _dp, _I, _I, C.c_double, C.c_double, _dp, C.c_void_p, _I, _I,
+                            _dp, _I, C.c_void_p]),
     "tp_project_Y": (_I, [_I, _I, _D, _D, _dp, _dp, _dp]),
     "tp_project_Y_het_node": (_I, [_I, _ip, _D, _D, _dp, _dp, _dp]),
     "tp_update_X": (_I, [_I, _I, _D, _D, _dp, _dp, _dp]),

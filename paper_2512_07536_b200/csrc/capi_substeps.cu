@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "../../include/topoopt_b200.h"
+#include "ozaki_kernels.cuh"
 #include "solver.cuh"
 
 using namespace tpb;
@@ -501,6 +502,81 @@ int tp_bench_gemm(int32_t n, int32_t nmat, int32_t variant, int32_t reps, double
         cudaEventDestroy(e1);
         set_sym_gemm_variant(old);
         *ms_per_launch = ms / reps;
+    });
+}
+
+// One Ozaki-scheme GEMM (ozaki_kernels.cuh) on nmat symmetric ld x ld
+// matrices (host, ld % 128 == 0): digit planes of A and B (exponents eA, eB)
+// are made on the device, then C = alpha A.B + beta E (E = A if use_e) with
+// FP64 output C and, if cd != null, the digit planes of C (exponent eC).
+// Repeats the GEMM `reps` times (event-timed, ms per launch in *ms).
+int tp_oz_gemm(int32_t ld, int32_t nmat, const double* a, int32_t ea, const double* b, int32_t eb,
+               int32_t use_e, double alpha, double beta, double* c, int8_t* cd, int32_t ec,
+               int32_t reps, double* ms) {
+    return tp_oz_gemm_dbg(ld, nmat, a, ea, b, eb, use_e, alpha, beta, c, cd, ec, reps, ms, 0, nullptr);
+}
+
+int tp_oz_gemm_dbg(int32_t ld, int32_t nmat, const double* a, int32_t ea, const double* b, int32_t eb,
+                   int32_t use_e, double alpha, double beta, double* c, int8_t* cd, int32_t ec,
+                   int32_t reps, double* ms, int32_t mode, long long* stamps) {
+    return guarded([&] {
+        require_device();
+        init_attrs();
+        if (ld <= 0 || ld % kOzBM != 0 || nmat <= 0)
+            throw Error(kInvalidArgument, "tp_oz_gemm: ld must be a positive multiple of 128");
+        const size_t sz = (size_t)nmat * ld * ld;
+        DBuf<double> A(sz), B(sz), C(sz);
+        DBuf<int8_t> Ad(sz * kOzSlices), Bd(sz * kOzSlices), Cd(sz * kOzSlices);
+        A.up(a, sz);
+        B.up(b, sz);
+        C.zero();
+        Cd.zero();
+        launch_oz_split(A.p, (long long)ld * ld, ld, nmat, nullptr, ea, Ad.p, nullptr, 0);
+        launch_oz_split(B.p, (long long)ld * ld, ld, nmat, nullptr, eb, Bd.p, nullptr, 0);
+        OzMaps ma, mb;
+        make_oz_maps(Ad.p, ld, nmat, &ma);
+        make_oz_maps(Bd.p, ld, nmat, &mb);
+        OzGemm g{};
+        g.ma = &ma;
+        g.mb = &mb;
+        g.eA = ea;
+        g.eB = eb;
+        g.ld = ld;
+        g.nmat = nmat;
+        g.alpha_c = alpha;
+        g.beta_c = beta;
+        g.E = use_e ? A.p : nullptr;
+        g.C = C.p;
+        g.c_stride_b = 2LL * ld * ld;
+        g.c_stride_w = (long long)ld * ld;
+        g.ldc = ld;
+        g.nvalid = ld;
+        g.Cd = cd ? Cd.p : nullptr;
+        g.eC = ec;
+        g.dbg_mode = mode;
+        const size_t nst = (size_t)4 * oz_gemm_tiles(ld) * nmat;
+        DBuf<long long> st(nst);
+        g.dbg_t = stamps ? st.p : nullptr;
+        launch_oz_gemm(g, 0);
+        TPB_CUDA(cudaDeviceSynchronize());
+        if (stamps) st.down(stamps, nst);
+        g.dbg_t = nullptr;
+        C.down(c, sz);
+        if (cd) Cd.down(cd, sz * kOzSlices);
+        if (reps > 0) {
+            cudaEvent_t e0, e1;
+            TPB_CUDA(cudaEventCreate(&e0));
+            TPB_CUDA(cudaEventCreate(&e1));
+            TPB_CUDA(cudaEventRecord(e0, 0));
+            for (int k = 0; k < reps; ++k) launch_oz_gemm(g, 0);
+            TPB_CUDA(cudaEventRecord(e1, 0));
+            TPB_CUDA(cudaEventSynchronize(e1));
+            float t = 0.f;
+            TPB_CUDA(cudaEventElapsedTime(&t, e0, e1));
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+            if (ms) *ms = t / reps;
+        }
     });
 }
 

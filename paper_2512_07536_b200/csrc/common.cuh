@@ -61,12 +61,14 @@ void init_attrs_slem();
 void init_attrs_cone();
 void init_attrs_admm();
 void init_attrs_misc();
+void init_attrs_ozaki();
 inline void init_attrs() {
     init_attrs_select();
     init_attrs_slem();
     init_attrs_cone();
     init_attrs_admm();
     init_attrs_misc();
+    init_attrs_ozaki();
 }
 
 // Flat state layout of one solve (proj/src/admm.cpp:24-44). g is the packed

@@ -1,0 +1,82 @@
+// FP64 products of symmetric matrices on the int8 tensor cores (tcgen05
+// kind::i8): Ozaki scheme I with fixed power-of-two operand scales.
+//
+//   M = 2^e sum_{s=1..KS} 2^{-7s} M_s,   M_s int8 "digit planes" in [-127, 127]
+//   A.B ~= 2^{eA+eB} sum_{d=2..KS+1} 2^{-7d} G_d,   G_d = sum_{s+t=d} A_s . B_t
+//
+// Every A_s . B_t is exact (int32 accumulation in TMEM, |G_d| < 2^31 for
+// K <= 16384); only the FP64 epilogue rounds. The scales are static bounds
+// from the sign iteration (|X| <= 1.21, |Y| <= 1.45,
+// |Z| <= 2.81 in spectral norm, hence entrywise), so a producer GEMM writes
+// its consumer's digit planes in its own epilogue. Accuracy study:
+// tools/proto/ozaki.py.
+#pragma once
+
+#include <cuda.h>
+
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace tpb {
+
+constexpr int kOzSlices = 8;   // digits per operand (56 bits)
+constexpr int kOzBM = 128;     // tile rows (UMMA M)
+constexpr int kOzBN = 64;      // tile cols (UMMA N); KS accumulators x BN <= 512 TMEM columns
+constexpr int kOzBK = 64;      // k bytes per pipeline stage (SWIZZLE_64B rows)
+
+// Digit planes of nmat symmetric ld x ld matrices: [mat][slice][ld][ld] int8.
+struct OzPlanes {
+    int8_t* d = nullptr;
+    int e = 0;  // matrix = 2^e sum_s 2^{-7s} plane_s
+};
+
+// TMA maps of one plane buffer in the A role (box kOzBM rows) and the B role
+// (box kOzBN rows).
+struct OzMaps {
+    CUtensorMap a, b;
+};
+void make_oz_maps(const int8_t* planes, int ld, int nmat, OzMaps* out);
+
+struct OzGemm {
+    const OzMaps* ma;        // operand A planes (row block i0)
+    const OzMaps* mb;        // operand B planes (row block j0 of B = column block of B^T)
+    int eA, eB;
+    int ld, nmat;
+    double alpha_c, beta_c;  // C = alpha (A.B) + beta E, alpha = alpha_c s^pa, beta = beta_c s^pb
+    int pa, pb;
+    const double* scale;     // per matrix s, or null (s = 1)
+    int sign_mode;           // alpha *= -1 for even matrices (S -> NSD)
+    const double* E;         // FP64 symmetric, mat stride ld*ld, or null
+    double* C;               // FP64 out, or null
+    long long c_stride_b, c_stride_w;
+    int ldc, nvalid;
+    int8_t* Cd;              // digit planes out ([mat][slice][ld][ld]), or null
+    int eC;
+    const int* ictl;         // done flags per solve (matrix / 2), or null
+    long long* dbg_t;        // instrumentation: 4 globaltimer stamps per CTA, or null
+    int dbg_mode;            // instrumentation: bit 0 skips the MMAs, bit 1 the TMA loads
+};
+
+void launch_oz_gemm(const OzGemm& g, cudaStream_t st);
+int oz_gemm_tiles(int ld);
+
+// Digit-plane buffers of the cone projection: [0..2] pair with the three FP64
+// work buffers, [3] holds X0 = A / ||A||_F.
+struct OzWork {
+    int8_t* d[4] = {nullptr, nullptr, nullptr, nullptr};
+    OzMaps maps[4];
+};
+
+struct SignSchedule;
+// Ozaki-scheme counterpart of enqueue_cone_tiled (cone_kernels.cuh): the
+// same sign iteration, every product on the int8 tensor cores.
+void enqueue_cone_ozaki(const double* A, double* w0, double* w1, double* w2, const OzWork& oz, int ld,
+                        int n, const double* scale, double* C, long long c_stride_b, long long c_stride_w,
+                        const int* ictl, int nmat, const SignSchedule& sch, cudaStream_t st);
+
+// Digit planes of s * A (s = scale[mat] or 1) with exponent e.
+void launch_oz_split(const double* A, long long mstride, int ld, int nmat, const double* scale,
+                     int e, int8_t* planes, const int* ictl, cudaStream_t st);
+
+}  // namespace tpb

@@ -103,7 +103,13 @@ Solver::Solver(int n, int B, bool het, const std::vector<int>& r, const std::vec
     }
     c_ = make_xconst(n, cfg.alpha, cfg.rho);
     small_ = n <= 64;
-    ld_ = small_ ? ((n + 7) & ~7) : ((n + 63) / 64) * 64;
+    // Tiled projections: int8 tensor-core (Ozaki) GEMMs by default, FP64 DMMA
+    // with TPB_CONE=dmma; the Ozaki tiles need ld % 128 == 0.
+    {
+        const char* cone = std::getenv("TPB_CONE");
+        ozaki_ = !small_ && !(cone && std::string(cone) == "dmma");
+    }
+    ld_ = small_ ? ((n + 7) & ~7) : (ozaki_ ? ((n + 127) / 128) * 128 : ((n + 63) / 64) * 64);
     list_cap_ = het ? m : *std::max_element(r_host_.begin(), r_host_.end());
     int chunk = cfg.chunk > 0 ? cfg.chunk : (n <= 64 ? 32 : (n <= 256 ? 16 : 8));
     chunk = ((chunk + cfg.trace_stride - 1) / cfg.trace_stride) * cfg.trace_stride;
@@ -191,6 +197,13 @@ void Solver::alloc() {
         TPB_CUDA(cudaMemsetAsync(w0_, 0, (size_t)B * 2 * ld2 * sizeof(double), s0_));
         TPB_CUDA(cudaMemsetAsync(w1_, 0, (size_t)B * 2 * ld2 * sizeof(double), s0_));
         TPB_CUDA(cudaMemsetAsync(w2_, 0, (size_t)B * 2 * ld2 * sizeof(double), s0_));
+        if (ozaki_) {
+            for (int q = 0; q < 4; ++q) {
+                oz_.d[q] = dalloc<int8_t>(s0_, allocs_, (size_t)B * 2 * kOzSlices * ld2);
+                TPB_CUDA(cudaMemsetAsync(oz_.d[q], 0, (size_t)B * 2 * kOzSlices * ld2, s0_));
+                make_oz_maps(oz_.d[q], ld_, 2 * B, &oz_.maps[q]);
+            }
+        }
         // stream-K GEMM workspace for single large instances
         const int G = B == 1 ? stream_k_ctas(ld_) : 0;
         if (G > 0) {
@@ -341,6 +354,7 @@ void Solver::enqueue_slem_trace(cudaStream_t st) {
     a.ritz = ritz_;
     a.ritz_ok = ritz_ok_;
     a.tol = cfg_.slem_tol;
+    if (const char* t = std::getenv("TPB_SLEM_TOL")) a.tol = std::atof(t);  // experiments
     a.out = nullptr;
     a.tr_acf = d_.tr_acf;
     a.ictl = d_.ictl;
@@ -353,6 +367,9 @@ void Solver::enqueue_projection() {
     if (small_) {
         launch_cone_small(d_.A, (long long)ld_ * ld_, ld_, lo_.n, d_.Y + lo_.off_s, cb, cw, d_.ictl,
                           2 * B_, sch_, s0_);
+    } else if (ozaki_) {
+        enqueue_cone_ozaki(d_.A, w0_, w1_, w2_, oz_, ld_, lo_.n, d_.inv_scale, d_.Y + lo_.off_s, cb, cw,
+                           d_.ictl, 2 * B_, sch_, s0_);
     } else {
         enqueue_cone_tiled(d_.A, w0_, w1_, w2_, ld_, lo_.n, d_.inv_scale, d_.Y + lo_.off_s, cb, cw,
                            d_.ictl, 2 * B_, sch_, s0_, sk_ws_, sk_flags_);

@@ -7,6 +7,7 @@
 #include "admm_kernels.cuh"
 #include "cone_kernels.cuh"
 #include "misc_kernels.cuh"
+#include "ozaki_kernels.cuh"
 #include "select_kernels.cuh"
 #include "slem_kernels.cuh"
 
@@ -20,7 +21,7 @@ struct Config {
     double weight_floor = 1e-6;
     double linear_tol = 1e-10;  // accepted for API parity; the x-step is exact
     int trace_stride = 1;       // acf_iterate every k-th iteration (reference: 1)
-    double slem_tol = 1e-7;     // trace Lanczos residual tolerance (eigenvalue error <= tol^2/gap)
+    double slem_tol = 1e-6;     // trace Lanczos residual tolerance (eigenvalue error <= tol^2/gap)
     int chunk = 0;              // iterations per CUDA graph (0: auto)
 };
 
@@ -114,6 +115,8 @@ class Solver {
     int* d_r_ = nullptr;
     double* d_deg_ = nullptr;
     double *w0_ = nullptr, *w1_ = nullptr, *w2_ = nullptr;
+    bool ozaki_ = false;        // cone GEMMs on the int8 tensor cores (else FP64 DMMA)
+    OzWork oz_;
     double* sk_ws_ = nullptr;   // stream-K partial tiles (B == 1, large n)
     int* sk_flags_ = nullptr;
     int *list_ = nullptr, *list_count_ = nullptr;

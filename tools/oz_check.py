@@ -1,0 +1,82 @@
+"""Ozaki-scheme tcgen05 GEMM (tp_oz_gemm) vs an exact numpy emulation and
+vs FP64 numpy; timing per launch. Run on a GPU box:
+    python tools/oz_check.py [ld ...]
+"""
+import ctypes as C
+import sys
+
+import numpy as np
+
+sys.path.insert(0, ".")
+from paper_2512_07536_b200 import _lib  # noqa: E402
+
+KS = 8
+
+
+def planes(M, e):
+    u = M * 2.0 ** (-e)
+    out = []
+    for _ in range(KS):
+        u = u * 128.0
+        d = np.trunc(u)
+        out.append(d)
+        u = u - d
+    return out
+
+
+def emulate(A, eA, B, eB):
+    As, Bs = planes(A, eA), planes(B, eB)
+    acc = np.zeros_like(A)
+    for d in range(KS + 1, 1, -1):
+        g = np.zeros_like(A)
+        for s in range(max(1, d - KS), min(KS, d - 1) + 1):
+            g += As[s - 1] @ Bs[d - s - 1]
+        acc += g * 2.0 ** (-7 * d)
+    acc *= 2.0 ** (eA + eB)
+    return np.tril(acc) + np.tril(acc, -1).T
+
+
+def sym_matrix(rng, n, bound):
+    Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    ev = rng.uniform(-bound, bound, n)
+    M = (Q * ev) @ Q.T
+    return 0.5 * (M + M.T)
+
+
+def run(ld, nmat=2, reps=20, use_e=0, beta=0.0):
+    lib = _lib.load()
+    rng = np.random.default_rng(ld)
+    A = np.stack([sym_matrix(rng, ld, 1.2) for _ in range(nmat)])
+    B = np.stack([sym_matrix(rng, ld, 1.4) for _ in range(nmat)])
+    Cg = np.zeros_like(A)
+    Cd = np.zeros((nmat, KS, ld, ld), dtype=np.int8)
+    ms = C.c_double(0)
+    dp = C.POINTER(C.c_double)
+    rc = lib.tp_oz_gemm(ld, nmat, A.ctypes.data_as(dp), 1, B.ctypes.data_as(dp), 1, use_e, 1.0, beta,
+                        Cg.ctypes.data_as(dp), Cd.ctypes.data_as(C.c_void_p), 2, reps, C.byref(ms))
+    if rc != 0:
+        raise RuntimeError(lib.tp_last_error_message().decode() if hasattr(lib, "tp_last_error_message") else rc)
+    worst_emu = worst_fp = worst_dig = 0.0
+    for m in range(nmat):
+        emu = emulate(A[m], 1, B[m], 1) + (beta * A[m] if use_e else 0.0)
+        ex = A[m] @ B[m]
+        ex = np.tril(ex) + np.tril(ex, -1).T + (beta * A[m] if use_e else 0.0)
+        sc = np.abs(ex).max()
+        worst_emu = max(worst_emu, np.abs(Cg[m] - emu).max() / sc)
+        worst_fp = max(worst_fp, np.abs(Cg[m] - ex).max() / sc)
+        rec = sum(Cd[m, s].astype(np.float64) * 2.0 ** (-7 * (s + 1)) for s in range(KS)) * 4.0
+        worst_dig = max(worst_dig, np.abs(rec - Cg[m]).max())
+    tiles = 2 * (ld // 128) * (ld // 128 + 1) // 2
+    ops = 2.0 * 128 * 64 * ld * (KS * (KS + 1) // 2) * tiles * nmat  # int8 MACs x 2
+    print(f"ld={ld:5d} nmat={nmat} |C-emu|/max={worst_emu:.2e} |C-fp64|/max={worst_fp:.2e} "
+          f"|digits-C|={worst_dig:.2e}  {ms.value * 1e3:8.1f} us/launch  "
+          f"int8 {ops / ms.value / 1e9:7.1f} TOP/s  fp64-equiv {2.0 * ld ** 3 * nmat / 2 / ms.value / 1e9:6.1f} TFLOP/s",
+          flush=True)
+    return worst_emu, worst_fp
+
+
+if __name__ == "__main__":
+    lds = [int(a) for a in sys.argv[1:]] or [128, 256, 512, 1024]
+    for ld in lds:
+        run(ld)
+    run(256, use_e=1, beta=0.5)
