@@ -533,9 +533,10 @@ int tp_oz_gemm_dbg(int32_t ld, int32_t nmat, const double* a, int32_t ea, const 
         Cd.zero();
         launch_oz_split(A.p, (long long)ld * ld, ld, nmat, nullptr, ea, Ad.p, nullptr, 0);
         launch_oz_split(B.p, (long long)ld * ld, ld, nmat, nullptr, eb, Bd.p, nullptr, 0);
-        OzMaps ma, mb;
+        OzMaps ma, mb, mc;
         make_oz_maps(Ad.p, ld, nmat, &ma);
         make_oz_maps(Bd.p, ld, nmat, &mb);
+        make_oz_maps(Cd.p, ld, nmat, &mc);
         OzGemm g{};
         g.ma = &ma;
         g.mb = &mb;
@@ -552,9 +553,10 @@ int tp_oz_gemm_dbg(int32_t ld, int32_t nmat, const double* a, int32_t ea, const 
         g.ldc = ld;
         g.nvalid = ld;
         g.Cd = cd ? Cd.p : nullptr;
+        g.mc = &mc;
         g.eC = ec;
         g.dbg_mode = mode;
-        const size_t nst = (size_t)4 * oz_gemm_tiles(ld) * nmat;
+        const size_t nst = (size_t)8 * oz_gemm_tiles(ld) * nmat;
         DBuf<long long> st(nst);
         g.dbg_t = stamps ? st.p : nullptr;
         launch_oz_gemm(g, 0);

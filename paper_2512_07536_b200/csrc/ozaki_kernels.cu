@@ -32,11 +32,10 @@ constexpr int STAGES = 2;
 constexpr int A_PLANE = BM * BK, B_PLANE = BN * BK;              // bytes
 constexpr int STAGE_BYTES = KS * (A_PLANE + B_PLANE);            // 96 KB
 constexpr int CP = BM + 1;       // epilogue FP64 staging pitch (doubles)
-constexpr int DP = BN / 4 + 1;   // epilogue digit-word staging pitch (words)
-constexpr int CS_BYTES = BN * CP * 8;
-constexpr int DW_BYTES = KS * BM * DP * 4;
-constexpr int TB_BYTES = KS * BN * BM;
-constexpr int EPI_BYTES = CS_BYTES + DW_BYTES + TB_BYTES;
+constexpr int CS_BYTES = (BN * CP * 8 + 1023) / 1024 * 1024;
+constexpr int BOX_BYTES = 64 * 64;                 // one 64 x 64-byte TMA store box (SWIZZLE_64B)
+constexpr int DIG_BYTES = 2 * KS * 2 * BOX_BYTES;  // direct + mirror, KS planes, 2 halves
+constexpr int EPI_BYTES = CS_BYTES + DIG_BYTES;
 constexpr int SMEM_BYTES = (STAGES * STAGE_BYTES > EPI_BYTES ? STAGES * STAGE_BYTES : EPI_BYTES) + 1024;
 constexpr int EPI_WARPS = 8, EPI_THREADS = 32 * EPI_WARPS;
 constexpr int THREADS = 64 + EPI_THREADS;  // producer warp, MMA warp, epilogue warps
@@ -144,6 +143,62 @@ __device__ __forceinline__ void put_digits(double v, double inv2e, int lane4, ui
         w[s] |= ((uint32_t)dg & 0xFFu) << (8 * lane4);
     }
 }
+// Magnitude digits of 4 values as 8 plane words (byte k of word s = digit
+// s+1 of value k), negated bytewise for negative values: |v| 2^-e < 1.
+__device__ __forceinline__ uint32_t neg4(uint32_t w) {  // bytewise -b for b in [0, 127]
+    return ((~w & 0x7F7F7F7Fu) + 0x01010101u) ^ 0x80808080u;
+}
+__device__ __forceinline__ uint32_t spread7(uint32_t a) {  // 28-bit a -> [a&127, a>>7&127, ...]
+    return (a & 0x7Fu) | ((a << 1) & 0x7F00u) | ((a << 2) & 0x7F0000u) | ((a << 3) & 0x7F000000u);
+}
+__device__ __forceinline__ void digits4(const double (&v)[4], double s28, uint32_t (&w)[KS]) {
+    // |v| 2^-e = hi 2^-28 + lo 2^-56 with hi = rint(|v| 2^(28-e)) in [0, 2^28)
+    // and |lo| <= 2^27 (its own sign), both taken from the low mantissa bits
+    // after adding 1.5 2^52 (no conversion instructions); digit bytes are
+    // 7-bit groups of hi and |lo|, negated bytewise where needed.
+    constexpr double kM = 6755399441055744.0;  // 1.5 * 2^52
+    uint32_t ph[4], pl[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const double a = fabs(v[k]) * s28;
+        const double th = a + kM;
+        uint32_t hi = (uint32_t)__double2loint(th);
+        const double rem = a - (th - kM);
+        const int lo = __double2loint(fma(rem, 268435456.0, kM));
+        hi = hi > 0xFFFFFFFu ? 0xFFFFFFFu : hi;  // saturate (outside the static bounds)
+        uint32_t xh = spread7(hi), xl = spread7((uint32_t)(lo < 0 ? -lo : lo));
+        const bool neg = v[k] < 0.0;
+        if (neg) xh = neg4(xh);
+        if (neg != (lo < 0)) xl = neg4(xl);
+        ph[k] = xh;  // bytes: digit 4, 3, 2, 1
+        pl[k] = xl;  // bytes: digit 8, 7, 6, 5
+    }
+    // 4x4 byte transposes: word s collects digit s+1 of the four values
+    const uint32_t a = __byte_perm(ph[0], ph[1], 0x7362), b = __byte_perm(ph[2], ph[3], 0x7362);
+    const uint32_t c = __byte_perm(ph[0], ph[1], 0x5140), d = __byte_perm(ph[2], ph[3], 0x5140);
+    w[0] = __byte_perm(a, b, 0x7632);
+    w[1] = __byte_perm(a, b, 0x5410);
+    w[2] = __byte_perm(c, d, 0x7632);
+    w[3] = __byte_perm(c, d, 0x5410);
+    const uint32_t e = __byte_perm(pl[0], pl[1], 0x7362), f = __byte_perm(pl[2], pl[3], 0x7362);
+    const uint32_t g = __byte_perm(pl[0], pl[1], 0x5140), h = __byte_perm(pl[2], pl[3], 0x5140);
+    w[4] = __byte_perm(e, f, 0x7632);
+    w[5] = __byte_perm(e, f, 0x5410);
+    w[6] = __byte_perm(g, h, 0x7632);
+    w[7] = __byte_perm(g, h, 0x5410);
+}
+
+// 16-byte chunk address inside a 64 x 64-byte SWIZZLE_64B box
+__device__ __forceinline__ uint32_t sw64_off(int row, int chunk) {
+    return (uint32_t)(row * 64 + ((chunk ^ ((row >> 1) & 3)) << 4));
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(src), "r"(c0), "r"(c1)
+                 : "memory");
+}
+
 // lower tiles of a (ld/BM) x (ld/BN) grid: row block I holds col blocks
 // J < ceil((I+1) BM / BN)
 __host__ __device__ inline int tiles_before(int I) {
@@ -161,7 +216,7 @@ __device__ inline void oz_tile(int t, int& I, int& J) {
 
 __global__ void __launch_bounds__(THREADS, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-                   OzGemm g) {
+                   const __grid_constant__ CUtensorMap mapC, OzGemm g) {
     const int mat = blockIdx.y;
     if (g.ictl && g.ictl[(mat >> 1) * 8 + 1]) return;
     const long long t_start = g.dbg_t ? gtimer() : 0;
@@ -272,17 +327,25 @@ __global__ void __launch_bounds__(THREADS, 1)
         double acc[HN];
 #pragma unroll
         for (int j = 0; j < HN; ++j) acc[j] = 0.0;
+        static_assert(KS % 2 == 0, "groups are drained in pairs");
 #pragma unroll
-        for (int d = KS + 1; d >= 2; --d) {  // smallest contributions first
-            const double sc = ldexp(1.0, -7 * d);
-            uint32_t v[HN];
+        for (int d = KS + 1; d >= 2; d -= 2) {  // smallest contributions first, two groups per wait
+            uint32_t v[2][HN];
 #pragma unroll
-            for (int c = 0; c < HN / 16; ++c)
-                tmem_ld16(taddr + (uint32_t)((d - 2) * BN + c * 16), *reinterpret_cast<uint32_t(*)[16]>(v + c * 16));
+            for (int q2 = 0; q2 < 2; ++q2)
+#pragma unroll
+                for (int c = 0; c < HN / 16; ++c)
+                    tmem_ld16(taddr + (uint32_t)((d - q2 - 2) * BN + c * 16),
+                              *reinterpret_cast<uint32_t(*)[16]>(&v[q2][c * 16]));
             tmem_wait_ld();
 #pragma unroll
-            for (int j = 0; j < HN; ++j) acc[j] = fma((double)(int)v[j], sc, acc[j]);
+            for (int q2 = 0; q2 < 2; ++q2) {
+                const double sc = ldexp(1.0, -7 * (d - q2));
+#pragma unroll
+                for (int j = 0; j < HN; ++j) acc[j] = fma((double)(int)v[q2][j], sc, acc[j]);
+            }
         }
+        const long long t_acc = g.dbg_t ? gtimer() : 0;
         const double s = g.scale ? g.scale[mat] : 1.0;
         double alpha = g.alpha_c * spow(s, g.pa) * ldexp(1.0, g.eA + g.eB);
         const double beta = g.beta_c * spow(s, g.pb);
@@ -293,100 +356,128 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int j = 0; j < HN; ++j) {
             double v = alpha * acc[j];
             if (E) v = fma(beta, __ldg(E + (long long)(j0 + c0 + j) * ld + i), v);  // E symmetric
+            if (i == j0 + c0 + j) v += g.dshift;
             acc[j] = v;
         }
         // Stores. Every element (a, b) of C is written by exactly one tile:
         // the lower tile holding (max, min) writes (a >= b) directly and
         // (a > b) mirrored, so runs are deterministic.
+        // Stores. Ownership keeps C exactly symmetric and every element
+        // written once (deterministic): off-diagonal tiles (J < 2I) write
+        // themselves and their mirror; in the diagonal 128-row block, tile
+        // J = 2I owns rows 0..127 (its upper 64 x 64 sub-block symmetrised)
+        // plus the mirror of rows 64..127, tile J = 2I+1 only rows 64..127
+        // (lower-right sub-block symmetrised).
+        const int kind = J < 2 * I ? 0 : (J == 2 * I ? 1 : 2);
+        const int dr0 = kind == 2 ? 64 : 0;         // first directly owned tile row
+        const int mr0 = kind == 0 ? 0 : (kind == 1 ? 64 : BM);  // first mirrored tile row
         const int nv = g.nvalid;
         double* C = g.C ? g.C + (long long)(mat >> 1) * g.c_stride_b + (long long)(mat & 1) * g.c_stride_w
                         : nullptr;
-        int8_t* Cd = g.Cd ? g.Cd + (long long)mat * KS * ld * ld : nullptr;
-        const long long ld2 = (long long)ld * ld;
-        double* Cs = reinterpret_cast<double*>(sgen);                      // [BN][CP] FP64
-        uint32_t* Dw = reinterpret_cast<uint32_t*>(sgen + CS_BYTES);       // [KS][BM][DP] words
-        uint8_t* Tb = sgen + CS_BYTES + DW_BYTES;                          // [KS][BN][BM] bytes
-        if (C) {
-            // mirrored part straight from registers: lanes hold consecutive columns
+        double* Cs = reinterpret_cast<double*>(sgen);  // [BN][CP]: Cs[c][r] = tile (r, c)
 #pragma unroll
-            for (int j = 0; j < HN; ++j) {
-                const int jj = j0 + c0 + j;
-                if (i > jj && i < nv && jj < nv) C[(long long)jj * g.ldc + i] = acc[j];
-            }
-#pragma unroll
-            for (int j = 0; j < HN; ++j) Cs[(c0 + j) * CP + r] = acc[j];
-        }
-        if (Cd) {
-            const double inv2e = ldexp(1.0, -g.eC);
-#pragma unroll
-            for (int jw = 0; jw < HN / 4; ++jw) {
-                uint32_t w[KS];
-#pragma unroll
-                for (int s2 = 0; s2 < KS; ++s2) w[s2] = 0;
-#pragma unroll
-                for (int k = 0; k < 4; ++k) put_digits(acc[4 * jw + k], inv2e, k, w);
-#pragma unroll
-                for (int s2 = 0; s2 < KS; ++s2) {
-                    Dw[(s2 * BM + r) * DP + c0 / 4 + jw] = w[s2];
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        Tb[(s2 * BN + c0 + 4 * jw + k) * BM + r] = (uint8_t)(w[s2] >> (8 * k));
-                }
-            }
-        }
+        for (int j = 0; j < HN; ++j) Cs[(c0 + j) * CP + r] = acc[j];
         asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");
         const int et = threadIdx.x - 64;        // 0 .. EPI_THREADS-1
         const int ew = et >> 5;                 // epilogue warp 0..7
+        const long long t_stage = g.dbg_t ? gtimer() : 0;
+        if (kind != 0) {
+            // symmetrise the diagonal 64 x 64 sub-block (tile rows dr0.., all columns)
+            for (int idx = et; idx < 64 * 64; idx += EPI_THREADS) {
+                const int u = idx >> 6, v = idx & 63;  // sub-block row, column
+                if (u < v) Cs[v * CP + dr0 + u] = Cs[u * CP + dr0 + v];
+            }
+            asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");
+        }
         if (C) {
-            // direct part (row ii, columns j0..j0+BN) from the staged tile
-            for (int rr = ew; rr < BM; rr += EPI_WARPS) {
+            for (int rr = dr0 + ew; rr < BM; rr += EPI_WARPS) {
                 const int ii = i0 + rr;
 #pragma unroll
                 for (int j = lane; j < BN; j += 32) {
                     const int jj = j0 + j;
-                    if (ii >= jj && ii < nv && jj < nv) C[(long long)ii * g.ldc + jj] = Cs[j * CP + rr];
+                    if (ii < nv && jj < nv) C[(long long)ii * g.ldc + jj] = Cs[j * CP + rr];
+                }
+            }
+            for (int j = ew; j < BN; j += EPI_WARPS) {
+                const int jj = j0 + j;
+                for (int rr = mr0 + lane; rr < BM; rr += 32) {
+                    const int ii = i0 + rr;
+                    if (ii < nv && jj < nv) C[(long long)jj * g.ldc + ii] = Cs[j * CP + rr];
                 }
             }
         }
-        if (Cd) {
-            // direct digit rows: BN bytes = BN/4 words, BN/4 threads per row
-            constexpr int WPR = BN / 4;
-            for (int row = et / WPR; row < KS * BM; row += EPI_THREADS / WPR) {
-                const int s2 = row / BM, rr = row % BM, w = et % WPR;
-                const int ii = i0 + rr, jj0 = j0 + 4 * w;
-                const uint32_t word = Dw[(s2 * BM + rr) * DP + w];
-                int8_t* dst = Cd + s2 * ld2 + (long long)ii * ld + jj0;
-                if (jj0 + 3 <= ii) {
-                    *reinterpret_cast<uint32_t*>(dst) = word;
-                } else {
+        const long long t_cst = g.dbg_t ? gtimer() : 0;
+        if (g.Cd) {
+            // digit planes staged in the TMA-store layout: direct boxes
+            // [s][h] (tile rows 64h.., 64 columns) and mirror boxes [s][h]
+            // (64 tile columns as rows, tile rows 64h.. as columns)
+            uint8_t* dig = sgen + CS_BYTES;
+            const uint32_t dig_s = su32(dig);
+            const double s28 = ldexp(1.0, 28 - g.eC);
+            for (int it = et; it < 2 * BM * (BN / 16) / 2; it += EPI_THREADS) {  // 512 direct items
+                const int rr = it & (BM - 1), cc = it >> 7;           // tile row, 16-column chunk
+                if (rr < dr0) continue;
+                uint32_t w[4][KS];
 #pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        if (jj0 + k <= ii) dst[k] = (int8_t)(word >> (8 * k));
+                for (int q4 = 0; q4 < 4; ++q4) {
+                    double v4[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) v4[k] = Cs[(16 * cc + 4 * q4 + k) * CP + rr];
+                    digits4(v4, s28, w[q4]);
+                }
+                const int h2 = rr >> 6, rb = rr & 63;
+#pragma unroll
+                for (int s2 = 0; s2 < KS; ++s2) {
+                    uint8_t* box = dig + (s2 * 2 + h2) * BOX_BYTES;
+                    *reinterpret_cast<uint4*>(box + sw64_off(rb, cc)) =
+                        make_uint4(w[0][s2], w[1][s2], w[2][s2], w[3][s2]);
                 }
             }
-            // mirrored digit rows (row j0 + j, columns i0..i0+BM): one warp per row
-            for (int row = ew; row < KS * BN; row += EPI_WARPS) {
-                const int s2 = row / BN, j = row % BN;
-                const int jj = j0 + j, ic = i0 + 4 * lane;
-                if (ic + 3 <= jj) continue;
-                const uint32_t word = reinterpret_cast<const uint32_t*>(Tb + (s2 * BN + j) * BM)[lane];
-                int8_t* dst = Cd + s2 * ld2 + (long long)jj * ld + ic;
-                if (ic > jj) {
-                    *reinterpret_cast<uint32_t*>(dst) = word;
-                } else {
+            for (int it = et; it < BN * (BM / 16); it += EPI_THREADS) {  // 512 mirror items
+                const int j = it & (BN - 1), rc = it >> 6;              // tile column, 16-row chunk
+                if (16 * rc < mr0) continue;
+                uint32_t w[4][KS];
 #pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        if (ic + k > jj) dst[k] = (int8_t)(word >> (8 * k));
+                for (int q4 = 0; q4 < 4; ++q4) {
+                    double v4[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) v4[k] = Cs[j * CP + 16 * rc + 4 * q4 + k];
+                    digits4(v4, s28, w[q4]);
                 }
+                const int h2 = rc >> 2, cb = rc & 3;
+#pragma unroll
+                for (int s2 = 0; s2 < KS; ++s2) {
+                    uint8_t* box = dig + (2 * KS + s2 * 2 + h2) * BOX_BYTES;
+                    *reinterpret_cast<uint4*>(box + sw64_off(j, cb)) =
+                        make_uint4(w[0][s2], w[1][s2], w[2][s2], w[3][s2]);
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");
+            if (et == 0) {
+                const int base_row = mat * KS * ld;
+                for (int s2 = 0; s2 < KS; ++s2) {
+                    for (int h2 = dr0 >> 6; h2 < 2; ++h2)
+                        tma_store_2d(&mapC, dig_s + (s2 * 2 + h2) * BOX_BYTES, j0,
+                                     base_row + s2 * ld + i0 + 64 * h2);
+                    for (int h2 = mr0 >> 6; h2 < 2; ++h2)
+                        tma_store_2d(&mapC, dig_s + (2 * KS + s2 * 2 + h2) * BOX_BYTES, i0 + 64 * h2,
+                                     base_row + s2 * ld + j0);
+                }
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             }
         }
         if (g.dbg_t) asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");  // warp-uniform
         if (g.dbg_t && et == 0) {
-            long long* o = g.dbg_t + 4LL * (blockIdx.y * gridDim.x + blockIdx.x);
+            long long* o = g.dbg_t + 8LL * (blockIdx.y * gridDim.x + blockIdx.x);
             o[0] = t_start;
             o[1] = t_setup;
             o[2] = t_full;
             o[3] = gtimer();
+            o[4] = t_acc;
+            o[5] = t_stage;
+            o[6] = t_cst;
         }
     }
     tc_fence_before();
@@ -472,7 +563,8 @@ void init_attrs_ozaki() {
 
 void launch_oz_gemm(const OzGemm& g, cudaStream_t st) {
     const dim3 grid(oz_gemm_tiles(g.ld), g.nmat);
-    oz_gemm_kernel<<<grid, THREADS, SMEM_BYTES, st>>>(g.ma->a, g.mb->b, g);
+    if (g.Cd && !g.mc) throw Error(kInvalidArgument, "ozaki GEMM: digit output needs its TMA map");
+    oz_gemm_kernel<<<grid, THREADS, SMEM_BYTES, st>>>(g.ma->a, g.mb->b, g.mc ? g.mc->b : g.mb->b, g);
     TPB_CHECK_LAUNCH();
 }
 
@@ -484,48 +576,47 @@ void launch_oz_split(const double* A, long long mstride, int ld, int nmat, const
     TPB_CHECK_LAUNCH();
 }
 
-// Static spectral bounds of the sign-iteration operands as
-// digit-plane exponents: |X| <= 1.21, |Y| <= 1.45 -> 2^1; |Z| <= 2.81 -> 2^2;
-// X0 = A / ||A||_F has |X0| <= 1 -> 2^1 (strict bound needed).
+// The sign iteration rewritten so that every product but the last is a plain
+// (scaled) product of two digit-plane operands plus a diagonal shift, with
+// digit planes as its only output (no FP64 intermediates, no E reads):
+//   inflation  X' = X (a + b X^2 + c X^4) = X Z',  Z' = c U^2 + gamma I,
+//              U = X^2 + beta I,  beta = b / 2c,  gamma = a - b^2 / 4c
+//   Newton-Schulz  X' = X V,  V = 1.5 I - 0.5 X^2
+//   final      P = 0.5 A -/+ 0.5 A X = 0.5 A -/+ (0.5 / s) X0 X   (FP64 out)
+// Static spectral bounds give the digit exponents: |X| <=
+// 1.21, |U| <= 1.18, |V| <= 1.5 -> 2^1; |Z'| <= 3.45 -> 2^2; |X0| <= 1 -> 2^1.
 namespace {
-constexpr int kEX = 1, kEY = 1, kEZ = 2, kEX0 = 1;
+constexpr int kEX = 1, kEU = 1, kEZ = 2, kEV = 1, kEX0 = 1;
 }
 
-void enqueue_cone_ozaki(const double* A, double* w0, double* w1, double* w2, const OzWork& oz, int ld,
-                        int n, const double* scale, double* C, long long c_stride_b, long long c_stride_w,
-                        const int* ictl, int nmat, const SignSchedule& sch, cudaStream_t st) {
+void enqueue_cone_ozaki(const double* A, double* /*w0*/, double* /*w1*/, double* /*w2*/, const OzWork& oz,
+                        int ld, int n, const double* scale, double* C, long long c_stride_b,
+                        long long c_stride_w, const int* ictl, int nmat, const SignSchedule& sch,
+                        cudaStream_t st) {
     const long long ms = (long long)ld * ld;
     launch_oz_split(A, ms, ld, nmat, scale, kEX0, oz.d[3], ictl, st);
+    const double beta = sch.qb / (2.0 * sch.qc);
+    const double gamma = sch.qa - sch.qb * sch.qb / (4.0 * sch.qc);
     OzGemm g{};
     g.ld = ld;
     g.nmat = nmat;
     g.scale = scale;
     g.ictl = ictl;
-    g.ldc = ld;
-    g.nvalid = ld;
-    g.c_stride_b = 2 * ms;
-    g.c_stride_w = ms;
-    double* fb[3] = {w0, w1, w2};
-    // one product: operands are digit buffers (index 0..3), outputs FP64
-    // buffer / digit buffer index (-1: none)
-    auto step = [&](int ia, int ea, int ib, int eb, double al, int pa, const double* e, double be, int pb,
-                    int oc, int od, int ec) {
+    // one product of digit buffers ia, ib into digit buffer od
+    auto step = [&](int ia, int ea, int ib, int eb, double al, double shift, int od, int ec) {
         g.ma = &oz.maps[ia];
         g.mb = &oz.maps[ib];
         g.eA = ea;
         g.eB = eb;
         g.alpha_c = al;
-        g.pa = pa;
-        g.E = e;
-        g.beta_c = be;
-        g.pb = pb;
-        g.C = oc >= 0 ? fb[oc] : nullptr;
-        g.Cd = od >= 0 ? oz.d[od] : nullptr;
+        g.dshift = shift;
+        g.Cd = oz.d[od];
+        g.mc = &oz.maps[od];
         g.eC = ec;
         launch_oz_gemm(g, st);
     };
-    int x = -1;  // FP64/digit buffer holding X (-1: X0 = s A, FP64 A, digits in [3])
-    auto free_pair = [&](int& f0, int& f1) {
+    int x = 3;  // digit buffer holding X (3: X0)
+    auto others = [&](int& f0, int& f1) {
         int k = 0, fr[3];
         for (int q = 0; q < 3; ++q)
             if (q != x) fr[k++] = q;
@@ -533,43 +624,39 @@ void enqueue_cone_ozaki(const double* A, double* w0, double* w1, double* w2, con
         f1 = fr[1];
     };
     for (int it = 0; it < sch.k1; ++it) {
-        int y, z;
-        free_pair(y, z);
-        const int xd = x < 0 ? 3 : x;
-        const double* xe = x < 0 ? A : fb[x];
-        const int xpb = x < 0 ? 1 : 0;
-        step(xd, kEX, xd, kEX, 1.0, 0, nullptr, 0.0, 0, y, y, kEY);                // Y = X^2
-        step(y, kEY, y, kEY, sch.qc, 0, fb[y], sch.qb, 0, -1, z, kEZ);             // Z = c Y^2 + b Y
-        step(xd, kEX, z, kEZ, 1.0, 0, xe, sch.qa, xpb, y, y, kEX);                // X' = X Z + a X
-        x = y;
+        int u, z;
+        others(u, z);
+        step(x, kEX, x, kEX, 1.0, beta, u, kEU);      // U = X^2 + beta I
+        step(u, kEU, u, kEU, sch.qc, gamma, z, kEZ);  // Z' = c U^2 + gamma I
+        step(x, kEX, z, kEZ, 1.0, 0.0, u, kEX);       // X' = X Z'
+        x = u;
     }
     for (int it = 0; it < sch.k2; ++it) {
-        int y, xn;
-        free_pair(y, xn);
-        const int xd = x < 0 ? 3 : x;
-        const double* xe = x < 0 ? A : fb[x];
-        const int xpb = x < 0 ? 1 : 0;
-        step(xd, kEX, xd, kEX, 1.0, 0, nullptr, 0.0, 0, -1, y, kEY);               // Y = X^2
-        step(xd, kEX, y, kEY, -0.5, 0, xe, 1.5, xpb, xn, xn, kEX);                // X' = 1.5 X - 0.5 X Y
+        int v, xn;
+        others(v, xn);
+        step(x, kEX, x, kEX, -0.5, 1.5, v, kEV);      // V = 1.5 I - 0.5 X^2
+        step(x, kEX, v, kEV, 1.0, 0.0, xn, kEX);      // X' = X V
         x = xn;
     }
-    // P = 0.5 A -/+ 0.5 A X = 0.5 A -/+ (0.5 / s) X0 X into the state blocks
-    g.ldc = n;
-    g.nvalid = n;
-    g.c_stride_b = c_stride_b;
-    g.c_stride_w = c_stride_w;
-    g.sign_mode = 1;
+    // P into the state blocks (column-major n x n == row-major by symmetry)
     g.ma = &oz.maps[3];
-    g.mb = &oz.maps[x < 0 ? 3 : x];
+    g.mb = &oz.maps[x];
     g.eA = kEX0;
     g.eB = kEX;
     g.alpha_c = 0.5;
     g.pa = -1;
+    g.dshift = 0.0;
     g.E = A;
     g.beta_c = 0.5;
     g.pb = 0;
+    g.sign_mode = 1;
     g.C = C;
+    g.c_stride_b = c_stride_b;
+    g.c_stride_w = c_stride_w;
+    g.ldc = n;
+    g.nvalid = n;
     g.Cd = nullptr;
+    g.mc = nullptr;
     launch_oz_gemm(g, st);
 }
 

@@ -47,11 +47,13 @@ struct OzGemm {
     int pa, pb;
     const double* scale;     // per matrix s, or null (s = 1)
     int sign_mode;           // alpha *= -1 for even matrices (S -> NSD)
+    double dshift;           // added to the diagonal after alpha/beta
     const double* E;         // FP64 symmetric, mat stride ld*ld, or null
     double* C;               // FP64 out, or null
     long long c_stride_b, c_stride_w;
     int ldc, nvalid;
     int8_t* Cd;              // digit planes out ([mat][slice][ld][ld]), or null
+    const OzMaps* mc;        // TMA maps of Cd (stores use the 64-row box)
     int eC;
     const int* ictl;         // done flags per solve (matrix / 2), or null
     long long* dbg_t;        // instrumentation: 4 globaltimer stamps per CTA, or null

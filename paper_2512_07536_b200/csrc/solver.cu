@@ -190,20 +190,13 @@ void Solver::alloc() {
     d_.tr_res = dalloc<double>(s0_, allocs_,(size_t)B * cfg_.max_iter);
     d_.tr_lam = dalloc<double>(s0_, allocs_,(size_t)B * cfg_.max_iter);
     d_.tr_acf = dalloc<double>(s0_, allocs_,(size_t)B * cfg_.max_iter);
-    if (!small_) {
+    if (!small_ && !ozaki_) {
         w0_ = dalloc<double>(s0_, allocs_,(size_t)B * 2 * ld2);
         w1_ = dalloc<double>(s0_, allocs_,(size_t)B * 2 * ld2);
         w2_ = dalloc<double>(s0_, allocs_,(size_t)B * 2 * ld2);
         TPB_CUDA(cudaMemsetAsync(w0_, 0, (size_t)B * 2 * ld2 * sizeof(double), s0_));
         TPB_CUDA(cudaMemsetAsync(w1_, 0, (size_t)B * 2 * ld2 * sizeof(double), s0_));
         TPB_CUDA(cudaMemsetAsync(w2_, 0, (size_t)B * 2 * ld2 * sizeof(double), s0_));
-        if (ozaki_) {
-            for (int q = 0; q < 4; ++q) {
-                oz_.d[q] = dalloc<int8_t>(s0_, allocs_, (size_t)B * 2 * kOzSlices * ld2);
-                TPB_CUDA(cudaMemsetAsync(oz_.d[q], 0, (size_t)B * 2 * kOzSlices * ld2, s0_));
-                make_oz_maps(oz_.d[q], ld_, 2 * B, &oz_.maps[q]);
-            }
-        }
         // stream-K GEMM workspace for single large instances
         const int G = B == 1 ? stream_k_ctas(ld_) : 0;
         if (G > 0) {
@@ -211,6 +204,14 @@ void Solver::alloc() {
             sk_ws_ = dalloc<double>(s0_, allocs_, (size_t)G * 64 * 64);
             sk_flags_ = dalloc<int>(s0_, allocs_, (size_t)2 * T);
             TPB_CUDA(cudaMemsetAsync(sk_flags_, 0, (size_t)2 * T * sizeof(int), s0_));
+        }
+    }
+    if (ozaki_) {
+        // digit planes of the cone-projection iterates
+        for (int q = 0; q < 4; ++q) {
+            oz_.d[q] = dalloc<int8_t>(s0_, allocs_, (size_t)B * 2 * kOzSlices * ld2);
+            TPB_CUDA(cudaMemsetAsync(oz_.d[q], 0, (size_t)B * 2 * kOzSlices * ld2, s0_));
+            make_oz_maps(oz_.d[q], ld_, 2 * B, &oz_.maps[q]);
         }
     }
     list_ = dalloc<int>(s0_, allocs_,(size_t)B * list_cap_);

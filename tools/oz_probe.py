@@ -23,7 +23,7 @@ for ld in args[:1] or [128, 1024]:
     Cd = np.zeros((nmat, 8, ld, ld), dtype=np.int8)
     tiles = 2 * (ld // 128) * (ld // 128 + 1) // 2
     for mode in modes:
-        st = np.zeros((nmat * tiles, 4), dtype=np.int64)
+        st = np.zeros((nmat * tiles, 8), dtype=np.int64)
         ms = C.c_double(0)
         rc = lib.tp_oz_gemm_dbg(ld, nmat, A.ctypes.data_as(dp), 1, A.ctypes.data_as(dp), 1, 0, 1.0, 0.0,
                                 Cg.ctypes.data_as(dp), Cd.ctypes.data_as(C.c_void_p) if DIG else None, 2, 10, C.byref(ms), mode,
@@ -35,5 +35,10 @@ for ld in args[:1] or [128, 1024]:
         epi = np.median(st[:, 3] - st[:, 2]) / 1e3
         span = (st[:, 3].max() - t0) / 1e3
         launch_skew = (st[:, 0].max() - t0) / 1e3
+        acc = np.median(st[:, 4] - st[:, 2]) / 1e3
+        stg = np.median(st[:, 5] - st[:, 4]) / 1e3
+        cst = np.median(st[:, 6] - st[:, 5]) / 1e3
+        dig = np.median(st[:, 3] - st[:, 6]) / 1e3
+        print(f"   epi: tmem->acc {acc:5.2f} stage {stg:5.2f} C-stores {cst:5.2f} digits {dig:5.2f} us")
         print(f"ld={ld:5d} mode={mode} {ms.value*1e3:7.1f} us/launch | CTA: setup {setup:6.2f} main {main:7.2f} "
               f"epi {epi:6.2f} us | span {span:7.2f} start-skew {launch_skew:6.2f}", flush=True)
