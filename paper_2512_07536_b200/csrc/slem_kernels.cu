@@ -25,14 +25,32 @@ namespace {
 
 constexpr int kThreads = 512;
 
-// number of eigenvalues of the k x k tridiagonal (al, be) below x
+// number of eigenvalues of the k x k tridiagonal (al, be) below x: sign
+// changes of the Sturm sequence p_i = det(T_i - x I),
+//   p_i = (al_i - x) p_{i-1} - be_{i-1}^2 p_{i-2},
+// division-free (two FMAs per step; the LDL^T form has a dependent FP64
+// division per step), rescaled by exact powers of two. A zero p_i counts as
+// a change (the LDL^T convention d_i -> -0).
 __device__ int sturm_count(const double* al, const double* be, int k, double x) {
     int cnt = 0;
-    double d = 1.0;
+    double pm = 1.0, p = 1.0;  // p_{i-2}, p_{i-1}
+    bool prev_neg = false;     // sign of p_{i-1} (p_0 = 1 > 0), zero -> opposite of its predecessor
     for (int i = 0; i < k; ++i) {
-        d = (al[i] - x) - (i > 0 ? be[i - 1] * be[i - 1] / d : 0.0);
-        if (fabs(d) < 1e-300) d = -1e-300;
-        if (d < 0.0) ++cnt;
+        const double b2 = i > 0 ? be[i - 1] * be[i - 1] : 0.0;
+        const double pn = fma(al[i] - x, p, -b2 * pm);
+        const bool neg = pn < 0.0 || (pn == 0.0 && !prev_neg);
+        cnt += neg != prev_neg;
+        prev_neg = neg;
+        pm = p;
+        p = pn;
+        const double mx = fmax(fabs(p), fabs(pm));
+        if (mx > 0x1p400) {
+            p *= 0x1p-400;
+            pm *= 0x1p-400;
+        } else if (mx < 0x1p-400 && mx > 0.0) {
+            p *= 0x1p400;
+            pm *= 0x1p400;
+        }
     }
     return cnt;
 }
@@ -67,7 +85,8 @@ __device__ void gershgorin(const double* al, const double* be, int k, double& lo
 }
 
 // Unit eigenvector s of T_k for eigenvalue theta (two inverse iterations,
-// Thomas algorithm); returns |s_{k-1}|. Single thread; work: 2k doubles.
+// Thomas algorithm, one reciprocal per row); returns |s_{k-1}|. Single
+// thread; work: 2k doubles.
 __device__ double tri_vec(const double* al, const double* be, int k, double theta, double* work,
                           double* s) {
     double* cp = work;
@@ -77,24 +96,29 @@ __device__ double tri_vec(const double* al, const double* be, int k, double thet
     for (int it = 0; it < 2; ++it) {
         double den = al[0] - shift;
         if (fabs(den) < 1e-300) den = 1e-300;
-        cp[0] = k > 1 ? be[0] / den : 0.0;
-        dp[0] = s[0] / den;
+        double inv = 1.0 / den;
+        cp[0] = k > 1 ? be[0] * inv : 0.0;
+        dp[0] = s[0] * inv;
         for (int i = 1; i < k; ++i) {
-            double dn = (al[i] - shift) - be[i - 1] * cp[i - 1];
+            double dn = fma(-be[i - 1], cp[i - 1], al[i] - shift);
             if (fabs(dn) < 1e-300) dn = 1e-300;
-            cp[i] = i < k - 1 ? be[i] / dn : 0.0;
-            dp[i] = (s[i] - be[i - 1] * dp[i - 1]) / dn;
+            inv = 1.0 / dn;
+            cp[i] = i < k - 1 ? be[i] * inv : 0.0;
+            dp[i] = fma(-be[i - 1], dp[i - 1], s[i]) * inv;
         }
         s[k - 1] = dp[k - 1];
-        for (int i = k - 2; i >= 0; --i) s[i] = dp[i] - cp[i] * s[i + 1];
-        double nrm = 0.0;
-        for (int i = 0; i < k; ++i) nrm += s[i] * s[i];
+        double nrm = s[k - 1] * s[k - 1];
+        for (int i = k - 2; i >= 0; --i) {
+            s[i] = fma(-cp[i], s[i + 1], dp[i]);
+            nrm = fma(s[i], s[i], nrm);
+        }
         nrm = sqrt(nrm);
         if (!(nrm > 0.0) || !isfinite(nrm)) {
             for (int i = 0; i < k; ++i) s[i] = (i == k - 1) ? 1.0 : 0.0;
             return 1.0;
         }
-        for (int i = 0; i < k; ++i) s[i] /= nrm;
+        const double rn = 1.0 / nrm;
+        for (int i = 0; i < k; ++i) s[i] *= rn;
     }
     return fabs(s[k - 1]);
 }
@@ -366,6 +390,10 @@ __global__ void __launch_bounds__(kThreads) slem_kernel(SlemArgs a) {
         if (converged) break;
     }
     if (tid == 0) {
+        if (a.stats) {
+            atomicAdd(a.stats, 1);
+            atomicAdd(a.stats + 1, steps);
+        }
         if (a.ritz_ok) a.ritz_ok[b] = 1;
         const double l2 = 1.0 - th_min, ln = 1.0 - th_max;
         const double acf = fmax(fabs(l2), fabs(ln));
@@ -500,11 +528,200 @@ __global__ void __launch_bounds__(256) slem_small_kernel(SlemArgs a) {
     }
 }
 
+// ---------------------------------------------------------------- trace
+// Trace SLEM (acf_iterate every ADMM iteration): plain three-term Lanczos
+// without reorthogonalisation, the 1-vector deflated every step. Loss of
+// orthogonality only adds ghost copies of converged extremes; the extreme
+// Ritz values and the residual bound beta_k |s_k| stay valid (Paige), so the
+// per-step cost is one SpMV and two block reductions instead of CGS2 against
+// the stored basis (which streams kmax x n doubles per step). The basis rows
+// are written (not read) each step for the Ritz vectors that warm-start the
+// next iteration. Every Ritz value lies in [mu_min, mu_max], so the extremes
+// are tracked across restarts.
+constexpr int kTraceThreads = 1024;
+
+__global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
+    const int b = blockIdx.x;
+    if (a.ictl && a.ictl[b * 8 + 1]) return;  // solve already finished
+    const int n = a.n;
+    const int tid = threadIdx.x, nthr = blockDim.x, wid = tid >> 5;
+    const int ne = min(a.count[b], a.list_cap);
+    const int* list = a.list + (long long)b * a.list_cap;
+    const double* g = a.g + (long long)b * a.stride;
+    int* ei = a.e_i + (long long)b * a.list_cap;
+    int* ej = a.e_j + (long long)b * a.list_cap;
+    double* ew = a.e_w + (long long)b * a.list_cap;
+    int* cidx = a.col_idx + (long long)b * a.list_cap;
+    const int dim = n - 1;
+    const int kcap = max(2, min(a.kmax, dim));
+
+    extern __shared__ double sh[];
+    double* q = sh;                   // n
+    double* qp = q + n;               // n
+    double* w = qp + n;               // n
+    double* al = w + n;               // kcap
+    double* be = al + kcap;           // kcap
+    double* smin = be + kcap;         // kcap
+    double* smax = smin + kcap;       // kcap
+    double* wk = smax + kcap;         // 2 kcap
+    int* rowptr = (int*)(wk + 2 * kcap);  // n+1
+    int* colptr = rowptr + (n + 1);       // n+1
+    int* cur = colptr + (n + 1);          // n
+    double* Q = a.basis + (long long)b * a.kmax * n;
+    __shared__ double scratch[64];
+    __shared__ int iscr[32];
+    __shared__ int s_flag;  // bit0 stop, bit1 converged
+    __shared__ double s_th[2];
+
+    build_csr(n, ne, list, g, ei, ej, ew, rowptr, colptr, cur, cidx, iscr);
+
+    const bool warm = a.ritz && a.ritz_ok && a.ritz_ok[b];
+    double* rz = a.ritz ? a.ritz + (long long)b * 2 * n : nullptr;
+    for (int v = tid; v < n; v += nthr) q[v] = warm ? rz[v] + rz[n + v] : hash_unit(v);
+    __syncthreads();
+    deflate_normalize(q, n, scratch);
+
+    double th_min = 1e300, th_max = -1e300;
+    int steps = 0, converged = 0, kk = 0;
+    for (int cycle = 0; cycle <= a.max_restarts; ++cycle) {
+        if (tid == 0) s_flag = 0;
+        for (int v = tid; v < n; v += nthr) qp[v] = 0.0;
+        double beta_prev = 0.0;
+        double c_min = 0.0, c_max = 0.0;
+        bool broke = false;
+        __syncthreads();
+        for (int k = 0; k < kcap; ++k) {
+            // w = L q - beta_{k-1} q_{k-1} (gather, ascending edge order); alpha = q.w
+            double pa = 0.0;
+            for (int v = tid; v < n; v += nthr) {
+                const double qv = q[v];
+                Q[(long long)k * n + v] = qv;
+                double acc = 0.0;
+                for (int p = colptr[v]; p < colptr[v + 1]; ++p) {
+                    const int e = __ldg(cidx + p);
+                    acc += __ldg(ew + e) * (qv - q[__ldg(ei + e)]);
+                }
+                for (int e = rowptr[v]; e < rowptr[v + 1]; ++e) acc += __ldg(ew + e) * (qv - q[__ldg(ej + e)]);
+                acc -= beta_prev * qp[v];
+                w[v] = acc;
+                pa += qv * acc;
+            }
+            const double alpha = block_sum(pa, scratch);
+            double s = 0.0, s2 = 0.0;
+            for (int v = tid; v < n; v += nthr) {
+                const double x = w[v] - alpha * q[v];
+                w[v] = x;
+                s += x;
+                s2 += x * x;
+            }
+            block_sum2(s, s2, scratch);
+            const double mean = s / n;
+            const double beta = sqrt(fmax(s2 - n * mean * mean, 0.0));
+            if (tid == 0) {
+                al[k] = alpha;
+                be[k] = beta;
+            }
+            kk = k + 1;
+            ++steps;
+            const bool breakdown = !(beta > 1e-13 * fmax(fabs(alpha), fabs(c_max)) + 1e-300);
+            const bool want_check = breakdown || kk == kcap || (steps >= a.min_steps && check_step(kk));
+            if (want_check) {
+                __syncthreads();
+                if (wid == 0) {
+                    double lo, hi;
+                    gershgorin(al, be, kk, lo, hi);
+                    const double tmin = tri_eig(al, be, kk, 0, lo, hi);
+                    const double tmax = tri_eig(al, be, kk, kk - 1, lo, hi);
+                    if (tid == 0) {
+                        const double r1 = beta * tri_vec(al, be, kk, tmin, wk, smin);
+                        const double r2 = beta * tri_vec(al, be, kk, tmax, wk, smax);
+                        const double sc = fmax(fabs(tmax), 1e-300);
+                        const bool conv = !breakdown && r1 <= a.tol * sc && r2 <= a.tol * sc;
+                        s_th[0] = tmin;
+                        s_th[1] = tmax;
+                        s_flag = (conv || breakdown || kk == kcap) ? (1 | (conv ? 2 : 0) | (breakdown ? 4 : 0)) : 0;
+                    }
+                }
+                __syncthreads();
+                c_min = s_th[0];
+                c_max = s_th[1];
+                if (s_flag & 1) {
+                    converged = (s_flag >> 1) & 1;
+                    broke = (s_flag >> 2) & 1;
+                    break;
+                }
+            }
+            const double inv = beta > 0.0 ? 1.0 / beta : 0.0;
+            for (int v = tid; v < n; v += nthr) {
+                qp[v] = q[v];
+                q[v] = (w[v] - mean) * inv;
+            }
+            beta_prev = beta;
+            __syncthreads();
+        }
+        th_min = fmin(th_min, c_min);
+        th_max = fmax(th_max, c_max);
+        // Ritz vectors y = Q s of both extremes (restart vector / next warm start)
+        for (int v = tid; v < n; v += nthr) {
+            double y1 = 0.0, y2 = 0.0;
+            for (int j = 0; j < kk; ++j) {
+                const double qj = Q[(long long)j * n + v];
+                y1 += smin[j] * qj;
+                y2 += smax[j] * qj;
+            }
+            w[v] = y1;
+            q[v] = y2;
+        }
+        __syncthreads();
+        if (rz && !broke) {
+            for (int v = tid; v < n; v += nthr) {
+                rz[v] = w[v];
+                rz[n + v] = q[v];
+            }
+        }
+        if (converged) break;
+        // restart from the Ritz pair (a fresh random direction after a breakdown)
+        for (int v = tid; v < n; v += nthr) q[v] = broke ? hash_unit(v * 7 + 13 * cycle + 1) : q[v] + w[v];
+        __syncthreads();
+        deflate_normalize(q, n, scratch);
+    }
+    if (tid == 0) {
+        if (a.stats) {
+            atomicAdd(a.stats, 1);
+            atomicAdd(a.stats + 1, steps);
+        }
+        if (a.ritz_ok) a.ritz_ok[b] = 1;
+        const double l2 = 1.0 - th_min, ln = 1.0 - th_max;
+        const double acf = fmax(fabs(l2), fabs(ln));
+        if (a.tr_acf) a.tr_acf[(long long)b * a.max_iter + a.ictl[b * 8]] = acf;
+        if (a.out) {
+            double* o = a.out + b * 8;
+            o[0] = acf;
+            o[1] = l2;
+            o[2] = ln;
+            o[3] = (l2 < 1.0 - 1e-8) ? 1.0 : 0.0;
+            o[4] = steps;
+            o[5] = converged;
+        }
+    }
+}
+
+size_t slem_trace_smem_bytes(int n, int kmax) {
+    const int kcap = std::max(2, std::min(kmax, n - 1));
+    return (3 * (size_t)n + 6 * (size_t)kcap) * sizeof(double) + (3 * (size_t)n + 2) * sizeof(int);
+}
+
 void launch_slem(const SlemArgs& a, int B, cudaStream_t st) {
     const int n = a.n;
     if (n <= kSmallDense) {
         const size_t smem = ((size_t)n * (n + 1) + 4 * (size_t)n) * sizeof(double);
         slem_small_kernel<<<B, 256, smem, st>>>(a);
+        TPB_CHECK_LAUNCH();
+        return;
+    }
+    if (a.plain) {
+        const int threads = std::min(kTraceThreads, std::max(128, ((n + 31) / 32) * 32));
+        slem_trace_kernel<<<B, threads, slem_trace_smem_bytes(n, a.kmax), st>>>(a);
         TPB_CHECK_LAUNCH();
         return;
     }
@@ -625,6 +842,7 @@ void launch_slem_dense(const double* w, int n, double* basis, double* out, int d
 
 void init_attrs_slem() {
     set_max_dyn_smem(slem_kernel);
+    set_max_dyn_smem(slem_trace_kernel);
     set_max_dyn_smem(slem_dense_kernel);
     set_max_dyn_smem(slem_small_kernel);
 }

@@ -34,6 +34,8 @@ struct SlemArgs {
     double* tr_acf;
     const int* ictl;
     int max_iter;
+    int* stats;            // instrumentation: {calls, matvecs} accumulated, or null
+    int plain;             // trace mode: plain Lanczos (no reorthogonalisation), basis write-only
 };
 
 // n <= kSmallDense: dense Householder tridiagonalisation in shared memory

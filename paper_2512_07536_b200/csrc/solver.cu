@@ -134,6 +134,13 @@ Solver::Solver(int n, int B, bool het, const std::vector<int>& r, const std::vec
 
 Solver::~Solver() {
     phase_mark("(before teardown)");
+    if (slem_stats_) {
+        int st[2] = {0, 0};
+        cudaStreamSynchronize(s2_);
+        cudaMemcpy(st, slem_stats_, sizeof(st), cudaMemcpyDeviceToHost);
+        std::fprintf(stderr, "[slem] trace calls %d, matvecs %d (%.1f per call)\n", st[0], st[1],
+                     st[0] ? (double)st[1] / st[0] : 0.0);
+    }
     if (g_chunk_) cudaGraphExecDestroy(g_chunk_);
     if (g_one_) cudaGraphExecDestroy(g_one_);
     phase_mark("graph destroy");
@@ -214,6 +221,10 @@ void Solver::alloc() {
             make_oz_maps(oz_.d[q], ld_, 2 * B, &oz_.maps[q]);
         }
     }
+    if (std::getenv("TPB_SLEM_STATS")) {
+        slem_stats_ = dalloc<int>(s0_, allocs_, 2);
+        TPB_CUDA(cudaMemsetAsync(slem_stats_, 0, 2 * sizeof(int), s0_));
+    }
     list_ = dalloc<int>(s0_, allocs_,(size_t)B * list_cap_);
     list_count_ = dalloc<int>(s0_, allocs_,B);
     e_i_ = dalloc<int>(s0_, allocs_,(size_t)B * list_cap_);
@@ -224,7 +235,8 @@ void Solver::alloc() {
     // the previous Ritz vectors; basis in shared memory when it fits
     // Krylov basis in global memory: a shared-memory basis (~200 KB at n=256)
     // would pin one SLEM CTA per SM and starve the concurrent cone GEMMs.
-    trace_kmax_ = std::max(1, std::min(n - 1, 96));
+    // plain trace Lanczos (slem_trace_kernel): longer recurrences, write-only basis
+    trace_kmax_ = std::max(1, std::min(n - 1, (n > kSmallDense && !std::getenv("TPB_SLEM_CGS2")) ? 256 : 96));
     basis_ = dalloc<double>(s0_, allocs_,(size_t)B * trace_kmax_ * n);
     ritz_ = dalloc<double>(s0_, allocs_,(size_t)B * 2 * n);
     ritz_ok_ = dalloc<int>(s0_, allocs_,B);
@@ -360,6 +372,8 @@ void Solver::enqueue_slem_trace(cudaStream_t st) {
     a.tr_acf = d_.tr_acf;
     a.ictl = d_.ictl;
     a.max_iter = cfg_.max_iter;
+    a.stats = slem_stats_;
+    a.plain = lo_.n > kSmallDense && !std::getenv("TPB_SLEM_CGS2");
     launch_slem(a, B_, st);
 }
 

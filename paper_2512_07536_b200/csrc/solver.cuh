@@ -126,6 +126,7 @@ class Solver {
     int trace_kmax_ = 0;
     double* ritz_ = nullptr;         // B x 2n extreme Ritz vectors (warm start)
     int* ritz_ok_ = nullptr;
+    int* slem_stats_ = nullptr;      // TPB_SLEM_STATS: {trace SLEM calls, matvecs}
     double* basis_final_ = nullptr;  // final report
     double* slem_out_ = nullptr;     // B x 8
     double* tmp_m_ = nullptr;        // B x m
