@@ -129,3 +129,25 @@ def test_exponential_dominance(T, O):
         exp_acf = O.spectral_report(O.gossip_matrix(n, e, w))["acf"]
         s = T.solve(n, len(e), rho=10.0, epsilon=1e-8, max_iter=40000)
         assert s.connected and s.acf_value <= exp_acf + 0.01
+
+
+def test_config3_golden(T, golden):
+    # n=256, r=1024, the reference's default warm start
+    if not os.path.exists(os.path.join(GOLDEN, "config3.json")):
+        pytest.skip("config3 fixture missing")
+    g = golden("config3.json")
+    ref = g["solution"]
+    assert T.default_warm_start(g["n"], g["r"], 0).tolist() == g["warm"]
+    s = T.solve(g["n"], g["r"], warm_start=g["warm"], **g["cfg"])
+    assert s.converged == ref["converged"]
+    assert s.edges.tolist() == ref["edges"]
+    assert rel(s.weights, ref["weights"]) < 1e-6
+    assert s.acf_value == pytest.approx(ref["acf"], rel=1e-6)
+    assert s.lambda_tilde == pytest.approx(ref["lambda_tilde"], rel=1e-6)
+    assert s.connected == ref["connected"]
+    # the iteration count depends on when ||X - Y||^2 crosses 1e-8: within 1 %
+    assert abs(s.iterations - ref["iterations"]) <= 0.01 * ref["iterations"]
+    rows = [i for i in ref["trace_rows"] if i < s.trace.shape[0]]
+    tr = np.array(ref["trace"])[: len(rows)]
+    assert np.max(np.abs(s.trace[rows, 2] - tr[:, 2])) < 1e-6   # lambda_tilde
+    assert np.max(np.abs(s.trace[rows, 3] - tr[:, 3])) < 1e-6   # acf_iterate
