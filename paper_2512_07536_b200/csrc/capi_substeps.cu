@@ -3,6 +3,7 @@
 // drive their own loop, e.g. proj/tests/test_admm.cpp's substep checks).
 #include <algorithm>
 #include <cstring>
+#include <memory>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -146,7 +147,8 @@ void cone_dense(int n, const double* a, double* out, bool psd) {
     if (n < 1) throw Error(kInvalidArgument, "project: empty matrix");
     init_attrs();
     const bool small = n <= 64;
-    const int ld = small ? ((n + 7) & ~7) : ((n + 63) / 64) * 64;
+    const bool oz = !small && cone_uses_ozaki();
+    const int ld = small ? ((n + 7) & ~7) : (oz ? ((n + 127) / 128) * 128 : ((n + 63) / 64) * 64);
     const long long ld2 = (long long)ld * ld;
     const int w = psd ? 1 : 0;  // slot 0 -> NSD, slot 1 -> PSD
     DBuf<double> da((size_t)n * n), A(2 * ld2), C(2 * (size_t)n * n), scale(2);
@@ -159,6 +161,20 @@ void cone_dense(int n, const double* a, double* out, bool psd) {
     SignSchedule sch;
     if (small) {
         launch_cone_small(A.p, ld2, ld, n, C.p, 0, (long long)n * n, nullptr, 2, sch, 0);
+    } else if (oz) {
+        frob_kernel<<<1, 1024>>>(A.p, ld, w, scale.p);
+        TPB_CHECK_LAUNCH();
+        OzWork oz_w;
+        std::vector<std::unique_ptr<DBuf<int8_t>>> bufs;
+        for (int q = 0; q < 4; ++q) {
+            bufs.emplace_back(new DBuf<int8_t>((size_t)2 * kOzSlices * ld2));
+            bufs.back()->zero();
+            oz_w.d[q] = bufs.back()->p;
+            make_oz_maps(oz_w.d[q], ld, 2, &oz_w.maps[q]);
+        }
+        enqueue_cone_ozaki(A.p, nullptr, nullptr, nullptr, oz_w, ld, n, scale.p, C.p, 0, (long long)n * n,
+                           nullptr, 2, sch, 0);
+        TPB_CUDA(cudaDeviceSynchronize());
     } else {
         frob_kernel<<<1, 1024>>>(A.p, ld, w, scale.p);
         TPB_CHECK_LAUNCH();

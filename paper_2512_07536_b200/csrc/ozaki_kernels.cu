@@ -18,6 +18,7 @@
 #include "cone_kernels.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -556,6 +557,11 @@ void make_oz_maps(const int8_t* planes, int ld, int nmat, OzMaps* out) {
 }
 
 int oz_gemm_tiles(int ld) { return tiles_before(ld / BM); }
+
+bool cone_uses_ozaki() {
+    const char* c = std::getenv("TPB_CONE");
+    return !(c && std::strcmp(c, "dmma") == 0);
+}
 
 void init_attrs_ozaki() {
     TPB_CUDA(cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));

@@ -61,6 +61,8 @@ struct OzGemm {
 };
 
 void launch_oz_gemm(const OzGemm& g, cudaStream_t st);
+// Tiled cone projections use this kernel unless TPB_CONE=dmma (FP64 DMMA).
+bool cone_uses_ozaki();
 int oz_gemm_tiles(int ld);
 
 // Digit-plane buffers of the cone projection: [0..2] pair with the three FP64

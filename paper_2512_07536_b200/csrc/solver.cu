@@ -105,10 +105,7 @@ Solver::Solver(int n, int B, bool het, const std::vector<int>& r, const std::vec
     small_ = n <= 64;
     // Tiled projections: int8 tensor-core (Ozaki) GEMMs by default, FP64 DMMA
     // with TPB_CONE=dmma; the Ozaki tiles need ld % 128 == 0.
-    {
-        const char* cone = std::getenv("TPB_CONE");
-        ozaki_ = !small_ && !(cone && std::string(cone) == "dmma");
-    }
+    ozaki_ = !small_ && cone_uses_ozaki();
     ld_ = small_ ? ((n + 7) & ~7) : (ozaki_ ? ((n + 127) / 128) * 128 : ((n + 63) / 64) * 64);
     list_cap_ = het ? m : *std::max_element(r_host_.begin(), r_host_.end());
     int chunk = cfg.chunk > 0 ? cfg.chunk : (n <= 64 ? 32 : (n <= 256 ? 16 : 8));
