@@ -68,6 +68,7 @@ T* dalloc(cudaStream_t st, std::vector<void*>& pool, size_t count) {
 Solver::Solver(int n, int B, bool het, const std::vector<int>& r, const std::vector<int>& degrees,
                const Config& cfg)
     : B_(B), het_(het), cfg_(cfg) {
+    phase_mark("(caller, before the solver)");
     validate(cfg);
     if (n < 2) throw Error(kInvalidArgument, "assemble: need at least 2 nodes");
     if (B < 1) throw Error(kInvalidArgument, "batch must be >= 1");
@@ -112,6 +113,7 @@ Solver::Solver(int n, int B, bool het, const std::vector<int>& r, const std::vec
     chunk = ((chunk + cfg.trace_stride - 1) / cfg.trace_stride) * cfg.trace_stride;
     chunk_ = chunk;
     init_attrs();
+    phase_mark("solver init_attrs");
     TPB_CUDA(cudaStreamCreateWithFlags(&s0_, cudaStreamNonBlocking));
     TPB_CUDA(cudaStreamCreateWithFlags(&s1_, cudaStreamNonBlocking));
     TPB_CUDA(cudaStreamCreateWithFlags(&s2_, cudaStreamNonBlocking));
@@ -237,7 +239,7 @@ void Solver::alloc() {
     basis_ = dalloc<double>(s0_, allocs_,(size_t)B * trace_kmax_ * n);
     ritz_ = dalloc<double>(s0_, allocs_,(size_t)B * 2 * n);
     ritz_ok_ = dalloc<int>(s0_, allocs_,B);
-    const int kfin = n - 1 <= kFinalExactDim ? std::max(1, n - 1) : kFinalKrylov;
+    const int kfin = n - 1 <= kFinalExactDim ? std::max(1, n - 1) : (std::getenv("TPB_SLEM_CGS2") ? kFinalKrylov : 1);
     basis_final_ = dalloc<double>(s0_, allocs_,(size_t)B * kfin * n);
     slem_out_ = dalloc<double>(s0_, allocs_,(size_t)B * 8);
     tmp_m_ = dalloc<double>(s0_, allocs_,(size_t)B * m);
@@ -309,10 +311,14 @@ void Solver::final_slem(const double* packed, const int* list, const int* count,
     a.e_j = e_j_;
     a.e_w = e_w_;
     a.col_idx = col_idx_;
-    // exact (complete Krylov space) up to n = 257, restarted beyond
+    // exact (complete Krylov space, CGS2) up to n = 257; beyond, the plain
+    // Lanczos recurrence of the trace kernel at residual tolerance 1e-10
+    // (eigenvalue error <= 1e-20 / gap), reusing the trace basis buffer
     const int n = lo_.n;
-    a.basis = basis_final_;
-    a.kmax = n - 1 <= kFinalExactDim ? std::max(1, n - 1) : kFinalKrylov;
+    const bool exact = n - 1 <= kFinalExactDim;
+    a.plain = exact || std::getenv("TPB_SLEM_CGS2") ? 0 : 1;
+    a.basis = a.plain ? basis_ : basis_final_;
+    a.kmax = exact ? std::max(1, n - 1) : (a.plain ? trace_kmax_ : kFinalKrylov);
     a.max_restarts = 200;
     a.min_steps = 64;
     a.tol = 1e-10;

@@ -121,15 +121,19 @@ def edge_index(n: int, i: int, j: int) -> int:
 
 def gossip_matrix(n: int, edges, weights) -> np.ndarray:
     """W = I - L (proj/src/topology.cpp:96-123), output formatting of a result."""
-    lap = np.zeros((n, n))
-    for (i, j), w in zip(np.asarray(edges).reshape(-1, 2), np.asarray(weights)):
-        lap[i, i] += w
-        lap[j, j] += w
-        lap[i, j] -= w
-        lap[j, i] -= w
-    if n and np.any(np.diag(lap) > 1.0 + 1e-12):
+    e = np.asarray(edges, dtype=np.int64).reshape(-1, 2)
+    wt = np.asarray(weights, dtype=np.float64).reshape(-1)
+    # degrees accumulate per node in edge order (np.add.at is unbuffered and
+    # sequential), as the reference's loop does; pairs are distinct
+    deg = np.zeros(n)
+    np.add.at(deg, e.reshape(-1), np.repeat(wt, 2))
+    if n and np.any(deg > 1.0 + 1e-12):
         raise ValueError("gossip_matrix: weighted degree exceeds 1")
-    return np.eye(n) - lap
+    w = np.zeros((n, n))
+    w[e[:, 0], e[:, 1]] = wt
+    w[e[:, 1], e[:, 0]] = wt
+    w[np.arange(n), np.arange(n)] = 1.0 - deg
+    return w
 
 
 def spectral_report(w) -> dict:
