@@ -29,7 +29,8 @@ namespace tpb {
 namespace {
 
 constexpr int KS = kOzSlices, BM = kOzBM, BN = kOzBN, BK = kOzBK;
-constexpr int STAGES = 2;
+constexpr int STAGES = 192 * 1024 / (KS * (BM + BN) * BK);  // 2 at BK = 64, 4 at BK = 32
+static_assert(BK == 32 || BK == 64, "k block is one or two MMA k-steps");
 constexpr int A_PLANE = BM * BK, B_PLANE = BN * BK;              // bytes
 constexpr int STAGE_BYTES = KS * (A_PLANE + B_PLANE);            // 96 KB
 constexpr int CP = BM + 1;       // epilogue FP64 staging pitch (doubles)
@@ -107,11 +108,12 @@ __device__ __forceinline__ void tmem_wait_ld() {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// K-major operand tile in SWIZZLE_64B layout (64-byte rows, 8-row atoms of
-// 512 B): start address, SBO = 512 B, version 1, layout type 4.
-__device__ __forceinline__ uint64_t sw64_desc(uint32_t addr) {
-    return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
-           ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
+// K-major operand tile, BK-byte rows in the matching swizzle (8-row atoms of
+// 8 BK bytes): start address, SBO = 8 BK, version 1, layout type 4 (64B) /
+// 6 (32B).
+__device__ __forceinline__ uint64_t op_desc(uint32_t addr) {
+    return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)((8 * BK) >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)(BK == 64 ? 4 : 6) << 61);
 }
 
 // instruction descriptor: s8 x s8 -> s32, K-major A and B, M = 128, N = nn
@@ -256,6 +258,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    // Programmatic dependent launch: everything above overlaps the previous
+    // GEMM's tail; its digit planes (our operands) and its reads of the
+    // buffer we overwrite are complete after this wait. Our own dependents
+    // may then be scheduled as SMs free up.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const uint32_t tmem = tmem_slot;
     const int KB = ld / BK;
     const long long plane_rows = (long long)mat * KS * ld;
@@ -298,12 +306,12 @@ __global__ void __launch_bounds__(THREADS, 1)
                     // contiguous 64-column blocks in TMEM.
 #pragma unroll
                     for (int s = 1; s <= KS; ++s) {
-                        const uint64_t ad = sw64_desc(a_tile(st, s - 1) + kk * 32);
+                        const uint64_t ad = op_desc(a_tile(st, s - 1) + kk * 32);
 #pragma unroll
                         for (int t0 = 1; t0 <= KS + 1 - s; t0 += 4) {
                             const int t1 = t0 + 3 < KS + 1 - s ? t0 + 3 : KS + 1 - s;
                             const int nn = BN * (t1 - t0 + 1);
-                            const uint64_t bd = sw64_desc(b_tile(st, t0 - 1) + kk * 32);
+                            const uint64_t bd = op_desc(b_tile(st, t0 - 1) + kk * 32);
                             const uint32_t acc = (kb | kk) != 0 || s != 1;
                             mma_i8(tmem + (uint32_t)((s + t0 - 2) * BN), ad, bd, idesc_n(nn), acc);
                         }
@@ -535,14 +543,15 @@ EncodeTiled encode_fn() {
     return fn;
 }
 
-void encode(CUtensorMap* m, const int8_t* base, int ld, long long rows, int box_rows) {
+void encode(CUtensorMap* m, const int8_t* base, int ld, long long rows, int box_cols, int box_rows) {
     const cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
     const cuuint64_t strides[1] = {(cuuint64_t)ld};
-    const cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+    const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
     const cuuint32_t estr[2] = {1, 1};
     const CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(base), dims,
                                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                   CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   box_cols == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(kCuda, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
 }
@@ -552,8 +561,9 @@ void encode(CUtensorMap* m, const int8_t* base, int ld, long long rows, int box_
 void make_oz_maps(const int8_t* planes, int ld, int nmat, OzMaps* out) {
     if (ld % BM != 0) throw Error(kInvalidArgument, "ozaki GEMM needs ld % 128 == 0");
     const long long rows = (long long)nmat * KS * ld;
-    encode(&out->a, planes, ld, rows, BM);
-    encode(&out->b, planes, ld, rows, BN);
+    encode(&out->a, planes, ld, rows, BK, BM);
+    encode(&out->b, planes, ld, rows, BK, BN);
+    encode(&out->st, planes, ld, rows, 64, 64);
 }
 
 int oz_gemm_tiles(int ld) { return tiles_before(ld / BM); }
@@ -570,8 +580,17 @@ void init_attrs_ozaki() {
 void launch_oz_gemm(const OzGemm& g, cudaStream_t st) {
     const dim3 grid(oz_gemm_tiles(g.ld), g.nmat);
     if (g.Cd && !g.mc) throw Error(kInvalidArgument, "ozaki GEMM: digit output needs its TMA map");
-    oz_gemm_kernel<<<grid, THREADS, SMEM_BYTES, st>>>(g.ma->a, g.mb->b, g.mc ? g.mc->b : g.mb->b, g);
-    TPB_CHECK_LAUNCH();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = SMEM_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = g.no_pdl ? 0 : 1;
+    TPB_CUDA(cudaLaunchKernelEx(&cfg, oz_gemm_kernel, g.ma->a, g.mb->b, g.mc ? g.mc->st : g.mb->st, g));
 }
 
 void launch_oz_split(const double* A, long long mstride, int ld, int nmat, const double* scale, int e,

@@ -23,7 +23,7 @@ namespace tpb {
 constexpr int kOzSlices = 8;   // digits per operand (56 bits)
 constexpr int kOzBM = 128;     // tile rows (UMMA M)
 constexpr int kOzBN = 64;      // tile cols (UMMA N); KS accumulators x BN <= 512 TMEM columns
-constexpr int kOzBK = 64;      // k bytes per pipeline stage (SWIZZLE_64B rows)
+constexpr int kOzBK = 64;      // k bytes per pipeline stage (SWIZZLE_64B rows; 32 with SWIZZLE_32B measured slower)
 
 // Digit planes of nmat symmetric ld x ld matrices: [mat][slice][ld][ld] int8.
 struct OzPlanes {
@@ -31,10 +31,11 @@ struct OzPlanes {
     int e = 0;  // matrix = 2^e sum_s 2^{-7s} plane_s
 };
 
-// TMA maps of one plane buffer in the A role (box kOzBM rows) and the B role
-// (box kOzBN rows).
+// TMA maps of one plane buffer: loads in the A role (box kOzBK x kOzBM rows)
+// and the B role (box kOzBK x kOzBN rows); epilogue stores (64 x 64-byte
+// boxes, SWIZZLE_64B).
 struct OzMaps {
-    CUtensorMap a, b;
+    CUtensorMap a, b, st;
 };
 void make_oz_maps(const int8_t* planes, int ld, int nmat, OzMaps* out);
 
@@ -58,6 +59,7 @@ struct OzGemm {
     const int* ictl;         // done flags per solve (matrix / 2), or null
     long long* dbg_t;        // instrumentation: 4 globaltimer stamps per CTA, or null
     int dbg_mode;            // instrumentation: bit 0 skips the MMAs, bit 1 the TMA loads
+    int no_pdl;              // launch without programmatic dependent launch
 };
 
 void launch_oz_gemm(const OzGemm& g, cudaStream_t st);

@@ -21,7 +21,7 @@ print(f"cone={__import__('os').environ.get('TPB_CONE','ozaki'):6s} trace_stride=
 bs.close()
 '''
 
-for cone, ts, tol in [("ozaki", 1, "1e-6"), ("ozaki", 1, "1e-7"), ("ozaki", 1, "1e-8"), ("ozaki", 1000, "1e-6")]:
+for cone, ts, tol in [("ozaki", 1, "1e-6"), ("ozaki", 1000, "1e-6")]:
     env = dict(os.environ, TPB_CONE=cone, TPB_SLEM_TOL=tol, TPB_SLEM_STATS="1")
     print("tol", tol, flush=True)
     subprocess.run([sys.executable, "-c", CODE, str(ts)], env=env, check=False)
