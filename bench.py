@@ -233,6 +233,8 @@ def run_ours(args):
     t_sel, _ = phase(2, 5)
     t_slem, _ = phase(3, 3)
     t_prep, _ = phase(4, 10)
+    t_xa, _ = phase(5, 10)
+    t_xb, _ = phase(6, 10)
     bs.close()
 
     # roofline of the dominant kernel: the Ozaki-scheme GEMM on the int8
@@ -263,10 +265,15 @@ def run_ours(args):
                 "traffic": 16.797184e6 if n == 1024 else None, "traffic_unit": "bytes/launch",
                 "peak_source": "measured FP64 DMMA microbenchmark (tools/microbench/fp64_peak.cu)",
                 "gemms_per_iteration": gemms, "gemm_avg_ms": gemm_avg * 1e3}
-    # x-step algorithmic bytes: passes a+b read Y,D (S,T blocks, edges), write X,D
+    # x-step algorithmic bytes: pass A reads Y, D over the S
+    # and T blocks (4n^2) and the edge block (2m), writes h (m); pass B reads
+    # h, Y_g, D_g (3m) and the S, T blocks of Y, D (4n^2), writes X_g, D_g (2m)
+    # and the S, T blocks of X, D (4n^2). Node/diag passes are O(n) latency
+    # kernels (one CTA per solve).
     m = n * (n - 1) // 2
-    xbytes = 8.0 * (4 * n * n + 2 * m + m) + 8.0 * (4 * n * n + m + 2 * m + 4 * n * n + 2 * m)
-
+    bytes_a = 8.0 * (4 * n * n + 3 * m)
+    bytes_b = 8.0 * (8 * n * n + 5 * m)
+    xbytes = bytes_a + bytes_b
     # e2e: the C-ABI solve with host buffers (warm edges in, solution out)
     barrier()
     t0 = time.time()
@@ -305,10 +312,17 @@ def run_ours(args):
             "roofline": roof,
             "phases_ms": {"cone_projection": t_cone * 1e3, "xstep": t_x * 1e3, "topr": t_sel * 1e3,
                           "trace_slem": t_slem * 1e3, "prep": t_prep * 1e3},
-            "xstep_roofline": {"bound": "hbm", "achieved": xbytes / t_x / 1e9,
-                               "peak": pk.get("hbm_gbs", 6538.9), "unit": "GB/s",
-                               "frac": xbytes / t_x / 1e9 / pk.get("hbm_gbs", 6538.9),
-                               "bytes_per_launch_set": xbytes},
+            "xstep_roofline": {
+                "bound": "hbm", "peak": pk.get("hbm_gbs", 6538.9), "unit": "GB/s",
+                "pass_a": {"kernel": "xstep_a_kernel", "bytes": bytes_a, "ms": t_xa * 1e3,
+                           "achieved": bytes_a / t_xa / 1e9,
+                           "frac": bytes_a / t_xa / 1e9 / pk.get("hbm_gbs", 6538.9)},
+                "pass_b": {"kernel": "xstep_b_kernel", "bytes": bytes_b, "ms": t_xb * 1e3,
+                           "achieved": bytes_b / t_xb / 1e9,
+                           "frac": bytes_b / t_xb / 1e9 / pk.get("hbm_gbs", 6538.9)},
+                "whole_xstep": {"bytes": xbytes, "ms": t_x * 1e3, "achieved": xbytes / t_x / 1e9,
+                                "frac": xbytes / t_x / 1e9 / pk.get("hbm_gbs", 6538.9),
+                                "note": "incl. the single-CTA node and diag passes"}},
             "e2e": {"value": e2e, "unit": "iter/s", "h2d_bytes_per_step": h2d / K,
                     "d2h_bytes_per_step": d2h / K,
                     "note": "tp_solve through the C ABI with host warm-start edges in and the host "

@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(TB* TY) prep_kernel(Dev d, XConst c) {
             double v = 0.0;
             if (i < n && j < n) {
                 const long long p = off + (long long)j * n + i;
-                v = X[p] + D[p] / c.rho;
+                v = X[p] + D[p] * c.inv_rho;
             }
             Vs[cc][tx] = v;
         }
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(TB* TY) prep_kernel(Dev d, XConst c) {
             const int j = j0 + tx, i = i0 + cc;  // entry (row j, col i)
             if (i < n && j < n) {
                 const long long p = off + (long long)i * n + j;
-                const double vji = X[p] + D[p] / c.rho;
+                const double vji = X[p] + D[p] * c.inv_rho;
                 const double vij = Vs[tx][cc];
                 const double a = 0.5 * (vij + vji);  // symmetrize (proj/src/eig.cpp:157)
                 // A is symmetric; write (j, i) here (row-major j*ld + i)
@@ -149,23 +149,23 @@ __global__ void __launch_bounds__(TB* TY) prep_kernel(Dev d, XConst c) {
         const int i = i0 + il, j = j0 + tx;
         if (i >= n || j >= n || j <= i) continue;
         const long long l = edge_idx(n, i, j);
-        const double vg = X[l] + D[l] / c.rho;
+        const double vg = X[l] + D[l] * c.inv_rho;
         Y[l] = (0.0 < vg) ? vg : 0.0;  // std::max(0.0, v) (proj/src/admm.cpp:273)
         if (d.het) {
             const long long lz = lo.off_z + l, lv = lo.off_nu + l;
-            Y[lz] = X[lz] + D[lz] / c.rho;  // z-score; binary projection follows
-            const double vn = X[lv] + D[lv] / c.rho;
+            Y[lz] = X[lz] + D[lz] * c.inv_rho;  // z-score; binary projection follows
+            const double vn = X[lv] + D[lv] * c.inv_rho;
             Y[lv] = (0.0 < vn) ? vn : 0.0;
         }
     }
     if (blockIdx.x == 0) {
         const int t = ty * TB + tx;
         if (t == 0) {
-            const double vl = X[lo.lambda_ix] + D[lo.lambda_ix] / c.rho;
+            const double vl = X[lo.lambda_ix] + D[lo.lambda_ix] * c.inv_rho;
             Y[lo.lambda_ix] = (0.0 < vl) ? vl : 0.0;
         }
         for (int i = t; i < n; i += TB * TY) {
-            const double vy = X[lo.off_y + i] + D[lo.off_y + i] / c.rho;
+            const double vy = X[lo.off_y + i] + D[lo.off_y + i] * c.inv_rho;
             Y[lo.off_y + i] = (0.0 < vy) ? vy : 0.0;
         }
     }
@@ -234,8 +234,8 @@ __global__ void __launch_bounds__(TB* TY) xstep_a_kernel(Dev d, XConst c) {
     __shared__ double Zs[TB][TB + 1];  // het: h_z'(i,j)
     __shared__ double rd_i[TB], rd_j[TB], v2_i[TB], v2_j[TB];
 
-    auto rS = [&](long long p) { return Y[lo.off_s + p] - D[lo.off_s + p] / c.rho; };
-    auto rT = [&](long long p) { return Y[lo.off_t + p] - D[lo.off_t + p] / c.rho; };
+    auto rS = [&](long long p) { return Y[lo.off_s + p] - D[lo.off_s + p] * c.inv_rho; };
+    auto rT = [&](long long p) { return Y[lo.off_t + p] - D[lo.off_t + p] * c.inv_rho; };
     // orientation 1: R(i, j) at j*n + i
     for (int cc = ty; cc < TB; cc += TY) {
         const int i = i0 + tx, j = j0 + cc;
@@ -252,12 +252,12 @@ __global__ void __launch_bounds__(TB* TY) xstep_a_kernel(Dev d, XConst c) {
         if (i < n) {
             const long long p = (long long)i * n + i;
             rd_i[tx] = rS(p) + rT(p);
-            v2_i[tx] = 1.0 - (Y[lo.off_y + i] - D[lo.off_y + i] / c.rho);
+            v2_i[tx] = 1.0 - (Y[lo.off_y + i] - D[lo.off_y + i] * c.inv_rho);
         }
         if (j < n) {
             const long long p = (long long)j * n + j;
             rd_j[tx] = rS(p) + rT(p);
-            v2_j[tx] = 1.0 - (Y[lo.off_y + j] - D[lo.off_y + j] / c.rho);
+            v2_j[tx] = 1.0 - (Y[lo.off_y + j] - D[lo.off_y + j] * c.inv_rho);
         }
     }
     __syncthreads();
@@ -276,12 +276,12 @@ __global__ void __launch_bounds__(TB* TY) xstep_a_kernel(Dev d, XConst c) {
         double hv = 0.0, hz = 0.0;
         if (i < n && j < n && j > i) {
             const long long l = edge_idx(n, i, j);
-            const double rg = Y[l] - D[l] / c.rho;
+            const double rg = Y[l] - D[l] * c.inv_rho;
             hv = rg + c.s * (4.0 - rd_i[il] - rd_j[jl] + Rs[il][jl] + v2_i[il] + v2_j[jl]);
             if (d.het) {
                 const long long lz = lo.off_z + l, lv = lo.off_nu + l;
-                const double rnu = Y[lv] - D[lv] / c.rho;
-                const double rz = Y[lz] - D[lz] / c.rho;
+                const double rnu = Y[lv] - D[lv] * c.inv_rho;
+                const double rz = Y[lz] - D[lz] * c.inv_rho;
                 hv -= c.s * rnu;
                 hz = rz + c.s * rnu;
             }
@@ -357,8 +357,8 @@ __global__ void xstep_node_kernel(Dev d, XConst c) {
     double trS = 0.0, trT = 0.0, su = 0.0, sz = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const long long p = (long long)i * n + i;
-        trS += Y[lo.off_s + p] - D[lo.off_s + p] / c.rho;
-        trT += Y[lo.off_t + p] - D[lo.off_t + p] / c.rho;
+        trS += Y[lo.off_s + p] - D[lo.off_s + p] * c.inv_rho;
+        trT += Y[lo.off_t + p] - D[lo.off_t + p] * c.inv_rho;
         const double u = sum_partials(PU, d.nb, n, i);
         const double z = d.het ? sum_partials(PZ, d.nb, n, i) : 0.0;
         ug[i] = u;
@@ -371,7 +371,7 @@ __global__ void xstep_node_kernel(Dev d, XConst c) {
     su = block_sum(su, scratch);
     sz = block_sum(sz, scratch);
     if (threadIdx.x == 0) {
-        const double rl = Y[lo.lambda_ix] - D[lo.lambda_ix] / c.rho + c.inv_rho;  // +1/rho: c = -1 at lambda
+        const double rl = Y[lo.lambda_ix] - D[lo.lambda_ix] * c.inv_rho + c.inv_rho;  // +1/rho: c = -1 at lambda
         const double hl = rl + c.s * (c.alpha + trS + 2.0 * n - trT);
         d.scal[b * 8 + kLambda] = hl / c.lam_den;
     }
@@ -480,8 +480,8 @@ __global__ void __launch_bounds__(TB* TY) xstep_b_kernel(Dev d, XConst c) {
             const double hv = d.h[(long long)b * lo.m + l];
             {
                 const long long lz = lo.off_z + l, lv = lo.off_nu + l;
-                const double rz = Y[lz] - D[lz] / c.rho;
-                const double rnu = Y[lv] - D[lv] / c.rho;
+                const double rz = Y[lz] - D[lz] * c.inv_rho;
+                const double rnu = Y[lv] - D[lv] * c.inv_rho;
                 const double hz2 = rz + c.s * rnu - node[2 * n + i] - node[2 * n + j];
                 g = c.g11_0 * hv + c.g12_0 * hz2 + node[i] + node[j];
                 const double z = c.g12_0 * hv + c.g22_0 * hz2 + node[n + i] + node[n + j];
@@ -523,7 +523,7 @@ __global__ void __launch_bounds__(TB* TY) xstep_b_kernel(Dev d, XConst c) {
 #pragma unroll
         for (int k = 0; k < NE; ++k) {
             if (!ok[k]) continue;
-            const double rs = ys[k] - ds[k] / c.rho, rt = yt[k] - dt[k] / c.rho;
+            const double rs = ys[k] - ds[k] * c.inv_rho, rt = yt[k] - dt[k] * c.inv_rho;
             const double xs = c.s * (c.delta * rs - c.alpha_over_n + gv[k]);
             const double xt = c.s * (c.delta * rt + gv[k]);
             X[lo.off_s + pos[k]] = xs;
@@ -636,7 +636,7 @@ __global__ void xstep_diag_kernel(Dev d, XConst c) {
         const long long p = (long long)i * n + i;
         const long long ps = lo.off_s + p, pt = lo.off_t + p, py = lo.off_y + i;
         const double ys = Y[ps], yt = Y[pt], yy = Y[py];
-        const double rs = ys - D[ps] / c.rho, rt = yt - D[pt] / c.rho, ry = yy - D[py] / c.rho;
+        const double rs = ys - D[ps] * c.inv_rho, rt = yt - D[pt] * c.inv_rho, ry = yy - D[py] * c.inv_rho;
         const double xs = c.s * (c.delta * rs - c.alpha_over_n - deg + lam);
         const double xt = c.s * (c.delta * rt + 2.0 - deg - lam);
         const double xy = c.s * (c.delta * ry + 1.0 - deg);
@@ -700,7 +700,7 @@ __global__ void best_copy_kernel(Dev d, XConst c) {
         const double* D = d.D + (long long)b * d.nx;
         double* sc = d.bestScore + (long long)b * lo.m;
         for (long long l = (long long)blockIdx.x * blockDim.x + threadIdx.x; l < lo.m; l += stride)
-            sc[l] = X[lo.off_z + l] + D[lo.off_z + l] / c.rho;  // proj/src/admm_het.cpp:293-294
+            sc[l] = X[lo.off_z + l] + D[lo.off_z + l] * c.inv_rho;  // proj/src/admm_het.cpp:293-294
     }
 }
 

@@ -741,14 +741,27 @@ int Solver::bench_phase(int phase, int reps) {
                 per = small_ ? 1 : sch_.gemms();
                 break;
             case 1: {
+                // as in the iteration (dual update on); the diag pass without
+                // the O(n) dual update so the iteration counter is untouched
                 Dev d = d_;
-                d.upd_duals = 0;
                 d.track_best = 0;
                 launch_xstep_a(d, c_, s0_);
                 launch_xstep_node(d, c_, s0_);
                 launch_xstep_b(d, c_, s0_);
+                d.upd_duals = 0;
                 launch_xstep_diag(d, c_, s0_);
                 per = 4;
+                break;
+            }
+            case 5:
+                launch_xstep_a(d_, c_, s0_);  // scatter/gather pass A alone
+                per = 1;
+                break;
+            case 6: {
+                Dev d = d_;                   // pass B alone (dual update on)
+                d.track_best = 0;
+                launch_xstep_b(d, c_, s0_);
+                per = 1;
                 break;
             }
             case 2:

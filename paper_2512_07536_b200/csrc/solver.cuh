@@ -81,7 +81,8 @@ class Solver {
     const double* node_dev() const { return d_.node; }
     // Enqueue `reps` repetitions of one phase of the iteration on the main
     // stream (for live per-kernel timing): 0 projection (cone GEMMs),
-    // 1 x-step, 2 top-r selection, 3 trace SLEM, 4 prep. Returns the number
+    // 1 x-step, 2 top-r selection, 3 trace SLEM, 4 prep, 5 x-step pass A,
+    // 6 x-step pass B. Returns the number
     // of kernel launches per repetition.
     int bench_phase(int phase, int reps);
     int launches_per_iteration() const;
