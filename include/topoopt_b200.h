@@ -99,6 +99,10 @@ int tp_solve_het_node(int32_t n, const int32_t* degrees, const tp_config* cfg,
 int tp_anneal_degree(int32_t n, const int32_t* degrees, double t0, double cooling, int32_t steps,
                      int32_t moves_per_temp, uint64_t seed, int32_t* edges, int32_t* n_edges);
 int tp_default_warm_start(int32_t n, int32_t r, uint64_t seed, int32_t* edges, int32_t* n_edges);
+/* The annealing loop runs on the device when one is present (the reference's
+ * random stream reproduced there; TPB_HOST_ANNEAL=1 forces the host loop).
+ * First k outputs of the device std::mt19937_64 for `seed` (tests). */
+int tp_device_mt19937_64(uint64_t seed, int32_t k, uint64_t* out);
 
 /* ------------------------------------------------ batched solver handle */
 /* Independent solves of one n in lockstep (edge-budget sweeps, bandwidth

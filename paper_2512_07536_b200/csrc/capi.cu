@@ -7,6 +7,7 @@
 
 #include "../../include/topoopt_b200.h"
 #include "host_anneal.hpp"
+#include "anneal_kernels.cuh"
 #include "solver.cuh"
 
 using namespace tpb;
@@ -288,6 +289,13 @@ int tp_anneal_degree(int32_t n, const int32_t* degrees, double t0, double coolin
             edges[2 * k + 1] = es[k].second;
         }
         *n_edges = (int32_t)es.size();
+    });
+}
+
+int tp_device_mt19937_64(uint64_t seed, int32_t k, uint64_t* out) {
+    return guarded([&] {
+        if (k < 0) throw Error(kInvalidArgument, "negative count");
+        device_mt19937_64(seed, k, out);
     });
 }
 
