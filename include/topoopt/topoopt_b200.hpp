@@ -102,6 +102,31 @@ enum class BenchmarkKind { ring, grid2d, torus2d, exponential };
 BenchmarkKind benchmark_kind_from_string(const std::string& name);
 Topology generate_benchmark(BenchmarkKind kind, int n);
 
+// ------------------------------------------------------------------ consensus
+// proj/include/topoopt/consensus.hpp:11-54
+inline constexpr int kDefaultSimDim = 128;
+struct ConsensusTrace {
+    std::vector<double> errors;  // length iters + 1; errors[0] is the start
+    double t_iter_ms = 0.0;
+    std::string label;
+    std::uint64_t seed = 0;
+    std::string to_csv() const;  // "iter,time_ms,error"
+};
+ConsensusTrace simulate(const Matrix& w, int dim, int iters, std::uint64_t seed);  // GPU
+double convergence_time(const ConsensusTrace& trace, double threshold, double t_iter);
+struct CompareEntry {
+    std::string label;
+    Matrix w;
+    double t_iter_ms = 0.0;
+};
+struct CompareReport {
+    std::vector<ConsensusTrace> traces;
+    std::vector<double> convergence_ms;
+    std::string to_csv() const;  // "time_ms,label,error"
+};
+CompareReport compare(const std::vector<CompareEntry>& entries, int dim, int iters, double threshold,
+                      std::uint64_t seed, int threads = 1);
+
 // ------------------------------------------------------------------ eig
 Matrix project_nsd(const Matrix& s);  // GPU sign iteration
 Matrix project_psd(const Matrix& s);

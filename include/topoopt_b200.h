@@ -151,6 +151,13 @@ int tp_oz_gemm_dbg(int32_t ld, int32_t nmat, const double* a, int32_t ea, const 
                    int32_t use_e, double alpha, double beta, double* c, int8_t* cd, int32_t ec,
                    int32_t reps, double* ms, int32_t mode, long long* stamps);
 
+/* ---------------------------------------------------------------- evaluation */
+/* Consensus simulation (proj/src/consensus.cpp:29-67): errors[0..iters] of
+ * x <- W x from the reference's seeded normal start, W dense row-major n x n
+ * (validate_gossip rules: TP_ERR_INVALID_ARGUMENT). */
+int tp_consensus_simulate(int32_t n, const double* w, int32_t dim, int32_t iters, uint64_t seed,
+                          double* errors);
+
 /* ---------------------------------------------------------------- substeps */
 /* project_Y (proj/src/admm.cpp:268-277); x, d, y of length nx. */
 int tp_project_Y(int32_t n, int32_t r, double alpha, double rho, const double* x, const double* d,

@@ -65,6 +65,7 @@ def lib():
         L.ref_default_warm_start.argtypes = [I, I, U64, ip, ip]
         L.ref_anneal_degree.argtypes = [I, ip, D, D, I, I, U64, ip, ip]
         L.ref_generate_benchmark.argtypes = [C.c_char_p, I, ip, dp, ip]
+        L.ref_simulate.argtypes = [I, dp, I, I, C.c_uint64, dp]
         L.ref_spectral_report.argtypes = [I, dp, dp]
         L.ref_sym_eig.argtypes = [I, dp, dp, dp]
         L.ref_project_psd.argtypes = [I, dp, dp]
@@ -204,6 +205,14 @@ def generate_benchmark(kind: str, n: int):
     k = C.c_int(0)
     _check(lib().ref_generate_benchmark(kind.encode(), n, _ip(e), _dp(w), C.byref(k)))
     return e[: k.value].copy(), w[: k.value].copy()
+
+
+def simulate(w, dim: int, iters: int, seed: int):
+    """consensus simulate (proj/src/consensus.cpp:29-67) -> errors (iters + 1)."""
+    w = np.ascontiguousarray(np.asarray(w, np.float64))
+    out = np.zeros(iters + 1)
+    _check(lib().ref_simulate(w.shape[0], _dp(w), dim, iters, seed, _dp(out)))
+    return out
 
 
 def spectral_report(w):

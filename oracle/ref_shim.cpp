@@ -26,6 +26,7 @@
 #include "topoopt/admm.hpp"
 #include "topoopt/admm_het.hpp"
 #include "topoopt/anneal.hpp"
+#include "topoopt/consensus.hpp"
 #include "topoopt/bandwidth.hpp"
 #include "topoopt/eig.hpp"
 #include "topoopt/errors.hpp"
@@ -247,6 +248,15 @@ int ref_generate_benchmark(const char* kind, int n, int* edges, double* weights,
             edges[2 * k + 1] = t.edges[k].second;
             weights[k] = t.weights[k];
         }
+    });
+}
+
+// ---------------------------------------------------------------- consensus
+// simulate (proj/src/consensus.cpp:29-67): errors[0..iters]
+int ref_simulate(int n, const double* w, int dim, int iters, uint64_t seed, double* errors) {
+    return guarded([&] {
+        ConsensusTrace t = simulate(from_flat(n, w), dim, iters, seed);
+        for (size_t k = 0; k < t.errors.size(); ++k) errors[k] = t.errors[k];
     });
 }
 

@@ -645,3 +645,96 @@ def solve_het_node(degrees, warm_edges, rho=1.0, epsilon=1e-6, max_iter=20000, a
     rep = spectral_report(w)
     return Solution(edges, wts, w, rep["acf"], pick[lo.lambda_ix], converged, rep["connected"],
                     res if converged else best_res, ran, np.array(trace), note, changed)
+
+
+# ---------------------------------------------------------------- consensus
+class MT19937_64:
+    """std::mt19937_64 (the standard's parameters; the reference's Rng engine,
+    proj/include/topoopt/rng.hpp:12-53)."""
+
+    M = (1 << 64) - 1
+
+    def __init__(self, seed: int):
+        x = [seed & self.M]
+        for i in range(1, 312):
+            x.append((6364136223846793005 * (x[-1] ^ (x[-1] >> 62)) + i) & self.M)
+        self.x, self.i = x, 312
+
+    def __call__(self) -> int:
+        x = self.x
+        if self.i >= 312:
+            for i in range(312):
+                y = (x[i] & 0xFFFFFFFF80000000) | (x[(i + 1) % 312] & 0x7FFFFFFF)
+                x[i] = x[(i + 156) % 312] ^ (y >> 1) ^ (0xB5026F5AA96619E9 if y & 1 else 0)
+            self.i = 0
+        y = x[self.i]
+        self.i += 1
+        y ^= (y >> 29) & 0x5555555555555555
+        y ^= (y << 17) & 0x71D67FFFEDA60000 & self.M
+        y ^= (y << 37) & 0xFFF7EEE000000000 & self.M
+        y ^= y >> 43
+        return y & self.M
+
+
+class Rng:
+    """proj/include/topoopt/rng.hpp:12-53: uniform() and Box-Muller normal()
+    with the cached spare."""
+
+    def __init__(self, seed: int):
+        self.eng = MT19937_64(seed)
+        self.spare = None
+
+    def uniform(self) -> float:
+        return float(self.eng() >> 11) * 2.0 ** -53
+
+    def normal(self) -> float:
+        import math
+        if self.spare is not None:
+            s, self.spare = self.spare, None
+            return s
+        u1 = self.uniform()
+        while u1 <= 0.0:
+            u1 = self.uniform()
+        u2 = self.uniform()
+        radius = math.sqrt(-2.0 * math.log(u1))
+        angle = 6.283185307179586476925286766559 * u2
+        self.spare = radius * math.sin(angle)
+        return radius * math.cos(angle)
+
+
+def consensus_start(n: int, dim: int, seed: int) -> np.ndarray:
+    """The simulate() start state: i.i.d. normals, row-major fill, recentred
+    per coordinate (proj/src/consensus.cpp:34-54)."""
+    rng = Rng(seed)
+    s = np.array([[rng.normal() for _ in range(dim)] for _ in range(n)])
+    return s - s.mean(axis=0)
+
+
+def simulate(w: np.ndarray, dim: int, iters: int, seed: int) -> np.ndarray:
+    """consensus simulate (proj/src/consensus.cpp:29-67): Frobenius norm of the
+    deviation from the per-coordinate mean under x <- W x, recentred every
+    step; errors[0..iters]."""
+    w = np.asarray(w, dtype=np.float64)
+    if dim < 1:
+        raise ValueError("simulate: dim must be >= 1")
+    if iters < 0:
+        raise ValueError("simulate: iters must be >= 0")
+    s = consensus_start(w.shape[0], dim, seed)
+    errs = [np.linalg.norm(s)]
+    for _ in range(iters):
+        s = w @ s
+        s = s - s.mean(axis=0)
+        errs.append(np.linalg.norm(s))
+    return np.array(errs)
+
+
+def convergence_time(errors, threshold: float, t_iter: float) -> float:
+    """proj/src/consensus.cpp:69-75."""
+    if not threshold > 0.0:
+        raise ValueError("convergence_time: threshold <= 0")
+    if not t_iter > 0.0:
+        raise ValueError("convergence_time: t_iter <= 0")
+    for k, e in enumerate(errors):
+        if e <= threshold:
+            return k * t_iter
+    return float("inf")

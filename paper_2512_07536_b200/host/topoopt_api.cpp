@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdio>
 #include <numeric>
+#include <limits>
 #include <set>
 
 #include "topoopt_b200.h"
@@ -335,6 +336,61 @@ Topology generate_benchmark(BenchmarkKind kind, int n) {
     t.weights.assign(t.edges.size(), weight);
     t.normalize_and_validate();
     return t;
+}
+
+// ------------------------------------------------------------------ consensus
+static std::string g17(double v) {
+    char buf[40];
+    std::snprintf(buf, sizeof(buf), "%.17g", v);
+    return buf;
+}
+
+std::string ConsensusTrace::to_csv() const {
+    std::string out = "iter,time_ms,error\n";
+    for (size_t k = 0; k < errors.size(); ++k)
+        out += std::to_string(k) + "," + g17(static_cast<double>(k) * t_iter_ms) + "," + g17(errors[k]) + "\n";
+    return out;
+}
+
+ConsensusTrace simulate(const Matrix& w, int dim, int iters, std::uint64_t seed) {
+    if (w.rows() != w.cols()) throw std::invalid_argument("gossip matrix must be square");
+    ConsensusTrace t;
+    t.seed = seed;
+    t.errors.assign(iters >= 0 ? iters + 1 : 1, 0.0);
+    raise(tp_consensus_simulate(w.rows(), w.data().data(), dim, iters, seed, t.errors.data()));
+    return t;
+}
+
+double convergence_time(const ConsensusTrace& trace, double threshold, double t_iter) {
+    // proj/src/consensus.cpp:69-75
+    if (!(threshold > 0.0)) throw std::invalid_argument("convergence_time: threshold <= 0");
+    if (!(t_iter > 0.0)) throw std::invalid_argument("convergence_time: t_iter <= 0");
+    for (size_t k = 0; k < trace.errors.size(); ++k)
+        if (trace.errors[k] <= threshold) return static_cast<double>(k) * t_iter;
+    return std::numeric_limits<double>::infinity();
+}
+
+std::string CompareReport::to_csv() const {
+    std::string out = "time_ms,label,error\n";
+    for (const auto& trace : traces)
+        for (size_t k = 0; k < trace.errors.size(); ++k)
+            out += g17(static_cast<double>(k) * trace.t_iter_ms) + "," + trace.label + "," + g17(trace.errors[k]) +
+                   "\n";
+    return out;
+}
+
+CompareReport compare(const std::vector<CompareEntry>& entries, int dim, int iters, double threshold,
+                      std::uint64_t seed, int /*threads: the simulations run on the device in turn*/) {
+    // proj/src/consensus.cpp:91-120: every entry with the same seed and dim
+    CompareReport report;
+    for (const auto& e : entries) {
+        ConsensusTrace t = simulate(e.w, dim, iters, seed);
+        t.label = e.label;
+        t.t_iter_ms = e.t_iter_ms;
+        report.convergence_ms.push_back(convergence_time(t, threshold, e.t_iter_ms));
+        report.traces.push_back(std::move(t));
+    }
+    return report;
 }
 
 // ------------------------------------------------------------------ eig

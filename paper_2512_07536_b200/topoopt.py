@@ -136,6 +136,74 @@ def gossip_matrix(n: int, edges, weights) -> np.ndarray:
     return w
 
 
+def generate_benchmark(kind: str, n: int):
+    """proj/src/topology.cpp:227-281 -> (edges (k, 2), weights (k,)): ring,
+    grid2d, torus2d or exponential baselines with uniform weights."""
+    if n < 2:
+        raise ValueError("generate_benchmark: need at least two nodes")
+    es = set()
+
+    def add(a, b):
+        if a != b:
+            es.add((min(a, b), max(a, b)))
+
+    if kind == "ring":
+        if n < 3:
+            raise ValueError("generate_benchmark: ring needs n >= 3")
+        for i in range(n):
+            add(i, (i + 1) % n)
+        weight = 1.0 / 3.0
+    elif kind == "exponential":
+        hops, h = 0, 1
+        while h <= n - 1:
+            for i in range(n):
+                add(i, (i + h) % n)
+            h *= 2
+            hops += 1
+        weight = 1.0 / (2.0 * (hops + 1))
+    elif kind in ("grid2d", "torus2d"):
+        s = int(round(n ** 0.5))
+        if s * s != n or s < 2:
+            raise ValueError(f"generate_benchmark: {kind} needs a perfect square n >= 4")
+        for r in range(s):
+            for c in range(s):
+                u = r * s + c
+                if kind == "torus2d":
+                    add(u, r * s + (c + 1) % s)
+                    add(u, ((r + 1) % s) * s + c)
+                else:
+                    if c + 1 < s:
+                        add(u, u + 1)
+                    if r + 1 < s:
+                        add(u, u + s)
+        weight = 1.0 / ((4 if s >= 3 else 2) + 1)
+    else:
+        raise ValueError(f"unknown benchmark kind: {kind}")
+    edges = np.array(sorted(es), dtype=np.int32).reshape(-1, 2)
+    return edges, np.full(len(edges), weight)
+
+
+def simulate(w, dim: int = 128, iters: int = 100, seed: int = 0) -> np.ndarray:
+    """Consensus error trace (proj/src/consensus.cpp:29-67) on the GPU ->
+    errors (iters + 1)."""
+    w = _f64(w)
+    out = np.zeros(max(iters, 0) + 1)
+    _check(_lib.load().tp_consensus_simulate(w.shape[0], _dp(w), dim, iters, seed, _dp(out)))
+    return out
+
+
+def convergence_time(errors, threshold: float, t_iter: float) -> float:
+    """proj/src/consensus.cpp:69-75."""
+    if not threshold > 0.0:
+        raise ValueError("convergence_time: threshold <= 0")
+    if not t_iter > 0.0:
+        raise ValueError("convergence_time: t_iter <= 0")
+    for k, e in enumerate(errors):
+        if e <= threshold:
+            return k * t_iter
+    return float("inf")
+
+
 def spectral_report(w) -> dict:
     """proj/src/topology.cpp:125-144, on the GPU (Lanczos)."""
     w = _f64(w)

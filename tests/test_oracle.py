@@ -140,3 +140,23 @@ def test_oracle_against_live_reference():
         fs = p.feasible_start(ref.default_warm_start(n, r, 1))
         fo = O.feasible_start(pd.lo, ref.default_warm_start(n, r, 1), 2.0)
         assert np.max(np.abs(fs - fo)) < 1e-12
+
+
+def test_consensus_simulate_vs_golden(O, golden):
+    # proj/src/consensus.cpp:29-67 against the compiled reference
+    for c in golden("consensus.json"):
+        if c["n"] > 64:
+            continue  # the n=256 cases are checked on the GPU
+        w = O.gossip_matrix(c["n"], np.array(c["edges"]), np.array(c["weights"]))
+        err = O.simulate(w, c["dim"], c["iters"], c["seed"])
+        ref = np.array(c["errors"])
+        assert np.allclose(err, ref, rtol=1e-10, atol=1e-13 * ref[0])
+
+
+def test_generate_benchmark_python_mirror(T, golden):
+    # the Python mirror of generate_benchmark against the reference's graphs
+    for c in golden("spectral.json"):
+        if c["kind"] in ("ring", "grid2d", "torus2d", "exponential"):
+            e, w = T.generate_benchmark(c["kind"], c["n"])
+            assert e.tolist() == c["edges"]
+            assert np.array_equal(w, np.array(c["weights"]))
