@@ -158,6 +158,27 @@ struct CapacitySystem {
 };
 CapacitySystem node_level_constraints(int n, const std::vector<int>& degrees);
 
+// proj/include/topoopt/bandwidth.hpp:57-110: capacity-bound (inequality) systems
+struct ServerLink {
+    std::string name;
+    double bandwidth = 0.0;
+    int capacity = 0;
+};
+struct ServerTree {
+    int n_devices = 0;
+    std::vector<ServerLink> links;
+    std::vector<std::vector<int>> routes;  // per device pair column: links it uses
+    void validate() const;
+};
+ServerTree tiered8_tree(double leaf_bw, double group_bw, double root_bw);
+CapacitySystem intra_server_constraints(const ServerTree& tree);
+struct BCubeSpec {
+    int p = 2, k = 1;
+    std::vector<double> layer_bandwidths;
+    int n_servers() const;
+};
+CapacitySystem bcube_constraints(const BCubeSpec& spec);
+
 // ------------------------------------------------------------------ anneal
 struct AnnealConfig {  // proj/include/topoopt/anneal.hpp:12-20
     double t0 = 1.0;
@@ -243,13 +264,21 @@ struct ProblemDataHet {
     Vec beq;
 };
 
-// Node-level (equality, one row per node) systems run on the GPU; other
-// capacity systems raise std::invalid_argument.
+// Node-level equality systems (degree rows) and capacity-bound systems
+// (intra-server trees, BCube; capped binary projection) run on the GPU.
 ProblemDataHet assemble_het(const CapacitySystem& sys, std::optional<int> r, double alpha,
                             double rho);
 Vec project_binary_z(const Vec& v, int r);
 Vec project_Y_het(const ProblemDataHet& pd, const Vec& x_state, const Vec& duals);
 Solution solve_het(const CapacitySystem& sys, std::optional<int> r, const SolverConfig& cfg,
                    const std::optional<Topology>& warm_start = std::nullopt);
+
+struct UtilizationRow {
+    std::string label;
+    int capacity = 0;
+    int used = 0;
+};
+std::vector<UtilizationRow> utilization(const CapacitySystem& sys, const Topology& t);
+std::string utilization_csv(const std::vector<UtilizationRow>& rows);
 
 }  // namespace topoopt

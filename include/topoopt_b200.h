@@ -151,6 +151,26 @@ int tp_oz_gemm_dbg(int32_t ld, int32_t nmat, const double* a, int32_t ea, const 
                    int32_t use_e, double alpha, double beta, double* c, int8_t* cd, int32_t ec,
                    int32_t reps, double* ms, int32_t mode, long long* stamps);
 
+/* ---------------------------------------------------------------- capacity systems */
+/* Capacity-bound (inequality) systems (proj/include/topoopt/bandwidth.hpp:41-51,
+ * equality = false; intra_server_constraints / bcube_constraints): nrows rows
+ * given as CSR over the n(n-1)/2 edge columns (row_ptr[nrows+1], cols),
+ * upper-bound capacities caps[nrows], allowed[n(n-1)/2] mask.
+ * solve_het with an explicit edge total r (proj/src/admm_het.cpp:231-369);
+ * warm_edges null / n_warm < 0: anneal_topology on the system (host). */
+int tp_solve_het_capacity(int32_t n, int32_t nrows, const int32_t* row_ptr, const int32_t* cols,
+                          const int32_t* caps, const int32_t* allowed, int32_t r, const tp_config* cfg,
+                          const int32_t* warm_edges, int32_t n_warm, tp_result* out, int32_t* edges,
+                          double* weights, double* trace, char* note, int32_t note_cap);
+/* anneal_capacity_topology (proj/src/anneal.cpp:275-391), host. */
+int tp_anneal_capacity(int32_t n, int32_t nrows, const int32_t* row_ptr, const int32_t* cols, const int32_t* caps,
+                       const int32_t* allowed, int32_t r, double t0, double cooling, int32_t steps,
+                       int32_t moves_per_temp, uint64_t seed, int32_t* edges, int32_t* n_edges);
+/* project_binary_z_capped (proj/src/admm_het.cpp:125-154), v and z of n(n-1)/2. */
+int tp_project_binary_z_capped(int32_t n, int32_t nrows, const int32_t* row_ptr, const int32_t* cols,
+                               const int32_t* caps, const int32_t* allowed, const double* v, int32_t r,
+                               double* z);
+
 /* ---------------------------------------------------------------- evaluation */
 /* Consensus simulation (proj/src/consensus.cpp:29-67): errors[0..iters] of
  * x <- W x from the reference's seeded normal start, W dense row-major n x n

@@ -62,6 +62,12 @@ def lib():
         L.ref_solution_note.argtypes = [P, C.c_char_p, I]
         L.ref_solution_note.restype = I
         L.ref_allocate.argtypes = [dp, ip, I, I, dp, ip]
+        L.ref_capacity_system_sizes.argtypes = [I, D, D, D, I, ip]
+        L.ref_capacity_system.argtypes = [I, D, D, D, I, ip, ip, ip, ip]
+        L.ref_project_binary_z_capped.argtypes = [I, D, D, D, I, dp, I, dp]
+        L.ref_anneal_capacity.argtypes = [I, D, D, D, I, I, I, I, U64, ip, ip]
+        L.ref_solve_het_capacity.argtypes = [I, D, D, D, I, I, dp, ip, I, I, ip]
+        L.ref_solve_het_capacity.restype = P
         L.ref_default_warm_start.argtypes = [I, I, U64, ip, ip]
         L.ref_anneal_degree.argtypes = [I, ip, D, D, I, I, U64, ip, ip]
         L.ref_generate_benchmark.argtypes = [C.c_char_p, I, ip, dp, ip]
@@ -164,6 +170,61 @@ def solve_het_node(degrees, warm_edges=None, **cfg) -> RefSolution:
     h = lib().ref_solve_het_node(n, _ip(deg), _dp(_cfg(**cfg)), _ip(we), len(we),
                                  int(warm_edges is not None), C.byref(st))
     _check(st.value)
+    return _collect(h, n)
+
+
+# ---------------------------------------------------------------- capacity systems
+# spec: ("tiered8", leaf_bw, group_bw, root_bw) or ("bcube", p, k), optional
+# drop_last (the relaxed system of proj/tests/test_admm_het.cpp:214-229)
+def _spec(spec, drop_last=False):
+    kind = {"tiered8": 0, "bcube": 1}[spec[0]]
+    a, b, c = (list(spec[1:]) + [0.0, 0.0, 0.0])[:3]
+    return kind, float(a), float(b), float(c), int(drop_last)
+
+
+def capacity_system(spec, drop_last=False) -> dict:
+    """intra_server_constraints(tiered8_tree(...)) / bcube_constraints({p, k})
+    (proj/src/bandwidth.cpp:172-261) as CSR rows + capacities + allowed mask."""
+    args = _spec(spec, drop_last)
+    sz = np.zeros(4, np.int32)
+    _check(lib().ref_capacity_system_sizes(*args, _ip(sz)))
+    n, m, nr, nnz = (int(x) for x in sz)
+    rp = np.zeros(nr + 1, np.int32)
+    cols = np.zeros(max(nnz, 1), np.int32)
+    caps = np.zeros(max(nr, 1), np.int32)
+    allowed = np.zeros(m, np.int32)
+    _check(lib().ref_capacity_system(*args, _ip(rp), _ip(cols), _ip(caps), _ip(allowed)))
+    return {"n": n, "m": m, "row_ptr": rp.tolist(), "cols": cols[:nnz].tolist(), "caps": caps[:nr].tolist(),
+            "allowed": allowed.tolist()}
+
+
+def project_binary_z_capped(spec, v, r, drop_last=False):
+    """proj/src/admm_het.cpp:125-154."""
+    v = np.ascontiguousarray(np.asarray(v, np.float64))
+    z = np.zeros_like(v)
+    _check(lib().ref_project_binary_z_capped(*_spec(spec, drop_last), _dp(v), r, _dp(z)))
+    return z
+
+
+def anneal_capacity(spec, r, steps=200, moves_per_temp=0, seed=0, drop_last=False):
+    """anneal_topology on a capacity-bound system (proj/src/anneal.cpp:275-407)."""
+    args = _spec(spec, drop_last)
+    e = np.zeros((max(r, 1), 2), np.int32)
+    k = C.c_int(0)
+    _check(lib().ref_anneal_capacity(*args, r, steps, moves_per_temp, seed, _ip(e), C.byref(k)))
+    return e[: k.value].copy()
+
+
+def solve_het_capacity(spec, r, warm_edges=None, drop_last=False, **cfg) -> RefSolution:
+    """topoopt::solve_het on a capacity-bound system (proj/src/admm_het.cpp:231-369)."""
+    st = C.c_int(0)
+    we = np.ascontiguousarray(np.asarray(warm_edges if warm_edges is not None else np.zeros((0, 2)),
+                                         np.int32).reshape(-1, 2))
+    args = _spec(spec, drop_last)
+    h = lib().ref_solve_het_capacity(*args, r, _dp(_cfg(**cfg)), _ip(we), len(we), int(warm_edges is not None),
+                                     C.byref(st))
+    _check(st.value)
+    n = capacity_system(spec, drop_last)["n"]
     return _collect(h, n)
 
 

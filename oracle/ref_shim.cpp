@@ -147,6 +147,87 @@ void* ref_solve_het_node(int n, const int* degrees, const double* cfg, const int
     return out;
 }
 
+// ---------------------------------------------------------------- capacity systems
+// kind 0: intra_server_constraints(tiered8_tree(a, b, c)); kind 1:
+// bcube_constraints({p = a, k = b}); drop_last removes the last row (the
+// relaxation of proj/tests/test_admm_het.cpp:214-229).
+static CapacitySystem make_capacity_system(int kind, double a, double b, double c, int drop_last) {
+    CapacitySystem sys = kind == 0 ? intra_server_constraints(tiered8_tree(a, b, c))
+                                   : bcube_constraints({static_cast<int>(a), static_cast<int>(b), {}});
+    if (drop_last) sys.rows.pop_back();
+    return sys;
+}
+
+// sizes: {n, num_edges, rows, total row entries}
+int ref_capacity_system_sizes(int kind, double a, double b, double c, int drop_last, int* sizes) {
+    return guarded([&] {
+        CapacitySystem sys = make_capacity_system(kind, a, b, c, drop_last);
+        int nnz = 0;
+        for (const auto& row : sys.rows) nnz += static_cast<int>(row.edge_cols.size());
+        sizes[0] = sys.n;
+        sizes[1] = sys.num_edges;
+        sizes[2] = static_cast<int>(sys.rows.size());
+        sizes[3] = nnz;
+    });
+}
+
+int ref_capacity_system(int kind, double a, double b, double c, int drop_last, int* row_ptr, int* cols,
+                        int* caps, int* allowed) {
+    return guarded([&] {
+        CapacitySystem sys = make_capacity_system(kind, a, b, c, drop_last);
+        int k = 0;
+        row_ptr[0] = 0;
+        for (size_t r = 0; r < sys.rows.size(); ++r) {
+            for (int col : sys.rows[r].edge_cols) cols[k++] = col;
+            row_ptr[r + 1] = k;
+            caps[r] = sys.rows[r].capacity;
+        }
+        for (int l = 0; l < sys.num_edges; ++l) allowed[l] = sys.allowed[l];
+    });
+}
+
+int ref_project_binary_z_capped(int kind, double a, double b, double c, int drop_last, const double* v,
+                                int r, double* z) {
+    return guarded([&] {
+        CapacitySystem sys = make_capacity_system(kind, a, b, c, drop_last);
+        const Vec out = project_binary_z_capped(Vec(v, v + sys.num_edges), r, sys);
+        std::copy(out.begin(), out.end(), z);
+    });
+}
+
+int ref_anneal_capacity(int kind, double a, double b, double c, int drop_last, int r, int steps,
+                        int moves_per_temp, uint64_t seed, int* edges, int* n_edges) {
+    return guarded([&] {
+        CapacitySystem sys = make_capacity_system(kind, a, b, c, drop_last);
+        AnnealConfig ac;
+        ac.steps = steps;
+        ac.moves_per_temp = moves_per_temp;
+        ac.seed = seed;
+        Topology t = anneal_topology(sys, r, ac);
+        *n_edges = static_cast<int>(t.edges.size());
+        for (size_t k = 0; k < t.edges.size(); ++k) {
+            edges[2 * k] = t.edges[k].first;
+            edges[2 * k + 1] = t.edges[k].second;
+        }
+    });
+}
+
+void* ref_solve_het_capacity(int kind, double a, double b, double c, int drop_last, int r, const double* cfg,
+                             const int* warm_edges, int n_warm, int has_warm, int* status) {
+    auto* out = new SolOut;
+    *status = guarded([&] {
+        CapacitySystem sys = make_capacity_system(kind, a, b, c, drop_last);
+        std::optional<Topology> warm;
+        if (has_warm) warm = make_topo(sys.n, warm_edges, nullptr, n_warm);
+        out->sol = solve_het(sys, r, make_cfg(cfg), warm);
+    });
+    if (*status != 0) {
+        delete out;
+        return nullptr;
+    }
+    return out;
+}
+
 void ref_solution_free(void* h) { delete static_cast<SolOut*>(h); }
 
 // scalars: {acf, lambda_tilde, residual, wall_ms, converged, connected, repaired,

@@ -248,6 +248,7 @@ class Problem:
     A: sp.csr_matrix
     beq: np.ndarray
     degrees: np.ndarray | None = None
+    capsys: tuple | None = None  # capacity-bound rows: (rows, caps, allowed)
     _lu: object = field(default=None, repr=False)
 
     @property
@@ -325,6 +326,27 @@ def assemble_het_node(degrees, alpha: float = 2.0, rho: float = 1.0) -> Problem:
     return Problem(lo, total, alpha, rho, A, beq, degrees)
 
 
+def assemble_het_capacity(n: int, r: int, rows, caps, allowed, alpha: float = 2.0,
+                          rho: float = 1.0) -> Problem:
+    """Capacity-bound (inequality) system: no selection rows in the KKT
+    (q = 0), only the coupling rows g - z + nu = 0 (proj/src/admm_het.cpp:58-114)."""
+    m = n * (n - 1) // 2
+    if r < 1 or r > m:
+        raise ValueError("assemble_het: edge total outside [1, |E|]")
+    lo = het_layout(n, 0)
+    rows_t, cols_t, vals_t = _hom_triplets(lo)
+    hom_rows = 2 * n * n + n
+    l = np.arange(m)
+    crow = hom_rows + l
+    rows_t += [crow, crow, crow]
+    cols_t += [l, lo.off_z + l, lo.off_nu + l]
+    vals_t += [np.ones(m), -np.ones(m), np.ones(m)]
+    A = sp.csr_matrix((np.concatenate(vals_t), (np.concatenate(rows_t), np.concatenate(cols_t))),
+                      shape=(lo.neq, lo.nx))
+    beq = np.concatenate([hom_beq(n, alpha), np.zeros(m)])
+    return Problem(lo, r, alpha, rho, A, beq, None, (rows, caps, allowed))
+
+
 # ------------------------------------------------------------- projections
 def clamp_spectrum(a: np.ndarray, keep_negative: bool) -> np.ndarray:
     """Eigen-clamp of the symmetrized input, output symmetrized
@@ -398,9 +420,39 @@ def project_Y_het(pd: Problem, x: np.ndarray, d: np.ndarray) -> np.ndarray:
     y = v.copy()
     y[:pd.m + 1] = np.maximum(0.0, v[:pd.m + 1])
     project_cones(lo, v, y)
-    y[lo.off_z:lo.off_z + pd.m] = project_binary_z(v[lo.off_z:lo.off_z + pd.m], pd.r)
+    vz = v[lo.off_z:lo.off_z + pd.m]
+    y[lo.off_z:lo.off_z + pd.m] = (project_binary_z(vz, pd.r) if pd.capsys is None
+                                   else project_binary_z_capped(vz, pd.r, *pd.capsys))
     y[lo.off_nu:lo.off_nu + pd.m] = np.maximum(0.0, v[lo.off_nu:lo.off_nu + pd.m])
     return y
+
+
+def project_binary_z_capped(v, r: int, rows, caps, allowed) -> np.ndarray:
+    """proj/src/admm_het.cpp:125-154: ones in (v desc, index asc) order while
+    the column is allowed and every capacity row through it has room."""
+    v = np.asarray(v, np.float64)
+    m = len(v)
+    if r < 0 or r > m:
+        raise ValueError("project_binary_z_capped: r outside [0, |E|]")
+    col_rows = [[] for _ in range(m)]
+    for k, row in enumerate(rows):
+        for c in row:
+            col_rows[c].append(k)
+    load = [0] * len(rows)
+    z = np.zeros(m)
+    taken = 0
+    for col in order_desc(v):
+        if taken == r:
+            break
+        if not allowed[col]:
+            continue
+        if any(load[k] + 1 > caps[k] for k in col_rows[col]):
+            continue
+        z[col] = 1.0
+        for k in col_rows[col]:
+            load[k] += 1
+        taken += 1
+    return z
 
 
 def kkt_rhs(pd: Problem, y: np.ndarray, d: np.ndarray) -> np.ndarray:
@@ -738,3 +790,55 @@ def convergence_time(errors, threshold: float, t_iter: float) -> float:
         if e <= threshold:
             return k * t_iter
     return float("inf")
+
+
+def solve_het_capacity(n: int, rows, caps, allowed, r: int, warm_edges, rho=1.0, epsilon=1e-6,
+                       max_iter=20000, alpha=2.0, trace_acf=True) -> Solution:
+    """Capacity-bound heterogeneous driver (proj/src/admm_het.cpp:231-369 with
+    sys.equality false: capped binary projection, no degree repair)."""
+    pd = assemble_het_capacity(n, r, rows, caps, allowed, alpha, rho)
+    lo, m = pd.lo, pd.m
+    warm_edges = np.asarray(warm_edges, np.int64).reshape(-1, 2)
+    if len(warm_edges) > r:
+        raise ValueError("solve_het: warm start has more than r edges")
+    x = feasible_start(lo, warm_edges, alpha)
+    for i, j in warm_edges:
+        x[lo.off_z + edge_index(n, i, j)] = 1.0
+    x[lo.off_nu:lo.off_nu + m] = np.maximum(0.0, x[lo.off_z:lo.off_z + m] - x[:m])
+    d = np.zeros(pd.nx)
+    y = x.copy()
+    best_res, best_y, best_iter = math.inf, y.copy(), 0
+    res, converged, ran = math.inf, False, 0
+    trace = []
+    for it in range(1, max_iter + 1):
+        ran = it
+        y = project_Y_het(pd, x, d)
+        x, _ = update_X(pd, y, d)
+        d += pd.rho * (x - y)
+        res = float(np.sum((x - y) ** 2))
+        trace.append((it, res, y[lo.lambda_ix], acf_of_g(n, y) if trace_acf else np.nan))
+        if res < best_res:
+            best_res, best_y, best_iter = res, y.copy(), it
+        if res <= epsilon:
+            converged = True
+            break
+    pick = y if converged else best_y
+    note = "" if converged else f"stopped at max_iter; best iterate from iteration {best_iter}"
+    sel = np.nonzero(pick[lo.off_z:lo.off_z + m] > 0.5)[0]
+    weights = np.maximum(0.0, pick[:m])
+    if len(sel) == 0:
+        raise DegenerateSolutionError("no edge selected")
+    if len(sel) < r:
+        note = (note + "; " if note else "") + f"capacity limits stopped selection at {len(sel)} of {r} edges"
+    e = enumerate_edges(n)
+    node_sum = np.zeros(n)
+    for l in sel:
+        node_sum[e[l, 0]] += weights[l]
+        node_sum[e[l, 1]] += weights[l]
+    worst = node_sum.max()
+    scale = 1.0 / worst if worst > 1.0 else 1.0
+    edges, wts = e[sel], weights[sel] * scale
+    w = gossip_matrix(n, edges, wts)
+    rep = spectral_report(w)
+    return Solution(edges, wts, w, rep["acf"], pick[lo.lambda_ix], converged, rep["connected"],
+                    res if converged else best_res, ran, np.array(trace), note, False)

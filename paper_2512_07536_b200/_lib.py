@@ -84,6 +84,10 @@ SIGNATURES = {
     "tp_solver_launches_per_iteration": (_I, [_P, _ip]),
     "tp_set_gemm_variant": (_I, [_I]),
     "tp_bench_gemm": (_I, [_I, _I, _I, _I, _dp]),
+    "tp_solve_het_capacity": (_I, [_I, _I, _ip, _ip, _ip, _ip, _I, _cfgp, _ip, _I, _resp, _ip, _dp, _dp,
+                                   C.c_char_p, _I]),
+    "tp_anneal_capacity": (_I, [_I, _I, _ip, _ip, _ip, _ip, _I, _D, _D, _I, _I, _U64, _ip, _ip]),
+    "tp_project_binary_z_capped": (_I, [_I, _I, _ip, _ip, _ip, _ip, _dp, _I, _dp]),
     "tp_consensus_simulate": (_I, [_I, _dp, _I, _I, _U64, _dp]),
     "tp_device_mt19937_64": (_I, [_U64, _I, C.POINTER(C.c_uint64)]),
     "tp_oz_gemm": (_I, [_I, _I, _dp, _I, _dp, _I, _I, C.c_double, C.c_double, _dp, C.c_void_p, _I, _I, _dp]),

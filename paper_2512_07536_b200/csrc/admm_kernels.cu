@@ -381,8 +381,19 @@ __global__ void xstep_node_kernel(Dev d, XConst c) {
             node[i] = c.c1 * (ug[i] - ubar) + c.c2 * ubar;
         return;
     }
-    // het: rhs_d = G21(Q) u_g + G22(Q) u_z - e ; Q = (n-2) I + J
     const double zbar = sz / n;
+    if (d.cap) {
+        // capacity-bound rows are not in the KKT (q = 0): the commuting 2x2
+        // block G(K) alone, no degree multipliers
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const double pg = ug[i] - ubar, pz = uz[i] - zbar;
+            node[i] = c.c1_11 * pg + c.c2_11 * ubar + c.c1_12 * pz + c.c2_12 * zbar;
+            node[n + i] = c.c1_12 * pg + c.c2_12 * ubar + c.c1_22 * pz + c.c2_22 * zbar;
+            node[2 * n + i] = 0.0;
+        }
+        return;
+    }
+    // het: rhs_d = G21(Q) u_g + G22(Q) u_z - e ; Q = (n-2) I + J
     double srhs = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const double rhs = c.g12_p * (ug[i] - ubar) + c.g12_1 * ubar + c.g22_p * (uz[i] - zbar) +

@@ -25,6 +25,7 @@ XConst make_xconst(int n, double alpha, double rho);
 struct Dev {
     Layout lo;
     int B = 1;       // solves in lockstep
+    int cap = 0;             // capacity-bound het system: no degree rows (q = 0)
     int het = 0;
     int nb = 0;      // 32-wide node blocks
     int ntile = 0;   // nb (nb+1) / 2 upper block pairs

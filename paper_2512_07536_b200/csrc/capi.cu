@@ -343,3 +343,96 @@ std::vector<int> default_warm(int n, int r, uint64_t seed) {
 }
 
 }  // namespace
+
+namespace {
+
+// capacity rows from the C ABI arrays, checked as check_system does
+// (proj/src/admm_het.cpp:20-31)
+CapSystem cap_system(int n, int nrows, const int32_t* row_ptr, const int32_t* cols, const int32_t* caps,
+                     const int32_t* allowed) {
+    if (n < 2) throw Error(kInvalidArgument, "capacity system: need at least 2 nodes");
+    if (nrows < 0 || !row_ptr || !allowed || (nrows > 0 && (!cols || !caps)))
+        throw Error(kInvalidArgument, "capacity system: malformed rows");
+    const int m = n * (n - 1) / 2;
+    CapSystem s;
+    s.nrows = nrows;
+    s.row_ptr.assign(row_ptr, row_ptr + nrows + 1);
+    if (s.row_ptr[0] != 0) throw Error(kInvalidArgument, "capacity system: malformed rows");
+    for (int r = 0; r < nrows; ++r)
+        if (s.row_ptr[r + 1] < s.row_ptr[r]) throw Error(kInvalidArgument, "capacity system: malformed rows");
+    s.cols.assign(cols ? cols : row_ptr, (cols ? cols : row_ptr) + s.row_ptr[nrows]);
+    for (int r = 0; r < nrows; ++r)
+        for (int q = s.row_ptr[r]; q < s.row_ptr[r + 1]; ++q)
+            if (s.cols[q] < 0 || s.cols[q] >= m)
+                throw Error(kInvalidArgument, "capacity system: row " + std::to_string(r) +
+                                                  " references a column outside [0, |E|)");
+    s.caps.assign(caps ? caps : row_ptr, (caps ? caps : row_ptr) + nrows);
+    s.allowed.assign(allowed, allowed + m);
+    return s;
+}
+
+CapRows cap_rows(const CapSystem& s) {
+    CapRows r;
+    r.nrows = s.nrows;
+    r.row_ptr = s.row_ptr;
+    r.cols = s.cols;
+    r.caps = s.caps;
+    r.allowed = s.allowed;
+    return r;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tp_solve_het_capacity(int32_t n, int32_t nrows, const int32_t* row_ptr, const int32_t* cols,
+                          const int32_t* caps, const int32_t* allowed, int32_t r, const tp_config* cfg,
+                          const int32_t* warm_edges, int32_t n_warm, tp_result* out, int32_t* edges,
+                          double* weights, double* trace, char* note, int32_t note_cap) {
+    return guarded([&] {
+        require_device();
+        const Config c = to_cfg(cfg);
+        validate(c);
+        const CapSystem sys = cap_system(n, nrows, row_ptr, cols, caps, allowed);
+        const int m = n * (n - 1) / 2;
+        if (r < 1 || r > m) throw Error(kInvalidArgument, "assemble_het: edge total outside [1, |E|]");
+        std::vector<int> warm;
+        if (warm_edges && n_warm >= 0) {
+            warm = packed_edges(n, warm_edges, n_warm);
+        } else {
+            // anneal_topology -> anneal_capacity_topology (proj/src/anneal.cpp:393-407)
+            AnnealParams ap;
+            ap.seed = cfg ? cfg->seed : 0;
+            for (const auto& e : anneal_capacity_edges(n, cap_rows(sys), r, ap))
+                warm.push_back((int)edge_idx(n, e.first, e.second));
+        }
+        Solver s(n, 1, true, {r}, {}, c, &sys);
+        s.set_warm(0, warm);
+        s.start();
+        s.run_to_completion();
+        s.finish();
+        fill_result(s.result(0), out, edges, weights, trace, note, note_cap);
+    });
+}
+
+int tp_anneal_capacity(int32_t n, int32_t nrows, const int32_t* row_ptr, const int32_t* cols, const int32_t* caps,
+                       const int32_t* allowed, int32_t r, double t0, double cooling, int32_t steps,
+                       int32_t moves_per_temp, uint64_t seed, int32_t* edges, int32_t* n_edges) {
+    return guarded([&] {
+        const CapSystem sys = cap_system(n, nrows, row_ptr, cols, caps, allowed);
+        AnnealParams ap;
+        ap.t0 = t0;
+        ap.cooling = cooling;
+        ap.steps = steps;
+        ap.moves_per_temp = moves_per_temp;
+        ap.seed = seed;
+        const auto es = anneal_capacity_edges(n, cap_rows(sys), r, ap);
+        for (size_t k = 0; k < es.size(); ++k) {
+            edges[2 * k] = es[k].first;
+            edges[2 * k + 1] = es[k].second;
+        }
+        *n_edges = (int32_t)es.size();
+    });
+}
+
+}  // extern "C"

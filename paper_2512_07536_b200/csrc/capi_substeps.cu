@@ -598,4 +598,56 @@ int tp_oz_gemm_dbg(int32_t ld, int32_t nmat, const double* a, int32_t ea, const 
     });
 }
 
+
+// project_binary_z_capped (proj/src/admm_het.cpp:125-154) on the device.
+int tp_project_binary_z_capped(int32_t n, int32_t nrows, const int32_t* row_ptr, const int32_t* cols,
+                               const int32_t* caps, const int32_t* allowed, const double* v, int32_t r,
+                               double* z) {
+    return guarded([&] {
+        require_device();
+        if (n < 2) throw Error(kInvalidArgument, "capacity system: need at least 2 nodes");
+        const int m = n * (n - 1) / 2;
+        if (r < 0 || r > m) throw Error(kInvalidArgument, "project_binary_z_capped: r outside [0, |E|]");
+        const int nnz = row_ptr[nrows];
+        for (int q = 0; q < nnz; ++q)
+            if (cols[q] < 0 || cols[q] >= m)
+                throw Error(kInvalidArgument, "capacity system: a row references a column outside [0, |E|)");
+        std::vector<int> cnt(m + 1, 0), colr(std::max(nnz, 1));
+        for (int q = 0; q < nnz; ++q) ++cnt[cols[q] + 1];
+        for (int l = 0; l < m; ++l) cnt[l + 1] += cnt[l];
+        std::vector<int> pos(cnt.begin(), cnt.end() - 1);
+        for (int rr = 0; rr < nrows; ++rr)
+            for (int q = row_ptr[rr]; q < row_ptr[rr + 1]; ++q) colr[pos[cols[q]]++] = rr;
+        int pad = 1;
+        while (pad < m) pad <<= 1;
+        DBuf<double> dv(m);
+        DBuf<int> dcp(m + 1), dcr(colr.size()), dcaps(std::max(nrows, 1)), dal(m), dr(1), didx(pad),
+            dload(std::max(nrows, 1));
+        DBuf<unsigned long long> dkeys(pad);
+        dv.up(v, m);
+        dcp.up(cnt.data(), m + 1);
+        dcr.up(colr.data(), colr.size());
+        if (nrows > 0) dcaps.up(caps, nrows);
+        dal.up(allowed, m);
+        dr.up(&r, 1);
+        CappedArgs a{};
+        a.base = dv.p;
+        a.stride = m;
+        a.m = m;
+        a.r = dr.p;
+        a.colr_ptr = dcp.p;
+        a.colr = dcr.p;
+        a.caps = dcaps.p;
+        a.nrows = nrows;
+        a.allowed = dal.p;
+        a.keys = dkeys.p;
+        a.idx = didx.p;
+        a.load = dload.p;
+        a.pad = pad;
+        a.done = nullptr;
+        launch_capped_z(a, 1, 0);
+        TPB_CUDA(cudaDeviceSynchronize());
+        dv.down(z, m);
+    });
+}
 }  // extern "C"

@@ -27,4 +27,16 @@ std::vector<int> anneal_degree_packed(const std::vector<int>& degrees, const Ann
 std::vector<std::pair<int, int>> anneal_degree_edges(const std::vector<int>& degrees,
                                                      const AnnealParams& p);
 
+// Capacity rows (rows -> edge columns CSR, upper-bound capacities, allowed
+// mask) of an inequality system.
+struct CapRows {
+    int nrows = 0;
+    std::vector<int> row_ptr, cols, caps, allowed;
+};
+
+// anneal_topology on a capacity-bound system (proj/src/anneal.cpp:275-407),
+// host; lexicographic (i, j) pairs. Throws kInfeasible / kInvalidArgument.
+std::vector<std::pair<int, int>> anneal_capacity_edges(int n, const CapRows& sys, int r,
+                                                       const AnnealParams& p);
+
 }  // namespace tpb

@@ -247,4 +247,69 @@ void init_attrs_select() {
     set_max_dyn_smem(topr_kernel);
 }
 
+
+// ---------------------------------------------------------------- capped
+__global__ void __launch_bounds__(1024) capped_z_kernel(CappedArgs a) {
+    const int b = blockIdx.x;
+    if (a.done && a.done[b * 8 + 1]) return;
+    const long long m = a.m;
+    const int pad = a.pad, tid = threadIdx.x, nt = blockDim.x;
+    double* v = a.base + (long long)b * a.stride;
+    unsigned long long* key = a.keys + (long long)b * pad;
+    int* idx = a.idx + (long long)b * pad;
+    int* load = a.load + (long long)b * a.nrows;
+    // ascending (key, index) with key = ~order_key(v): v descending, ties to
+    // the lower index (the reference's order_desc comparator)
+    for (int k = tid; k < pad; k += nt) {
+        key[k] = k < m ? ~order_key(v[k]) : ~0ULL;
+        idx[k] = k;
+    }
+    for (int k = tid; k < a.nrows; k += nt) load[k] = 0;
+    __syncthreads();
+    for (int size = 2; size <= pad; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int k = tid; k < pad; k += nt) {
+                const int p = k ^ stride;
+                if (p <= k) continue;
+                const bool up = (k & size) == 0;
+                const unsigned long long ka = key[k], kb = key[p];
+                const int ia = idx[k], ib = idx[p];
+                const bool gt = ka > kb || (ka == kb && ia > ib);
+                if (gt == up) {
+                    key[k] = kb;
+                    key[p] = ka;
+                    idx[k] = ib;
+                    idx[p] = ia;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (long long k = tid; k < m; k += nt) v[k] = 0.0;
+    __syncthreads();
+    if (tid == 0) {
+        const int r = a.r[b];
+        int taken = 0;
+        for (int p = 0; p < pad && taken < r; ++p) {
+            const int col = idx[p];
+            if (col >= m || !a.allowed[col]) continue;
+            bool fits = true;
+            for (int q = a.colr_ptr[col]; q < a.colr_ptr[col + 1]; ++q)
+                if (load[a.colr[q]] + 1 > a.caps[a.colr[q]]) {
+                    fits = false;
+                    break;
+                }
+            if (!fits) continue;
+            v[col] = 1.0;
+            for (int q = a.colr_ptr[col]; q < a.colr_ptr[col + 1]; ++q) ++load[a.colr[q]];
+            ++taken;
+        }
+    }
+}
+
+void launch_capped_z(const CappedArgs& a, int B, cudaStream_t st) {
+    capped_z_kernel<<<B, 1024, 0, st>>>(a);
+    TPB_CHECK_LAUNCH();
+}
+
 }  // namespace tpb

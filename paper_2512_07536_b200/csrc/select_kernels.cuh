@@ -18,6 +18,28 @@ struct SelectArgs {
 };
 
 void launch_topr(const SelectArgs& a, int B, cudaStream_t st);
+
+// project_binary_z_capped (proj/src/admm_het.cpp:125-154): ones taken in the
+// order (v desc, index asc) while every capacity row through the column has
+// room and the column is allowed, until r are taken. One CTA per solve:
+// bitonic sort of (key, index) in the per-solve scratch, then the greedy scan.
+struct CappedArgs {
+    double* base;           // per-solve z values (in place), base + b*stride
+    long long stride;
+    long long m;
+    const int* r;           // per-solve edge total
+    const int* colr_ptr;    // column -> capacity rows (CSR, m+1)
+    const int* colr;
+    const int* caps;        // per row
+    int nrows;
+    const int* allowed;     // per column
+    unsigned long long* keys;  // scratch B x pad
+    int* idx;                  // scratch B x pad
+    int* load;                 // scratch B x nrows
+    int pad;                   // power of two >= m
+    const int* done;           // ictl or null
+};
+void launch_capped_z(const CappedArgs& a, int B, cudaStream_t st);
 void launch_compact(const double* g, long long stride, long long m, int* list, int* count, int cap,
                     int B, cudaStream_t st);
 

@@ -66,8 +66,9 @@ T* dalloc(cudaStream_t st, std::vector<void*>& pool, size_t count) {
 }  // namespace
 
 Solver::Solver(int n, int B, bool het, const std::vector<int>& r, const std::vector<int>& degrees,
-               const Config& cfg)
-    : B_(B), het_(het), cfg_(cfg) {
+               const Config& cfg, const CapSystem* cap)
+    : B_(B), het_(het || cap != nullptr), cfg_(cfg) {
+    het = het_;
     phase_mark("(caller, before the solver)");
     validate(cfg);
     if (n < 2) throw Error(kInvalidArgument, "assemble: need at least 2 nodes");
@@ -75,7 +76,23 @@ Solver::Solver(int n, int B, bool het, const std::vector<int>& r, const std::vec
     lo_ = het ? het_layout(n, n) : hom_layout(n);
     const int m = lo_.m;
     r_host_.resize(B);
-    if (het) {
+    if (cap) {
+        // proj/src/admm_het.cpp:20-31, 37-48 (check_system, resolve_edge_total)
+        cap_ = true;
+        capsys_ = *cap;
+        if ((int)capsys_.allowed.size() != m)
+            throw Error(kInvalidArgument, "capacity system: allowed mask size differs from |E|");
+        if ((int)capsys_.row_ptr.size() != capsys_.nrows + 1 || (int)capsys_.caps.size() != capsys_.nrows)
+            throw Error(kInvalidArgument, "capacity system: malformed rows");
+        for (int c : capsys_.cols)
+            if (c < 0 || c >= m)
+                throw Error(kInvalidArgument, "capacity system: a row references a column outside [0, |E|)");
+        if ((int)r.size() != B) throw Error(kInvalidArgument, "capacity-bound system needs an explicit edge total");
+        for (int b = 0; b < B; ++b) {
+            if (r[b] < 1 || r[b] > m) throw Error(kInvalidArgument, "assemble_het: edge total outside [1, |E|]");
+            r_host_[b] = r[b];
+        }
+    } else if (het) {
         if ((int)degrees.size() != B * n)
             throw Error(kInvalidArgument, "node_level_constraints: degree list size mismatch");
         for (int b = 0; b < B; ++b) {
@@ -121,9 +138,23 @@ Solver::Solver(int n, int B, bool het, const std::vector<int>& r, const std::vec
     TPB_CUDA(cudaEventCreateWithFlags(&ev_sel_, cudaEventDisableTiming));
     TPB_CUDA(cudaEventCreateWithFlags(&ev_slem_, cudaEventDisableTiming));
     alloc();
-    if (het) {
+    if (het && !cap_) {
         std::vector<double> dg(degrees.begin(), degrees.end());
         TPB_CUDA(cudaMemcpy(d_deg_, dg.data(), dg.size() * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    if (cap_) {
+        // column -> rows CSR for the capped projection
+        std::vector<int> cnt(m + 1, 0), colr(capsys_.cols.size());
+        for (int c : capsys_.cols) ++cnt[c + 1];
+        for (int l = 0; l < m; ++l) cnt[l + 1] += cnt[l];
+        std::vector<int> pos(cnt.begin(), cnt.end() - 1);
+        for (int rr = 0; rr < capsys_.nrows; ++rr)
+            for (int q = capsys_.row_ptr[rr]; q < capsys_.row_ptr[rr + 1]; ++q) colr[pos[capsys_.cols[q]]++] = rr;
+        TPB_CUDA(cudaMemcpy(cap_colr_ptr_, cnt.data(), cnt.size() * sizeof(int), cudaMemcpyHostToDevice));
+        if (!colr.empty())
+            TPB_CUDA(cudaMemcpy(cap_colr_, colr.data(), colr.size() * sizeof(int), cudaMemcpyHostToDevice));
+        TPB_CUDA(cudaMemcpy(cap_caps_, capsys_.caps.data(), capsys_.nrows * sizeof(int), cudaMemcpyHostToDevice));
+        TPB_CUDA(cudaMemcpy(cap_allowed_, capsys_.allowed.data(), m * sizeof(int), cudaMemcpyHostToDevice));
     }
     TPB_CUDA(cudaMemcpy(d_r_, r_host_.data(), B * sizeof(int), cudaMemcpyHostToDevice));
     warm_.assign(B, {});
@@ -163,6 +194,7 @@ void Solver::alloc() {
     d_.lo = lo_;
     d_.B = B;
     d_.het = het_ ? 1 : 0;
+    d_.cap = cap_ ? 1 : 0;
     d_.nb = (n + 31) / 32;
     d_.ntile = d_.nb * (d_.nb + 1) / 2;
     d_.ld = ld_;
@@ -223,6 +255,18 @@ void Solver::alloc() {
     if (std::getenv("TPB_SLEM_STATS")) {
         slem_stats_ = dalloc<int>(s0_, allocs_, 2);
         TPB_CUDA(cudaMemsetAsync(slem_stats_, 0, 2 * sizeof(int), s0_));
+    }
+    if (cap_) {
+        cap_pad_ = 1;
+        while (cap_pad_ < m) cap_pad_ <<= 1;
+        cap_colr_ptr_ = dalloc<int>(s0_, allocs_, (size_t)m + 1);
+        cap_colr_ = dalloc<int>(s0_, allocs_, std::max<size_t>(capsys_.cols.size(), 1));
+        cap_caps_ = dalloc<int>(s0_, allocs_, std::max(capsys_.nrows, 1));
+        cap_allowed_ = dalloc<int>(s0_, allocs_, (size_t)m);
+        cap_keys_ = dalloc<unsigned long long>(s0_, allocs_, (size_t)B * cap_pad_);
+        cap_idx_ = dalloc<int>(s0_, allocs_, (size_t)B * cap_pad_);
+        cap_load_ = dalloc<int>(s0_, allocs_, (size_t)B * std::max(capsys_.nrows, 1));
+        TPB_CUDA(cudaStreamSynchronize(s0_));
     }
     list_ = dalloc<int>(s0_, allocs_,(size_t)B * list_cap_);
     list_count_ = dalloc<int>(s0_, allocs_,B);
@@ -337,6 +381,27 @@ void Solver::enqueue_select(cudaStream_t st) {
     a.list_count = list_count_;
     a.list_cap = list_cap_;
     a.done = d_.ictl;
+    if (cap_) {
+        // project_binary_z_capped on the z block, then the g support for the SLEM
+        CappedArgs c{};
+        c.base = d_.Y + lo_.off_z;
+        c.stride = lo_.nx;
+        c.m = lo_.m;
+        c.r = d_r_;
+        c.colr_ptr = cap_colr_ptr_;
+        c.colr = cap_colr_;
+        c.caps = cap_caps_;
+        c.nrows = capsys_.nrows;
+        c.allowed = cap_allowed_;
+        c.keys = cap_keys_;
+        c.idx = cap_idx_;
+        c.load = cap_load_;
+        c.pad = cap_pad_;
+        c.done = d_.ictl;
+        launch_capped_z(c, B_, st);
+        launch_compact(d_.Y, lo_.nx, lo_.m, list_, list_count_, list_cap_, B_, st);
+        return;
+    }
     if (het_) {
         a.base = d_.Y + lo_.off_z;
         a.gbase = d_.Y;
@@ -625,7 +690,7 @@ void Solver::epilogue_het() {
         std::vector<int> target(n);
         for (int i = 0; i < n; ++i) target[i] = (int)degd[(size_t)b * n + i];
         bool changed = false;
-        if (!repair_selection(n, target, sel, w, score, &changed)) {
+        if (!cap_ && !repair_selection(n, target, sel, w, score, &changed)) {
             if (!R.note.empty()) R.note += "; ";
             R.note += "degree repair incomplete";
         }

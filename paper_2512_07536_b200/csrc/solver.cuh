@@ -26,6 +26,16 @@ struct Config {
 };
 
 void validate(const Config& c);
+
+// Capacity-bound (inequality) het system (proj/include/topoopt/bandwidth.hpp:
+// 41-51 with equality = false): rows over edge columns with upper-bound
+// capacities and an allowed mask; no selection rows in the KKT (q = 0), the
+// binary projection is project_binary_z_capped.
+struct CapSystem {
+    int nrows = 0;
+    std::vector<int> row_ptr, cols, caps;  // rows -> edge columns (CSR)
+    std::vector<int> allowed;              // per edge column
+};
 void phase_mark(const char* what);
 
 // One-off spectral reports (feasible start, final topology): complete Krylov
@@ -52,7 +62,7 @@ class Solver {
    public:
     // r: per-solve edge budget (hom) ; degrees: B x n targets (het node-level).
     Solver(int n, int B, bool het, const std::vector<int>& r, const std::vector<int>& degrees,
-           const Config& cfg);
+           const Config& cfg, const CapSystem* cap = nullptr);
     ~Solver();
     Solver(const Solver&) = delete;
     Solver& operator=(const Solver&) = delete;
@@ -117,6 +127,12 @@ class Solver {
     double* d_deg_ = nullptr;
     double *w0_ = nullptr, *w1_ = nullptr, *w2_ = nullptr;
     bool ozaki_ = false;        // cone GEMMs on the int8 tensor cores (else FP64 DMMA)
+    bool cap_ = false;          // capacity-bound het system
+    CapSystem capsys_;
+    int cap_pad_ = 0;
+    int *cap_colr_ptr_ = nullptr, *cap_colr_ = nullptr, *cap_caps_ = nullptr, *cap_allowed_ = nullptr;
+    unsigned long long* cap_keys_ = nullptr;
+    int *cap_idx_ = nullptr, *cap_load_ = nullptr;
     OzWork oz_;
     double* sk_ws_ = nullptr;   // stream-K partial tiles (B == 1, large n)
     int* sk_flags_ = nullptr;

@@ -494,13 +494,170 @@ Topology anneal_degree_topology(const std::vector<int>& degrees, const AnnealCon
     return t;
 }
 
+namespace {
+struct FlatRows {
+    std::vector<int32_t> row_ptr{0}, cols, caps, allowed;
+};
+FlatRows flat_rows(const CapacitySystem& sys) {
+    FlatRows f;
+    for (const auto& row : sys.rows) {
+        for (int c : row.edge_cols) f.cols.push_back(c);
+        f.row_ptr.push_back((int32_t)f.cols.size());
+        f.caps.push_back(row.capacity);
+    }
+    f.allowed.assign(sys.allowed.begin(), sys.allowed.end());
+    if ((int)f.allowed.size() != sys.num_edges)
+        throw std::invalid_argument("capacity system: allowed mask size differs from |E|");
+    if (f.cols.empty()) f.cols.push_back(0);
+    if (f.caps.empty()) f.caps.push_back(0);
+    return f;
+}
+}  // namespace
+
 Topology anneal_topology(const CapacitySystem& sys, std::optional<int> r, const AnnealConfig& cfg) {
-    std::vector<int32_t> deg;
-    if (!node_level_degrees(sys, deg))
-        throw std::invalid_argument("anneal_topology: only node-level equality systems are supported");
-    if (r && *r != sys.implied_edge_total())
-        throw std::invalid_argument("anneal_topology: r conflicts with the degree sum");
-    return anneal_degree_topology(std::vector<int>(deg.begin(), deg.end()), cfg);
+    // proj/src/anneal.cpp:393-407
+    if (sys.equality) {
+        std::vector<int32_t> deg;
+        if (!node_level_degrees(sys, deg))
+            throw std::invalid_argument("anneal_topology: equality system is not node-level");
+        if (r && *r != sys.implied_edge_total())
+            throw std::invalid_argument("anneal_topology: r conflicts with the degree sum");
+        return anneal_degree_topology(std::vector<int>(deg.begin(), deg.end()), cfg);
+    }
+    if (!r) throw std::invalid_argument("anneal_topology: capacity mode needs an explicit r");
+    cfg.validate();
+    const FlatRows f = flat_rows(sys);
+    std::vector<int32_t> e(2 * (size_t)std::max(*r, 1));
+    int32_t k = 0;
+    raise(tp_anneal_capacity(sys.n, (int32_t)sys.rows.size(), f.row_ptr.data(), f.cols.data(), f.caps.data(),
+                             f.allowed.data(), *r, cfg.t0, cfg.cooling, cfg.steps, cfg.moves_per_temp, cfg.seed,
+                             e.data(), &k));
+    Topology t;
+    t.n = sys.n;
+    int dmax = 0;
+    std::vector<int> deg(sys.n, 0);
+    for (int q = 0; q < k; ++q) {
+        t.edges.push_back({e[2 * q], e[2 * q + 1]});
+        dmax = std::max({dmax, ++deg[e[2 * q]], ++deg[e[2 * q + 1]]});
+    }
+    t.weights.assign(t.edges.size(), 1.0 / (dmax + 1));  // finish (proj/src/anneal.cpp:172-185)
+    return t;
+}
+
+// ------------------------------------------------------------------ capacity systems
+void ServerTree::validate() const {
+    // proj/src/bandwidth.cpp:148-170
+    if (n_devices < 2) throw std::invalid_argument("ServerTree: need at least 2 devices");
+    const int m = n_devices * (n_devices - 1) / 2;
+    if ((int)routes.size() != m) throw std::invalid_argument("ServerTree: expected one route per device pair");
+    for (const auto& link : links) {
+        if (link.name.empty()) throw std::invalid_argument("ServerTree: unnamed link");
+        if (!(link.bandwidth > 0.0))
+            throw std::invalid_argument("ServerTree: link " + link.name + " needs positive bandwidth");
+        if (link.capacity < 0) throw std::invalid_argument("ServerTree: link " + link.name + " has negative capacity");
+    }
+    for (int col = 0; col < m; ++col) {
+        if (routes[col].empty())
+            throw std::invalid_argument("ServerTree: pair column " + std::to_string(col) + " routes over no link");
+        for (int lix : routes[col])
+            if (lix < 0 || lix >= (int)links.size())
+                throw std::invalid_argument("ServerTree: route references unknown link");
+    }
+}
+
+ServerTree tiered8_tree(double leaf_bw, double group_bw, double root_bw) {
+    ServerTree tree;
+    tree.n_devices = 8;
+    for (int l = 0; l < 4; ++l) tree.links.push_back({"leaf" + std::to_string(l), leaf_bw, 1});
+    tree.links.push_back({"group0", group_bw, 4});
+    tree.links.push_back({"group1", group_bw, 4});
+    tree.links.push_back({"root", root_bw, 16});
+    for (int i = 0; i + 1 < 8; ++i)
+        for (int j = i + 1; j < 8; ++j)
+            tree.routes.push_back({i / 2 == j / 2 ? i / 2 : (i / 4 == j / 4 ? 4 + i / 4 : 6)});
+    tree.validate();
+    return tree;
+}
+
+CapacitySystem intra_server_constraints(const ServerTree& tree) {
+    tree.validate();
+    CapacitySystem sys;
+    sys.n = tree.n_devices;
+    sys.num_edges = sys.n * (sys.n - 1) / 2;
+    sys.equality = false;
+    sys.allowed.assign(sys.num_edges, 1);
+    sys.rows.resize(tree.links.size());
+    for (size_t l = 0; l < tree.links.size(); ++l) {
+        sys.rows[l].label = tree.links[l].name;
+        sys.rows[l].capacity = tree.links[l].capacity;
+    }
+    for (int col = 0; col < sys.num_edges; ++col)
+        for (int lix : tree.routes[col]) sys.rows[lix].edge_cols.push_back(col);
+    return sys;
+}
+
+int BCubeSpec::n_servers() const {
+    if (p < 2 || k < 1) throw std::invalid_argument("BCubeSpec: need p >= 2 and k >= 1");
+    long long n = 1;
+    for (int i = 0; i < k; ++i) {
+        n *= p;
+        if (n > 4096) throw std::invalid_argument("BCubeSpec: p^k exceeds 4096 servers");
+    }
+    return (int)n;
+}
+
+CapacitySystem bcube_constraints(const BCubeSpec& spec) {
+    const int n = spec.n_servers();
+    if (!spec.layer_bandwidths.empty() && (int)spec.layer_bandwidths.size() != spec.k)
+        throw std::invalid_argument("BCubeSpec: expected one bandwidth per layer");
+    CapacitySystem sys;
+    sys.n = n;
+    sys.num_edges = n * (n - 1) / 2;
+    sys.equality = false;
+    sys.allowed.assign(sys.num_edges, 0);
+    sys.rows.resize((size_t)spec.k * n);
+    for (int layer = 0; layer < spec.k; ++layer)
+        for (int u = 0; u < n; ++u) {
+            auto& row = sys.rows[(size_t)layer * n + u];
+            row.label = "layer" + std::to_string(layer) + "/server" + std::to_string(u);
+            row.capacity = spec.p - 1;
+        }
+    int col = 0;
+    for (int u = 0; u + 1 < n; ++u)
+        for (int v = u + 1; v < n; ++v, ++col) {
+            int diff_layer = -1, diffs = 0, du = u, dv = v;
+            for (int layer = 0; layer < spec.k; ++layer) {
+                if (du % spec.p != dv % spec.p) {
+                    ++diffs;
+                    diff_layer = layer;
+                }
+                du /= spec.p;
+                dv /= spec.p;
+            }
+            if (diffs != 1) continue;
+            sys.allowed[col] = 1;
+            sys.rows[(size_t)diff_layer * n + u].edge_cols.push_back(col);
+            sys.rows[(size_t)diff_layer * n + v].edge_cols.push_back(col);
+        }
+    return sys;
+}
+
+std::vector<UtilizationRow> utilization(const CapacitySystem& sys, const Topology& t) {
+    // proj/src/admm_het.cpp:371-392
+    t.validate();
+    if (t.n != sys.n) throw std::invalid_argument("utilization: node count mismatch");
+    std::vector<char> sel(sys.num_edges, 0);
+    for (const auto& [i, j] : t.edges) sel[edge_index(t.n, i, j)] = 1;
+    const auto used = sys.loads(sel);
+    std::vector<UtilizationRow> out;
+    for (size_t k = 0; k < sys.rows.size(); ++k) out.push_back({sys.rows[k].label, sys.rows[k].capacity, used[k]});
+    return out;
+}
+
+std::string utilization_csv(const std::vector<UtilizationRow>& rows) {
+    std::string out = "resource,capacity,used\n";
+    for (const auto& r : rows) out += r.label + "," + std::to_string(r.capacity) + "," + std::to_string(r.used) + "\n";
+    return out;
 }
 
 // ------------------------------------------------------------------ admm
@@ -677,9 +834,34 @@ Solution solve_het(const CapacitySystem& sys, std::optional<int> r, const Solver
                    const std::optional<Topology>& warm) {
     const auto t0 = std::chrono::steady_clock::now();
     cfg.validate();
+    if (!sys.equality) {
+        // capacity-bound rows (proj/src/admm_het.cpp:37-48: explicit edge total)
+        if (!r) throw std::invalid_argument("capacity-bound system needs an explicit edge total");
+        const FlatRows f = flat_rows(sys);
+        const tp_config c = to_c(cfg);
+        tp_result res{};
+        const int m = sys.n * (sys.n - 1) / 2;
+        std::vector<int32_t> edges(2 * std::max(m, 1));
+        std::vector<double> weights(std::max(m, 1)), trace(3 * (size_t)cfg.max_iter);
+        char note[512] = {0};
+        std::vector<int32_t> we;
+        if (warm) {
+            warm->validate();
+            if (warm->n != sys.n) throw std::invalid_argument("solve_het: warm start node count mismatch");
+            we = flat_edges(*warm);
+        }
+        raise(tp_solve_het_capacity(sys.n, (int32_t)sys.rows.size(), f.row_ptr.data(), f.cols.data(), f.caps.data(),
+                                    f.allowed.data(), *r, &c, warm ? we.data() : nullptr,
+                                    warm ? (int32_t)warm->edges.size() : -1, &res, edges.data(), weights.data(),
+                                    trace.data(), note, sizeof note));
+        Solution sol = collect(sys.n, res, edges, weights, trace, note);
+        sol.wall_time_ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        return sol;
+    }
     std::vector<int32_t> deg;
     if (!node_level_degrees(sys, deg))
-        throw std::invalid_argument("solve_het: only node-level equality systems are supported");
+        throw std::invalid_argument("assemble_het: equality system must be one row per node");
     long long total = 0;
     for (int d : deg) total += d;
     if (total % 2 == 0 && r && *r != total / 2)

@@ -389,6 +389,122 @@ def solve_het(degrees, cfg: SolverConfig | None = None, warm_start=None, r=None,
     return _solution(n, res, edges, weights, trace, note)
 
 
+# ---------------------------------------------------------------- capacity systems
+@dataclass
+class CapacitySystem:
+    """proj/include/topoopt/bandwidth.hpp:41-51 (rows over the n(n-1)/2 edge
+    columns; equality = False: capacities are upper bounds)."""
+    n: int
+    rows: list            # per row: list of edge columns
+    capacities: list      # per row
+    allowed: np.ndarray   # per edge column, 0/1
+    labels: list = None
+    equality: bool = False
+
+    def csr(self):
+        ptr = np.zeros(len(self.rows) + 1, np.int32)
+        for k, r in enumerate(self.rows):
+            ptr[k + 1] = ptr[k] + len(r)
+        cols = np.array([c for r in self.rows for c in r] or [0], np.int32)
+        caps = np.array(self.capacities or [0], np.int32)
+        return ptr, cols, caps, _i32(self.allowed)
+
+    def loads(self, selected) -> list:
+        sel = np.asarray(selected)
+        return [int(sum(1 for c in r if sel[c])) for r in self.rows]
+
+
+def tiered8_tree_system(leaf_bw: float = 4.88, group_bw: float = 4.88, root_bw: float = 9.76) -> CapacitySystem:
+    """intra_server_constraints(tiered8_tree(...)) (proj/src/bandwidth.cpp:172-219):
+    8 devices, 4 leaf links (cap 1), 2 group links (cap 4), a root (cap 16)."""
+    n = 8
+    names = [f"leaf{l}" for l in range(4)] + ["group0", "group1", "root"]
+    caps = [1, 1, 1, 1, 4, 4, 16]
+    rows = [[] for _ in names]
+    col = 0
+    for i in range(n - 1):
+        for j in range(i + 1, n):
+            if i // 2 == j // 2:
+                rows[i // 2].append(col)
+            elif i // 4 == j // 4:
+                rows[4 + i // 4].append(col)
+            else:
+                rows[6].append(col)
+            col += 1
+    return CapacitySystem(n, rows, caps, np.ones(col, np.int32), names)
+
+
+def bcube_constraints(p: int, k: int) -> CapacitySystem:
+    """bcube_constraints({p, k}) (proj/src/bandwidth.cpp:221-261): n = p^k
+    servers; a pair is allowed when its base-p digits differ in exactly one
+    layer, and uses one port (cap p-1) on each endpoint in that layer."""
+    if p < 2 or k < 1:
+        raise ValueError("BCubeSpec: need p >= 2 and k >= 1")
+    n = p ** k
+    if n > 4096:
+        raise ValueError("BCubeSpec: p^k exceeds 4096 servers")
+    rows = [[] for _ in range(k * n)]
+    labels = [f"layer{l}/server{u}" for l in range(k) for u in range(n)]
+    allowed = np.zeros(n * (n - 1) // 2, np.int32)
+    col = 0
+    for u in range(n - 1):
+        for v in range(u + 1, n):
+            diffs, layer, du, dv = 0, -1, u, v
+            for lyr in range(k):
+                if du % p != dv % p:
+                    diffs += 1
+                    layer = lyr
+                du //= p
+                dv //= p
+            if diffs == 1:
+                allowed[col] = 1
+                rows[layer * n + u].append(col)
+                rows[layer * n + v].append(col)
+            col += 1
+    return CapacitySystem(n, rows, [p - 1] * (k * n), allowed, labels)
+
+
+def project_binary_z_capped(v, r: int, sys: CapacitySystem) -> np.ndarray:
+    """proj/src/admm_het.cpp:125-154 on the GPU."""
+    v = _f64(v)
+    z = np.zeros_like(v)
+    ptr, cols, caps, al = sys.csr()
+    _check(_lib.load().tp_project_binary_z_capped(sys.n, len(sys.rows), _ip(ptr), _ip(cols), _ip(caps), _ip(al),
+                                                   _dp(v), r, _dp(z)))
+    return z
+
+
+def anneal_capacity_topology(sys: CapacitySystem, r: int, t0=1.0, cooling=0.995, steps=200, moves_per_temp=0,
+                             seed=0):
+    """anneal_topology on a capacity-bound system (proj/src/anneal.cpp:275-407)."""
+    ptr, cols, caps, al = sys.csr()
+    e = np.zeros((max(r, 1), 2), np.int32)
+    k = C.c_int32(0)
+    _check(_lib.load().tp_anneal_capacity(sys.n, len(sys.rows), _ip(ptr), _ip(cols), _ip(caps), _ip(al), r, t0,
+                                          cooling, steps, moves_per_temp, seed, _ip(e), C.byref(k)))
+    return e[: k.value].copy()
+
+
+def solve_het_capacity(sys: CapacitySystem, r: int, cfg: SolverConfig | None = None, warm_start=None,
+                       **kw) -> Solution:
+    """topoopt::solve_het on a capacity-bound system (proj/src/admm_het.cpp:231-369)."""
+    cfg = _config(cfg, kw)
+    c = cfg.to_c()
+    res = tp_result()
+    n = sys.n
+    m = n * (n - 1) // 2
+    edges = np.zeros((max(m, 1), 2), np.int32)
+    weights = np.zeros(max(m, 1))
+    trace = np.zeros((cfg.max_iter, 3))
+    note = C.create_string_buffer(512)
+    we, nw = _warm_arg(warm_start)
+    ptr, cols, caps, al = sys.csr()
+    _check(_lib.load().tp_solve_het_capacity(n, len(sys.rows), _ip(ptr), _ip(cols), _ip(caps), _ip(al), r,
+                                             C.byref(c), _ip(we) if we is not None else None, nw, C.byref(res),
+                                             _ip(edges), _dp(weights), _dp(trace), note, 512))
+    return _solution(n, res, edges, weights, trace, note)
+
+
 # ---------------------------------------------------------------- layout / substeps
 @dataclass
 class Layout:

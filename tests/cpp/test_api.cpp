@@ -128,6 +128,35 @@ int main() {
     Topology ex = generate_benchmark(BenchmarkKind::exponential, 256);
     CHECK(near(acf(gossip_matrix(ex)), 7.0 / 9.0, 1e-12));
 
+    // capacity-bound systems (proj/tests/test_admm_het.cpp:171-202)
+    CapacitySystem tree = intra_server_constraints(tiered8_tree(4.88, 4.88, 9.76));
+    CHECK(!tree.equality && tree.rows.size() == 7 && tree.rows[6].capacity == 16);
+    SolverConfig tight;
+    tight.rho = 10.0;
+    tight.epsilon = 1e-8;
+    tight.max_iter = 3000;
+    Solution ts = solve_het(tree, 12, tight);
+    CHECK(ts.connected && ts.topology.edges.size() <= 12);
+    const auto util = utilization(tree, ts.topology);
+    for (size_t k = 0; k < util.size(); ++k) CHECK(util[k].used <= util[k].capacity);
+    CHECK(utilization_csv(util).rfind("resource,capacity,used\n", 0) == 0);
+    CapacitySystem cube = bcube_constraints({2, 2, {}});
+    Topology cycle;
+    cycle.n = 4;
+    cycle.edges = {{0, 1}, {0, 2}, {1, 3}, {2, 3}};
+    cycle.weights.assign(4, 1.0 / 3.0);
+    Solution cs = solve_het(cube, 5, tight, cycle);
+    CHECK(cs.topology.edges.size() == 4);
+    CHECK(cs.note.find("capacity limits stopped selection at 4 of 5") != std::string::npos);
+    CHECK_THROWS_AS(solve_het(cube, std::nullopt, tight), std::invalid_argument);
+
+    // consensus evaluation (proj/src/consensus.cpp)
+    ConsensusTrace tr = simulate(gossip_matrix(ex), 8, 50, 3);
+    CHECK(tr.errors.size() == 51 && tr.errors[50] < tr.errors[0]);
+    CHECK(convergence_time(tr, tr.errors[10], 2.0) <= 20.0);
+    CompareReport rep = compare({{"exp", gossip_matrix(ex), 1.0}}, 4, 20, 1e-3, 0);
+    CHECK(rep.traces.size() == 1 && rep.to_csv().rfind("time_ms,label,error\n", 0) == 0);
+
     // errors
     CHECK_THROWS_AS(extract_topology(3, 2, Vec{0.0, 0.0, 0.0}, 1e-6), DegenerateSolutionError);
     CHECK_THROWS_AS(node_level_constraints(3, {1, 1, 1}), InfeasibleError);

@@ -160,3 +160,42 @@ def test_generate_benchmark_python_mirror(T, golden):
             e, w = T.generate_benchmark(c["kind"], c["n"])
             assert e.tolist() == c["edges"]
             assert np.array_equal(w, np.array(c["weights"]))
+
+
+def _capsys(c):
+    rows = [c["cols"][c["row_ptr"][k]:c["row_ptr"][k + 1]] for k in range(len(c["caps"]))]
+    return rows, c["caps"], c["allowed"]
+
+
+def test_capacity_system_builders(T, golden):
+    # intra_server_constraints(tiered8_tree) / bcube_constraints vs the reference
+    g = golden("capacity.json")["systems"]
+    built = {"tiered8": T.tiered8_tree_system(4.88, 4.88, 9.76), "bcube_4_2": T.bcube_constraints(4, 2),
+             "bcube_2_2": T.bcube_constraints(2, 2), "bcube_3_2": T.bcube_constraints(3, 2),
+             "bcube_3_1": T.bcube_constraints(3, 1)}
+    for name, sys_ in built.items():
+        ptr, cols, caps, al = sys_.csr()
+        c = g[name]
+        assert ptr.tolist() == c["row_ptr"] and cols[: len(c["cols"])].tolist() == c["cols"]
+        assert caps[: len(c["caps"])].tolist() == c["caps"] and al.tolist() == c["allowed"]
+
+
+def test_capped_projection_oracle(O, golden):
+    g = golden("capacity.json")
+    name = lambda s: "tiered8" if s[0] == "tiered8" else f"bcube_{s[1]}_{s[2]}"  # noqa: E731
+    for c in g["capped"]:
+        z = O.project_binary_z_capped(np.array(c["v"]), c["r"], *_capsys(g["systems"][name(c["spec"])]))
+        assert z.tolist() == c["z"]
+
+
+def test_capacity_solve_oracle(O, golden):
+    g = golden("capacity.json")
+    name = lambda s: "tiered8" if s[0] == "tiered8" else f"bcube_{s[1]}_{s[2]}"  # noqa: E731
+    for c in g["solves"][:3]:
+        rows, caps, al = _capsys(g["systems"][name(c["spec"])])
+        n = g["systems"][name(c["spec"])]["n"]
+        s = O.solve_het_capacity(n, rows, caps, al, c["r"], c["warm"], trace_acf=False, **c["cfg"])
+        ref = c["solution"]
+        assert s.iterations == ref["iterations"] and s.edges.tolist() == ref["edges"]
+        assert rel(s.weights, ref["weights"]) < 1e-6
+        assert s.acf == pytest.approx(ref["acf"], rel=1e-6) and s.note == ref["note"]
