@@ -44,6 +44,7 @@ struct GemmArgs {
 };
 
 void launch_sym_gemm(const GemmArgs& g, int nmat, cudaStream_t st);
+int sm_count();  // multiprocessors of the current device (cached)
 // CTAs of the stream-K decomposition for one (S, T) pair of order ld (0: not used)
 int stream_k_ctas(int ld);
 // tile/pipeline variants of the DMMA GEMM (for tuning; 0 = production)

@@ -28,22 +28,42 @@ namespace tpb {
 
 namespace {
 
-constexpr int KS = kOzSlices, BM = kOzBM, BN = kOzBN, BK = kOzBK;
-constexpr int STAGES = 192 * 1024 / (KS * (BM + BN) * BK);  // 2 at BK = 64, 4 at BK = 32
-static_assert(BK == 32 || BK == 64, "k block is one or two MMA k-steps");
-constexpr int A_PLANE = BM * BK, B_PLANE = BN * BK;              // bytes
-constexpr int STAGE_BYTES = KS * (A_PLANE + B_PLANE);            // 96 KB
-constexpr int CP = BM + 1;       // epilogue FP64 staging pitch (doubles)
-constexpr int CS_BYTES = (BN * CP * 8 + 1023) / 1024 * 1024;
-constexpr int BOX_BYTES = 64 * 64;                 // one 64 x 64-byte TMA store box (SWIZZLE_64B)
-constexpr int DIG_BYTES = 2 * KS * 2 * BOX_BYTES;  // direct + mirror, KS planes, 2 halves
-constexpr int EPI_BYTES = CS_BYTES + DIG_BYTES;
-constexpr int SMEM_BYTES = (STAGES * STAGE_BYTES > EPI_BYTES ? STAGES * STAGE_BYTES : EPI_BYTES) + 1024;
+constexpr int KS = kOzSlices, BM = kOzBM;
 constexpr int EPI_WARPS = 8, EPI_THREADS = 32 * EPI_WARPS;
 constexpr int THREADS = 64 + EPI_THREADS;  // producer warp, MMA warp, epilogue warps
-constexpr int HN = BN / 2;                  // tile columns per epilogue thread
-static_assert(KS * BN <= 512, "accumulator groups exceed TMEM");
-static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
+
+// Tile configuration: BN output columns (one accumulator group = BN TMEM
+// columns, KS groups), BK k-bytes per pipeline stage. <64, 64>: one CTA per
+// SM, 512 TMEM columns; <32, 32>: 256 TMEM columns and 98 KB of shared
+// memory, so two CTAs share an SM and one's epilogue overlaps the other's
+// main loop (batched small-n products, where the epilogue dominates).
+template <int BN_, int BK_>
+struct Tile {
+    static constexpr int BN = BN_, BK = BK_;
+    static constexpr int R = BM / BN;          // tiles per 128-row diagonal block
+    static constexpr int STAGES = 2;
+    static constexpr int A_PLANE = BM * BK, B_PLANE = BN * BK;  // bytes
+    static constexpr int STAGE_BYTES = KS * (A_PLANE + B_PLANE);
+    static constexpr int CP = BM + 1;          // epilogue FP64 staging pitch (doubles)
+    static constexpr int CS_BYTES = (BN * CP * 8 + 1023) / 1024 * 1024;
+    static constexpr int BB = BN;              // TMA store box: BB rows x BB bytes
+    static constexpr int BOX_BYTES = BB * BB;
+    static constexpr int NBOX = BM / BB;       // boxes per plane and orientation
+    static constexpr int DIG_BYTES = 2 * KS * NBOX * BOX_BYTES;
+    static constexpr int EPI_BYTES = CS_BYTES + DIG_BYTES;
+    static constexpr int SMEM_BYTES =
+        (STAGES * STAGE_BYTES > EPI_BYTES ? STAGES * STAGE_BYTES : EPI_BYTES) + 1024;
+    static constexpr int HN = BN / 2;          // tile columns per epilogue thread
+    static constexpr int TMEM_COLS = KS * BN <= 256 ? 256 : 512;
+    static constexpr int TCHUNK = 256 / BN;    // B planes per MMA (N <= 256)
+    static constexpr int MIN_BLOCKS = 2 * (SMEM_BYTES + 1024) <= 228 * 1024 ? 2 : 1;
+    static_assert(KS * BN <= 512, "accumulator groups exceed TMEM");
+    static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
+    static_assert(BK == 32 || BK == 64, "k block is one or two MMA k-steps");
+    static_assert(HN % 16 == 0, "TMEM loads of 16 columns");
+};
+using TileL = Tile<64, 64>;
+using TileS = Tile<32, 32>;
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -111,6 +131,7 @@ __device__ __forceinline__ void tmem_wait_ld() {
 // K-major operand tile, BK-byte rows in the matching swizzle (8-row atoms of
 // 8 BK bytes): start address, SBO = 8 BK, version 1, layout type 4 (64B) /
 // 6 (32B).
+template <int BK>
 __device__ __forceinline__ uint64_t op_desc(uint32_t addr) {
     return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)((8 * BK) >> 4) << 32) |
            ((uint64_t)1 << 46) | ((uint64_t)(BK == 64 ? 4 : 6) << 61);
@@ -191,9 +212,11 @@ __device__ __forceinline__ void digits4(const double (&v)[4], double s28, uint32
     w[7] = __byte_perm(g, h, 0x5410);
 }
 
-// 16-byte chunk address inside a 64 x 64-byte SWIZZLE_64B box
-__device__ __forceinline__ uint32_t sw64_off(int row, int chunk) {
-    return (uint32_t)(row * 64 + ((chunk ^ ((row >> 1) & 3)) << 4));
+// 16-byte chunk address inside a BB x BB-byte box in the SWIZZLE_{BB}B layout
+template <int BB>
+__device__ __forceinline__ uint32_t box_off(int row, int chunk) {
+    const int x = BB == 64 ? ((row >> 1) & 3) : ((row >> 2) & 1);
+    return (uint32_t)(row * BB + ((chunk ^ x) << 4));
 }
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
@@ -203,28 +226,30 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t sr
 }
 
 // lower tiles of a (ld/BM) x (ld/BN) grid: row block I holds col blocks
-// J < ceil((I+1) BM / BN)
-__host__ __device__ inline int tiles_before(int I) {
-    constexpr int R = BM / BN;  // 2
-    return R * I * (I + 1) / 2;
-}
-__device__ inline void oz_tile(int t, int& I, int& J) {
+// J < (I+1) R, R = BM / BN
+__host__ __device__ inline int tiles_before(int R, int I) { return R * I * (I + 1) / 2; }
+__device__ inline void oz_tile(int R, int t, int& I, int& J) {
     int b = 0;
-    while (tiles_before(b + 1) <= t) ++b;
+    while (tiles_before(R, b + 1) <= t) ++b;
     I = b;
-    J = t - tiles_before(b);
+    J = t - tiles_before(R, b);
 }
 
 }  // namespace
 
-__global__ void __launch_bounds__(THREADS, 1)
+template <typename TL>
+__global__ void __launch_bounds__(THREADS, TL::MIN_BLOCKS)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                    const __grid_constant__ CUtensorMap mapC, OzGemm g) {
+    constexpr int BN = TL::BN, BK = TL::BK, STAGES = TL::STAGES, R = TL::R, HN = TL::HN, CP = TL::CP;
+    constexpr int BB = TL::BB, NBOX = TL::NBOX;
+    constexpr int A_PLANE = TL::A_PLANE, B_PLANE = TL::B_PLANE, STAGE_BYTES = TL::STAGE_BYTES;
+    constexpr int TMEM_COLS = TL::TMEM_COLS;
     const int mat = blockIdx.y;
     if (g.ictl && g.ictl[(mat >> 1) * 8 + 1]) return;
     const long long t_start = g.dbg_t ? gtimer() : 0;
     int I, J;
-    oz_tile(blockIdx.x, I, J);
+    oz_tile(R, blockIdx.x, I, J);
     const int i0 = I * BM, j0 = J * BN;
     const int ld = g.ld;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -250,8 +275,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                         su32(&tmem_slot))
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_slot)),
+                     "n"(TMEM_COLS)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -303,15 +328,15 @@ __global__ void __launch_bounds__(THREADS, 1)
                 for (int kk = 0; kk < BK / 32; ++kk) {
                     // A_s . [B_t0 | ... | B_t1] in one MMA: the B planes are
                     // contiguous rows in smem and the groups d = s + t are
-                    // contiguous 64-column blocks in TMEM.
+                    // contiguous BN-column blocks in TMEM.
 #pragma unroll
                     for (int s = 1; s <= KS; ++s) {
-                        const uint64_t ad = op_desc(a_tile(st, s - 1) + kk * 32);
+                        const uint64_t ad = op_desc<BK>(a_tile(st, s - 1) + kk * 32);
 #pragma unroll
-                        for (int t0 = 1; t0 <= KS + 1 - s; t0 += 4) {
-                            const int t1 = t0 + 3 < KS + 1 - s ? t0 + 3 : KS + 1 - s;
+                        for (int t0 = 1; t0 <= KS + 1 - s; t0 += TL::TCHUNK) {
+                            const int t1 = t0 + TL::TCHUNK - 1 < KS + 1 - s ? t0 + TL::TCHUNK - 1 : KS + 1 - s;
                             const int nn = BN * (t1 - t0 + 1);
-                            const uint64_t bd = op_desc(b_tile(st, t0 - 1) + kk * 32);
+                            const uint64_t bd = op_desc<BK>(b_tile(st, t0 - 1) + kk * 32);
                             const uint32_t acc = (kb | kk) != 0 || s != 1;
                             mma_i8(tmem + (uint32_t)((s + t0 - 2) * BN), ad, bd, idesc_n(nn), acc);
                         }
@@ -368,18 +393,14 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (i == j0 + c0 + j) v += g.dshift;
             acc[j] = v;
         }
-        // Stores. Every element (a, b) of C is written by exactly one tile:
-        // the lower tile holding (max, min) writes (a >= b) directly and
-        // (a > b) mirrored, so runs are deterministic.
         // Stores. Ownership keeps C exactly symmetric and every element
-        // written once (deterministic): off-diagonal tiles (J < 2I) write
-        // themselves and their mirror; in the diagonal 128-row block, tile
-        // J = 2I owns rows 0..127 (its upper 64 x 64 sub-block symmetrised)
-        // plus the mirror of rows 64..127, tile J = 2I+1 only rows 64..127
-        // (lower-right sub-block symmetrised).
-        const int kind = J < 2 * I ? 0 : (J == 2 * I ? 1 : 2);
-        const int dr0 = kind == 2 ? 64 : 0;         // first directly owned tile row
-        const int mr0 = kind == 0 ? 0 : (kind == 1 ? 64 : BM);  // first mirrored tile row
+        // written once (deterministic): off-diagonal tiles (J < R I) write
+        // themselves and their mirror; in the diagonal 128-row block the tile
+        // t = J - R I owns rows BN t.. (its BN x BN diagonal sub-block
+        // symmetrised) and mirrors rows BN (t+1).. into the tiles to its right.
+        const int tdiag = J - R * I;
+        const int dr0 = tdiag < 0 ? 0 : BN * tdiag;          // first directly owned tile row
+        const int mr0 = tdiag < 0 ? 0 : BN * (tdiag + 1);    // first mirrored tile row
         const int nv = g.nvalid;
         double* C = g.C ? g.C + (long long)(mat >> 1) * g.c_stride_b + (long long)(mat & 1) * g.c_stride_w
                         : nullptr;
@@ -390,10 +411,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int et = threadIdx.x - 64;        // 0 .. EPI_THREADS-1
         const int ew = et >> 5;                 // epilogue warp 0..7
         const long long t_stage = g.dbg_t ? gtimer() : 0;
-        if (kind != 0) {
-            // symmetrise the diagonal 64 x 64 sub-block (tile rows dr0.., all columns)
-            for (int idx = et; idx < 64 * 64; idx += EPI_THREADS) {
-                const int u = idx >> 6, v = idx & 63;  // sub-block row, column
+        if (tdiag >= 0) {
+            // symmetrise the diagonal BN x BN sub-block (tile rows dr0.., all columns)
+            for (int idx = et; idx < BN * BN; idx += EPI_THREADS) {
+                const int u = idx / BN, v = idx % BN;  // sub-block row, column
                 if (u < v) Cs[v * CP + dr0 + u] = Cs[u * CP + dr0 + v];
             }
             asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");
@@ -418,13 +439,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         const long long t_cst = g.dbg_t ? gtimer() : 0;
         if (g.Cd) {
             // digit planes staged in the TMA-store layout: direct boxes
-            // [s][h] (tile rows 64h.., 64 columns) and mirror boxes [s][h]
-            // (64 tile columns as rows, tile rows 64h.. as columns)
-            uint8_t* dig = sgen + CS_BYTES;
+            // [s][h] (tile rows BB h.., the BN columns) and mirror boxes [s][h]
+            // (the BN tile columns as rows, tile rows BB h.. as bytes)
+            uint8_t* dig = sgen + TL::CS_BYTES;
             const uint32_t dig_s = su32(dig);
             const double s28 = ldexp(1.0, 28 - g.eC);
-            for (int it = et; it < 2 * BM * (BN / 16) / 2; it += EPI_THREADS) {  // 512 direct items
-                const int rr = it & (BM - 1), cc = it >> 7;           // tile row, 16-column chunk
+            for (int it = et; it < BM * (BN / 16); it += EPI_THREADS) {  // direct items
+                const int rr = it % BM, cc = it / BM;               // tile row, 16-column chunk
                 if (rr < dr0) continue;
                 uint32_t w[4][KS];
 #pragma unroll
@@ -434,16 +455,16 @@ __global__ void __launch_bounds__(THREADS, 1)
                     for (int k = 0; k < 4; ++k) v4[k] = Cs[(16 * cc + 4 * q4 + k) * CP + rr];
                     digits4(v4, s28, w[q4]);
                 }
-                const int h2 = rr >> 6, rb = rr & 63;
+                const int h2 = rr / BB, rb = rr % BB;
 #pragma unroll
                 for (int s2 = 0; s2 < KS; ++s2) {
-                    uint8_t* box = dig + (s2 * 2 + h2) * BOX_BYTES;
-                    *reinterpret_cast<uint4*>(box + sw64_off(rb, cc)) =
+                    uint8_t* box = dig + (s2 * NBOX + h2) * TL::BOX_BYTES;
+                    *reinterpret_cast<uint4*>(box + box_off<BB>(rb, cc)) =
                         make_uint4(w[0][s2], w[1][s2], w[2][s2], w[3][s2]);
                 }
             }
-            for (int it = et; it < BN * (BM / 16); it += EPI_THREADS) {  // 512 mirror items
-                const int j = it & (BN - 1), rc = it >> 6;              // tile column, 16-row chunk
+            for (int it = et; it < BN * (BM / 16); it += EPI_THREADS) {  // mirror items
+                const int j = it % BN, rc = it / BN;                  // tile column, 16-row chunk
                 if (16 * rc < mr0) continue;
                 uint32_t w[4][KS];
 #pragma unroll
@@ -453,11 +474,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                     for (int k = 0; k < 4; ++k) v4[k] = Cs[j * CP + 16 * rc + 4 * q4 + k];
                     digits4(v4, s28, w[q4]);
                 }
-                const int h2 = rc >> 2, cb = rc & 3;
+                const int h2 = (16 * rc) / BB, cb = ((16 * rc) % BB) / 16;
 #pragma unroll
                 for (int s2 = 0; s2 < KS; ++s2) {
-                    uint8_t* box = dig + (2 * KS + s2 * 2 + h2) * BOX_BYTES;
-                    *reinterpret_cast<uint4*>(box + sw64_off(j, cb)) =
+                    uint8_t* box = dig + (KS * NBOX + s2 * NBOX + h2) * TL::BOX_BYTES;
+                    *reinterpret_cast<uint4*>(box + box_off<BB>(j, cb)) =
                         make_uint4(w[0][s2], w[1][s2], w[2][s2], w[3][s2]);
                 }
             }
@@ -466,11 +487,11 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (et == 0) {
                 const int base_row = mat * KS * ld;
                 for (int s2 = 0; s2 < KS; ++s2) {
-                    for (int h2 = dr0 >> 6; h2 < 2; ++h2)
-                        tma_store_2d(&mapC, dig_s + (s2 * 2 + h2) * BOX_BYTES, j0,
-                                     base_row + s2 * ld + i0 + 64 * h2);
-                    for (int h2 = mr0 >> 6; h2 < 2; ++h2)
-                        tma_store_2d(&mapC, dig_s + (2 * KS + s2 * 2 + h2) * BOX_BYTES, i0 + 64 * h2,
+                    for (int h2 = dr0 / BB; h2 < NBOX; ++h2)
+                        tma_store_2d(&mapC, dig_s + (s2 * NBOX + h2) * TL::BOX_BYTES, j0,
+                                     base_row + s2 * ld + i0 + BB * h2);
+                    for (int h2 = mr0 / BB; h2 < NBOX; ++h2)
+                        tma_store_2d(&mapC, dig_s + (KS * NBOX + s2 * NBOX + h2) * TL::BOX_BYTES, i0 + BB * h2,
                                      base_row + s2 * ld + j0);
                 }
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -492,7 +513,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS)
+                     : "memory");
     }
 }
 
@@ -561,12 +583,29 @@ void encode(CUtensorMap* m, const int8_t* base, int ld, long long rows, int box_
 void make_oz_maps(const int8_t* planes, int ld, int nmat, OzMaps* out) {
     if (ld % BM != 0) throw Error(kInvalidArgument, "ozaki GEMM needs ld % 128 == 0");
     const long long rows = (long long)nmat * KS * ld;
-    encode(&out->a, planes, ld, rows, BK, BM);
-    encode(&out->b, planes, ld, rows, BK, BN);
-    encode(&out->st, planes, ld, rows, 64, 64);
+    encode(&out->a, planes, ld, rows, TileL::BK, BM);
+    encode(&out->b, planes, ld, rows, TileL::BK, TileL::BN);
+    encode(&out->st, planes, ld, rows, TileL::BB, TileL::BB);
+    encode(&out->a2, planes, ld, rows, TileS::BK, BM);
+    encode(&out->b2, planes, ld, rows, TileS::BK, TileS::BN);
+    encode(&out->st2, planes, ld, rows, TileS::BB, TileS::BB);
 }
 
-int oz_gemm_tiles(int ld) { return tiles_before(ld / BM); }
+int oz_gemm_tiles(int ld) { return tiles_before(TileL::R, ld / BM); }
+
+namespace {
+// 128 x 32 tiles (two CTAs per SM) only on request (TPB_OZ_TILE=32): measured
+// slower than 128 x 64 tiles even on multi-wave batched grids (n=256 x 384
+// matrices: 24.5 vs 22.1 ms per projection) — the narrower MMAs' extra
+// shared-memory traffic outweighs the epilogue overlap.
+bool use_small_tiles(int, int) {
+    static const bool on = [] {
+        const char* e = std::getenv("TPB_OZ_TILE");
+        return e && std::atoi(e) == 32;
+    }();
+    return on;
+}
+}  // namespace
 
 bool cone_uses_ozaki() {
     const char* c = std::getenv("TPB_CONE");
@@ -574,23 +613,30 @@ bool cone_uses_ozaki() {
 }
 
 void init_attrs_ozaki() {
-    TPB_CUDA(cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    TPB_CUDA(cudaFuncSetAttribute(oz_gemm_kernel<TileL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  TileL::SMEM_BYTES));
+    TPB_CUDA(cudaFuncSetAttribute(oz_gemm_kernel<TileS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  TileS::SMEM_BYTES));
 }
 
 void launch_oz_gemm(const OzGemm& g, cudaStream_t st) {
-    const dim3 grid(oz_gemm_tiles(g.ld), g.nmat);
     if (g.Cd && !g.mc) throw Error(kInvalidArgument, "ozaki GEMM: digit output needs its TMA map");
+    const bool small = use_small_tiles(g.ld, g.nmat);
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = grid;
+    cfg.gridDim = dim3(small ? tiles_before(TileS::R, g.ld / BM) : oz_gemm_tiles(g.ld), g.nmat);
     cfg.blockDim = dim3(THREADS);
-    cfg.dynamicSmemBytes = SMEM_BYTES;
+    cfg.dynamicSmemBytes = small ? TileS::SMEM_BYTES : TileL::SMEM_BYTES;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = g.no_pdl ? 0 : 1;
-    TPB_CUDA(cudaLaunchKernelEx(&cfg, oz_gemm_kernel, g.ma->a, g.mb->b, g.mc ? g.mc->st : g.mb->st, g));
+    const OzMaps* mc = g.mc ? g.mc : g.mb;
+    if (small)
+        TPB_CUDA(cudaLaunchKernelEx(&cfg, oz_gemm_kernel<TileS>, g.ma->a2, g.mb->b2, mc->st2, g));
+    else
+        TPB_CUDA(cudaLaunchKernelEx(&cfg, oz_gemm_kernel<TileL>, g.ma->a, g.mb->b, mc->st, g));
 }
 
 void launch_oz_split(const double* A, long long mstride, int ld, int nmat, const double* scale, int e,

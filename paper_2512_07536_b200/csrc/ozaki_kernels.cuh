@@ -22,8 +22,8 @@ namespace tpb {
 
 constexpr int kOzSlices = 8;   // digits per operand (56 bits)
 constexpr int kOzBM = 128;     // tile rows (UMMA M)
-constexpr int kOzBN = 64;      // tile cols (UMMA N); KS accumulators x BN <= 512 TMEM columns
-constexpr int kOzBK = 64;      // k bytes per pipeline stage (SWIZZLE_64B rows; 32 with SWIZZLE_32B measured slower)
+constexpr int kOzBN = 64;      // tile cols of the one-CTA-per-SM variant (a 128 x 32 variant runs
+                               // two CTAs per SM for multi-wave grids; ozaki_kernels.cu)
 
 // Digit planes of nmat symmetric ld x ld matrices: [mat][slice][ld][ld] int8.
 struct OzPlanes {
@@ -31,11 +31,11 @@ struct OzPlanes {
     int e = 0;  // matrix = 2^e sum_s 2^{-7s} plane_s
 };
 
-// TMA maps of one plane buffer: loads in the A role (box kOzBK x kOzBM rows)
-// and the B role (box kOzBK x kOzBN rows); epilogue stores (64 x 64-byte
-// boxes, SWIZZLE_64B).
+// TMA maps of one plane buffer for both tile variants: loads in the A role
+// (k block x 128 rows) and the B role (k block x BN rows), epilogue stores.
 struct OzMaps {
-    CUtensorMap a, b, st;
+    CUtensorMap a, b, st;     // 128 x 64 tiles (64-byte k blocks, 64 x 64 store boxes)
+    CUtensorMap a2, b2, st2;  // 128 x 32 tiles (32-byte k blocks, 32 x 32 store boxes)
 };
 void make_oz_maps(const int8_t* planes, int ld, int nmat, OzMaps* out);
 

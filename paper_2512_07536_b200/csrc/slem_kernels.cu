@@ -574,6 +574,36 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
     __shared__ double s_th[2];
 
     build_csr(n, ne, list, g, ei, ej, ew, rowptr, colptr, cur, cidx, iscr);
+    // dense supports (het trace: every positive g): node-major incidence
+    // (column part then row part, i.e. ascending edge order) for a warp-per-
+    // node SpMV with coalesced loads
+    const bool dense = a.nbr && 2 * ne >= 32 * n;
+    int* nptr = cur;  // n+1 ints: reuses the counting-sort cursor
+    int* nbr = a.nbr ? a.nbr + (long long)b * 2 * a.list_cap : nullptr;
+    double* nwt = a.nwt ? a.nwt + (long long)b * 2 * a.list_cap : nullptr;
+    if (dense) {
+        __syncthreads();
+        if (tid == 0) nptr[0] = 0;
+        for (int v = tid; v < n; v += nthr)
+            nptr[v + 1] = (colptr[v + 1] - colptr[v]) + (rowptr[v + 1] - rowptr[v]);
+        __syncthreads();
+        if (tid == 0)
+            for (int v = 0; v < n; ++v) nptr[v + 1] += nptr[v];
+        __syncthreads();
+        for (int v = tid; v < n; v += nthr) {
+            int o = nptr[v];
+            for (int p = colptr[v]; p < colptr[v + 1]; ++p, ++o) {
+                const int e = cidx[p];
+                nbr[o] = ei[e];
+                nwt[o] = ew[e];
+            }
+            for (int e = rowptr[v]; e < rowptr[v + 1]; ++e, ++o) {
+                nbr[o] = ej[e];
+                nwt[o] = ew[e];
+            }
+        }
+        __syncthreads();
+    }
 
     const bool warm = a.ritz && a.ritz_ok && a.ritz_ok[b];
     double* rz = a.ritz ? a.ritz + (long long)b * 2 * n : nullptr;
@@ -593,18 +623,37 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
         for (int k = 0; k < kcap; ++k) {
             // w = L q - beta_{k-1} q_{k-1} (gather, ascending edge order); alpha = q.w
             double pa = 0.0;
-            for (int v = tid; v < n; v += nthr) {
-                const double qv = q[v];
-                Q[(long long)k * n + v] = qv;
-                double acc = 0.0;
-                for (int p = colptr[v]; p < colptr[v + 1]; ++p) {
-                    const int e = __ldg(cidx + p);
-                    acc += __ldg(ew + e) * (qv - q[__ldg(ei + e)]);
+            if (dense) {
+                // warp per node over the node-major incidence (coalesced), fixed
+                // lane/tree order: deterministic
+                const int lane = tid & 31, nw = nthr >> 5;
+                for (int v = wid; v < n; v += nw) {
+                    const double qv = q[v];
+                    double acc = 0.0;
+                    for (int p = nptr[v] + lane; p < nptr[v + 1]; p += 32) acc += nwt[p] * (qv - q[nbr[p]]);
+                    acc = warp_sum(acc);
+                    if (lane == 0) {
+                        Q[(long long)k * n + v] = qv;
+                        acc -= beta_prev * qp[v];
+                        w[v] = acc;
+                        pa += qv * acc;
+                    }
                 }
-                for (int e = rowptr[v]; e < rowptr[v + 1]; ++e) acc += __ldg(ew + e) * (qv - q[__ldg(ej + e)]);
-                acc -= beta_prev * qp[v];
-                w[v] = acc;
-                pa += qv * acc;
+            } else {
+                for (int v = tid; v < n; v += nthr) {
+                    const double qv = q[v];
+                    Q[(long long)k * n + v] = qv;
+                    double acc = 0.0;
+                    for (int p = colptr[v]; p < colptr[v + 1]; ++p) {
+                        const int e = __ldg(cidx + p);
+                        acc += __ldg(ew + e) * (qv - q[__ldg(ei + e)]);
+                    }
+                    for (int e = rowptr[v]; e < rowptr[v + 1]; ++e)
+                        acc += __ldg(ew + e) * (qv - q[__ldg(ej + e)]);
+                    acc -= beta_prev * qp[v];
+                    w[v] = acc;
+                    pa += qv * acc;
+                }
             }
             const double alpha = block_sum(pa, scratch);
             double s = 0.0, s2 = 0.0;
@@ -708,7 +757,7 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
 
 size_t slem_trace_smem_bytes(int n, int kmax) {
     const int kcap = std::max(2, std::min(kmax, n - 1));
-    return (3 * (size_t)n + 6 * (size_t)kcap) * sizeof(double) + (3 * (size_t)n + 2) * sizeof(int);
+    return (3 * (size_t)n + 6 * (size_t)kcap) * sizeof(double) + (3 * (size_t)n + 3) * sizeof(int);
 }
 
 void launch_slem(const SlemArgs& a, int B, cudaStream_t st) {

@@ -36,6 +36,8 @@ struct SlemArgs {
     int max_iter;
     int* stats;            // instrumentation: {calls, matvecs} accumulated, or null
     int plain;             // trace mode: plain Lanczos (no reorthogonalisation), basis write-only
+    int* nbr;              // plain mode, dense supports: node-major incidence scratch (2 list_cap per solve)
+    double* nwt;
 };
 
 // n <= kSmallDense: dense Householder tridiagonalisation in shared memory

@@ -268,6 +268,11 @@ void Solver::alloc() {
         cap_load_ = dalloc<int>(s0_, allocs_, (size_t)B * std::max(capsys_.nrows, 1));
         TPB_CUDA(cudaStreamSynchronize(s0_));
     }
+    if (het_ && n > kSmallDense) {
+        // node-major incidence of dense het supports for the trace SLEM
+        slem_nbr_ = dalloc<int>(s0_, allocs_, (size_t)B * 2 * list_cap_);
+        slem_nwt_ = dalloc<double>(s0_, allocs_, (size_t)B * 2 * list_cap_);
+    }
     list_ = dalloc<int>(s0_, allocs_,(size_t)B * list_cap_);
     list_count_ = dalloc<int>(s0_, allocs_,B);
     e_i_ = dalloc<int>(s0_, allocs_,(size_t)B * list_cap_);
@@ -442,6 +447,8 @@ void Solver::enqueue_slem_trace(cudaStream_t st) {
     a.max_iter = cfg_.max_iter;
     a.stats = slem_stats_;
     a.plain = lo_.n > kSmallDense && !std::getenv("TPB_SLEM_CGS2");
+    a.nbr = slem_nbr_;
+    a.nwt = slem_nwt_;
     launch_slem(a, B_, st);
 }
 

@@ -144,6 +144,8 @@ class Solver {
     double* ritz_ = nullptr;         // B x 2n extreme Ritz vectors (warm start)
     int* ritz_ok_ = nullptr;
     int* slem_stats_ = nullptr;      // TPB_SLEM_STATS: {trace SLEM calls, matvecs}
+    int* slem_nbr_ = nullptr;        // het trace SLEM: node-major incidence scratch
+    double* slem_nwt_ = nullptr;
     double* basis_final_ = nullptr;  // final report
     double* slem_out_ = nullptr;     // B x 8
     double* tmp_m_ = nullptr;        // B x m
