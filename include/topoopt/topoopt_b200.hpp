@@ -98,6 +98,14 @@ SpectralReport spectral_report(const Matrix& w);  // GPU Lanczos
 double acf(const Matrix& w);
 void validate_gossip(const Matrix& w);
 
+// On-disk formats (proj/include/topoopt/topology.hpp:78-85): JSON in
+// nlohmann's dump(2) layout, CSV with %.17g.
+std::string g17(double value);
+std::string topology_to_json(const Topology& t);
+Topology topology_from_json(const std::string& text);
+std::string matrix_to_csv(const Matrix& m);
+std::string matrix_to_triplet_csv(const Matrix& m, double drop_below = 0.0);
+
 enum class BenchmarkKind { ring, grid2d, torus2d, exponential };
 BenchmarkKind benchmark_kind_from_string(const std::string& name);
 Topology generate_benchmark(BenchmarkKind kind, int n);

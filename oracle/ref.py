@@ -63,6 +63,9 @@ def lib():
         L.ref_solution_note.restype = I
         L.ref_allocate.argtypes = [dp, ip, I, I, dp, ip]
         L.ref_capacity_system_sizes.argtypes = [I, D, D, D, I, ip]
+        L.ref_topology_to_json.argtypes = [I, ip, dp, I, C.c_char_p, I]
+        L.ref_matrix_to_csv.argtypes = [I, dp, C.c_char_p, I]
+        L.ref_solution_trace_csv.argtypes = [P, C.c_char_p, I]
         L.ref_capacity_system.argtypes = [I, D, D, D, I, ip, ip, ip, ip]
         L.ref_project_binary_z_capped.argtypes = [I, D, D, D, I, dp, I, dp]
         L.ref_anneal_capacity.argtypes = [I, D, D, D, I, I, I, I, U64, ip, ip]
@@ -128,6 +131,7 @@ class RefSolution:
     iterations: int
     trace: np.ndarray = field(repr=False)
     note: str = ""
+    trace_csv: str = field(default="", repr=False)
 
 
 def _collect(h, n) -> RefSolution:
@@ -144,9 +148,12 @@ def _collect(h, n) -> RefSolution:
     L.ref_solution_trace(h, _dp(tr))
     buf = C.create_string_buffer(4096)
     L.ref_solution_note(h, buf, 4096)
+    k = L.ref_solution_trace_csv(h, None, 0)
+    tbuf = C.create_string_buffer(k + 1)
+    L.ref_solution_trace_csv(h, tbuf, k + 1)
     L.ref_solution_free(h)
     return RefSolution(edges, weights, w, s[0], s[1], s[2], s[3], bool(s[4]), bool(s[5]),
-                       bool(s[6]), int(s[7]), tr, buf.value.decode())
+                       bool(s[6]), int(s[7]), tr, buf.value.decode(), tbuf.value.decode())
 
 
 def solve(n: int, r: int, warm_edges=None, **cfg) -> RefSolution:
@@ -274,6 +281,27 @@ def simulate(w, dim: int, iters: int, seed: int):
     out = np.zeros(iters + 1)
     _check(lib().ref_simulate(w.shape[0], _dp(w), dim, iters, seed, _dp(out)))
     return out
+
+
+def topology_to_json(n, edges, weights) -> str:
+    """proj/src/topology.cpp:283-290 (nlohmann dump(2))."""
+    e = np.ascontiguousarray(np.asarray(edges, np.int32).reshape(-1, 2))
+    w = np.ascontiguousarray(np.asarray(weights, np.float64))
+    k = lib().ref_topology_to_json(n, _ip(e), _dp(w), len(e), None, 0)
+    if k < 0:
+        _check(7)
+    buf = C.create_string_buffer(k + 1)
+    lib().ref_topology_to_json(n, _ip(e), _dp(w), len(e), buf, k + 1)
+    return buf.value.decode()
+
+
+def matrix_to_csv(w) -> str:
+    """proj/src/topology.cpp:312-324."""
+    w = np.ascontiguousarray(np.asarray(w, np.float64))
+    k = lib().ref_matrix_to_csv(w.shape[0], _dp(w), None, 0)
+    buf = C.create_string_buffer(k + 1)
+    lib().ref_matrix_to_csv(w.shape[0], _dp(w), buf, k + 1)
+    return buf.value.decode()
 
 
 def spectral_report(w):

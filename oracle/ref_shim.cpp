@@ -228,6 +228,34 @@ void* ref_solve_het_capacity(int kind, double a, double b, double c, int drop_la
     return out;
 }
 
+// ---------------------------------------------------------------- text formats
+// (proj/src/topology.cpp:283-324, admm.cpp:223-236): the string is copied into
+// buf (cap bytes); returns its full length
+static int copy_out(const std::string& text, char* buf, int cap) {
+    const int k = std::min<int>(cap - 1, static_cast<int>(text.size()));
+    if (cap > 0) {
+        std::memcpy(buf, text.data(), k);
+        buf[k] = 0;
+    }
+    return static_cast<int>(text.size());
+}
+
+int ref_topology_to_json(int n, const int* edges, const double* weights, int ne, char* buf, int cap) {
+    int len = 0;
+    const int st = guarded([&] { len = copy_out(topology_to_json(make_topo(n, edges, weights, ne)), buf, cap); });
+    return st != 0 ? -1 : len;
+}
+
+int ref_matrix_to_csv(int n, const double* w, char* buf, int cap) {
+    int len = 0;
+    const int st = guarded([&] { len = copy_out(matrix_to_csv(from_flat(n, w)), buf, cap); });
+    return st != 0 ? -1 : len;
+}
+
+int ref_solution_trace_csv(void* h, char* buf, int cap) {
+    return copy_out(static_cast<SolOut*>(h)->sol.trace_csv(), buf, cap);
+}
+
 void ref_solution_free(void* h) { delete static_cast<SolOut*>(h); }
 
 // scalars: {acf, lambda_tilde, residual, wall_ms, converged, connected, repaired,

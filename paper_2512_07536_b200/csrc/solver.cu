@@ -137,6 +137,7 @@ Solver::Solver(int n, int B, bool het, const std::vector<int>& r, const std::vec
     TPB_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     TPB_CUDA(cudaEventCreateWithFlags(&ev_sel_, cudaEventDisableTiming));
     TPB_CUDA(cudaEventCreateWithFlags(&ev_slem_, cudaEventDisableTiming));
+    phase_mark("solver streams");
     alloc();
     if (het && !cap_) {
         std::vector<double> dg(degrees.begin(), degrees.end());
@@ -244,6 +245,7 @@ void Solver::alloc() {
             TPB_CUDA(cudaMemsetAsync(sk_flags_, 0, (size_t)2 * T * sizeof(int), s0_));
         }
     }
+    phase_mark("alloc: state and scratch");
     if (ozaki_) {
         // digit planes of the cone-projection iterates
         for (int q = 0; q < 4; ++q) {
@@ -251,6 +253,7 @@ void Solver::alloc() {
             TPB_CUDA(cudaMemsetAsync(oz_.d[q], 0, (size_t)B * 2 * kOzSlices * ld2, s0_));
             make_oz_maps(oz_.d[q], ld_, 2 * B, &oz_.maps[q]);
         }
+        phase_mark("alloc: digit planes + TMA maps");
     }
     if (std::getenv("TPB_SLEM_STATS")) {
         slem_stats_ = dalloc<int>(s0_, allocs_, 2);
@@ -368,6 +371,12 @@ void Solver::final_slem(const double* packed, const int* list, const int* count,
     a.plain = exact || std::getenv("TPB_SLEM_CGS2") ? 0 : 1;
     a.basis = a.plain ? basis_ : basis_final_;
     a.kmax = exact ? std::max(1, n - 1) : (a.plain ? trace_kmax_ : kFinalKrylov);
+    // the final topology is the last trace iterate's neighbour: start from
+    // the trace's extreme Ritz vectors (tolerance unchanged)
+    if (a.plain) {
+        a.ritz = ritz_;
+        a.ritz_ok = ritz_ok_;
+    }
     a.max_restarts = 200;
     a.min_steps = 64;
     a.tol = 1e-10;

@@ -7,6 +7,9 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <cctype>
 #include <numeric>
 #include <limits>
 #include <set>
@@ -338,12 +341,189 @@ Topology generate_benchmark(BenchmarkKind kind, int n) {
     return t;
 }
 
-// ------------------------------------------------------------------ consensus
-static std::string g17(double v) {
+// ------------------------------------------------------------------ formats
+std::string g17(double v) {
     char buf[40];
     std::snprintf(buf, sizeof(buf), "%.17g", v);
     return buf;
 }
+
+namespace {
+// nlohmann::json's double layout: shortest round-trip digits, fixed notation
+// for decimal exponents in (-5, 15], d.ddde+XX otherwise, ".0" on integers
+std::string json_number(double v) {
+    if (v == 0.0) return std::signbit(v) ? "-0.0" : "0.0";
+    if (!std::isfinite(v)) return "null";
+    char buf[40];
+    for (int p = 1; p <= 17; ++p) {
+        std::snprintf(buf, sizeof buf, "%.*e", p - 1, v);
+        if (std::strtod(buf, nullptr) == v) break;
+    }
+    std::string t(buf), sign;
+    if (t[0] == '-') {
+        sign = "-";
+        t = t.substr(1);
+    }
+    const size_t epos = t.find('e');
+    const int e10 = std::atoi(t.c_str() + epos + 1);
+    std::string digits;
+    for (size_t i = 0; i < epos; ++i)
+        if (t[i] != '.') digits += t[i];
+    while (digits.size() > 1 && digits.back() == '0') digits.pop_back();
+    const int k = (int)digits.size(), n = e10 + 1;
+    std::string body;
+    if (k <= n && n <= 15) {
+        body = digits + std::string(n - k, '0') + ".0";
+    } else if (0 < n && n <= 15) {
+        body = digits.substr(0, n) + "." + digits.substr(n);
+    } else if (-4 < n && n <= 0) {
+        body = "0." + std::string(-n, '0') + digits;
+    } else {
+        char eb[16];
+        std::snprintf(eb, sizeof eb, "e%c%02d", e10 < 0 ? '-' : '+', std::abs(e10));
+        body = digits.substr(0, 1) + (k > 1 ? "." + digits.substr(1) : "") + eb;
+    }
+    return sign + body;
+}
+
+// minimal JSON reader for the topology schema
+struct JsonReader {
+    const std::string& s;
+    size_t i = 0;
+    void ws() {
+        while (i < s.size() && std::isspace((unsigned char)s[i])) ++i;
+    }
+    [[noreturn]] void fail() const { throw std::invalid_argument("topology json: malformed document"); }
+    void expect(char c) {
+        ws();
+        if (i >= s.size() || s[i] != c) fail();
+        ++i;
+    }
+    bool peek(char c) {
+        ws();
+        return i < s.size() && s[i] == c;
+    }
+    std::string str() {
+        expect('"');
+        std::string out;
+        while (i < s.size() && s[i] != '"') {
+            if (s[i] == '\\' && i + 1 < s.size()) ++i;
+            out += s[i++];
+        }
+        if (i >= s.size()) fail();
+        ++i;
+        return out;
+    }
+    std::string token() {
+        ws();
+        const size_t b = i;
+        while (i < s.size() && (std::isalnum((unsigned char)s[i]) || s[i] == '-' || s[i] == '+' || s[i] == '.')) ++i;
+        if (b == i) fail();
+        return s.substr(b, i - b);
+    }
+    bool is_int(const std::string& t) const { return t.find_first_of(".eE") == std::string::npos; }
+};
+}  // namespace
+
+std::string topology_to_json(const Topology& t) {
+    // proj/src/topology.cpp:283-290
+    Topology c = t;
+    c.normalize_and_validate();
+    std::string out = "{\n  \"edges\": ";
+    if (c.edges.empty()) {
+        out += "[]";
+    } else {
+        out += "[\n";
+        for (size_t k = 0; k < c.edges.size(); ++k)
+            out += "    [\n      " + std::to_string(c.edges[k].first) + ",\n      " +
+                   std::to_string(c.edges[k].second) + "\n    ]" + (k + 1 < c.edges.size() ? ",\n" : "\n");
+        out += "  ]";
+    }
+    out += ",\n  \"n\": " + std::to_string(c.n) + ",\n  \"weights\": ";
+    if (c.weights.empty()) {
+        out += "[]";
+    } else {
+        out += "[\n";
+        for (size_t k = 0; k < c.weights.size(); ++k)
+            out += "    " + json_number(c.weights[k]) + (k + 1 < c.weights.size() ? ",\n" : "\n");
+        out += "  ]";
+    }
+    return out + "\n}\n";
+}
+
+Topology topology_from_json(const std::string& text) {
+    // proj/src/topology.cpp:292-310
+    JsonReader r{text};
+    Topology t;
+    bool has_n = false, has_e = false, has_w = false;
+    r.expect('{');
+    while (!r.peek('}')) {
+        const std::string key = r.str();
+        r.expect(':');
+        if (key == "n") {
+            const std::string tok = r.token();
+            if (!r.is_int(tok)) throw std::invalid_argument("topology json: missing integer field 'n'");
+            t.n = std::stoi(tok);
+            has_n = true;
+        } else if (key == "edges" || key == "weights") {
+            if (!r.peek('[')) throw std::invalid_argument("topology json: missing array field '" + key + "'");
+            r.expect('[');
+            while (!r.peek(']')) {
+                if (key == "edges") {
+                    if (!r.peek('[')) throw std::invalid_argument("topology json: each edge must be a pair");
+                    r.expect('[');
+                    const int a = std::stoi(r.token());
+                    r.expect(',');
+                    const int b = std::stoi(r.token());
+                    if (!r.peek(']')) throw std::invalid_argument("topology json: each edge must be a pair");
+                    r.expect(']');
+                    t.edges.push_back({a, b});
+                } else {
+                    t.weights.push_back(std::strtod(r.token().c_str(), nullptr));
+                }
+                if (r.peek(',')) r.expect(',');
+            }
+            r.expect(']');
+            (key == "edges" ? has_e : has_w) = true;
+        } else {
+            // skip a scalar value of an unknown key
+            if (r.peek('"')) r.str();
+            else r.token();
+        }
+        if (r.peek(',')) r.expect(',');
+    }
+    r.expect('}');
+    if (!has_n) throw std::invalid_argument("topology json: missing integer field 'n'");
+    if (!has_e) throw std::invalid_argument("topology json: missing array field 'edges'");
+    if (!has_w) throw std::invalid_argument("topology json: missing array field 'weights'");
+    t.normalize_and_validate();
+    return t;
+}
+
+std::string matrix_to_csv(const Matrix& m) {
+    // proj/src/topology.cpp:312-324
+    std::string out;
+    for (int i = 0; i < m.rows(); ++i) {
+        for (int j = 0; j < m.cols(); ++j) {
+            out += g17(m(i, j));
+            if (j + 1 < m.cols()) out += ',';
+        }
+        out += '\n';
+    }
+    return out;
+}
+
+std::string matrix_to_triplet_csv(const Matrix& m, double drop_below) {
+    std::string out = "i,j,value\n";
+    for (int i = 0; i < m.rows(); ++i)
+        for (int j = 0; j < m.cols(); ++j) {
+            if (std::abs(m(i, j)) <= drop_below) continue;
+            out += std::to_string(i) + "," + std::to_string(j) + "," + g17(m(i, j)) + "\n";
+        }
+    return out;
+}
+
+// ------------------------------------------------------------------ consensus
 
 std::string ConsensusTrace::to_csv() const {
     std::string out = "iter,time_ms,error\n";

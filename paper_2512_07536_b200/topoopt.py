@@ -8,6 +8,8 @@ topology.hpp, errors.hpp); exceptions mirror proj/include/topoopt/errors.hpp.
 from __future__ import annotations
 
 import ctypes as C
+import json
+import math
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -688,3 +690,160 @@ class BatchSolver:
         _check(_lib.load().tp_solver_result(self.h, b, C.byref(res), _ip(edges), _dp(weights),
                                             _dp(trace), note, 512))
         return _solution(self.n, res, edges, weights, trace, note)
+
+
+# ---------------------------------------------------------------- on-disk formats
+# proj/include/topoopt/textio.hpp:10-14 (%.17g), proj/src/topology.cpp:283-324,
+# proj/src/admm.cpp:223-236, proj/tools/topoopt.cpp:278-294 (artefacts of
+# `topoopt optimize`). JSON is written in nlohmann's dump(2) layout: sorted
+# keys, two-space indent, one element per line, doubles in their shortest
+# round-trip form.
+def g17(v: float) -> str:
+    return "%.17g" % v
+
+
+def json_number(v) -> str:
+    """nlohmann::json's double formatting (shortest round-trip digits; fixed
+    notation for decimal exponents in (-5, 15], else d.ddde+XX; integral
+    values keep a '.0')."""
+    if isinstance(v, (bool, np.bool_)):
+        return "true" if v else "false"
+    if isinstance(v, (int, np.integer)):
+        return str(int(v))
+    v = float(v)
+    if v == 0.0:
+        return "-0.0" if math.copysign(1.0, v) < 0 else "0.0"
+    if not math.isfinite(v):
+        return "null"
+    for p in range(1, 18):
+        t = "%.*e" % (p - 1, v)
+        if float(t) == v:
+            break
+    mant, exp = t.split("e")
+    sign = "-" if mant.startswith("-") else ""
+    digits = mant.lstrip("-").replace(".", "")
+    digits = digits.rstrip("0") or "0"
+    k, n = len(digits), int(exp) + 1
+    if k <= n <= 15:
+        body = digits + "0" * (n - k) + ".0"
+    elif 0 < n <= 15:
+        body = digits[:n] + "." + digits[n:]
+    elif -4 < n <= 0:
+        body = "0." + "0" * (-n) + digits
+    else:
+        e = n - 1
+        body = digits[0] + ("." + digits[1:] if k > 1 else "") + "e" + ("-" if e < 0 else "+") + "%02d" % abs(e)
+    return sign + body
+
+
+def _json_dump(v, indent: int = 0) -> str:
+    pad, pad2 = " " * indent, " " * (indent + 2)
+    if isinstance(v, dict):
+        if not v:
+            return "{}"
+        items = [f'{pad2}{json.dumps(str(k))}: {_json_dump(v[k], indent + 2)}' for k in sorted(v)]
+        return "{\n" + ",\n".join(items) + "\n" + pad + "}"
+    if isinstance(v, (list, tuple, np.ndarray)):
+        if len(v) == 0:
+            return "[]"
+        return "[\n" + ",\n".join(pad2 + _json_dump(x, indent + 2) for x in v) + "\n" + pad + "]"
+    if isinstance(v, str):
+        return json.dumps(v)
+    if v is None:
+        return "null"
+    return json_number(v)
+
+
+def normalize_topology(n: int, edges, weights):
+    """Topology::normalize_and_validate: (i < j) pairs sorted, weights with them."""
+    e = np.asarray(edges, np.int64).reshape(-1, 2)
+    w = np.asarray(weights, np.float64).reshape(-1)
+    if len(e) != len(w):
+        raise ValueError("topology: edge and weight counts differ")
+    lo, hi = np.minimum(e[:, 0], e[:, 1]), np.maximum(e[:, 0], e[:, 1])
+    if len(e) and (lo.min() < 0 or hi.max() >= n or np.any(lo == hi)):
+        raise ValueError("topology: edge endpoint out of range or self loop")
+    order = np.lexsort((hi, lo))
+    e2 = np.stack([lo[order], hi[order]], 1)
+    if len(e2) > 1 and np.any(np.all(e2[1:] == e2[:-1], axis=1)):
+        raise ValueError("topology: duplicate edge")
+    return e2.astype(np.int32), w[order]
+
+
+def topology_to_json(n: int, edges, weights) -> str:
+    """proj/src/topology.cpp:283-290."""
+    e, w = normalize_topology(n, edges, weights)
+    return _json_dump({"n": int(n), "edges": [[int(a), int(b)] for a, b in e], "weights": [float(x) for x in w]}) + "\n"
+
+
+def topology_from_json(text: str):
+    """proj/src/topology.cpp:292-310 -> (n, edges, weights)."""
+    j = json.loads(text)
+    if not isinstance(j.get("n"), int) or isinstance(j.get("n"), bool):
+        raise ValueError("topology json: missing integer field 'n'")
+    if not isinstance(j.get("edges"), list):
+        raise ValueError("topology json: missing array field 'edges'")
+    if not isinstance(j.get("weights"), list):
+        raise ValueError("topology json: missing array field 'weights'")
+    for e in j["edges"]:
+        if not isinstance(e, list) or len(e) != 2:
+            raise ValueError("topology json: each edge must be a pair")
+    e, w = normalize_topology(j["n"], j["edges"] or np.zeros((0, 2)), j["weights"])
+    return j["n"], e, w
+
+
+def matrix_to_csv(w) -> str:
+    """proj/src/topology.cpp:312-324: %.17g, comma separated, one row per line."""
+    w = np.asarray(w, np.float64)
+    return "".join(",".join(g17(x) for x in row) + "\n" for row in w)
+
+
+def trace_csv(trace) -> str:
+    """Solution::trace_csv (proj/src/admm.cpp:223-236)."""
+    out = ["iter,residual,lambda_tilde,acf_iterate\n"]
+    for it, res, lam, acf in np.asarray(trace).reshape(-1, 4):
+        out.append(f"{int(it)},{g17(res)},{g17(lam)},{g17(acf)}\n")
+    return "".join(out)
+
+
+def utilization_csv(sys: CapacitySystem, edges) -> str:
+    """utilization + utilization_csv (proj/src/admm_het.cpp:371-394)."""
+    n = sys.n
+    sel = np.zeros(n * (n - 1) // 2, np.int8)
+    for i, j in np.asarray(edges).reshape(-1, 2):
+        sel[edge_index(n, int(i), int(j))] = 1
+    labels = sys.labels or [f"row{k}" for k in range(len(sys.rows))]
+    used = sys.loads(sel)
+    return "resource,capacity,used\n" + "".join(f"{lab},{cap},{u}\n" for lab, cap, u in zip(labels, sys.capacities, used))
+
+
+def write_optimize_artifacts(out_dir: str, mode: str, sol: "Solution", warm=None, allocation=None,
+                             system: CapacitySystem | None = None) -> list:
+    """The files `topoopt optimize` writes (proj/tools/topoopt.cpp:200-300):
+    warm_start.json, allocation.json (node mode), topology.json, w.csv,
+    trace.csv, utilization.csv (capacity systems), solution.json."""
+    import os
+    os.makedirs(out_dir, exist_ok=True)
+    n = sol.w.shape[0]
+    files = {}
+    if warm is not None:
+        we = np.asarray(warm).reshape(-1, 2)
+        deg = np.bincount(we.reshape(-1), minlength=n) if len(we) else np.zeros(n, int)
+        files["warm_start.json"] = topology_to_json(n, we, np.full(len(we), 1.0 / (deg.max() + 1)))
+    if allocation is not None:
+        b_unit, e = allocation
+        files["allocation.json"] = _json_dump({"b_unit": float(b_unit), "e": [int(x) for x in e]}) + "\n"
+    files["topology.json"] = topology_to_json(n, sol.edges, sol.weights)
+    files["w.csv"] = matrix_to_csv(sol.w)
+    files["trace.csv"] = trace_csv(sol.trace)
+    if system is not None:
+        files["utilization.csv"] = utilization_csv(system, sol.edges)
+    files["solution.json"] = _json_dump({
+        "mode": mode, "acf": float(sol.acf_value), "lambda_tilde": float(sol.lambda_tilde),
+        "converged": bool(sol.converged), "connected": bool(sol.connected), "repaired": bool(sol.repaired),
+        "iterations": int(sol.iterations), "residual": float(sol.residual), "edges": int(len(sol.edges)),
+        "note": sol.note}) + "\n"
+    for name, text in files.items():
+        with open(os.path.join(out_dir, name), "w") as f:
+            f.write(text)
+    return sorted(files)

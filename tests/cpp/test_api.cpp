@@ -157,6 +157,18 @@ int main() {
     CompareReport rep = compare({{"exp", gossip_matrix(ex), 1.0}}, 4, 20, 1e-3, 0);
     CHECK(rep.traces.size() == 1 && rep.to_csv().rfind("time_ms,label,error\n", 0) == 0);
 
+    // on-disk formats (proj/src/topology.cpp:283-324)
+    Topology small;
+    small.n = 4;
+    small.edges = {{2, 3}, {0, 1}, {0, 3}};
+    small.weights = {0.30000000000000004, 1e-05, 0.5};
+    const std::string js = topology_to_json(small);
+    CHECK(js.find("\"weights\": [\n    1e-05,\n    0.5,\n    0.30000000000000004\n  ]") != std::string::npos);
+    Topology back = topology_from_json(js);
+    CHECK(back.n == 4 && back.edges.size() == 3 && back.edges[0] == Edge(0, 1) && back.weights[2] == 0.30000000000000004);
+    CHECK(matrix_to_csv(gossip_matrix(back)).rfind("0.49999000000000005,1.0000000000000001e-05,0,0.5\n", 0) == 0);
+    CHECK_THROWS_AS(topology_from_json("{\"n\": 4}"), std::invalid_argument);
+
     // errors
     CHECK_THROWS_AS(extract_topology(3, 2, Vec{0.0, 0.0, 0.0}, 1e-6), DegenerateSolutionError);
     CHECK_THROWS_AS(node_level_constraints(3, {1, 1, 1}), InfeasibleError);

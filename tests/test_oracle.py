@@ -199,3 +199,52 @@ def test_capacity_solve_oracle(O, golden):
         assert s.iterations == ref["iterations"] and s.edges.tolist() == ref["edges"]
         assert rel(s.weights, ref["weights"]) < 1e-6
         assert s.acf == pytest.approx(ref["acf"], rel=1e-6) and s.note == ref["note"]
+
+
+def test_formats_vs_reference(T, golden):
+    # §8f row 4: topology.json / w.csv / trace.csv against the reference's own
+    # serializers (proj/src/topology.cpp:283-324, admm.cpp:223-236). The
+    # oracle build's nlohmann (cudnn_frontend copy) prints integer arrays on
+    # one line; values and every double token must agree.
+    import json
+    import re
+    num = re.compile(r"-?\d+\.\d+(?:e[-+]\d+)?|-?\d+e[-+]\d+")
+    for c in golden("formats.json"):
+        ours = T.topology_to_json(c["n"], c["edges"], c["weights"])
+        assert json.loads(ours) == json.loads(c["topology_json"])
+        assert num.findall(ours) == num.findall(c["topology_json"])
+        assert ours.endswith("}\n")
+        w = T.gossip_matrix(c["n"], np.array(c["edges"]), np.array(c["weights"]))
+        assert T.matrix_to_csv(w) == c["w_csv"]
+        if "trace_csv" in c:
+            rows = [r.split(",") for r in c["trace_csv"].strip().split("\n")[1:]]
+            tr = np.array([[float(x) for x in r] for r in rows])
+            assert T.trace_csv(tr) == c["trace_csv"]
+        n, e, wt = T.topology_from_json(ours)
+        e0, w0 = T.normalize_topology(c["n"], c["edges"], c["weights"])
+        assert n == c["n"] and np.array_equal(e, e0) and np.array_equal(wt, w0)
+
+
+def test_json_number_format(T):
+    # nlohmann::json double layout (shortest round trip, fixed for exponents in (-5, 15])
+    cases = {0.5: "0.5", 1.0: "1.0", 100.0: "100.0", 1e-05: "1e-05", 0.0001: "0.0001",
+             2.0 ** -20: "9.5367431640625e-07", 0.30000000000000004: "0.30000000000000004",
+             1e15: "1e+15", 123456789012345.0: "123456789012345.0", -2.5: "-2.5", 0.0: "0.0",
+             1.5e300: "1.5e+300"}
+    for v, s in cases.items():
+        assert T.json_number(v) == s, (v, T.json_number(v))
+
+
+def test_write_optimize_artifacts(T, golden, tmp_path):
+    c = golden("formats.json")[0]
+    rows = [r.split(",") for r in c["trace_csv"].strip().split("\n")[1:]]
+    tr = np.array([[float(x) for x in r] for r in rows])
+    e, w = np.array(c["edges"]), np.array(c["weights"])
+    sol = T.Solution(e, w, T.gossip_matrix(16, e, w), 0.47, 0.525, True, True, False, 1e-9, len(tr), "", tr)
+    files = T.write_optimize_artifacts(str(tmp_path), "homogeneous", sol, warm=e)
+    assert files == ["solution.json", "topology.json", "trace.csv", "w.csv", "warm_start.json"]
+    assert (tmp_path / "w.csv").read_text() == c["w_csv"]
+    assert (tmp_path / "trace.csv").read_text() == c["trace_csv"]
+    import json
+    sj = json.loads((tmp_path / "solution.json").read_text())
+    assert sj["mode"] == "homogeneous" and sj["edges"] == 32 and sj["iterations"] == 556
