@@ -168,6 +168,56 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------- CG x-step
+def measure_cg_variant(T, torch, n, r, warm, K, W):
+    """The paper's CG linear substep (linear_solver = 1) on
+    the same workload: ADMM iter/s with the CG x-step, and the CG solve's HBM
+    roofline. Per CG iteration k the direction pass reads r (and p, k > 0)
+    and writes p; the update pass reads r, p (and x, k > 0) and writes x, r:
+    (2 + 4) m doubles at k = 0, (3 + 5) m after."""
+    bs = T.BatchSolver(n, r=[r], max_iter=W + K + 8, linear_solver=1, **CFG)
+    try:
+        bs.set_warm(0, warm)
+        bs.start()
+        stream = torch.cuda.ExternalStream(bs.stream)
+        bs.iterate(W)
+        bs.sync()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        bs.iterate(K)
+        e1.record(stream)
+        e1.synchronize()
+        it_s = K / (e0.elapsed_time(e1) / 1e3)
+        its, rel = bs.cg_stats(0)
+
+        def phase(ph, reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            bs.bench_phase(ph, 1)
+            torch.cuda.synchronize()
+            a.record(stream)
+            bs.bench_phase(ph, reps)
+            b.record(stream)
+            b.synchronize()
+            return a.elapsed_time(b) / 1e3 / reps
+
+        t_a = phase(5, 20)
+        t_acg = phase(7, 20)
+        its2, _ = bs.cg_stats(0)
+    finally:
+        bs.close()
+    m = n * (n - 1) // 2
+    t_cg = max(t_acg - t_a, 1e-9)
+    k = max(its2, 1)
+    cg_bytes = 8.0 * m * (6 + 8 * (k - 1))
+    hbm = peaks().get("hbm_gbs", 6538.9)
+    return {"admm_iter_per_s": it_s, "cg_iterations_per_xstep": its, "cg_rel_residual": rel,
+            "cg_solve_ms": t_cg * 1e3, "cg_bytes": cg_bytes, "achieved_gbs": cg_bytes / t_cg / 1e9,
+            "frac_of_hbm": cg_bytes / t_cg / 1e9 / hbm, "peak_gbs": hbm,
+            "kernels": "xstep_cg_kernel: one persistent cooperative launch, direction + update pass per CG iteration, grid barriers between",
+            "note": "working set (x, r, p: 12.6 MB at n=1024) is L2-resident between passes"}
+
+
 # ---------------------------------------------------------------- our arm
 def run_ours(args):
     import torch
@@ -236,6 +286,7 @@ def run_ours(args):
     t_xa, _ = phase(5, 10)
     t_xb, _ = phase(6, 10)
     bs.close()
+    cgm = measure_cg_variant(T, torch, n, r, warm, K, W)
 
     # roofline of the dominant kernel: the Ozaki-scheme GEMM on the int8
     # tensor cores (default) or the FP64 DMMA GEMM (TPB_CONE=dmma)
@@ -323,6 +374,7 @@ def run_ours(args):
                 "whole_xstep": {"bytes": xbytes, "ms": t_x * 1e3, "achieved": xbytes / t_x / 1e9,
                                 "frac": xbytes / t_x / 1e9 / pk.get("hbm_gbs", 6538.9),
                                 "note": "incl. the single-CTA node and diag passes"}},
+            "cg_xstep": cgm,
             "e2e": {"value": e2e, "unit": "iter/s", "h2d_bytes_per_step": h2d / K,
                     "d2h_bytes_per_step": d2h / K,
                     "note": "tp_solve through the C ABI with host warm-start edges in and the host "

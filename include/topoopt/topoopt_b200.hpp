@@ -208,6 +208,9 @@ struct SolverConfig {  // proj/include/topoopt/admm.hpp:15-25
     double weight_floor = 1e-6;
     std::uint64_t seed = 0;
     double linear_tol = 1e-10;
+    // device extension: 0 closed-form x-step, 1 the paper's matrix-free CG
+    // linear substep to linear_tol (homogeneous solves)
+    int linear_solver = 0;
     void validate() const;
 };
 
@@ -249,6 +252,10 @@ Vec project_Y(const ProblemData& pd, const Vec& x_state, const Vec& duals);
 // kkt_warm (length nx + neq) receives the exact KKT solution [x; mu].
 Vec update_X(const ProblemData& pd, const Vec& y_state, const Vec& duals, Vec& kkt_warm,
              double linear_tol);
+// The same x-step with the CG linear substep (matrix-free over the edge
+// incidence); throws LinearSolveError above 1e-8 relative residual.
+Vec update_X_cg(const ProblemData& pd, const Vec& y_state, const Vec& duals, Vec& kkt_warm,
+                double linear_tol, int* cg_iters = nullptr);
 void update_duals(const ProblemData& pd, const Vec& x_state, const Vec& y_state, Vec& duals);
 
 struct Extraction {

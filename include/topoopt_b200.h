@@ -51,6 +51,9 @@ typedef struct tp_config {
     double linear_tol;     /* 1e-10 (accepted; the x-step is solved exactly) */
     int32_t trace_stride;  /* 1: acf_iterate every iteration, as the reference */
     int32_t chunk;         /* 0: auto; iterations per CUDA graph launch */
+    int32_t linear_solver; /* 0: closed-form x-step (default); 1: matrix-free CG on
+                              the edge-incidence operator to linear_tol (hom only) */
+    int32_t cg_max_iter;   /* 8: CG iterations per x-step (early exit) */
 } tp_config;
 
 /* Solution scalars (proj/include/topoopt/admm.hpp:38-53). */
@@ -130,6 +133,9 @@ int tp_solver_state(tp_solver* s, double** x, double** y, double** d);
  * so callers can time it with events; the state is left undefined. */
 int tp_solver_bench_phase(tp_solver* s, int32_t phase, int32_t reps, int32_t* launches_per_rep);
 int tp_solver_launches_per_iteration(tp_solver* s, int32_t* out);
+/* CG x-step statistics of solve b's last iteration (linear_solver = 1):
+ * iterations and |r| / |h|. */
+int tp_solver_cg_stats(tp_solver* s, int32_t b, int32_t* iters, double* rel_res);
 
 /* Tuning hooks of the FP64 DMMA GEMM behind the cone projections:
  * variant 0 = production; tp_bench_gemm times one GEMM step on nmat
@@ -190,6 +196,16 @@ int tp_project_Y_het_node(int32_t n, const int32_t* degrees, double alpha, doubl
  * with BiCGSTAB. */
 int tp_update_X(int32_t n, int32_t r, double alpha, double rho, const double* y, const double* d,
                 double* kkt_out);
+/* update_X with the paper's CG linear substep (proj/src/admm.cpp:279-293,
+ * linear_tol as in the reference's update_X signature): matrix-free CG on
+ * the g block of the reduced KKT system, H_gg = (1+4s) I + 3s D^T D, to
+ * |r| <= linear_tol |h|. Same kkt_out layout; cg_iters / cg_rel_res report
+ * the solve (either may be NULL). Fails with TP_ERR_LINEAR_SOLVE when the
+ * relative residual is above 1e-8 after cg_max_iter iterations, as the
+ * reference's BiCGSTAB guard (admm.cpp:287). */
+int tp_update_X_cg(int32_t n, int32_t r, double alpha, double rho, const double* y, const double* d,
+                   double linear_tol, int32_t cg_max_iter, double* kkt_out, int32_t* cg_iters,
+                   double* cg_rel_res);
 int tp_update_X_het_node(int32_t n, const int32_t* degrees, double alpha, double rho,
                          const double* y, const double* d, double* kkt_out);
 /* update_duals (proj/src/admm.cpp:295-297): d += rho (x - y). */

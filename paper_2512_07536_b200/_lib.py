@@ -33,6 +33,8 @@ class tp_config(C.Structure):
         ("linear_tol", C.c_double),
         ("trace_stride", C.c_int32),
         ("chunk", C.c_int32),
+        ("linear_solver", C.c_int32),
+        ("cg_max_iter", C.c_int32),
     ]
 
 
@@ -96,6 +98,8 @@ SIGNATURES = {
     "tp_project_Y": (_I, [_I, _I, _D, _D, _dp, _dp, _dp]),
     "tp_project_Y_het_node": (_I, [_I, _ip, _D, _D, _dp, _dp, _dp]),
     "tp_update_X": (_I, [_I, _I, _D, _D, _dp, _dp, _dp]),
+    "tp_update_X_cg": (_I, [_I, _I, _D, _D, _dp, _dp, _D, _I, _dp, _ip, _dp]),
+    "tp_solver_cg_stats": (_I, [_P, _I, _ip, _dp]),
     "tp_update_X_het_node": (_I, [_I, _ip, _D, _D, _dp, _dp, _dp]),
     "tp_update_duals": (_I, [_I64, _D, _dp, _dp, _dp]),
     "tp_project_binary_z": (_I, [_dp, _I64, _I, _dp]),

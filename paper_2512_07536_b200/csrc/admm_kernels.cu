@@ -12,7 +12,13 @@
 //                      (src/admm.cpp:388-405, src/admm_het.cpp:281-300).
 #include "admm_kernels.cuh"
 
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
 namespace tpb {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -42,6 +48,29 @@ __device__ inline double sum_partials(const double* P, int nb, long long stride,
     }
     for (; k < nb; ++k) s += P[(long long)k * stride + i];
     return s;
+}
+
+// 2-D block (TB x TY) deterministic sum; every thread receives the result.
+__device__ inline double block_sum_2d(double v, double* scratch) {
+    const int t = threadIdx.y * TB + threadIdx.x;
+    const int lane = t & 31, wid = t >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) scratch[wid] = v;
+    __syncthreads();
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < TB * TY / 32; ++w) s += scratch[w];
+    __syncthreads();
+    return s;
+}
+
+// fixed-order total of `cnt` partials (identical in every CTA)
+__device__ inline double sum_tiles(const double* P, int cnt, double* scratch) {
+    const int t = threadIdx.y * TB + threadIdx.x;
+    double v = 0.0;
+    for (int k = t; k < cnt; k += TB * TY) v += P[k];
+    return block_sum_2d(v, scratch);
 }
 
 }  // namespace
@@ -82,6 +111,8 @@ XConst make_xconst(int n, double alpha, double rho) {
     c.g22_1 = (a1 + b1 * q1) / d1;
     c.mu_den_p = qp * c.g22_p + delta;
     c.mu_den_1 = q1 * c.g22_1 + delta;
+    c.cg_a = a;
+    c.cg_b = b;
     return c;
 }
 
@@ -291,6 +322,14 @@ __global__ void __launch_bounds__(TB* TY) xstep_a_kernel(Dev d, XConst c) {
         if (d.het) Zs[il][jl] = hz;
     }
     __syncthreads();
+    if (d.cg) {
+        // |h|^2 partial of the tile: r_0 = h for the CG x-step
+        __shared__ double red[TB * TY / 32];
+        double hh = 0.0;
+        for (int il = ty; il < TB; il += TY) hh += Hs[il][tx] * Hs[il][tx];
+        hh = block_sum_2d(hh, red);
+        if (ty == 0 && tx == 0) d.cg_rr[(long long)b * 2 * d.ntile + blockIdx.x] = hh;
+    }
     // node partials: PU[bj][i] (rows of block bi) and PU[bi][j] (cols of block bj)
     const int t = ty * TB + tx;
     double* PU = d.PU + (long long)b * d.nb * n;
@@ -434,6 +473,281 @@ void launch_xstep_node(const Dev& d, const XConst& c, cudaStream_t st) {
     TPB_CHECK_LAUNCH();
 }
 
+// ---------------------------------------------------------------- CG x-step
+// The paper's linear substep as matrix-free CG on the g block of the reduced
+// KKT system: H_gg = (1 + 4s) I + 3s D^T D, applied as one
+// node-sum scatter (u = D p, fixed-order tile partials) and one per-edge
+// gather (u_i + u_j). On the complete candidate graph H_gg has three
+// eigenvalues, so CG stops after three iterations at ~1e-15; the closed form
+// (launch_xstep_node + pass B) is the default and this path is its
+// operator-level cross-check and the general-graph formulation.
+
+namespace {
+
+// node partials of a tile's packed values Vs (pairs il < jl on diagonal tiles)
+__device__ inline void tile_node_partials(const double (&Vs)[TB][TB + 1], int bi, int bj, int n, double* P) {
+    const int t = threadIdx.y * TB + threadIdx.x;
+    const int i0 = bi * TB, j0 = bj * TB;
+    if (t < TB) {
+        const int il = t, i = i0 + il;
+        if (i < n) {
+            double s = 0.0;
+            for (int jl = 0; jl < TB; ++jl) {
+                if (bi == bj) {
+                    if (jl == il) continue;
+                    s += jl > il ? Vs[il][jl] : Vs[jl][il];
+                } else {
+                    s += Vs[il][jl];
+                }
+            }
+            P[(long long)bj * n + i] = s;
+        }
+    } else if (t < 2 * TB && bi != bj) {
+        const int jl = t - TB, j = j0 + jl;
+        if (j < n) {
+            double s = 0.0;
+            for (int il = 0; il < TB; ++il) s += Vs[il][jl];
+            P[(long long)bi * n + j] = s;
+        }
+    }
+}
+
+}  // namespace
+
+// One persistent cooperative grid runs the whole CG solve: the CTAs stride
+// over the (solve, tile) work items; per iteration a direction
+// pass (beta, u = D p from node partials, p = r + beta p, p.Hp partials) and
+// an update pass (alpha, x += alpha p, r -= alpha Hp, |r|^2 and D r
+// partials), separated by grid-wide barriers. Every CTA derives the
+// per-solve scalars itself from the fixed-order partials (a warp per solve),
+// so the decisions are identical everywhere without extra barriers, and the
+// result is bitwise reproducible. The loop ends when every solve has stopped.
+__global__ void __launch_bounds__(TB* TY, 4) xstep_cg_kernel(Dev d, XConst c) {
+    cg::grid_group grid = cg::this_grid();
+    const Layout& lo = d.lo;
+    const int n = lo.n;
+    const int nitems = d.B * d.ntile;
+    const int tx = threadIdx.x, ty = threadIdx.y, t = ty * TB + tx;
+    const int lane = t & 31, warp = t >> 5;
+    constexpr int NR_ = TB / TY, NW = TB * TY / 32;
+    __shared__ double scratch[NW];
+    __shared__ double ui[TB], uj[TB];
+    __shared__ double Rs[TB][TB + 1];
+    __shared__ int s_any;
+    extern __shared__ double dyn[];  // per solve: rr0, rr_k, beta | active flags
+    double* s_rr0 = dyn;
+    double* s_rrk = dyn + d.B;
+    double* s_beta = dyn + 2 * d.B;
+    int* s_act = reinterpret_cast<int*>(dyn + 3 * d.B);
+
+    // fixed-order warp sum of one solve's tile partials
+    auto wsum = [&](const double* P) {
+        // loads batched 8 deep so their L2 latencies overlap
+        double v = 0.0;
+        int k = lane;
+        for (; k + 7 * 32 < d.ntile; k += 8 * 32) {
+            double q[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) q[j] = P[k + j * 32];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v += q[j];
+        }
+        for (; k < d.ntile; k += 32) v += P[k];
+        return warp_sum(v);
+    };
+
+    for (int k = 0; k <= d.cg_max; ++k) {
+        // ---- per-solve scalars (every CTA; warp per solve)
+        for (int b = warp; b < d.B; b += NW) {
+            const double* RR = d.cg_rr + (long long)b * 2 * d.ntile;
+            const bool was = k == 0 ? !solve_done(d, b) : s_act[b] != 0;
+            double rr1 = 0.0;
+            if (k == 0) {
+                rr1 = wsum(RR);  // |h|^2 (pass A)
+                if (lane == 0) s_rr0[b] = rr1;
+            } else if (was) {
+                rr1 = wsum(RR + d.ntile);  // |r_k|^2 (update pass k-1)
+            }
+            if (lane == 0) {
+                bool act = was;
+                if (was) {
+                    const double rr0 = s_rr0[b];
+                    const bool conv = k == 0 ? !(rr0 > 0.0) : rr1 <= d.cg_tol2 * rr0;
+                    if (conv || k == d.cg_max) {
+                        act = false;
+                        if (blockIdx.x == 0) {
+                            d.ictl[b * 8 + kCgIters] = k;
+                            d.scal[b * 8 + kCgRes] = rr0 > 0.0 ? sqrt(rr1 / rr0) : 0.0;
+                        }
+                    }
+                    s_beta[b] = k == 0 ? 0.0 : rr1 / s_rrk[b];
+                    s_rrk[b] = rr1;
+                }
+                s_act[b] = act;
+            }
+        }
+        __syncthreads();
+        if (t == 0) {
+            int any = 0;
+            for (int b = 0; b < d.B && !any; ++b) any = s_act[b];
+            s_any = any;
+        }
+        __syncthreads();
+        if (!s_any) break;  // uniform: every CTA computed the same flags
+
+        // ---- direction pass
+        for (int w = blockIdx.x; w < nitems; w += gridDim.x) {
+            const int b = w / d.ntile, tile = w - b * d.ntile;
+            if (!s_act[b]) continue;
+            const double beta = s_beta[b];
+            int bi, bj;
+            tile_of(tile, bi, bj);
+            const int i0 = bi * TB, j0 = bj * TB;
+            const double* NRp = k == 0 ? d.PU + (long long)b * d.nb * n : d.cg_nr + (long long)b * d.nb * n;
+            const double* Uprev = d.cg_u + ((long long)b * 2 + ((k - 1) & 1)) * n;
+            double* Ucur = d.cg_u + ((long long)b * 2 + (k & 1)) * n;
+            {
+                // u of the tile's 64 nodes: 4 threads per node (adjacent
+                // lanes) sum interleaved quarters of the nb node partials
+                const int nl = t >> 2, part = t & 3;
+                const int node = nl < TB ? i0 + nl : j0 + nl - TB;
+                double u = 0.0;
+                if (node < n) {
+                    int q = part;
+                    for (; q + 12 < d.nb; q += 16) {
+                        double v[4];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) v[j] = NRp[(long long)(q + 4 * j) * n + node];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) u += v[j];
+                    }
+                    for (; q < d.nb; q += 4) u += NRp[(long long)q * n + node];
+                }
+                u += __shfl_xor_sync(0xffffffffu, u, 1);
+                u += __shfl_xor_sync(0xffffffffu, u, 2);
+                if (part == 0 && node < n) {
+                    if (k > 0) u += beta * Uprev[node];
+                    if (bi == bj && nl < TB) Ucur[node] = u;  // one diagonal tile per node block
+                }
+                if (part == 0) {
+                    if (nl < TB) ui[nl] = u; else uj[nl - TB] = u;
+                }
+            }
+            __syncthreads();
+            const double* R = d.h + (long long)b * lo.m;
+            double* P = d.cg_p + (long long)b * lo.m;
+            long long l[NR_];
+            bool ok[NR_];
+            double rv[NR_], pv[NR_];
+#pragma unroll
+            for (int q = 0; q < NR_; ++q) {
+                const int i = i0 + ty + q * TY, j = j0 + tx;
+                ok[q] = i < n && j < n && j > i;
+                l[q] = ok[q] ? edge_idx(n, i, j) : 0;
+                if (ok[q]) {
+                    rv[q] = R[l[q]];
+                    pv[q] = k == 0 ? 0.0 : P[l[q]];
+                }
+            }
+            double pq = 0.0;
+#pragma unroll
+            for (int q = 0; q < NR_; ++q) {
+                if (!ok[q]) continue;
+                const double p = rv[q] + beta * pv[q];
+                P[l[q]] = p;
+                pq += p * (c.cg_a * p + c.cg_b * (ui[ty + q * TY] + uj[tx]));
+            }
+            pq = block_sum_2d(pq, scratch);  // (its barriers also retire ui/uj)
+            if (t == 0) d.cg_pq[w] = pq;
+        }
+        grid.sync();
+
+        // ---- update pass
+        int alpha_b = -1;
+        double alpha = 0.0;
+        for (int w = blockIdx.x; w < nitems; w += gridDim.x) {
+            const int b = w / d.ntile, tile = w - b * d.ntile;
+            if (!s_act[b]) continue;
+            if (b != alpha_b) {
+                const double pq = sum_tiles(d.cg_pq + (long long)b * d.ntile, d.ntile, scratch);
+                alpha = pq > 0.0 ? s_rrk[b] / pq : 0.0;
+                alpha_b = b;
+            }
+            int bi, bj;
+            tile_of(tile, bi, bj);
+            const int i0 = bi * TB, j0 = bj * TB;
+            const double* U = d.cg_u + ((long long)b * 2 + (k & 1)) * n;
+            if (t < TB) ui[t] = i0 + t < n ? U[i0 + t] : 0.0;
+            else if (t < 2 * TB) uj[t - TB] = j0 + t - TB < n ? U[j0 + t - TB] : 0.0;
+            __syncthreads();
+            double* R = d.h + (long long)b * lo.m;
+            double* X = d.cg_x + (long long)b * lo.m;
+            const double* P = d.cg_p + (long long)b * lo.m;
+            long long l[NR_];
+            bool ok[NR_];
+            double rv[NR_], pv[NR_], xv[NR_];
+#pragma unroll
+            for (int q = 0; q < NR_; ++q) {
+                const int i = i0 + ty + q * TY, j = j0 + tx;
+                ok[q] = i < n && j < n && j > i;
+                l[q] = ok[q] ? edge_idx(n, i, j) : 0;
+                if (ok[q]) {
+                    rv[q] = R[l[q]];
+                    pv[q] = P[l[q]];
+                    xv[q] = k == 0 ? 0.0 : X[l[q]];
+                }
+            }
+            double rr = 0.0;
+#pragma unroll
+            for (int q = 0; q < NR_; ++q) {
+                double r = 0.0;
+                if (ok[q]) {
+                    const double hp = c.cg_a * pv[q] + c.cg_b * (ui[ty + q * TY] + uj[tx]);
+                    X[l[q]] = xv[q] + alpha * pv[q];
+                    r = rv[q] - alpha * hp;
+                    R[l[q]] = r;
+                    rr += r * r;
+                }
+                Rs[ty + q * TY][tx] = r;
+            }
+            __syncthreads();
+            tile_node_partials(Rs, bi, bj, n, d.cg_nr + (long long)b * d.nb * n);
+            rr = block_sum_2d(rr, scratch);  // (its barriers also retire ui/uj/Rs)
+            if (t == 0) d.cg_rr[((long long)b * 2 + 1) * d.ntile + tile] = rr;
+        }
+        grid.sync();
+    }
+}
+
+size_t cg_dyn_smem(const Dev& d) { return (size_t)d.B * (3 * sizeof(double) + sizeof(int)); }
+
+int cg_grid_size(const Dev& d) {
+    static int cached = 0;
+    if (!cached) {
+        int dev = 0, sms = 0, per_sm = 0;
+        TPB_CUDA(cudaGetDevice(&dev));
+        TPB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        TPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, xstep_cg_kernel, TB * TY,
+                                                               cg_dyn_smem(d)));
+        cached = std::max(1, sms * per_sm);
+    }
+    return std::max(1, std::min(cached, d.B * d.ntile));
+}
+
+void launch_xstep_cg(const Dev& d, const XConst& c, cudaStream_t st) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(cg_grid_size(d));
+    cfg.blockDim = dim3(TB, TY);
+    cfg.stream = st;
+    cfg.dynamicSmemBytes = cg_dyn_smem(d);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    TPB_CUDA(cudaLaunchKernelEx(&cfg, xstep_cg_kernel, d, c));
+}
+
 // ---------------------------------------------------------------- x-step B
 __global__ void __launch_bounds__(TB* TY) xstep_b_kernel(Dev d, XConst c) {
     const int b = blockIdx.y;
@@ -453,6 +767,7 @@ __global__ void __launch_bounds__(TB* TY) xstep_b_kernel(Dev d, XConst c) {
     double res = 0.0;
 
     // edge blocks (hom: batched loads of h, Y_g, D_g for the thread's rows)
+    const int cg_it = d.cg ? d.ictl[b * 8 + kCgIters] : 0;
     if (!d.het) {
         constexpr int NR = TB / TY;
         long long l[NR];
@@ -474,7 +789,9 @@ __global__ void __launch_bounds__(TB* TY) xstep_b_kernel(Dev d, XConst c) {
             const int il = ty + k * TY, i = i0 + il, j = j0 + tx;
             double g = 0.0;
             if (ok[k]) {
-                g = c.f0 * hv[k] + node[i] + node[j];
+                // CG: zero iterations means h = 0 and g = 0
+                g = d.cg ? (cg_it > 0 ? d.cg_x[(long long)b * lo.m + l[k]] : 0.0)
+                         : c.f0 * hv[k] + node[i] + node[j];
                 const double e = g - yg[k];
                 X[l[k]] = g;
                 if (d.upd_duals) D[l[k]] = dg[k] + c.rho * e;

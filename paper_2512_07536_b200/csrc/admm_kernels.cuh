@@ -17,6 +17,8 @@ struct XConst {
     double c1_11, c2_11, c1_12, c2_12, c1_22, c2_22;      // (G(q)-G(0))/q at q=n-2, 2n-2
     double g12_p, g22_p, g12_1, g22_1;                    // G12/G22 at n-2 and 2n-2
     double mu_den_p, mu_den_1;                            // (n-2)G22(n-2)+delta, (2n-2)G22(2n-2)+delta
+    // matrix-free CG on H_gg = cg_a I + cg_b D^T D
+    double cg_a, cg_b;
 };
 
 XConst make_xconst(int n, double alpha, double rho);
@@ -54,6 +56,16 @@ struct Dev {
     double epsilon;
     int track_best;
     int upd_duals;   // 0: x-step only (substep API), no dual update / bookkeeping
+    // matrix-free CG x-step (hom; linear_solver = 1). r lives in h (in place).
+    int cg = 0;        // 1: g from CG on H_gg g = h instead of the closed form
+    int cg_max = 0;    // CG iterations launched per x-step
+    double cg_tol2 = 0.0;  // stop when |r|^2 <= cg_tol2 |h|^2
+    double* cg_x;      // B x m  solution
+    double* cg_p;      // B x m  search direction
+    double* cg_pq;     // B x ntile      partials of p.Hp
+    double* cg_rr;     // B x 2 x ntile  partials of |r|^2: [h (pass A), r_k+1]
+    double* cg_nr;     // B x nb x n     node partials of D r
+    double* cg_u;      // B x 2 x n      D p (parity)
 };
 
 enum Ctl { kIter = 0, kDone = 1, kBestIter = 2, kImproved = 3 };
@@ -68,6 +80,15 @@ void launch_frob_finalize(const Dev& d, cudaStream_t st);
 void launch_xstep_a(const Dev& d, const XConst& c, cudaStream_t st);
 // node-space solve (lambda, t, mu_d).
 void launch_xstep_node(const Dev& d, const XConst& c, cudaStream_t st);
+// Matrix-free CG on H_gg g = h (hom) in one persistent cooperative launch:
+// iteration k = direction pass (p, Hp inline, p.Hp partials) + update pass
+// (x, r, |r|^2 and D r partials), per-solve scalars from fixed-order partial
+// sums on the device, grid barriers between phases; the loop stops when
+// every solve has reached |r| <= linear_tol |h| (or cg_max iterations).
+void launch_xstep_cg(const Dev& d, const XConst& c, cudaStream_t st);
+// Statistics of the last CG solve: ictl[b*8+5] = iterations,
+// scal[b*8+3] = |r| / |h|.
+enum CgStat { kCgIters = 5, kCgRes = 3 };
 // x-step pass B: g (z, nu), off-diagonal S/T, dual update, residual partials.
 void launch_xstep_b(const Dev& d, const XConst& c, cudaStream_t st);
 // diagonal entries, y, lambda, residual, trace, best/done flags.

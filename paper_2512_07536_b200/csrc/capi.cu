@@ -43,6 +43,8 @@ Config to_cfg(const tp_config* c) {
         k.linear_tol = c->linear_tol;
         k.trace_stride = c->trace_stride;
         k.chunk = c->chunk;
+        k.linear_solver = c->linear_solver;
+        k.cg_max_iter = c->cg_max_iter;
     }
     return k;
 }
@@ -134,6 +136,8 @@ void tp_config_default(tp_config* c) {
     c->linear_tol = 1e-10;
     c->trace_stride = 1;
     c->chunk = 0;
+    c->linear_solver = 0;
+    c->cg_max_iter = 8;
 }
 
 int tp_config_validate(const tp_config* c) {
@@ -225,6 +229,16 @@ int tp_solver_bench_phase(tp_solver* s, int32_t phase, int32_t reps, int32_t* la
 
 int tp_solver_launches_per_iteration(tp_solver* s, int32_t* out) {
     return guarded([&] { *out = s->s->launches_per_iteration(); });
+}
+
+int tp_solver_cg_stats(tp_solver* s, int32_t b, int32_t* iters, double* rel_res) {
+    return guarded([&] {
+        int it = 0;
+        double rr = 0.0;
+        s->s->cg_stats(b, &it, &rr);
+        if (iters) *iters = it;
+        if (rel_res) *rel_res = rr;
+    });
 }
 
 int tp_solve(int32_t n, int32_t r, const tp_config* cfg, const int32_t* warm_edges, int32_t n_warm,

@@ -282,6 +282,30 @@ int tp_update_X(int32_t n, int32_t r, double alpha, double rho, const double* y,
     });
 }
 
+int tp_update_X_cg(int32_t n, int32_t r, double alpha, double rho, const double* y, const double* d,
+                   double linear_tol, int32_t cg_max_iter, double* kkt_out, int32_t* cg_iters,
+                   double* cg_rel_res) {
+    return guarded([&] {
+        require_device();
+        Config c = sub_cfg(alpha, rho);
+        c.linear_solver = 1;
+        c.linear_tol = linear_tol;
+        c.cg_max_iter = cg_max_iter;
+        validate(c);
+        Solver s(n, 1, false, {r}, {}, c);
+        update_x_common(s, rho, y, d, kkt_out);
+        int it = 0;
+        double rr = 0.0;
+        s.cg_stats(0, &it, &rr);
+        if (cg_iters) *cg_iters = it;
+        if (cg_rel_res) *cg_rel_res = rr;
+        // the reference's guard after BiCGSTAB (proj/src/admm.cpp:287)
+        if (!(rr <= 1e-8))
+            throw Error(kLinearSolve, "update_X: CG relative residual " + std::to_string(rr) +
+                                          " after " + std::to_string(it) + " iterations");
+    });
+}
+
 int tp_update_X_het_node(int32_t n, const int32_t* degrees, double alpha, double rho,
                          const double* y, const double* d, double* kkt_out) {
     return guarded([&] {

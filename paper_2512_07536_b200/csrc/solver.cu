@@ -25,6 +25,10 @@ void validate(const Config& c) {
     if (c.weight_floor < 0.0) throw Error(kInvalidArgument, "SolverConfig: weight_floor must be >= 0");
     if (!(c.linear_tol > 0.0)) throw Error(kInvalidArgument, "SolverConfig: linear_tol must be positive");
     if (c.trace_stride < 1) throw Error(kInvalidArgument, "SolverConfig: trace_stride must be >= 1");
+    if (c.linear_solver != 0 && c.linear_solver != 1)
+        throw Error(kInvalidArgument, "SolverConfig: linear_solver must be 0 (closed form) or 1 (CG)");
+    if (c.linear_solver == 1 && (c.cg_max_iter < 1 || c.cg_max_iter > 64))
+        throw Error(kInvalidArgument, "SolverConfig: cg_max_iter must be in [1, 64]");
 }
 
 // TPB_TIMING=1: device-synchronised phase timings on stderr (setup overheads)
@@ -119,6 +123,10 @@ Solver::Solver(int n, int B, bool het, const std::vector<int>& r, const std::vec
             r_host_[b] = r[b];
         }
     }
+    if (cfg.linear_solver == 1 && het_)
+        throw Error(kInvalidArgument,
+                    "SolverConfig: the CG x-step covers the homogeneous system; the node-level "
+                    "system (stiff 1e8 coupling) uses the closed form");
     c_ = make_xconst(n, cfg.alpha, cfg.rho);
     small_ = n <= 64;
     // Tiled projections: int8 tensor-core (Ozaki) GEMMs by default, FP64 DMMA
@@ -215,6 +223,17 @@ void Solver::alloc() {
     d_.frob_part = dalloc<double>(s0_, allocs_,(size_t)B * 2 * d_.ntile);
     d_.inv_scale = dalloc<double>(s0_, allocs_,(size_t)B * 2);
     d_.h = dalloc<double>(s0_, allocs_,B * m);
+    if (cfg_.linear_solver == 1) {
+        d_.cg = 1;
+        d_.cg_max = cfg_.cg_max_iter;
+        d_.cg_tol2 = cfg_.linear_tol * cfg_.linear_tol;
+        d_.cg_x = dalloc<double>(s0_, allocs_, B * m);
+        d_.cg_p = dalloc<double>(s0_, allocs_, B * m);
+        d_.cg_pq = dalloc<double>(s0_, allocs_, (size_t)B * d_.ntile);
+        d_.cg_rr = dalloc<double>(s0_, allocs_, (size_t)B * 2 * d_.ntile);
+        d_.cg_nr = dalloc<double>(s0_, allocs_, (size_t)B * d_.nb * n);
+        d_.cg_u = dalloc<double>(s0_, allocs_, (size_t)B * 2 * n);
+    }
     d_.PU = dalloc<double>(s0_, allocs_,(size_t)B * d_.nb * n);
     d_.PZ = dalloc<double>(s0_, allocs_,(size_t)B * d_.nb * n);
     d_.PG = dalloc<double>(s0_, allocs_,(size_t)B * d_.nb * n);
@@ -489,12 +508,30 @@ void Solver::enqueue_iteration(bool with_slem) {
     }
     enqueue_projection();
     TPB_CUDA(cudaStreamWaitEvent(s0_, ev_sel_, 0));
-    launch_xstep_a(d_, c_, s0_);
-    launch_xstep_node(d_, c_, s0_);
-    launch_xstep_b(d_, c_, s0_);
+    enqueue_xstep(d_);
     if (with_slem) TPB_CUDA(cudaStreamWaitEvent(s0_, ev_slem_, 0));
     launch_xstep_diag(d_, c_, s0_);
     launch_best_copy(d_, c_, s0_);
+}
+
+void Solver::enqueue_xstep(const Dev& d) {
+    launch_xstep_a(d, c_, s0_);
+    launch_xstep_node(d, c_, s0_);
+    if (d.cg) launch_xstep_cg(d, c_, s0_);
+    launch_xstep_b(d, c_, s0_);
+}
+
+void Solver::cg_stats(int b, int* iters, double* rel_res) {
+    if (b < 0 || b >= B_) throw Error(kInvalidArgument, "cg_stats: solve index out of range");
+    int it = 0;
+    double rr = 0.0;
+    TPB_CUDA(cudaStreamSynchronize(s0_));
+    if (d_.cg) {
+        TPB_CUDA(cudaMemcpy(&it, d_.ictl + b * 8 + kCgIters, sizeof(int), cudaMemcpyDeviceToHost));
+        TPB_CUDA(cudaMemcpy(&rr, d_.scal + b * 8 + kCgRes, sizeof(double), cudaMemcpyDeviceToHost));
+    }
+    *iters = it;
+    *rel_res = rr;
 }
 
 void Solver::build_graphs() {
@@ -799,18 +836,22 @@ void Solver::xstep_only(bool update_duals) {
     Dev d = d_;
     d.upd_duals = update_duals ? 1 : 0;
     d.track_best = 0;
-    launch_xstep_a(d, c_, s0_);
-    launch_xstep_node(d, c_, s0_);
-    launch_xstep_b(d, c_, s0_);
+    enqueue_xstep(d);
     launch_xstep_diag(d, c_, s0_);
     TPB_CUDA(cudaStreamSynchronize(s0_));
-    TPB_CUDA(cudaMemsetAsync(d_.ictl, 0, (size_t)B_ * 8 * sizeof(int), s0_));
+    // keep the CG statistics for cg_stats(); clear the iteration control words
+    std::vector<int> keep(B_ * 8, 0);
+    TPB_CUDA(cudaMemcpy(keep.data(), d_.ictl, keep.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    for (int b = 0; b < B_; ++b)
+        for (int w = 0; w < 8; ++w)
+            if (w != kCgIters) keep[b * 8 + w] = 0;
+    TPB_CUDA(cudaMemcpyAsync(d_.ictl, keep.data(), keep.size() * sizeof(int), cudaMemcpyHostToDevice, s0_));
     TPB_CUDA(cudaStreamSynchronize(s0_));
 }
 
 int Solver::launches_per_iteration() const {
     const int cone = small_ ? 1 : sch_.gemms();
-    return 1 + (small_ ? 0 : 1) + 1 + 1 + cone + 4 + 2;
+    return 1 + (small_ ? 0 : 1) + 1 + 1 + cone + 4 + 2 + (d_.cg ? 1 : 0);
 }
 
 int Solver::bench_phase(int phase, int reps) {
@@ -826,12 +867,19 @@ int Solver::bench_phase(int phase, int reps) {
                 // the O(n) dual update so the iteration counter is untouched
                 Dev d = d_;
                 d.track_best = 0;
-                launch_xstep_a(d, c_, s0_);
-                launch_xstep_node(d, c_, s0_);
-                launch_xstep_b(d, c_, s0_);
+                enqueue_xstep(d);
                 d.upd_duals = 0;
                 launch_xstep_diag(d, c_, s0_);
-                per = 4;
+                per = 4 + (d.cg ? 1 : 0);
+                break;
+            }
+            case 7: {
+                // pass A (fresh right-hand side h; CG keeps r in h) + the CG
+                // solve: subtract phase 5 for the CG alone
+                if (!d_.cg) throw Error(kInvalidArgument, "bench_phase 7: linear_solver is not CG");
+                launch_xstep_a(d_, c_, s0_);
+                launch_xstep_cg(d_, c_, s0_);
+                per = 2;
                 break;
             }
             case 5:

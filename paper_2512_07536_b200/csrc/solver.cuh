@@ -23,6 +23,8 @@ struct Config {
     int trace_stride = 1;       // acf_iterate every k-th iteration (reference: 1)
     double slem_tol = 1e-6;     // trace Lanczos residual tolerance (eigenvalue error <= tol^2/gap)
     int chunk = 0;              // iterations per CUDA graph (0: auto)
+    int linear_solver = 0;      // x-step: 0 closed form, 1 matrix-free CG (hom; tol = linear_tol)
+    int cg_max_iter = 8;        // CG iterations launched per x-step (early exit on convergence)
 };
 
 void validate(const Config& c);
@@ -94,12 +96,16 @@ class Solver {
     // 1 x-step, 2 top-r selection, 3 trace SLEM, 4 prep, 5 x-step pass A,
     // 6 x-step pass B. Returns the number
     // of kernel launches per repetition.
+    // 7: pass A + the CG solve of one x-step (linear_solver = 1).
     int bench_phase(int phase, int reps);
+    // CG statistics of the last x-step of solve b: iterations, |r|/|h|
+    void cg_stats(int b, int* iters, double* rel_res);
     int launches_per_iteration() const;
 
    private:
     void alloc();
     void enqueue_iteration(bool with_slem);
+    void enqueue_xstep(const Dev& d);  // pass A, node, [CG], pass B
     void enqueue_projection();
     void enqueue_select(cudaStream_t st);
     void enqueue_slem_trace(cudaStream_t st);

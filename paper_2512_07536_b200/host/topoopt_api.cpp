@@ -44,6 +44,7 @@ tp_config to_c(const SolverConfig& c) {
     k.weight_floor = c.weight_floor;
     k.seed = c.seed;
     k.linear_tol = c.linear_tol;
+    k.linear_solver = c.linear_solver;
     return k;
 }
 
@@ -896,6 +897,18 @@ Vec update_X(const ProblemData& pd, const Vec& y, const Vec& d, Vec& kkt_warm, d
         throw std::invalid_argument("update_X: state length differs from nx");
     kkt_warm.resize(pd.nx + pd.neq);
     raise(tp_update_X(pd.n, pd.r, pd.alpha, pd.rho, y.data(), d.data(), kkt_warm.data()));
+    return Vec(kkt_warm.begin(), kkt_warm.begin() + pd.nx);
+}
+
+Vec update_X_cg(const ProblemData& pd, const Vec& y, const Vec& d, Vec& kkt_warm, double linear_tol,
+                int* cg_iters) {
+    if ((int)y.size() != pd.nx || (int)d.size() != pd.nx)
+        throw std::invalid_argument("update_X: state length differs from nx");
+    kkt_warm.resize(pd.nx + pd.neq);
+    int32_t it = 0;
+    raise(tp_update_X_cg(pd.n, pd.r, pd.alpha, pd.rho, y.data(), d.data(), linear_tol, 8, kkt_warm.data(),
+                         &it, nullptr));
+    if (cg_iters) *cg_iters = it;
     return Vec(kkt_warm.begin(), kkt_warm.begin() + pd.nx);
 }
 

@@ -85,11 +85,14 @@ class SolverConfig:
     linear_tol: float = 1e-10
     trace_stride: int = 1
     chunk: int = 0
+    linear_solver: int = 0  # 0 closed-form x-step, 1 matrix-free CG to linear_tol (hom)
+    cg_max_iter: int = 8
 
     def to_c(self) -> tp_config:
         return tp_config(self.rho, self.epsilon, int(self.max_iter), self.alpha,
                          self.weight_floor, int(self.seed), self.linear_tol,
-                         int(self.trace_stride), int(self.chunk))
+                         int(self.trace_stride), int(self.chunk), int(self.linear_solver),
+                         int(self.cg_max_iter))
 
     def validate(self):
         c = self.to_c()
@@ -566,6 +569,20 @@ def update_X(n, r, y, d, alpha=2.0, rho=1.0) -> tuple[np.ndarray, np.ndarray]:
     return kkt[: lo.nx].copy(), kkt
 
 
+def update_X_cg(n, r, y, d, alpha=2.0, rho=1.0, linear_tol=1e-10, cg_max_iter=8):
+    """update_X with the CG linear substep (proj/src/admm.cpp:279-293, with
+    linear_tol as in the reference signature) -> (x, kkt, cg_iters, rel_res).
+    Raises LinearSolveError above 1e-8 relative residual (admm.cpp:287)."""
+    lo = hom_layout(n)
+    y, d = _f64(y), _f64(d)
+    kkt = np.zeros(lo.nx + lo.neq)
+    it = C.c_int32(0)
+    rr = C.c_double(0.0)
+    _check(_lib.load().tp_update_X_cg(n, r, alpha, rho, _dp(y), _dp(d), float(linear_tol),
+                                      int(cg_max_iter), _dp(kkt), C.byref(it), C.byref(rr)))
+    return kkt[: lo.nx].copy(), kkt, it.value, rr.value
+
+
 def update_X_het(degrees, y, d, alpha=2.0, rho=1.0) -> tuple[np.ndarray, np.ndarray]:
     deg = _i32(degrees)
     n = len(deg)
@@ -669,6 +686,13 @@ class BatchSolver:
         x, y, d = C.c_void_p(), C.c_void_p(), C.c_void_p()
         _check(_lib.load().tp_solver_state(self.h, C.byref(x), C.byref(y), C.byref(d)))
         return x.value, y.value, d.value
+
+    def cg_stats(self, b: int = 0) -> tuple[int, float]:
+        """CG x-step statistics of solve b's last iteration: (iterations, |r|/|h|)."""
+        it = C.c_int32(0)
+        rr = C.c_double(0.0)
+        _check(_lib.load().tp_solver_cg_stats(self.h, b, C.byref(it), C.byref(rr)))
+        return it.value, rr.value
 
     def bench_phase(self, phase: int, reps: int) -> int:
         per = C.c_int32(0)
