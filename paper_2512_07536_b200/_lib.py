@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtopoopt_b200.so")
+# TPB_LIB: alternative build of the same library (experiments only)
+LIB_PATH = os.environ.get("TPB_LIB") or os.path.join(HERE, "libtopoopt_b200.so")
 
 TP_OK = 0
 TP_ERR_INVALID_ARGUMENT = 1

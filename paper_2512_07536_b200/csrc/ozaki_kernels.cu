@@ -26,20 +26,24 @@
 
 namespace tpb {
 
+#ifndef OZ_EPI_WARPS
+#define OZ_EPI_WARPS 16
+#endif
+
 namespace {
 
 constexpr int KS = kOzSlices, BM = kOzBM;
-constexpr int EPI_WARPS = 8, EPI_THREADS = 32 * EPI_WARPS;
-constexpr int THREADS = 64 + EPI_THREADS;  // producer warp, MMA warp, epilogue warps
 
 // Tile configuration: BN output columns (one accumulator group = BN TMEM
 // columns, KS groups), BK k-bytes per pipeline stage. <64, 64>: one CTA per
 // SM, 512 TMEM columns; <32, 32>: 256 TMEM columns and 98 KB of shared
 // memory, so two CTAs share an SM and one's epilogue overlaps the other's
 // main loop (batched small-n products, where the epilogue dominates).
-template <int BN_, int BK_>
+template <int BN_, int BK_, int EW_>
 struct Tile {
     static constexpr int BN = BN_, BK = BK_;
+    // producer warp, MMA warp, EW epilogue warps (EW / 4 per TMEM lane quarter)
+    static constexpr int EPI_WARPS = EW_, EPI_THREADS = 32 * EW_, THREADS = 64 + 32 * EW_;
     static constexpr int R = BM / BN;          // tiles per 128-row diagonal block
     static constexpr int STAGES = 2;
     static constexpr int A_PLANE = BM * BK, B_PLANE = BN * BK;  // bytes
@@ -53,7 +57,7 @@ struct Tile {
     static constexpr int EPI_BYTES = CS_BYTES + DIG_BYTES;
     static constexpr int SMEM_BYTES =
         (STAGES * STAGE_BYTES > EPI_BYTES ? STAGES * STAGE_BYTES : EPI_BYTES) + 1024;
-    static constexpr int HN = BN / 2;          // tile columns per epilogue thread
+    static constexpr int HN = BN / (EW_ / 4);  // tile columns per epilogue thread
     static constexpr int TMEM_COLS = KS * BN <= 256 ? 256 : 512;
     static constexpr int TCHUNK = 256 / BN;    // B planes per MMA (N <= 256)
     static constexpr int MIN_BLOCKS = 2 * (SMEM_BYTES + 1024) <= 228 * 1024 ? 2 : 1;
@@ -62,8 +66,8 @@ struct Tile {
     static_assert(BK == 32 || BK == 64, "k block is one or two MMA k-steps");
     static_assert(HN % 16 == 0, "TMEM loads of 16 columns");
 };
-using TileL = Tile<64, 64>;
-using TileS = Tile<32, 32>;
+using TileL = Tile<64, 64, OZ_EPI_WARPS>;
+using TileS = Tile<32, 32, 8>;
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -140,6 +144,13 @@ __device__ __forceinline__ uint64_t op_desc(uint32_t addr) {
 // instruction descriptor: s8 x s8 -> s32, K-major A and B, M = 128, N = nn
 __host__ __device__ constexpr uint32_t idesc_n(int nn) {
     return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(nn >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+// Exact int32 -> FP64 without the quarter-rate conversion pipe: the bits
+// 0x43300000:(x ^ 2^31) are the double 2^52 + 2^31 + x; one DADD removes the
+// offset (exact). Same value as (double)(int)x.
+__device__ __forceinline__ double i32_to_f64(uint32_t x) {
+    return __hiloint2double(0x43300000, (int)(x ^ 0x80000000u)) - 4503601774854144.0;
 }
 
 __device__ __forceinline__ long long gtimer() {
@@ -238,10 +249,11 @@ __device__ inline void oz_tile(int R, int t, int& I, int& J) {
 }  // namespace
 
 template <typename TL>
-__global__ void __launch_bounds__(THREADS, TL::MIN_BLOCKS)
+__global__ void __launch_bounds__(TL::THREADS, TL::MIN_BLOCKS)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                    const __grid_constant__ CUtensorMap mapC, OzGemm g) {
     constexpr int BN = TL::BN, BK = TL::BK, STAGES = TL::STAGES, R = TL::R, HN = TL::HN, CP = TL::CP;
+    constexpr int EPI_WARPS = TL::EPI_WARPS, EPI_THREADS = TL::EPI_THREADS;
     constexpr int BB = TL::BB, NBOX = TL::NBOX;
     constexpr int A_PLANE = TL::A_PLANE, B_PLANE = TL::B_PLANE, STAGE_BYTES = TL::STAGE_BYTES;
     constexpr int TMEM_COLS = TL::TMEM_COLS;
@@ -350,7 +362,7 @@ __global__ void __launch_bounds__(THREADS, TL::MIN_BLOCKS)
         // ---------------- epilogue: warps 2..9; thread <-> (tile row = TMEM
         // lane of its warp's quarter, one half of the tile's columns)
         const int q = warp & 3;                 // TMEM lane quarter this warp may access
-        const int h = (warp - 2) >> 2;          // column half
+        const int h = (warp - 2) >> 2;          // column slice
         const int r = q * 32 + lane;            // tile row
         const int c0 = h * HN;                  // first tile column of this thread
         const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
@@ -376,7 +388,7 @@ __global__ void __launch_bounds__(THREADS, TL::MIN_BLOCKS)
             for (int q2 = 0; q2 < 2; ++q2) {
                 const double sc = ldexp(1.0, -7 * (d - q2));
 #pragma unroll
-                for (int j = 0; j < HN; ++j) acc[j] = fma((double)(int)v[q2][j], sc, acc[j]);
+                for (int j = 0; j < HN; ++j) acc[j] = fma(i32_to_f64(v[q2][j]), sc, acc[j]);
             }
         }
         const long long t_acc = g.dbg_t ? gtimer() : 0;
@@ -437,7 +449,48 @@ __global__ void __launch_bounds__(THREADS, TL::MIN_BLOCKS)
             }
         }
         const long long t_cst = g.dbg_t ? gtimer() : 0;
-        if (g.Cd) {
+        if (g.Cd && g.dstore) {
+            // digit planes straight from registers to global memory: 16-byte
+            // stores, four (direct) / eight (mirror) adjacent threads per
+            // plane row segment, so every warp store fills whole sectors and
+            // the writes stream out while the rest of the tile is split
+            const double s28 = ldexp(1.0, 28 - g.eC);
+            int8_t* base = g.Cd + (long long)mat * KS * ld * ld;
+            const long long pstride = (long long)ld * ld;
+            constexpr int DC = BN / 16, MC = BM / 16;
+            for (int it = et; it < BM * DC; it += EPI_THREADS) {  // direct: tile row rr, chunk cc
+                const int cc = it % DC, rr = it / DC;
+                if (rr < dr0) continue;
+                uint32_t w[4][KS];
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) {
+                    double v4[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) v4[k] = Cs[(16 * cc + 4 * q4 + k) * CP + rr];
+                    digits4(v4, s28, w[q4]);
+                }
+                int8_t* dst = base + (long long)(i0 + rr) * ld + j0 + 16 * cc;
+#pragma unroll
+                for (int s2 = 0; s2 < KS; ++s2)
+                    *reinterpret_cast<uint4*>(dst + s2 * pstride) = make_uint4(w[0][s2], w[1][s2], w[2][s2], w[3][s2]);
+            }
+            for (int it = et; it < BN * MC; it += EPI_THREADS) {  // mirror: tile column j, chunk rc
+                const int rc = it % MC, j = it / MC;
+                if (16 * rc < mr0) continue;
+                uint32_t w[4][KS];
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) {
+                    double v4[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) v4[k] = Cs[j * CP + 16 * rc + 4 * q4 + k];
+                    digits4(v4, s28, w[q4]);
+                }
+                int8_t* dst = base + (long long)(j0 + j) * ld + i0 + 16 * rc;
+#pragma unroll
+                for (int s2 = 0; s2 < KS; ++s2)
+                    *reinterpret_cast<uint4*>(dst + s2 * pstride) = make_uint4(w[0][s2], w[1][s2], w[2][s2], w[3][s2]);
+            }
+        } else if (g.Cd) {
             // digit planes staged in the TMA-store layout: direct boxes
             // [s][h] (tile rows BB h.., the BN columns) and mirror boxes [s][h]
             // (the BN tile columns as rows, tile rows BB h.. as bytes)
@@ -619,12 +672,25 @@ void init_attrs_ozaki() {
                                   TileS::SMEM_BYTES));
 }
 
-void launch_oz_gemm(const OzGemm& g, cudaStream_t st) {
+// Digit-plane output path: direct 16-byte global stores (default; the
+// writes stream out during the split, -1 us per GEMM at n=1024) or, with
+// TPB_OZ_DSTORE=0, TMA bulk stores of swizzled boxes staged in shared memory.
+int dstore_mode() {
+    static const int m = [] {
+        const char* e = std::getenv("TPB_OZ_DSTORE");
+        return e ? std::atoi(e) : 1;
+    }();
+    return m;
+}
+
+void launch_oz_gemm(const OzGemm& g0, cudaStream_t st) {
+    OzGemm g = g0;
+    g.dstore = dstore_mode();
     if (g.Cd && !g.mc) throw Error(kInvalidArgument, "ozaki GEMM: digit output needs its TMA map");
     const bool small = use_small_tiles(g.ld, g.nmat);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(small ? tiles_before(TileS::R, g.ld / BM) : oz_gemm_tiles(g.ld), g.nmat);
-    cfg.blockDim = dim3(THREADS);
+    cfg.blockDim = dim3(small ? TileS::THREADS : TileL::THREADS);
     cfg.dynamicSmemBytes = small ? TileS::SMEM_BYTES : TileL::SMEM_BYTES;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];

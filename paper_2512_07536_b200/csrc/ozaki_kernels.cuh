@@ -60,6 +60,7 @@ struct OzGemm {
     long long* dbg_t;        // instrumentation: 4 globaltimer stamps per CTA, or null
     int dbg_mode;            // instrumentation: bit 0 skips the MMAs, bit 1 the TMA loads
     int no_pdl;              // launch without programmatic dependent launch
+    int dstore;              // digit planes by direct 16-byte global stores (else TMA stores)
 };
 
 void launch_oz_gemm(const OzGemm& g, cudaStream_t st);
