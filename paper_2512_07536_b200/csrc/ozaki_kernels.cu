@@ -223,6 +223,20 @@ __device__ __forceinline__ void digits4(const double (&v)[4], double s28, uint32
     w[7] = __byte_perm(g, h, 0x5410);
 }
 
+// Row slot of the FP64 staging tile: conflict-free both for 32 consecutive
+// rows (TMEM drain) and for rows 4 rb + q, rb = 0..31 (4 x 4 digit blocks).
+__device__ __forceinline__ int csr(int r) { return r ^ ((r >> 4) & 3); }
+
+// 4 x 4 byte transpose: rows r[q] (byte c = column c) -> columns o[c] (byte q = row q)
+__device__ __forceinline__ void transpose4x4(const uint32_t (&r)[4], uint32_t (&o)[4]) {
+    const uint32_t t0 = __byte_perm(r[0], r[1], 0x5140), t1 = __byte_perm(r[0], r[1], 0x7362);
+    const uint32_t t2 = __byte_perm(r[2], r[3], 0x5140), t3 = __byte_perm(r[2], r[3], 0x7362);
+    o[0] = __byte_perm(t0, t2, 0x5410);
+    o[1] = __byte_perm(t0, t2, 0x7632);
+    o[2] = __byte_perm(t1, t3, 0x5410);
+    o[3] = __byte_perm(t1, t3, 0x7632);
+}
+
 // 16-byte chunk address inside a BB x BB-byte box in the SWIZZLE_{BB}B layout
 template <int BB>
 __device__ __forceinline__ uint32_t box_off(int row, int chunk) {
@@ -416,9 +430,9 @@ __global__ void __launch_bounds__(TL::THREADS, TL::MIN_BLOCKS)
         const int nv = g.nvalid;
         double* C = g.C ? g.C + (long long)(mat >> 1) * g.c_stride_b + (long long)(mat & 1) * g.c_stride_w
                         : nullptr;
-        double* Cs = reinterpret_cast<double*>(sgen);  // [BN][CP]: Cs[c][r] = tile (r, c)
+        double* Cs = reinterpret_cast<double*>(sgen);  // [BN][CP]: Cs[c][csr(r)] = tile (r, c)
 #pragma unroll
-        for (int j = 0; j < HN; ++j) Cs[(c0 + j) * CP + r] = acc[j];
+        for (int j = 0; j < HN; ++j) Cs[(c0 + j) * CP + csr(r)] = acc[j];
         asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");
         const int et = threadIdx.x - 64;        // 0 .. EPI_THREADS-1
         const int ew = et >> 5;                 // epilogue warp 0..7
@@ -427,7 +441,7 @@ __global__ void __launch_bounds__(TL::THREADS, TL::MIN_BLOCKS)
             // symmetrise the diagonal BN x BN sub-block (tile rows dr0.., all columns)
             for (int idx = et; idx < BN * BN; idx += EPI_THREADS) {
                 const int u = idx / BN, v = idx % BN;  // sub-block row, column
-                if (u < v) Cs[v * CP + dr0 + u] = Cs[u * CP + dr0 + v];
+                if (u < v) Cs[v * CP + csr(dr0 + u)] = Cs[u * CP + csr(dr0 + v)];
             }
             asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");
         }
@@ -437,59 +451,85 @@ __global__ void __launch_bounds__(TL::THREADS, TL::MIN_BLOCKS)
 #pragma unroll
                 for (int j = lane; j < BN; j += 32) {
                     const int jj = j0 + j;
-                    if (ii < nv && jj < nv) C[(long long)ii * g.ldc + jj] = Cs[j * CP + rr];
+                    if (ii < nv && jj < nv) C[(long long)ii * g.ldc + jj] = Cs[j * CP + csr(rr)];
                 }
             }
             for (int j = ew; j < BN; j += EPI_WARPS) {
                 const int jj = j0 + j;
                 for (int rr = mr0 + lane; rr < BM; rr += 32) {
                     const int ii = i0 + rr;
-                    if (ii < nv && jj < nv) C[(long long)jj * g.ldc + ii] = Cs[j * CP + rr];
+                    if (ii < nv && jj < nv) C[(long long)jj * g.ldc + ii] = Cs[j * CP + csr(rr)];
                 }
             }
         }
         const long long t_cst = g.dbg_t ? gtimer() : 0;
         if (g.Cd && g.dstore) {
-            // digit planes straight from registers to global memory: 16-byte
-            // stores, four (direct) / eight (mirror) adjacent threads per
-            // plane row segment, so every warp store fills whole sectors and
-            // the writes stream out while the rest of the tile is split
+            // Each thread splits one 4 x 4 block (rows 4 rb.., columns 4 cb..)
+            // into digits once. Mirror rows: a 4 x 4 byte transpose per plane
+            // and 4-byte stores, 32 lanes = 128 contiguous bytes of a plane
+            // row. Direct rows: words staged in shared memory (XOR-swizzled),
+            // then 16-byte stores, four lanes per 64-byte row segment.
+            constexpr int NCB = BN / 4;              // column blocks
             const double s28 = ldexp(1.0, 28 - g.eC);
             int8_t* base = g.Cd + (long long)mat * KS * ld * ld;
             const long long pstride = (long long)ld * ld;
-            constexpr int DC = BN / 16, MC = BM / 16;
-            for (int it = et; it < BM * DC; it += EPI_THREADS) {  // direct: tile row rr, chunk cc
-                const int cc = it % DC, rr = it / DC;
-                if (rr < dr0) continue;
+            uint32_t* Dg = reinterpret_cast<uint32_t*>(sgen + TL::CS_BYTES);  // [KS][BM][NCB]
+            uint32_t sink = 0;
+            const bool nost = (g.dbg_mode & 4) != 0;  // instrumentation: split without the stores
+            for (int blk = et; blk < 32 * NCB; blk += EPI_THREADS) {
+                const int rb = blk & 31, cb = blk >> 5;
+                const int r0 = 4 * rb;
+                if (r0 < dr0 && r0 < mr0) continue;
                 uint32_t w[4][KS];
 #pragma unroll
-                for (int q4 = 0; q4 < 4; ++q4) {
+                for (int q = 0; q < 4; ++q) {
                     double v4[4];
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) v4[k] = Cs[(16 * cc + 4 * q4 + k) * CP + rr];
-                    digits4(v4, s28, w[q4]);
+                    for (int c = 0; c < 4; ++c) v4[c] = Cs[(4 * cb + c) * CP + csr(r0 + q)];
+#pragma unroll
+                    for (int s2 = 0; s2 < KS; ++s2) w[q][s2] = 0u;
+                    digits4(v4, s28, w[q]);
                 }
-                int8_t* dst = base + (long long)(i0 + rr) * ld + j0 + 16 * cc;
+                if (r0 >= dr0) {
+                    const int sw = cb ^ (rb & (NCB - 1));
 #pragma unroll
-                for (int s2 = 0; s2 < KS; ++s2)
-                    *reinterpret_cast<uint4*>(dst + s2 * pstride) = make_uint4(w[0][s2], w[1][s2], w[2][s2], w[3][s2]);
-            }
-            for (int it = et; it < BN * MC; it += EPI_THREADS) {  // mirror: tile column j, chunk rc
-                const int rc = it % MC, j = it / MC;
-                if (16 * rc < mr0) continue;
-                uint32_t w[4][KS];
+                    for (int s2 = 0; s2 < KS; ++s2)
 #pragma unroll
-                for (int q4 = 0; q4 < 4; ++q4) {
-                    double v4[4];
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) v4[k] = Cs[j * CP + 16 * rc + 4 * q4 + k];
-                    digits4(v4, s28, w[q4]);
+                        for (int q = 0; q < 4; ++q) Dg[(s2 * BM + r0 + q) * NCB + sw] = w[q][s2];
                 }
-                int8_t* dst = base + (long long)(j0 + j) * ld + i0 + 16 * rc;
+                if (r0 >= mr0) {
+                    // plane-0 address of mirror row j0 + 4 cb, bytes i0 + r0..
+                    int8_t* mp = base + (long long)(j0 + 4 * cb) * ld + i0 + r0;
 #pragma unroll
-                for (int s2 = 0; s2 < KS; ++s2)
-                    *reinterpret_cast<uint4*>(dst + s2 * pstride) = make_uint4(w[0][s2], w[1][s2], w[2][s2], w[3][s2]);
+                    for (int s2 = 0; s2 < KS; ++s2, mp += pstride) {
+                        const uint32_t rows[4] = {w[0][s2], w[1][s2], w[2][s2], w[3][s2]};
+                        uint32_t cols[4];
+                        transpose4x4(rows, cols);
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            if (nost) { sink ^= cols[c]; continue; }
+                            *reinterpret_cast<uint32_t*>(mp + c * ld) = cols[c];
+                        }
+                    }
+                }
             }
+            asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");
+            constexpr int NC4 = BN / 16;             // 16-byte chunks per row segment
+            static_assert(EPI_THREADS % NC4 == 0, "read-back mapping");
+            for (int rr = dr0 + et / NC4; rr < BM; rr += EPI_THREADS / NC4) {
+                const int c4 = et % NC4;
+                const int f = (rr >> 2) & (NCB - 1);
+                const int k0 = (4 * c4) ^ f, k1 = (4 * c4 + 1) ^ f, k2 = (4 * c4 + 2) ^ f, k3 = (4 * c4 + 3) ^ f;
+                const uint32_t* src = Dg + rr * NCB;
+                int8_t* dp = base + (long long)(i0 + rr) * ld + j0 + 16 * c4;
+#pragma unroll
+                for (int s2 = 0; s2 < KS; ++s2, src += BM * NCB, dp += pstride) {
+                    const uint4 v = make_uint4(src[k0], src[k1], src[k2], src[k3]);
+                    if (nost) { sink ^= v.x ^ v.y ^ v.z ^ v.w; continue; }
+                    *reinterpret_cast<uint4*>(dp) = v;
+                }
+            }
+            if (nost && sink == 0x9E3779B9u) base[0] = 1;  // keep the split live
         } else if (g.Cd) {
             // digit planes staged in the TMA-store layout: direct boxes
             // [s][h] (tile rows BB h.., the BN columns) and mirror boxes [s][h]
@@ -505,7 +545,7 @@ __global__ void __launch_bounds__(TL::THREADS, TL::MIN_BLOCKS)
                 for (int q4 = 0; q4 < 4; ++q4) {
                     double v4[4];
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) v4[k] = Cs[(16 * cc + 4 * q4 + k) * CP + rr];
+                    for (int k = 0; k < 4; ++k) v4[k] = Cs[(16 * cc + 4 * q4 + k) * CP + csr(rr)];
                     digits4(v4, s28, w[q4]);
                 }
                 const int h2 = rr / BB, rb = rr % BB;
@@ -524,7 +564,7 @@ __global__ void __launch_bounds__(TL::THREADS, TL::MIN_BLOCKS)
                 for (int q4 = 0; q4 < 4; ++q4) {
                     double v4[4];
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) v4[k] = Cs[j * CP + 16 * rc + 4 * q4 + k];
+                    for (int k = 0; k < 4; ++k) v4[k] = Cs[j * CP + csr(16 * rc + 4 * q4 + k)];
                     digits4(v4, s28, w[q4]);
                 }
                 const int h2 = (16 * rc) / BB, cb = ((16 * rc) % BB) / 16;
