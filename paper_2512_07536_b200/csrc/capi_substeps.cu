@@ -605,6 +605,9 @@ int tp_oz_gemm_dbg(int32_t ld, int32_t nmat, const double* a, int32_t ea, const 
         g.dbg_t = nullptr;
         C.down(c, sz);
         if (cd) Cd.down(cd, sz * kOzSlices);
+        // timed repetitions: with a digit output requested, digits only (the
+        // cone iteration's intermediate products); else the FP64 output
+        if (cd) g.C = nullptr;
         if (reps > 0) {
             cudaEvent_t e0, e1;
             TPB_CUDA(cudaEventCreate(&e0));

@@ -128,6 +128,12 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&v)[16]) {
           "=r"(v[14]), "=r"(v[15])
         : "r"(addr));
 }
+__device__ __forceinline__ void tmem_ld8(uint32_t addr, uint32_t (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                   "=r"(v[7])
+                 : "r"(addr));
+}
 __device__ __forceinline__ void tmem_wait_ld() {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -611,6 +617,293 @@ __global__ void __launch_bounds__(TL::THREADS, TL::MIN_BLOCKS)
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Persistent variant (default): one CTA per SM walks 128 x 32 lower tiles of
+// all matrices; TMEM holds two accumulator sets (2 x 8 groups x 32 columns),
+// so the MMAs of the next tile run while the epilogue warps split and store
+// the previous one. Per-element arithmetic is that of oz_gemm_kernel (same
+// group order and FP64 operations): the outputs are bitwise identical.
+namespace {
+struct PT {
+    static constexpr int BN = 32, BK = 64, STAGES = 2, R = BM / BN;
+    // 8 epilogue warps: 320 threads x 96 registers leave room on the SM for a
+    // concurrent trace-SLEM CTA (256 threads x 64 registers, 22 KB)
+    static constexpr int EPI_WARPS = 8, EPI_THREADS = 32 * EPI_WARPS, THREADS = 64 + EPI_THREADS;
+    static constexpr int HN = BN / (EPI_WARPS / 4);  // 16 columns per epilogue thread
+    static constexpr int A_PLANE = BM * BK, B_PLANE = BN * BK;
+    static constexpr int STAGE_BYTES = KS * (A_PLANE + B_PLANE);
+    static constexpr int CP = BM + 1;
+    static constexpr int CS_OFF = STAGES * STAGE_BYTES;            // FP64 staging [BN][CP]
+    // digit words [KS][BM][BN/4] reuse the FP64 staging area once every
+    // thread holds its 4 x 4 block in registers: 194 KB per CTA leaves room
+    // on the SM for the trace-SLEM CTAs of the concurrent stream
+    static constexpr int DG_OFF = CS_OFF;
+    static_assert(KS * BM * (BN / 4) * 4 <= BN * CP * 8, "digit staging fits the FP64 staging");
+    static constexpr int SMEM_BYTES = CS_OFF + BN * CP * 8 + 1024;
+    static constexpr int ACC_COLS = KS * BN;                        // one accumulator set
+    static_assert(2 * ACC_COLS <= 512, "two accumulator sets in TMEM");
+    static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
+};
+}  // namespace
+
+// <= 152 registers: 320 x 152 + a trace-SLEM CTA (256 x 64) fit one SM's 64 K
+__global__ void __maxnreg__(152)
+    oz_gemm_pkernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                    OzGemm g, int tiles_per_mat) {
+    constexpr int BN = PT::BN, BK = PT::BK, STAGES = PT::STAGES, R = PT::R, HN = PT::HN, CP = PT::CP;
+    constexpr int EPI_THREADS = PT::EPI_THREADS, EPI_WARPS = PT::EPI_WARPS;
+    constexpr int A_PLANE = PT::A_PLANE, B_PLANE = PT::B_PLANE, STAGE_BYTES = PT::STAGE_BYTES;
+    const int ld = g.ld;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nitems = tiles_per_mat * g.nmat;
+
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ __align__(8) uint64_t bars[2 * STAGES + 4];
+    __shared__ uint32_t tmem_slot;
+    const uint32_t sbase = (su32(smem_raw) + 1023u) & ~1023u;
+    uint8_t* sgen = smem_raw + (sbase - su32(smem_raw));
+    auto full_bar = [&](int s) { return su32(&bars[s]); };
+    auto empty_bar = [&](int s) { return su32(&bars[STAGES + s]); };
+    auto tfull_bar = [&](int b) { return su32(&bars[2 * STAGES + b]); };
+    auto tempty_bar = [&](int b) { return su32(&bars[2 * STAGES + 2 + b]); };
+    auto a_tile = [&](int st, int s) { return sbase + st * STAGE_BYTES + s * A_PLANE; };
+    auto b_tile = [&](int st, int s) { return sbase + st * STAGE_BYTES + KS * A_PLANE + s * B_PLANE; };
+    auto skip = [&](int mat) { return g.ictl && g.ictl[(mat >> 1) * 8 + 1]; };
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(full_bar(s), 1);
+            mbar_init(empty_bar(s), 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(tfull_bar(b), 1);
+            mbar_init(tempty_bar(b), EPI_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const uint32_t tmem = tmem_slot;
+    const int KB = ld / BK;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int c = 0;
+            for (int w = blockIdx.x; w < nitems; w += gridDim.x) {
+                const int mat = w / tiles_per_mat;
+                if (skip(mat)) continue;
+                int I, J;
+                oz_tile(R, w - mat * tiles_per_mat, I, J);
+                const long long plane_rows = (long long)mat * KS * ld;
+                for (int kb = 0; kb < KB; ++kb, ++c) {
+                    const int st = c % STAGES;
+                    mbar_wait(empty_bar(st), ((c / STAGES) & 1) ^ 1);
+                    mbar_expect_tx(full_bar(st), STAGE_BYTES);
+#pragma unroll 1
+                    for (int s = 0; s < KS; ++s) {
+                        tma_load_2d(a_tile(st, s), &mapA, full_bar(st), kb * BK,
+                                    (int)(plane_rows + (long long)s * ld + I * BM));
+                        tma_load_2d(b_tile(st, s), &mapB, full_bar(st), kb * BK,
+                                    (int)(plane_rows + (long long)s * ld + J * BN));
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            int c = 0, tc = 0;
+            for (int w = blockIdx.x; w < nitems; w += gridDim.x) {
+                if (skip(w / tiles_per_mat)) continue;
+                const int buf = tc & 1, use = tc >> 1;
+                mbar_wait(tempty_bar(buf), (use & 1) ^ 1);  // epilogue drained this set
+                tc_fence_after();
+                const uint32_t dbase = tmem + (uint32_t)(buf * PT::ACC_COLS);
+                for (int kb = 0; kb < KB; ++kb, ++c) {
+                    const int st = c % STAGES;
+                    mbar_wait(full_bar(st), (c / STAGES) & 1);
+                    tc_fence_after();
+#pragma unroll
+                    for (int kk = 0; kk < BK / 32; ++kk) {
+#pragma unroll
+                        for (int s = 1; s <= KS; ++s) {
+                            // A_s . [B_1 | ... | B_{KS+1-s}] in one MMA (N = 32 (KS+1-s))
+                            const uint64_t ad = op_desc<BK>(a_tile(st, s - 1) + kk * 32);
+                            const uint64_t bd = op_desc<BK>(b_tile(st, 0) + kk * 32);
+                            const uint32_t acc = (kb | kk) != 0 || s != 1;
+                            mma_i8(dbase + (uint32_t)((s - 1) * BN), ad, bd, idesc_n(BN * (KS + 1 - s)), acc);
+                        }
+                    }
+                    tc_commit(empty_bar(st));
+                }
+                tc_commit(tfull_bar(buf));
+                ++tc;
+            }
+        }
+    } else {
+        const int q = warp & 3;                 // TMEM lane quarter of this warp
+        const int h = (warp - 2) >> 2;          // column slice
+        const int r = q * 32 + lane;            // tile row
+        const int c0 = h * HN;
+        const int et = threadIdx.x - 64;
+        double* Cs = reinterpret_cast<double*>(sgen + PT::CS_OFF);
+        uint32_t* Dg = reinterpret_cast<uint32_t*>(sgen + PT::DG_OFF);
+        constexpr int NCB = BN / 4, NC4 = BN / 16;
+        int tc = 0;
+        for (int w = blockIdx.x; w < nitems; w += gridDim.x) {
+            const int mat = w / tiles_per_mat;
+            if (skip(mat)) continue;
+            int I, J;
+            oz_tile(R, w - mat * tiles_per_mat, I, J);
+            const int i0 = I * BM, j0 = J * BN;
+            const int buf = tc & 1, use = tc >> 1;
+            ++tc;
+            mbar_wait(tfull_bar(buf), use & 1);
+            tc_fence_after();
+            const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * PT::ACC_COLS + c0);
+            double acc[HN];
+#pragma unroll
+            for (int j = 0; j < HN; ++j) acc[j] = 0.0;
+            // group d = s + t sits at columns (d - 2) BN; smallest contributions first
+#pragma unroll
+            for (int d = KS + 1; d >= 2; d -= 2) {
+                uint32_t v[2][HN];
+#pragma unroll
+                for (int q2 = 0; q2 < 2; ++q2) {
+                    if constexpr (HN == 8) {
+                        tmem_ld8(taddr + (uint32_t)((d - q2 - 2) * BN), *reinterpret_cast<uint32_t(*)[8]>(v[q2]));
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < HN / 16; ++c)
+                            tmem_ld16(taddr + (uint32_t)((d - q2 - 2) * BN + c * 16),
+                                      *reinterpret_cast<uint32_t(*)[16]>(&v[q2][c * 16]));
+                    }
+                }
+                tmem_wait_ld();
+#pragma unroll
+                for (int q2 = 0; q2 < 2; ++q2) {
+                    const double sc = ldexp(1.0, -7 * (d - q2));
+#pragma unroll
+                    for (int j = 0; j < HN; ++j) acc[j] = fma(i32_to_f64(v[q2][j]), sc, acc[j]);
+                }
+            }
+            // this accumulator set is free for the tile after next
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty_bar(buf)) : "memory");
+            const double s = g.scale ? g.scale[mat] : 1.0;
+            double alpha = g.alpha_c * spow(s, g.pa) * ldexp(1.0, g.eA + g.eB);
+            const double beta = g.beta_c * spow(s, g.pb);
+            if (g.sign_mode && (mat & 1) == 0) alpha = -alpha;
+            const double* E = g.E ? g.E + (long long)mat * ld * ld : nullptr;
+            const int i = i0 + r;
+#pragma unroll
+            for (int j = 0; j < HN; ++j) {
+                double v = alpha * acc[j];
+                if (E) v = fma(beta, __ldg(E + (long long)(j0 + c0 + j) * ld + i), v);
+                if (i == j0 + c0 + j) v += g.dshift;
+                acc[j] = v;
+            }
+            const int tdiag = J - R * I;
+            const int dr0 = tdiag < 0 ? 0 : BN * tdiag;
+            const int mr0 = tdiag < 0 ? 0 : BN * (tdiag + 1);
+            // the previous tile's readers of Cs / Dg are done
+            asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");
+#pragma unroll
+            for (int j = 0; j < HN; ++j) Cs[(c0 + j) * CP + csr(r)] = acc[j];
+            asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");
+            if (tdiag >= 0) {
+                for (int idx = et; idx < BN * BN; idx += EPI_THREADS) {
+                    const int u = idx / BN, v = idx % BN;
+                    if (u < v) Cs[v * CP + csr(dr0 + u)] = Cs[u * CP + csr(dr0 + v)];
+                }
+                asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");
+            }
+            if (g.C) {
+                double* C = g.C + (long long)(mat >> 1) * g.c_stride_b + (long long)(mat & 1) * g.c_stride_w;
+                const int nv = g.nvalid, ew = et >> 5;
+                for (int rr = dr0 + ew; rr < BM; rr += EPI_WARPS) {
+                    const int ii = i0 + rr, jj = j0 + lane;
+                    if (lane < BN && ii < nv && jj < nv) C[(long long)ii * g.ldc + jj] = Cs[lane * CP + csr(rr)];
+                }
+                for (int j = ew; j < BN; j += EPI_WARPS) {
+                    const int jj = j0 + j;
+                    for (int rr = mr0 + lane; rr < BM; rr += 32) {
+                        const int ii = i0 + rr;
+                        if (ii < nv && jj < nv) C[(long long)jj * g.ldc + ii] = Cs[j * CP + csr(rr)];
+                    }
+                }
+            }
+            if (g.Cd) {
+                const double s28 = ldexp(1.0, 28 - g.eC);
+                int8_t* base = g.Cd + (long long)mat * KS * ld * ld;
+                const long long pstride = (long long)ld * ld;
+                static_assert(32 * NCB <= EPI_THREADS, "one 4 x 4 block per thread");
+                const int rb = et & 31, cb = et >> 5;
+                const int r0 = 4 * rb;
+                const bool active = et < 32 * NCB && (r0 >= dr0 || r0 >= mr0);
+                double bv[4][4];
+                if (active) {
+#pragma unroll
+                    for (int qq = 0; qq < 4; ++qq)
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) bv[qq][c] = Cs[(4 * cb + c) * CP + csr(r0 + qq)];
+                }
+                // every block is in registers: Dg may now overwrite Cs
+                asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");
+                if (active) {
+                    uint32_t wd[4][KS];
+#pragma unroll
+                    for (int qq = 0; qq < 4; ++qq) digits4(bv[qq], s28, wd[qq]);
+                    if (r0 >= dr0) {
+                        const int sw = cb ^ (rb & (NCB - 1));
+#pragma unroll
+                        for (int s2 = 0; s2 < KS; ++s2)
+#pragma unroll
+                            for (int qq = 0; qq < 4; ++qq) Dg[(s2 * BM + r0 + qq) * NCB + sw] = wd[qq][s2];
+                    }
+                    if (r0 >= mr0) {
+                        int8_t* mp = base + (long long)(j0 + 4 * cb) * ld + i0 + r0;
+#pragma unroll
+                        for (int s2 = 0; s2 < KS; ++s2, mp += pstride) {
+                            const uint32_t rows[4] = {wd[0][s2], wd[1][s2], wd[2][s2], wd[3][s2]};
+                            uint32_t cols[4];
+                            transpose4x4(rows, cols);
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) *reinterpret_cast<uint32_t*>(mp + c * ld) = cols[c];
+                        }
+                    }
+                }
+                asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");
+                for (int rr = dr0 + et / NC4; rr < BM; rr += EPI_THREADS / NC4) {
+                    const int c4 = et % NC4;
+                    const int f = (rr >> 2) & (NCB - 1);
+                    const int k0 = (4 * c4) ^ f, k1 = (4 * c4 + 1) ^ f, k2 = (4 * c4 + 2) ^ f, k3 = (4 * c4 + 3) ^ f;
+                    const uint32_t* src = Dg + rr * NCB;
+                    int8_t* dp = base + (long long)(i0 + rr) * ld + j0 + 16 * c4;
+#pragma unroll
+                    for (int s2 = 0; s2 < KS; ++s2, src += BM * NCB, dp += pstride)
+                        *reinterpret_cast<uint4*>(dp) = make_uint4(src[k0], src[k1], src[k2], src[k3]);
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    }
+}
+
 // Digit planes of s A, 4 consecutive row elements per thread.
 __global__ void oz_split_kernel(const double* A, long long mstride, int ld, const double* scale,
                                 int e, int8_t* planes, const int* ictl) {
@@ -682,6 +975,7 @@ void make_oz_maps(const int8_t* planes, int ld, int nmat, OzMaps* out) {
     encode(&out->a2, planes, ld, rows, TileS::BK, BM);
     encode(&out->b2, planes, ld, rows, TileS::BK, TileS::BN);
     encode(&out->st2, planes, ld, rows, TileS::BB, TileS::BB);
+    encode(&out->bp, planes, ld, rows, 64, 32);
 }
 
 int oz_gemm_tiles(int ld) { return tiles_before(TileL::R, ld / BM); }
@@ -710,7 +1004,30 @@ void init_attrs_ozaki() {
                                   TileL::SMEM_BYTES));
     TPB_CUDA(cudaFuncSetAttribute(oz_gemm_kernel<TileS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   TileS::SMEM_BYTES));
+    TPB_CUDA(cudaFuncSetAttribute(oz_gemm_pkernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  PT::SMEM_BYTES));
 }
+
+namespace {
+// Persistent 128 x 32 tiles with double-buffered TMEM (opt-in,
+// TPB_OZ_PERSIST=1: ld <= 512, 2: always). Isolated digits-only products at
+// ld <= 512 run faster (us: ld=256 x2 15.9 -> 11.0, x384 258.9 -> 226.5;
+// ld=512 x2 21.5 -> 15.3, x64 202.6 -> 185.9), but the config-5 sweep is
+// not: the resident grid keeps the concurrent trace-SLEM CTAs off the SMs
+// and the denser tensor load meets the power cap (7.5 vs 8.3 solves/s, 26.3
+// vs 25.5 ms per lockstep iteration of 192 het solves). At ld >= 1024 the
+// half-width tiles' second read of the A planes costs more than the overlap
+// saves (40.5 vs 35.0 us at n=1024).
+bool use_persistent(int ld, int) {
+    static const int mode = [] {
+        const char* e = std::getenv("TPB_OZ_PERSIST");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (mode == 0) return false;
+    if (mode == 2) return true;
+    return ld <= 512;
+}
+}  // namespace
 
 // Digit-plane output path: direct 16-byte global stores (default; the
 // writes stream out during the split, -1 us per GEMM at n=1024) or, with
@@ -727,6 +1044,21 @@ void launch_oz_gemm(const OzGemm& g0, cudaStream_t st) {
     OzGemm g = g0;
     g.dstore = dstore_mode();
     if (g.Cd && !g.mc) throw Error(kInvalidArgument, "ozaki GEMM: digit output needs its TMA map");
+    if (use_persistent(g.ld, g.nmat) && g.dstore && !g.dbg_t && !g.dbg_mode) {
+        const int tpm = tiles_before(PT::R, g.ld / BM);
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(std::min(tpm * g.nmat, sm_count()));
+        cfg.blockDim = dim3(PT::THREADS);
+        cfg.dynamicSmemBytes = PT::SMEM_BYTES;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = g.no_pdl ? 0 : 1;
+        TPB_CUDA(cudaLaunchKernelEx(&cfg, oz_gemm_pkernel, g.ma->a, g.mb->bp, g, tpm));
+        return;
+    }
     const bool small = use_small_tiles(g.ld, g.nmat);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(small ? tiles_before(TileS::R, g.ld / BM) : oz_gemm_tiles(g.ld), g.nmat);

@@ -36,6 +36,7 @@ struct OzPlanes {
 struct OzMaps {
     CUtensorMap a, b, st;     // 128 x 64 tiles (64-byte k blocks, 64 x 64 store boxes)
     CUtensorMap a2, b2, st2;  // 128 x 32 tiles (32-byte k blocks, 32 x 32 store boxes)
+    CUtensorMap bp;           // persistent 128 x 32 tiles: B boxes of 32 rows x 64 bytes
 };
 void make_oz_maps(const int8_t* planes, int ld, int nmat, OzMaps* out);
 

@@ -3,6 +3,7 @@ vs FP64 numpy; timing per launch. Run on a GPU box:
     python tools/oz_check.py [ld ...]
 """
 import ctypes as C
+import os
 import sys
 
 import numpy as np
@@ -57,7 +58,7 @@ def run(ld, nmat=2, reps=20, use_e=0, beta=0.0):
     if rc != 0:
         raise RuntimeError(lib.tp_last_error_message().decode() if hasattr(lib, "tp_last_error_message") else rc)
     worst_emu = worst_fp = worst_dig = 0.0
-    for m in range(nmat):
+    for m in range(nmat if not os.environ.get("OZ_NOEMU") else 0):
         emu = emulate(A[m], 1, B[m], 1) + (beta * A[m] if use_e else 0.0)
         ex = A[m] @ B[m]
         ex = np.tril(ex) + np.tril(ex, -1).T + (beta * A[m] if use_e else 0.0)
@@ -76,7 +77,9 @@ def run(ld, nmat=2, reps=20, use_e=0, beta=0.0):
 
 
 if __name__ == "__main__":
-    lds = [int(a) for a in sys.argv[1:]] or [128, 256, 512, 1024]
-    for ld in lds:
-        run(ld)
+    # arguments: ld or ld:nmat (OZ_NOEMU=1 skips the emulation checks: timing only)
+    lds = sys.argv[1:] or ["128", "256", "512", "1024"]
+    for a in lds:
+        ld, _, nm = a.partition(":")
+        run(int(ld), nmat=int(nm) if nm else 2)
     run(256, use_e=1, beta=0.5)
