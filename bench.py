@@ -286,7 +286,7 @@ def run_ours(args):
     t_xa, _ = phase(5, 10)
     t_xb, _ = phase(6, 10)
     bs.close()
-    cgm = measure_cg_variant(T, torch, n, r, warm, K, W)
+    cgm = None if args.no_cg else measure_cg_variant(T, torch, n, r, warm, K, W)
 
     # roofline of the dominant kernel: the Ozaki-scheme GEMM on the int8
     # tensor cores (default) or the FP64 DMMA GEMM (TPB_CONE=dmma)
@@ -334,6 +334,8 @@ def run_ours(args):
         sol = T.solve(n, r, warm_start=warm, max_iter=K, **CFG)
         runs.append(time.time() - t0)
     e2e_s = statistics.median(runs)
+    if os.environ.get("BENCH_DEBUG"):
+        print(f"[bench] e2e runs {runs}", file=sys.stderr, flush=True)
     e2e_s = max_over_ranks(e2e_s)
     e2e = ws * K / e2e_s
     h2d = warm.nbytes + 64
@@ -482,6 +484,7 @@ def main():
     ap.add_argument("--sweep-max-iter", type=int, default=40000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-topology solve")
+    ap.add_argument("--no-cg", action="store_true", help="skip the CG x-step variant measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

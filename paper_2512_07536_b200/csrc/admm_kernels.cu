@@ -267,16 +267,61 @@ __global__ void __launch_bounds__(TB* TY) xstep_a_kernel(Dev d, XConst c) {
 
     auto rS = [&](long long p) { return Y[lo.off_s + p] - D[lo.off_s + p] * c.inv_rho; };
     auto rT = [&](long long p) { return Y[lo.off_t + p] - D[lo.off_t + p] * c.inv_rho; };
-    // orientation 1: R(i, j) at j*n + i
-    for (int cc = ty; cc < TB; cc += TY) {
-        const int i = i0 + tx, j = j0 + cc;
-        double v = 0.0;
-        if (i < n && j < n) {
-            const long long p = (long long)j * n + i;
-            v = rS(p) + rT(p);
+    constexpr int NE = TB / TY;
+    // the NE entries a thread owns per orientation: all 4 NE loads are issued
+    // before any use, so their HBM latencies overlap
+    auto load_r = [&](const long long (&pos)[NE], const bool (&ok)[NE], double (&out)[NE]) {
+        double ys[NE], ds[NE], yt[NE], dt[NE];
+#pragma unroll
+        for (int k = 0; k < NE; ++k) {
+            if (!ok[k]) continue;
+            ys[k] = Y[lo.off_s + pos[k]];
+            ds[k] = D[lo.off_s + pos[k]];
+            yt[k] = Y[lo.off_t + pos[k]];
+            dt[k] = D[lo.off_t + pos[k]];
         }
-        Rs[tx][cc] = v;
+#pragma unroll
+        for (int k = 0; k < NE; ++k)
+            out[k] = ok[k] ? (ys[k] - ds[k] * c.inv_rho) + (yt[k] - dt[k] * c.inv_rho) : 0.0;
+    };
+    // both orientations' loads are issued before any use: orientation 1
+    // R(i, j) at j*n + i, orientation 2 R(j, i) at i*n + j
+    long long pos1[NE], pos2[NE];
+    bool ok1[NE], ok2[NE];
+    double v1[NE], v2o[NE];
+#pragma unroll
+    for (int k = 0; k < NE; ++k) {
+        const int a = i0 + tx, bcol = j0 + ty + k * TY;
+        ok1[k] = a < n && bcol < n;
+        pos1[k] = (long long)bcol * n + a;
+        const int j = j0 + tx, i = i0 + ty + k * TY;
+        ok2[k] = i < n && j < n;
+        pos2[k] = (long long)i * n + j;
     }
+    load_r(pos1, ok1, v1);
+    load_r(pos2, ok2, v2o);
+    // hom: the thread's edge loads (h over the tile's pairs, packed index
+    // contiguous in j) are issued together with the block loads
+    double rg_pre[NE];
+    if (!d.het) {
+        long long lp[NE];
+        bool okp[NE];
+        double yg[NE], dg[NE];
+#pragma unroll
+        for (int k = 0; k < NE; ++k) {
+            const int i = i0 + ty + k * TY, j = j0 + tx;
+            okp[k] = i < n && j < n && j > i;
+            lp[k] = okp[k] ? edge_idx(n, i, j) : 0;
+            if (okp[k]) {
+                yg[k] = Y[lp[k]];
+                dg[k] = D[lp[k]];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < NE; ++k) rg_pre[k] = okp[k] ? yg[k] - dg[k] * c.inv_rho : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < NE; ++k) Rs[tx][ty + k * TY] = v1[k];
     // diagonals and v2 for both node blocks
     if (ty == 0) {
         const int i = i0 + tx, j = j0 + tx;
@@ -292,22 +337,17 @@ __global__ void __launch_bounds__(TB* TY) xstep_a_kernel(Dev d, XConst c) {
         }
     }
     __syncthreads();
-    // orientation 2: R(j, i) at i*n + j
-    for (int cc = ty; cc < TB; cc += TY) {
-        const int j = j0 + tx, i = i0 + cc;
-        if (i < n && j < n) {
-            const long long p = (long long)i * n + j;
-            Rs[cc][tx] += rS(p) + rT(p);
-        }
-    }
+    // orientation 2 (loaded above)
+#pragma unroll
+    for (int k = 0; k < NE; ++k)
+        if (ok2[k]) Rs[ty + k * TY][tx] += v2o[k];
     __syncthreads();
-    // h over pairs of the tile (packed index contiguous in j)
     for (int il = ty; il < TB; il += TY) {
         const int i = i0 + il, jl = tx, j = j0 + jl;
         double hv = 0.0, hz = 0.0;
         if (i < n && j < n && j > i) {
             const long long l = edge_idx(n, i, j);
-            const double rg = Y[l] - D[l] * c.inv_rho;
+            const double rg = d.het ? Y[l] - D[l] * c.inv_rho : rg_pre[(il - ty) / TY];
             hv = rg + c.s * (4.0 - rd_i[il] - rd_j[jl] + Rs[il][jl] + v2_i[il] + v2_j[jl]);
             if (d.het) {
                 const long long lz = lo.off_z + l, lv = lo.off_nu + l;

@@ -13,6 +13,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <map>
+#include <mutex>
 
 namespace tpb {
 
@@ -44,6 +46,34 @@ void phase_mark(const char* what) {
 }
 
 namespace {
+
+// Pinned host blocks for the control-word readback, recycled across solvers:
+// cudaMallocHost page-locks memory and occasionally takes tens of
+// milliseconds, which showed up in the end-to-end time of short solves.
+std::mutex g_pin_mu;
+std::multimap<size_t, void*> g_pin_free;
+
+int* pinned_take(size_t bytes) {
+    {
+        std::lock_guard<std::mutex> lk(g_pin_mu);
+        auto it = g_pin_free.lower_bound(bytes);
+        if (it != g_pin_free.end()) {
+            void* p = it->second;
+            g_pin_free.erase(it);
+            return static_cast<int*>(p);
+        }
+    }
+    void* p = nullptr;
+    const size_t cap = std::max<size_t>(bytes, 4096);
+    TPB_CUDA(cudaMallocHost(&p, cap));
+    std::memset(p, 0, cap);
+    return static_cast<int*>(p);
+}
+
+void pinned_give(int* p, size_t bytes) {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    g_pin_free.emplace(std::max<size_t>(bytes, 4096), p);
+}
 
 // Stream-ordered allocation from the device's default memory pool, whose
 // release threshold is raised so that freed blocks stay reserved: repeated
@@ -187,7 +217,7 @@ Solver::~Solver() {
     for (void* p : allocs_) cudaFreeAsync(p, s0_);
     cudaStreamSynchronize(s0_);
     phase_mark("free");
-    if (h_ctl_) cudaFreeHost(h_ctl_);
+    if (h_ctl_) pinned_give(h_ctl_, (size_t)B_ * 8 * sizeof(int));
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_sel_) cudaEventDestroy(ev_sel_);
     if (ev_slem_) cudaEventDestroy(ev_slem_);
@@ -317,7 +347,7 @@ void Solver::alloc() {
     tmp_m2_ = dalloc<double>(s0_, allocs_,(size_t)B * m);
     worst_ = dalloc<double>(s0_, allocs_,B);
     fs_scal_ = dalloc<double>(s0_, allocs_,(size_t)B * 2);
-    TPB_CUDA(cudaMallocHost(&h_ctl_, (size_t)B * 8 * sizeof(int)));
+    h_ctl_ = pinned_take((size_t)B * 8 * sizeof(int));
     TPB_CUDA(cudaMemsetAsync(d_.ictl, 0, (size_t)B * 8 * sizeof(int), s0_));
     // allocations are ordered on s0_; later work also runs on s1_/s2_ and the
     // legacy stream, so complete them here

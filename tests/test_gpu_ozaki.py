@@ -131,3 +131,30 @@ def test_cone_projection_ozaki_vs_dmma_and_lapack(T, O, n):
     assert np.max(np.abs(p_oz - ref)) < 1e-12 * scale
     assert np.max(np.abs(p_dm - ref)) < 1e-12 * scale
     assert np.max(np.abs(p_oz - p_oz.T)) == 0.0
+
+
+def test_persistent_variant_bitwise_equal():
+    """The opt-in persistent kernel (TPB_OZ_PERSIST=2: 128 x 32 tiles,
+    double-buffered TMEM) must reproduce the default kernel bit for bit; the
+    switch is read once per process, so each variant runs in a subprocess."""
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, numpy as np, ctypes as C; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
+        "from paper_2512_07536_b200 import _lib; from test_gpu_ozaki import oz_gemm, sym;"
+        "lib = _lib.load(); out = [];"
+        "[out.extend(oz_gemm(lib, np.stack([sym(np.random.default_rng(ld), ld, 1.2)] * 2),"
+        " np.stack([sym(np.random.default_rng(ld + 1), ld, 1.4)] * 2), digits=True)) for ld in (256, 1024)];"
+        "np.save(sys.argv[1], np.concatenate([o.astype(np.float64).ravel() for o in out]))"
+    )
+    res = {}
+    for mode in ("0", "2"):
+        path = os.path.join(here, f"gpurun_out_persist_{mode}.npy")
+        env = dict(os.environ, TPB_OZ_PERSIST=mode)
+        subprocess.run([sys.executable, "-c", code, path], cwd=here, env=env, check=True, timeout=300)
+        res[mode] = np.load(path)
+        os.remove(path)
+    assert res["0"].shape == res["2"].shape
+    assert np.array_equal(res["0"], res["2"])
