@@ -158,7 +158,7 @@ void cone_dense(int n, const double* a, double* out, bool psd) {
     const int blocks = (int)std::min<long long>(((long long)n * n + 255) / 256, 1024);
     sym_pad_kernel<<<blocks, 256>>>(da.p, n, ld, w, A.p);
     TPB_CHECK_LAUNCH();
-    SignSchedule sch;
+    const SignSchedule sch = (!small && oz) ? ozaki_schedule() : SignSchedule{};
     if (small) {
         launch_cone_small(A.p, ld2, ld, n, C.p, 0, (long long)n * n, nullptr, 2, sch, 0);
     } else if (oz) {

@@ -17,6 +17,15 @@ struct SignSchedule {
     int gemms() const { return 3 * k1 + 2 * k2 + 1; }
 };
 
+// Schedule of the tiled Ozaki path: the inflation quintic with the largest
+// guaranteed growth on [0, 0.55] that keeps [0.55, 1.3] invariant (an LP over
+// the coefficients, tools/proto/sign_schedule.py), 20 steps + 6 Newton-Schulz
+// = 73 products instead of 79. Scalar-map error max_mu mu |1 - s(mu)| / 2 =
+// 4.4e-14 of ||A||_F (1.8e-14 for the default above). Digit bounds: |X| <=
+// 1.3, |U| <= 1.26, |Z'| <= 3.73, |V| <= 1.5 (exponents unchanged).
+// TPB_SIGN_SCHEDULE=default selects the default above.
+SignSchedule ozaki_schedule();
+
 // One symmetric GEMM step over a batch of matrices (blockIdx.y = matrix):
 //   C = alpha * (A . B) + beta * E,   alpha = alpha_c * s^pa, beta = beta_c * s^pb
 // with s = scale[mat]; A, B, E symmetric ld x ld (row-major, zero padded),

@@ -1098,6 +1098,18 @@ namespace {
 constexpr int kEX = 1, kEU = 1, kEZ = 2, kEV = 1, kEX0 = 1;
 }
 
+SignSchedule ozaki_schedule() {
+    SignSchedule s;
+    const char* e = std::getenv("TPB_SIGN_SCHEDULE");
+    if (e && std::strcmp(e, "default") == 0) return s;
+    s.k1 = 20;
+    s.k2 = 6;
+    s.qa = 3.73052;
+    s.qb = -5.13486;
+    s.qc = 2.0372;
+    return s;
+}
+
 void enqueue_cone_ozaki(const double* A, double* /*w0*/, double* /*w1*/, double* /*w2*/, const OzWork& oz,
                         int ld, int n, const double* scale, double* C, long long c_stride_b,
                         long long c_stride_w, const int* ictl, int nmat, const SignSchedule& sch,

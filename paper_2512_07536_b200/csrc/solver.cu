@@ -162,6 +162,7 @@ Solver::Solver(int n, int B, bool het, const std::vector<int>& r, const std::vec
     // Tiled projections: int8 tensor-core (Ozaki) GEMMs by default, FP64 DMMA
     // with TPB_CONE=dmma; the Ozaki tiles need ld % 128 == 0.
     ozaki_ = !small_ && cone_uses_ozaki();
+    if (ozaki_) sch_ = ozaki_schedule();
     ld_ = small_ ? ((n + 7) & ~7) : (ozaki_ ? ((n + 127) / 128) * 128 : ((n + 63) / 64) * 64);
     list_cap_ = het ? m : *std::max_element(r_host_.begin(), r_host_.end());
     int chunk = cfg.chunk > 0 ? cfg.chunk : (n <= 64 ? 32 : (n <= 256 ? 16 : 8));
@@ -429,6 +430,7 @@ void Solver::final_slem(const double* packed, const int* list, const int* count,
     a.max_restarts = 200;
     a.min_steps = 64;
     a.tol = 1e-10;
+    if (const char* t = std::getenv("TPB_FINAL_TOL")) a.tol = std::atof(t);  // experiments
     a.out = out;
     a.tr_acf = nullptr;
     a.ictl = nullptr;
