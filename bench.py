@@ -214,8 +214,8 @@ def measure_cg_variant(T, torch, n, r, warm, K, W):
     return {"admm_iter_per_s": it_s, "cg_iterations_per_xstep": its, "cg_rel_residual": rel,
             "cg_solve_ms": t_cg * 1e3, "cg_bytes": cg_bytes, "achieved_gbs": cg_bytes / t_cg / 1e9,
             "frac_of_hbm": cg_bytes / t_cg / 1e9 / hbm, "peak_gbs": hbm,
-            "kernels": "xstep_cg_kernel: one persistent cooperative launch, direction + update pass per CG iteration, grid barriers between",
-            "note": "working set (x, r, p: 12.6 MB at n=1024) is L2-resident between passes"}
+            "kernels": "xstep_cg_reg_kernel: one persistent cooperative launch, one CTA per 32x32 edge tile; direction + update phase per CG iteration, grid barriers between",
+            "note": "algorithmic bytes = the vectors a CG iteration touches; x, r, p stay in registers (u in shared memory) for the whole solve, so only h in, x out and the per-tile partials reach L2/HBM: the kernel is barrier-latency-bound, not HBM-bound"}
 
 
 # ---------------------------------------------------------------- our arm

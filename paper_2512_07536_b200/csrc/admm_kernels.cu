@@ -68,9 +68,38 @@ __device__ inline double block_sum_2d(double v, double* scratch) {
 // fixed-order total of `cnt` partials (identical in every CTA)
 __device__ inline double sum_tiles(const double* P, int cnt, double* scratch) {
     const int t = threadIdx.y * TB + threadIdx.x;
+    constexpr int NT = TB * TY, NP = 4;
     double v = 0.0;
-    for (int k = t; k < cnt; k += TB * TY) v += P[k];
+    if (cnt <= NP * NT) {
+        // all loads in flight together, summed in the same k order
+        double q[NP];
+#pragma unroll
+        for (int j = 0; j < NP; ++j) q[j] = t + j * NT < cnt ? P[t + j * NT] : 0.0;
+#pragma unroll
+        for (int j = 0; j < NP; ++j)
+            if (t + j * NT < cnt) v += q[j];
+    } else {
+        for (int k = t; k < cnt; k += NT) v += P[k];
+    }
     return block_sum_2d(v, scratch);
+}
+
+// fixed-order warp sum of `cnt` partials: lane sums k = lane, lane + 32, ...
+// in k order (loads issued together), then the warp tree
+__device__ inline double warp_sum_partials(const double* P, int cnt, int lane) {
+    constexpr int NP = 17;  // ntile <= 544 (n <= 1056)
+    double v = 0.0;
+    if (cnt <= NP * 32) {
+        double q[NP];
+#pragma unroll
+        for (int j = 0; j < NP; ++j) q[j] = lane + j * 32 < cnt ? P[lane + j * 32] : 0.0;
+#pragma unroll
+        for (int j = 0; j < NP; ++j)
+            if (lane + j * 32 < cnt) v += q[j];
+    } else {
+        for (int k = lane; k < cnt; k += 32) v += P[k];
+    }
+    return warp_sum(v);
 }
 
 }  // namespace
@@ -524,31 +553,39 @@ void launch_xstep_node(const Dev& d, const XConst& c, cudaStream_t st) {
 
 namespace {
 
-// node partials of a tile's packed values Vs (pairs il < jl on diagonal tiles)
+// node partials of a tile's packed values Vs (pairs il < jl on diagonal tiles):
+// 4 adjacent lanes per node sum interleaved quarters, then two shuffles
 __device__ inline void tile_node_partials(const double (&Vs)[TB][TB + 1], int bi, int bj, int n, double* P) {
     const int t = threadIdx.y * TB + threadIdx.x;
     const int i0 = bi * TB, j0 = bj * TB;
-    if (t < TB) {
-        const int il = t, i = i0 + il;
-        if (i < n) {
-            double s = 0.0;
-            for (int jl = 0; jl < TB; ++jl) {
-                if (bi == bj) {
-                    if (jl == il) continue;
-                    s += jl > il ? Vs[il][jl] : Vs[jl][il];
-                } else {
-                    s += Vs[il][jl];
-                }
+    const int nl = t >> 2, part = t & 3;
+    double s = 0.0;
+    bool valid = false;
+    if (nl < TB) {
+        const int il = nl;
+        valid = i0 + il < n;
+#pragma unroll
+        for (int q = 0; q < TB / 4; ++q) {
+            const int jl = part + 4 * q;
+            if (bi == bj) {
+                if (jl != il) s += jl > il ? Vs[il][jl] : Vs[jl][il];
+            } else {
+                s += Vs[il][jl];
             }
-            P[(long long)bj * n + i] = s;
         }
-    } else if (t < 2 * TB && bi != bj) {
-        const int jl = t - TB, j = j0 + jl;
-        if (j < n) {
-            double s = 0.0;
-            for (int il = 0; il < TB; ++il) s += Vs[il][jl];
-            P[(long long)bi * n + j] = s;
-        }
+    } else if (bi != bj) {
+        const int jl = nl - TB;
+        valid = j0 + jl < n;
+#pragma unroll
+        for (int q = 0; q < TB / 4; ++q) s += Vs[part + 4 * q][jl];
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    if (part == 0 && valid) {
+        if (nl < TB)
+            P[(long long)bj * n + i0 + nl] = s;
+        else
+            P[(long long)bi * n + j0 + nl - TB] = s;
     }
 }
 
@@ -581,20 +618,7 @@ __global__ void __launch_bounds__(TB* TY, 4) xstep_cg_kernel(Dev d, XConst c) {
     int* s_act = reinterpret_cast<int*>(dyn + 3 * d.B);
 
     // fixed-order warp sum of one solve's tile partials
-    auto wsum = [&](const double* P) {
-        // loads batched 8 deep so their L2 latencies overlap
-        double v = 0.0;
-        int k = lane;
-        for (; k + 7 * 32 < d.ntile; k += 8 * 32) {
-            double q[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) q[j] = P[k + j * 32];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) v += q[j];
-        }
-        for (; k < d.ntile; k += 32) v += P[k];
-        return warp_sum(v);
-    };
+    auto wsum = [&](const double* P) { return warp_sum_partials(P, d.ntile, lane); };
 
     for (int k = 0; k <= d.cg_max; ++k) {
         // ---- per-solve scalars (every CTA; warp per solve)
@@ -759,24 +783,207 @@ __global__ void __launch_bounds__(TB* TY, 4) xstep_cg_kernel(Dev d, XConst c) {
     }
 }
 
+// Register-resident variant: when every (solve, tile) item gets its own
+// co-resident CTA, each thread keeps its edges' x, r and p in registers and
+// the tile's node values u in shared memory for the whole solve; between the
+// phases global memory carries only the per-tile and node partials. The
+// tile's node partials are prefetched before the scalar sums, so a phase is
+// one L2 round trip plus the grid barrier (instead of re-reading r, p, x and
+// u). Same arithmetic and reduction order as xstep_cg_kernel: bitwise
+// identical results (tested).
+constexpr int kCgRegNb = 32;  // node blocks the per-thread prefetch covers (n <= 1024)
+
+__global__ void __launch_bounds__(TB* TY, 4) xstep_cg_reg_kernel(Dev d, XConst c) {
+    cg::grid_group grid = cg::this_grid();
+    const Layout& lo = d.lo;
+    const int n = lo.n;
+    const int nitems = d.B * d.ntile;
+    const int tx = threadIdx.x, ty = threadIdx.y, t = ty * TB + tx;
+    const int lane = t & 31, warp = t >> 5;
+    constexpr int NR_ = TB / TY, NW = TB * TY / 32, NQ = (kCgRegNb + 3) / 4;
+    __shared__ double scratch[NW];
+    __shared__ double ui[TB], uj[TB];
+    __shared__ double Rs[TB][TB + 1];
+    __shared__ int s_any;
+    extern __shared__ double dyn[];  // per solve: rr0, rr_k, beta | active flags
+    double* s_rr0 = dyn;
+    double* s_rrk = dyn + d.B;
+    double* s_beta = dyn + 2 * d.B;
+    int* s_act = reinterpret_cast<int*>(dyn + 3 * d.B);
+
+    // this CTA's item (CTAs past the last item only take part in the barriers)
+    const int w = blockIdx.x;
+    const bool own = w < nitems;
+    const int b = own ? w / d.ntile : 0, tile = own ? w - b * d.ntile : 0;
+    int bi = 0, bj = 0;
+    if (own) tile_of(tile, bi, bj);
+    const int i0 = bi * TB, j0 = bj * TB;
+    int l[NR_];  // packed edge index (m < 2^31 here)
+    bool ok[NR_];
+    double xv[NR_], rv[NR_], pv[NR_];
+#pragma unroll
+    for (int q = 0; q < NR_; ++q) {
+        const int i = i0 + ty + q * TY, j = j0 + tx;
+        ok[q] = own && i < n && j < n && j > i;
+        l[q] = ok[q] ? (int)edge_idx(n, i, j) : 0;
+        rv[q] = ok[q] ? d.h[(long long)b * lo.m + l[q]] : 0.0;  // r_0 = h (pass A)
+        pv[q] = 0.0;
+        xv[q] = 0.0;
+    }
+    // node of the u sums: 4 threads per node, as in xstep_cg_kernel
+    const int nl = t >> 2, part = t & 3;
+    const int node = nl < TB ? i0 + nl : j0 + nl - TB;
+    const bool node_ok = own && node < n;
+    double uprev = 0.0;  // the node's u of the previous direction (part 0)
+    bool ran = false;
+
+    auto wsum = [&](const double* P) { return warp_sum_partials(P, d.ntile, lane); };
+
+    for (int k = 0; k <= d.cg_max; ++k) {
+        // prefetch the tile's node partials of r_k (independent of the scalars)
+        const double* NRp = k == 0 ? d.PU + (long long)b * d.nb * n : d.cg_nr + (long long)b * d.nb * n;
+        double nv[NQ];
+#pragma unroll
+        for (int j = 0; j < NQ; ++j) {
+            const int q = part + 4 * j;
+            nv[j] = (node_ok && q < d.nb) ? NRp[(long long)q * n + node] : 0.0;
+        }
+        // ---- per-solve scalars (every CTA; warp per solve)
+        for (int bb = warp; bb < d.B; bb += NW) {
+            const double* RR = d.cg_rr + (long long)bb * 2 * d.ntile;
+            const bool was = k == 0 ? !solve_done(d, bb) : s_act[bb] != 0;
+            double rr1 = 0.0;
+            if (k == 0) {
+                rr1 = wsum(RR);
+                if (lane == 0) s_rr0[bb] = rr1;
+            } else if (was) {
+                rr1 = wsum(RR + d.ntile);
+            }
+            if (lane == 0) {
+                bool act = was;
+                if (was) {
+                    const double rr0 = s_rr0[bb];
+                    const bool conv = k == 0 ? !(rr0 > 0.0) : rr1 <= d.cg_tol2 * rr0;
+                    if (conv || k == d.cg_max) {
+                        act = false;
+                        if (blockIdx.x == 0) {
+                            d.ictl[bb * 8 + kCgIters] = k;
+                            d.scal[bb * 8 + kCgRes] = rr0 > 0.0 ? sqrt(rr1 / rr0) : 0.0;
+                        }
+                    }
+                    s_beta[bb] = k == 0 ? 0.0 : rr1 / s_rrk[bb];
+                    s_rrk[bb] = rr1;
+                }
+                s_act[bb] = act;
+            }
+        }
+        __syncthreads();
+        if (t == 0) {
+            int any = 0;
+            for (int bb = 0; bb < d.B && !any; ++bb) any = s_act[bb];
+            s_any = any;
+        }
+        __syncthreads();
+        if (!s_any) break;  // uniform: every CTA computed the same flags
+        const bool act = own && s_act[b];
+
+        // ---- direction phase: u = D r_k + beta u_{k-1}, p = r + beta p
+        if (act) {
+            const double beta = s_beta[b];
+            double u = 0.0;
+#pragma unroll
+            for (int j = 0; j < NQ; ++j)
+                if (part + 4 * j < d.nb) u += nv[j];  // q order of xstep_cg_kernel
+            u += __shfl_xor_sync(0xffffffffu, u, 1);
+            u += __shfl_xor_sync(0xffffffffu, u, 2);
+            if (part == 0 && node_ok) {
+                if (k > 0) u += beta * uprev;
+                uprev = u;
+            }
+            if (part == 0) {
+                if (nl < TB) ui[nl] = u; else uj[nl - TB] = u;
+            }
+            __syncthreads();
+            double pq = 0.0;
+#pragma unroll
+            for (int q = 0; q < NR_; ++q) {
+                if (!ok[q]) continue;
+                const double p = rv[q] + beta * pv[q];
+                pv[q] = p;
+                pq += p * (c.cg_a * p + c.cg_b * (ui[ty + q * TY] + uj[tx]));
+            }
+            pq = block_sum_2d(pq, scratch);
+            if (t == 0) d.cg_pq[w] = pq;
+        }
+        grid.sync();
+
+        // ---- update phase: x += alpha p, r -= alpha Hp, |r|^2 and D r partials
+        if (act) {
+            ran = true;
+            const double pq = sum_tiles(d.cg_pq + (long long)b * d.ntile, d.ntile, scratch);
+            const double alpha = pq > 0.0 ? s_rrk[b] / pq : 0.0;
+            double rr = 0.0;
+#pragma unroll
+            for (int q = 0; q < NR_; ++q) {
+                double r = 0.0;
+                if (ok[q]) {
+                    const double hp = c.cg_a * pv[q] + c.cg_b * (ui[ty + q * TY] + uj[tx]);
+                    xv[q] = xv[q] + alpha * pv[q];
+                    r = rv[q] - alpha * hp;
+                    rv[q] = r;
+                    rr += r * r;
+                }
+                Rs[ty + q * TY][tx] = r;
+            }
+            __syncthreads();
+            tile_node_partials(Rs, bi, bj, n, d.cg_nr + (long long)b * d.nb * n);
+            rr = block_sum_2d(rr, scratch);
+            if (t == 0) d.cg_rr[((long long)b * 2 + 1) * d.ntile + tile] = rr;
+        }
+        grid.sync();
+    }
+    // x for pass B; r back into h, where xstep_cg_kernel leaves it
+    if (ran) {
+#pragma unroll
+        for (int q = 0; q < NR_; ++q) {
+            if (!ok[q]) continue;
+            d.cg_x[(long long)b * lo.m + l[q]] = xv[q];
+            d.h[(long long)b * lo.m + l[q]] = rv[q];
+        }
+    }
+}
+
 size_t cg_dyn_smem(const Dev& d) { return (size_t)d.B * (3 * sizeof(double) + sizeof(int)); }
+
+namespace {
+int cg_capacity(const void* kernel, const Dev& d) {
+    int dev = 0, sms = 0, per_sm = 0;
+    TPB_CUDA(cudaGetDevice(&dev));
+    TPB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    TPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, TB * TY, cg_dyn_smem(d)));
+    return std::max(1, sms * per_sm);
+}
+}  // namespace
 
 int cg_grid_size(const Dev& d) {
     static int cached = 0;
-    if (!cached) {
-        int dev = 0, sms = 0, per_sm = 0;
-        TPB_CUDA(cudaGetDevice(&dev));
-        TPB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        TPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, xstep_cg_kernel, TB * TY,
-                                                               cg_dyn_smem(d)));
-        cached = std::max(1, sms * per_sm);
-    }
+    if (!cached) cached = cg_capacity((const void*)xstep_cg_kernel, d);
     return std::max(1, std::min(cached, d.B * d.ntile));
 }
 
+// register-resident CG when every item fits one co-resident CTA
+// (TPB_CG_GLOBAL forces the global-memory variant: tests, comparisons)
+bool cg_use_registers(const Dev& d) {
+    if (std::getenv("TPB_CG_GLOBAL") || d.nb > kCgRegNb) return false;
+    static int cached = 0;
+    if (!cached) cached = cg_capacity((const void*)xstep_cg_reg_kernel, d);
+    return (long long)d.B * d.ntile <= cached;
+}
+
 void launch_xstep_cg(const Dev& d, const XConst& c, cudaStream_t st) {
+    const bool reg = cg_use_registers(d);
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(cg_grid_size(d));
+    cfg.gridDim = dim3(reg ? d.B * d.ntile : cg_grid_size(d));
     cfg.blockDim = dim3(TB, TY);
     cfg.stream = st;
     cfg.dynamicSmemBytes = cg_dyn_smem(d);
@@ -785,7 +992,10 @@ void launch_xstep_cg(const Dev& d, const XConst& c, cudaStream_t st) {
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    TPB_CUDA(cudaLaunchKernelEx(&cfg, xstep_cg_kernel, d, c));
+    if (reg)
+        TPB_CUDA(cudaLaunchKernelEx(&cfg, xstep_cg_reg_kernel, d, c));
+    else
+        TPB_CUDA(cudaLaunchKernelEx(&cfg, xstep_cg_kernel, d, c));
 }
 
 // ---------------------------------------------------------------- x-step B

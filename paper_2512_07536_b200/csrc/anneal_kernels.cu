@@ -326,7 +326,7 @@ bool anneal_device(int n, std::vector<std::pair<int, int>>& es, const AnnealPara
     Buf<unsigned long long> d_part(G);
     Buf<int> d_bad(G), d_cmd(16);
     Buf<double> d_energy(1);
-    TPB_CUDA(cudaMemcpy(d_in.p, h.data(), m * sizeof(int2), cudaMemcpyHostToDevice));
+    h2d(d_in.p, h.data(), m * sizeof(int2));
     TPB_CUDA(cudaMemset(d_cmd.p, 0, 16 * sizeof(int)));
     Args a{};
     a.n = n;

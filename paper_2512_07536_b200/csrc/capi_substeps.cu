@@ -41,7 +41,7 @@ struct DBuf {
     ~DBuf() { cudaFree(p); }
     DBuf(const DBuf&) = delete;
     void up(const T* h, size_t count) {
-        TPB_CUDA(cudaMemcpy(p, h, count * sizeof(T), cudaMemcpyHostToDevice));
+        h2d(p, h, count * sizeof(T));
     }
     void down(T* h, size_t count) const {
         TPB_CUDA(cudaMemcpy(h, p, count * sizeof(T), cudaMemcpyDeviceToHost));

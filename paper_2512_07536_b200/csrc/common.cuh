@@ -37,6 +37,14 @@ struct Error : std::runtime_error {
 
 #define TPB_CHECK_LAUNCH() TPB_CUDA(cudaGetLastError())
 
+// Host -> device copy that has landed when it returns. cudaMemcpy from
+// pageable memory may return before its DMA completes, and only the legacy
+// stream is ordered after it -- the solver's non-blocking streams are not.
+inline void h2d(void* dst, const void* src, size_t bytes) {
+    TPB_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+    TPB_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
+}
+
 // Thread-local message of the last failed C ABI call (capi.cu).
 std::string& last_error_ref();
 

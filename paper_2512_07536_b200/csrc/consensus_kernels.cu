@@ -105,7 +105,7 @@ struct Dev {
     T* p = nullptr;
     explicit Dev(size_t n) { TPB_CUDA(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T))); }
     ~Dev() { cudaFree(p); }
-    void up(const T* h, size_t n) { TPB_CUDA(cudaMemcpy(p, h, n * sizeof(T), cudaMemcpyHostToDevice)); }
+    void up(const T* h, size_t n) { h2d(p, h, n * sizeof(T)); }
 };
 
 }  // namespace

@@ -180,7 +180,7 @@ Solver::Solver(int n, int B, bool het, const std::vector<int>& r, const std::vec
     alloc();
     if (het && !cap_) {
         std::vector<double> dg(degrees.begin(), degrees.end());
-        TPB_CUDA(cudaMemcpy(d_deg_, dg.data(), dg.size() * sizeof(double), cudaMemcpyHostToDevice));
+        h2d(d_deg_, dg.data(), dg.size() * sizeof(double));
     }
     if (cap_) {
         // column -> rows CSR for the capped projection
@@ -190,13 +190,13 @@ Solver::Solver(int n, int B, bool het, const std::vector<int>& r, const std::vec
         std::vector<int> pos(cnt.begin(), cnt.end() - 1);
         for (int rr = 0; rr < capsys_.nrows; ++rr)
             for (int q = capsys_.row_ptr[rr]; q < capsys_.row_ptr[rr + 1]; ++q) colr[pos[capsys_.cols[q]]++] = rr;
-        TPB_CUDA(cudaMemcpy(cap_colr_ptr_, cnt.data(), cnt.size() * sizeof(int), cudaMemcpyHostToDevice));
+        h2d(cap_colr_ptr_, cnt.data(), cnt.size() * sizeof(int));
         if (!colr.empty())
-            TPB_CUDA(cudaMemcpy(cap_colr_, colr.data(), colr.size() * sizeof(int), cudaMemcpyHostToDevice));
-        TPB_CUDA(cudaMemcpy(cap_caps_, capsys_.caps.data(), capsys_.nrows * sizeof(int), cudaMemcpyHostToDevice));
-        TPB_CUDA(cudaMemcpy(cap_allowed_, capsys_.allowed.data(), m * sizeof(int), cudaMemcpyHostToDevice));
+            h2d(cap_colr_, colr.data(), colr.size() * sizeof(int));
+        h2d(cap_caps_, capsys_.caps.data(), capsys_.nrows * sizeof(int));
+        h2d(cap_allowed_, capsys_.allowed.data(), m * sizeof(int));
     }
-    TPB_CUDA(cudaMemcpy(d_r_, r_host_.data(), B * sizeof(int), cudaMemcpyHostToDevice));
+    h2d(d_r_, r_host_.data(), B * sizeof(int));
     warm_.assign(B, {});
     res_.assign(B, {});
     phase_mark("solver alloc");
@@ -821,9 +821,9 @@ void Solver::epilogue_het() {
         }
         counts[b] = (int)ls.size();
     }
-    TPB_CUDA(cudaMemcpy(tmp_m_, packed.data(), packed.size() * sizeof(double), cudaMemcpyHostToDevice));
-    TPB_CUDA(cudaMemcpy(list_, lists.data(), lists.size() * sizeof(int), cudaMemcpyHostToDevice));
-    TPB_CUDA(cudaMemcpy(list_count_, counts.data(), counts.size() * sizeof(int), cudaMemcpyHostToDevice));
+    h2d(tmp_m_, packed.data(), packed.size() * sizeof(double));
+    h2d(list_, lists.data(), lists.size() * sizeof(int));
+    h2d(list_count_, counts.data(), counts.size() * sizeof(int));
     final_slem(tmp_m_, list_, list_count_, slem_out_);
     std::vector<double> so((size_t)B_ * 8);
     TPB_CUDA(cudaMemcpyAsync(so.data(), slem_out_, so.size() * sizeof(double), cudaMemcpyDeviceToHost, s0_));
@@ -841,9 +841,9 @@ SolveResult Solver::result(int b) const { return res_.at(b); }
 
 void Solver::upload(const double* X, const double* Y, const double* D) {
     const size_t bytes = (size_t)B_ * lo_.nx * sizeof(double);
-    if (X) TPB_CUDA(cudaMemcpy(d_.X, X, bytes, cudaMemcpyHostToDevice));
-    if (Y) TPB_CUDA(cudaMemcpy(d_.Y, Y, bytes, cudaMemcpyHostToDevice));
-    if (D) TPB_CUDA(cudaMemcpy(d_.D, D, bytes, cudaMemcpyHostToDevice));
+    if (X) h2d(d_.X, X, bytes);
+    if (Y) h2d(d_.Y, Y, bytes);
+    if (D) h2d(d_.D, D, bytes);
 }
 
 void Solver::download(double* X, double* Y, double* D) {

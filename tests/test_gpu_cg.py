@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 TOL_X = 1e-9
 
 
-@pytest.mark.parametrize("n,r", [(3, 2), (16, 32), (65, 300), (256, 1024)])
+@pytest.mark.parametrize("n,r", [(3, 2), (16, 32), (65, 300), (256, 1024), (1024, 4096)])
 def test_update_X_cg_vs_closed_form_and_oracle(T, O, n, r):
     rng = np.random.default_rng(100 + n)
     pd = O.assemble(n, r, 2.0, 2.5)
@@ -103,3 +103,35 @@ def test_n1024_lockstep_cg_vs_closed_form(T, O):
         assert 1 <= its <= 3 and rel <= 1e-10
     finally:
         sv.close()
+
+
+@pytest.mark.parametrize("n,r", [(16, 32), (65, 300), (1024, 4096)])
+def test_cg_register_variant_bitwise(T, monkeypatch, n, r):
+    """The register-resident CG kernel (every tile's x, r, p held by its own
+    CTA) against the global-memory kernel (TPB_CG_GLOBAL): same arithmetic and
+    reduction order, so x-steps and whole lockstep runs agree bit for bit."""
+    m = n * (n - 1) // 2
+    nx = m + 1 + 2 * n * n + n
+    rng = np.random.default_rng(7 + n)
+    y = rng.standard_normal(nx)
+    d = rng.standard_normal(nx) * 0.3
+
+    def run():
+        x, kkt, its, rel = T.update_X_cg(n, r, y, d, rho=2.5, linear_tol=1e-10)
+        return x, its, rel
+
+    monkeypatch.delenv("TPB_CG_GLOBAL", raising=False)
+    x_r, its_r, rel_r = run()
+    monkeypatch.setenv("TPB_CG_GLOBAL", "1")
+    x_g, its_g, rel_g = run()
+    assert its_r == its_g and rel_r == rel_g
+    assert np.array_equal(x_r, x_g)
+    if n == 1024:
+        bu_e = T.allocate_edge_capacity([1.0] * n, r)
+        warm = T.anneal_degree_topology(bu_e[1], steps=1, moves_per_temp=1, seed=0)
+        cfg = dict(rho=10.0, epsilon=1e-8, max_iter=4, linear_solver=1)
+        g = T.solve(n, r, warm_start=warm, **cfg)
+        monkeypatch.delenv("TPB_CG_GLOBAL")
+        a = T.solve(n, r, warm_start=warm, **cfg)
+        assert np.array_equal(a.trace, g.trace)
+        assert np.array_equal(a.weights, g.weights) and a.edges.tolist() == g.edges.tolist()
