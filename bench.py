@@ -411,8 +411,11 @@ def run_ours(args):
             "cg_xstep": cgm,
             "e2e": {"value": e2e, "unit": "iter/s", "h2d_bytes_per_step": h2d / K,
                     "d2h_bytes_per_step": d2h / K,
+                    "runs_s": runs, "first_call_iter_per_s": ws * K / runs[0],
                     "note": "median of 3 tp_solve calls through the C ABI with host warm-start edges in and the host "
-                            "Solution out (setup, feasible start, K iterations, extraction, final SLEM)"},
+                            "Solution out (feasible start, K iterations, extraction, final SLEM); the first call "
+                            "also builds the thread's solve plan (device buffers + captured graphs, "
+                            "first_call_iter_per_s), the next two reuse it (tp_release_plans frees it)"},
             "gpu_launches": launches_per_iter * K,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,

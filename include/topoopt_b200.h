@@ -77,6 +77,11 @@ int tp_config_validate(const tp_config* cfg);
 const char* tp_last_error_message(void);
 int tp_version(void);
 int tp_set_device(int device);
+/* tp_solve keeps, per host thread, the last homogeneous solver plan (device
+ * buffers + captured iteration graphs) for the next call with the same n, r,
+ * configuration, device and TPB_* environment; every call resets the whole
+ * state, so results equal a fresh solver's bit for bit. This frees it. */
+int tp_release_plans(void);
 
 /* ---------------------------------------------------------------- solves */
 

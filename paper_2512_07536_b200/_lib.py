@@ -67,6 +67,7 @@ SIGNATURES = {
     "tp_last_error_message": (C.c_char_p, []),
     "tp_version": (_I, []),
     "tp_set_device": (_I, [C.c_int]),
+    "tp_release_plans": (_I, []),
     "tp_solve": (_I, [_I, _I, _cfgp, _ip, _I, _resp, _ip, _dp, _dp, C.c_char_p, _I]),
     "tp_solve_het_node": (_I, [_I, _ip, _cfgp, _ip, _I, _resp, _ip, _dp, _dp, C.c_char_p, _I]),
     "tp_anneal_degree": (_I, [_I, _ip, _D, _D, _I, _I, _U64, _ip, _ip]),

@@ -1,6 +1,7 @@
 // C ABI (include/topoopt_b200.h): host entry points over the device solver.
 #include <algorithm>
 #include <cstring>
+#include <unistd.h>  // environ
 #include <memory>
 #include <string>
 #include <vector>
@@ -241,6 +242,70 @@ int tp_solver_cg_stats(tp_solver* s, int32_t b, int32_t* iters, double* rel_res)
     });
 }
 
+namespace {
+// Per-thread plan cache of tp_solve: the last homogeneous solver (device
+// buffers, digit planes, TMA maps, captured iteration graphs) serves the next
+// call with the same shape. Solver::start() resets every piece of iteration
+// state, so a reused solver returns bitwise what a fresh one does (tested).
+// The pointer is leaked at thread exit on purpose: no CUDA calls after the
+// runtime may have shut down.
+struct HomPlan {
+    int dev = -1, n = 0, r = 0;
+    Config c;
+    std::string env;  // TPB_* variables select kernels at capture time
+    std::unique_ptr<Solver> s;
+};
+thread_local HomPlan* t_plan = nullptr;
+
+std::string tpb_env() {
+    std::string k;
+    for (char** e = environ; e && *e; ++e)
+        if (std::strncmp(*e, "TPB_", 4) == 0) {
+            k += *e;
+            k += '\n';
+        }
+    return k;
+}
+
+bool same_cfg(const Config& a, const Config& b) {
+    return a.rho == b.rho && a.epsilon == b.epsilon && a.max_iter == b.max_iter && a.alpha == b.alpha &&
+           a.weight_floor == b.weight_floor && a.linear_tol == b.linear_tol &&
+           a.trace_stride == b.trace_stride && a.slem_tol == b.slem_tol && a.chunk == b.chunk &&
+           a.linear_solver == b.linear_solver && a.cg_max_iter == b.cg_max_iter;
+}
+
+void release_plan() {
+    if (t_plan) {
+        t_plan->s.reset();
+        delete t_plan;
+        t_plan = nullptr;
+    }
+}
+
+Solver& hom_plan(int n, int r, const Config& c) {
+    int dev = 0;
+    TPB_CUDA(cudaGetDevice(&dev));
+    std::string env = tpb_env();
+    if (t_plan && t_plan->s && t_plan->dev == dev && t_plan->n == n && t_plan->r == r &&
+        same_cfg(t_plan->c, c) && t_plan->env == env)
+        return *t_plan->s;
+    release_plan();  // one plan per thread: free the old one before allocating
+    auto p = std::make_unique<HomPlan>();
+    p->dev = dev;
+    p->n = n;
+    p->r = r;
+    p->c = c;
+    p->env = std::move(env);
+    p->s = std::make_unique<Solver>(n, 1, false, std::vector<int>{r}, std::vector<int>{}, c);
+    t_plan = p.release();
+    return *t_plan->s;
+}
+}  // namespace
+
+int tp_release_plans(void) {
+    return guarded([&] { release_plan(); });
+}
+
 int tp_solve(int32_t n, int32_t r, const tp_config* cfg, const int32_t* warm_edges, int32_t n_warm,
              tp_result* out, int32_t* edges, double* weights, double* trace, char* note,
              int32_t note_cap) {
@@ -248,14 +313,19 @@ int tp_solve(int32_t n, int32_t r, const tp_config* cfg, const int32_t* warm_edg
         require_device();
         const Config c = to_cfg(cfg);
         validate(c);
-        Solver s(n, 1, false, std::vector<int>{r}, {}, c);
         std::vector<int> warm;
         if (warm_edges && n_warm >= 0) warm = packed_edges(n, warm_edges, n_warm);
         else warm = default_warm(n, r, cfg ? cfg->seed : 0);
-        s.set_warm(0, warm);
-        s.start();
-        s.run_to_completion();
-        s.finish();
+        Solver& s = hom_plan(n, r, c);
+        try {
+            s.set_warm(0, warm);
+            s.start();
+            s.run_to_completion();
+            s.finish();
+        } catch (...) {
+            release_plan();  // a failed solve may leave the plan unusable
+            throw;
+        }
         const SolveResult R = s.result(0);
         if (R.w.empty()) throw Error(kDegenerate, "every edge weight is at or below the floor");
         fill_result(R, out, edges, weights, trace, note, note_cap);

@@ -1047,7 +1047,12 @@ void launch_oz_gemm(const OzGemm& g0, cudaStream_t st) {
     if (use_persistent(g.ld, g.nmat) && g.dstore && !g.dbg_t && !g.dbg_mode) {
         const int tpm = tiles_before(PT::R, g.ld / BM);
         cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(std::min(tpm * g.nmat, sm_count()));
+        // TPB_OZ_PGRID: SMs left free for concurrent streams (trace SLEM)
+        static const int spare = [] {
+            const char* e = std::getenv("TPB_OZ_PGRID");
+            return e ? std::max(0, std::atoi(e)) : 0;
+        }();
+        cfg.gridDim = dim3(std::min(tpm * g.nmat, std::max(1, sm_count() - spare)));
         cfg.blockDim = dim3(PT::THREADS);
         cfg.dynamicSmemBytes = PT::SMEM_BYTES;
         cfg.stream = st;

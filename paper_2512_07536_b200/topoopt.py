@@ -357,6 +357,13 @@ def _warm_arg(warm_start):
     return we, len(we)
 
 
+def release_solver_plans() -> None:
+    """Free this thread's cached solve plan (tp_release_plans): solve() keeps
+    the last solver's device buffers and captured graphs for the next call of
+    the same shape; results are bitwise those of a fresh solver."""
+    _check(_lib.load().tp_release_plans())
+
+
 def solve(n: int, r: int, cfg: SolverConfig | None = None, warm_start=None, **kw) -> Solution:
     """topoopt::solve (proj/src/admm.cpp:356-428)."""
     cfg = _config(cfg, kw)

@@ -151,3 +151,26 @@ def test_config3_golden(T, golden):
     tr = np.array(ref["trace"])[: len(rows)]
     assert np.max(np.abs(s.trace[rows, 2] - tr[:, 2])) < 1e-6   # lambda_tilde
     assert np.max(np.abs(s.trace[rows, 3] - tr[:, 3])) < 1e-6   # acf_iterate
+
+
+def test_solve_plan_cache_bitwise(T, golden):
+    """tp_solve reuses the thread's last solver plan (buffers + graphs) for the
+    same shape: a reused plan, with another warm start and another shape in
+    between, returns bitwise what a fresh solver returns."""
+    n, r = 64, 150
+    bu, e = T.allocate_edge_capacity([1.0] * n, r)
+    w0 = T.anneal_degree_topology(e, steps=1, moves_per_temp=1, seed=0)
+    w1 = T.anneal_degree_topology(e, steps=1, moves_per_temp=1, seed=1)
+    cfg = dict(rho=10.0, epsilon=1e-8, max_iter=300)
+    T.release_solver_plans()
+    fresh = T.solve(n, r, warm_start=w0, **cfg)
+    T.solve(n, r, warm_start=w1, **cfg)           # same plan, other state
+    again = T.solve(n, r, warm_start=w0, **cfg)
+    T.solve(16, 32, warm_start=golden("config1.json")["warm"], rho=10.0, epsilon=1e-8)  # evicts
+    third = T.solve(n, r, warm_start=w0, **cfg)
+    for s in (again, third):
+        assert s.iterations == fresh.iterations and s.converged == fresh.converged
+        assert np.array_equal(s.trace, fresh.trace)
+        assert s.edges.tolist() == fresh.edges.tolist() and np.array_equal(s.weights, fresh.weights)
+        assert s.acf_value == fresh.acf_value
+    T.release_solver_plans()
