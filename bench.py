@@ -9,7 +9,11 @@ independent restart (warm-start seed = rank): weak scaling, no collective on
 the data path; the barrier and the max-over-ranks timing use torch.distributed.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload n1024|sweep]
+                  [--workload n1024|sweep|sharded]
+
+`--workload sweep`: config 5 (256 independent n=256 solves, sharded across
+ranks). `--workload sharded`: one n=4096 instance whose cone projections are
+row-sharded over the ranks (NCCL all-gather; strong scaling).
 
 `--impl reference` times the reference's own CPU implementation (compiled
 from /root/reference into oracle/_ref) on the host cores, rank 0 only.
@@ -476,13 +480,85 @@ def run_sweep(args):
         tdist.destroy_process_group()
 
 
+def run_sharded(args):
+    """One large instance (default n=4096, r=4n) with its cone
+    projections row-sharded over the N ranks (tp_solver_set_comm: NCCL
+    all-gather of each product's row blocks, overlapped with the other
+    chain's GEMM); everything else replicated. Strong scaling: value = ADMM
+    iterations/s of the one instance."""
+    import torch
+    import torch.distributed as tdist
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    from paper_2512_07536_b200 import _lib
+    from paper_2512_07536_b200 import topoopt as T
+
+    _lib.load().tp_set_device(local)
+    if ws > 1:
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    comm = T.Comm.from_torch() if ws > 1 else None
+    n = args.shard_n
+    r = 4 * n
+    K, W = args.steps, args.warmup
+    warm = warm_start(T, n, r, 0)
+    bs = T.BatchSolver(n, r=[r], max_iter=W + K + 8, **CFG)
+    try:
+        if comm is not None:
+            bs.set_comm(comm)
+        bs.set_warm(0, warm)
+        bs.start()
+        stream = torch.cuda.ExternalStream(bs.stream)
+        bs.iterate(W)
+        bs.sync()
+        if ws > 1:
+            tdist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clk:
+            e0.record(stream)
+            bs.iterate(K)
+            e1.record(stream)
+            e1.synchronize()
+        t = e0.elapsed_time(e1) / 1e3
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        gemms = bs.bench_phase(0, 2)
+        b.record(stream)
+        b.synchronize()
+        t_proj = a.elapsed_time(b) / 1e3 / 2
+    finally:
+        bs.close()
+    if ws > 1:
+        tt = torch.tensor([t, t_proj], device="cuda", dtype=torch.float64)
+        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
+        t, t_proj = float(tt[0].item()), float(tt[1].item())
+    if rank == 0:
+        nb = ((n + 127) // 128)
+        per = nb // ws
+        tiles = (2 * nb * (nb + 1) // 2) if ws == 1 else per * (2 * nb - per + 1)
+        print(json.dumps({
+            "metric": "admm_iter_per_s_single_instance_sharded", "value": K / t, "unit": "iter/s",
+            "n_gpus": ws, "steps": K, "warmup": W, "ms_per_step": t / K * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"n{n}_single_instance_row_sharded", "n": n, "r": r, "rho": 10.0,
+                       "epsilon": 1e-8, "warm_start": "anneal_degree_topology(Alg.1, steps=1, moves=1)"},
+            "projection_ms": t_proj * 1e3, "gemm_launches_per_projection": gemms,
+            "lower_tiles_per_rank_per_matrix": tiles, "clocks": clk.summary()}), flush=True)
+    if comm is not None:
+        comm.close()
+    if ws > 1:
+        tdist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="n1024", choices=["n1024", "sweep"])
+    ap.add_argument("--workload", default="n1024", choices=["n1024", "sweep", "sharded"])
+    ap.add_argument("--shard-n", type=int, default=4096, help="sharded workload: instance size")
     ap.add_argument("--sweep-budgets", type=int, default=64)
     ap.add_argument("--sweep-max-iter", type=int, default=40000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -495,6 +571,8 @@ def main():
         run_reference(args)
     elif args.workload == "sweep":
         run_sweep(args)
+    elif args.workload == "sharded":
+        run_sharded(args)
     else:
         run_ours(args)
 

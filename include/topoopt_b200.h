@@ -138,6 +138,24 @@ int tp_solver_state(tp_solver* s, double** x, double** y, double** d);
  * so callers can time it with events; the state is left undefined. */
 int tp_solver_bench_phase(tp_solver* s, int32_t phase, int32_t reps, int32_t* launches_per_rep);
 int tp_solver_launches_per_iteration(tp_solver* s, int32_t* out);
+
+/* ------------------------------------------- sharded single large instance */
+/* one instance too large for one GPU's projection row-shards its
+ * cone-projection GEMMs over G ranks (one process per GPU): rank k computes
+ * the tiles of its n/G rows of every sign-iteration product, then an
+ * in-place NCCL all-gather over NVLink completes the iterate on every rank.
+ * Everything else is replicated; results are bitwise the single-GPU ones.
+ * The reference has no multi-GPU path (its solve is single-threaded,
+ * proj/src/admm.cpp:356-428); these calls extend the handle API.
+ * Requires n > 64 and (n rounded up to 128)/128 divisible by G. */
+#define TP_COMM_ID_BYTES 128
+typedef struct tp_comm tp_comm;
+int tp_comm_unique_id(uint8_t* id);                 /* rank 0; broadcast the bytes */
+int tp_comm_create(const uint8_t* id, int32_t nranks, int32_t rank, tp_comm** out);
+int tp_comm_destroy(tp_comm* c);
+int tp_solver_set_comm(tp_solver* s, tp_comm* c);   /* before tp_solver_start; NULL: unsharded */
+/* this rank's lower-tile indices of an ld x ld iterate (host helper) */
+int tp_shard_tiles(int32_t ld, int32_t nranks, int32_t rank, int32_t* tiles, int32_t* count);
 /* CG x-step statistics of solve b's last iteration (linear_solver = 1):
  * iterations and |r| / |h|. */
 int tp_solver_cg_stats(tp_solver* s, int32_t b, int32_t* iters, double* rel_res);

@@ -68,6 +68,11 @@ SIGNATURES = {
     "tp_version": (_I, []),
     "tp_set_device": (_I, [C.c_int]),
     "tp_release_plans": (_I, []),
+    "tp_comm_unique_id": (_I, [C.c_char_p]),
+    "tp_comm_create": (_I, [C.c_char_p, _I, _I, C.POINTER(_P)]),
+    "tp_comm_destroy": (_I, [_P]),
+    "tp_solver_set_comm": (_I, [_P, _P]),
+    "tp_shard_tiles": (_I, [_I, _I, _I, _ip, _ip]),
     "tp_solve": (_I, [_I, _I, _cfgp, _ip, _I, _resp, _ip, _dp, _dp, C.c_char_p, _I]),
     "tp_solve_het_node": (_I, [_I, _ip, _cfgp, _ip, _I, _resp, _ip, _dp, _dp, C.c_char_p, _I]),
     "tp_anneal_degree": (_I, [_I, _ip, _D, _D, _I, _I, _U64, _ip, _ip]),

@@ -11,6 +11,8 @@
 #include "anneal_kernels.cuh"
 #include "solver.cuh"
 
+#include "nccl_shim.hpp"
+
 using namespace tpb;
 
 namespace {
@@ -202,6 +204,58 @@ int tp_solver_result(tp_solver* s, int32_t b, tp_result* out, int32_t* edges, do
 }
 
 void* tp_solver_stream(tp_solver* s) { return (void*)s->s->stream(); }
+
+// ---------------------------------------------------------------- sharded single instance
+struct tp_comm {
+    ncclComm_t c = nullptr;
+    int nranks = 1, rank = 0;
+};
+
+int tp_comm_unique_id(uint8_t* id) {
+    return guarded([&] {
+        static_assert(sizeof(ncclUniqueId) == TP_COMM_ID_BYTES, "ncclUniqueId size");
+        ncclUniqueId u;
+        TPB_NCCL(nccl().get_unique_id(&u));
+        std::memcpy(id, &u, sizeof(u));
+    });
+}
+
+int tp_comm_create(const uint8_t* id, int32_t nranks, int32_t rank, tp_comm** out) {
+    return guarded([&] {
+        require_device();
+        if (nranks < 1 || rank < 0 || rank >= nranks) throw Error(kInvalidArgument, "tp_comm_create: bad rank");
+        ncclUniqueId u;
+        std::memcpy(&u, id, sizeof(u));
+        auto c = std::make_unique<tp_comm>();
+        TPB_NCCL(nccl().comm_init_rank(&c->c, nranks, u, rank));
+        c->nranks = nranks;
+        c->rank = rank;
+        *out = c.release();
+    });
+}
+
+int tp_comm_destroy(tp_comm* c) {
+    return guarded([&] {
+        if (!c) return;
+        if (c->c) nccl().comm_destroy(c->c);
+        delete c;
+    });
+}
+
+int tp_solver_set_comm(tp_solver* s, tp_comm* c) {
+    return guarded([&] {
+        if (c) s->s->set_shard(c->c, c->nranks, c->rank);
+        else s->s->set_shard(nullptr, 1, 0);
+    });
+}
+
+int tp_shard_tiles(int32_t ld, int32_t nranks, int32_t rank, int32_t* tiles, int32_t* count) {
+    return guarded([&] {
+        const std::vector<int> t = oz_shard_tiles(ld, nranks, rank);
+        if (tiles) std::copy(t.begin(), t.end(), tiles);
+        *count = (int32_t)t.size();
+    });
+}
 
 int tp_solver_dims(tp_solver* s, int32_t* d) {
     return guarded([&] {

@@ -37,6 +37,14 @@ struct Error : std::runtime_error {
 
 #define TPB_CHECK_LAUNCH() TPB_CUDA(cudaGetLastError())
 
+#define TPB_NCCL(call)                                                                   \
+    do {                                                                                 \
+        const int r_ = (int)(call);                                                      \
+        if (r_ != 0)                                                                     \
+            throw ::tpb::Error(::tpb::kCuda, std::string("NCCL error ") + std::to_string(r_) + \
+                                                 " at " + __FILE__ + ":" + std::to_string(__LINE__)); \
+    } while (0)
+
 // Host -> device copy that has landed when it returns. cudaMemcpy from
 // pageable memory may return before its DMA completes, and only the legacy
 // stream is ordered after it -- the solver's non-blocking streams are not.

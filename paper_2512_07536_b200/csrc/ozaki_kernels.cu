@@ -15,6 +15,8 @@
 // The KS accumulator groups (KS x 64 int32 columns) fill TMEM's 512 columns.
 #include "ozaki_kernels.cuh"
 
+#include "nccl_shim.hpp"
+
 #include "cone_kernels.cuh"
 
 #include <algorithm>
@@ -277,11 +279,11 @@ __global__ void __launch_bounds__(TL::THREADS, TL::MIN_BLOCKS)
     constexpr int BB = TL::BB, NBOX = TL::NBOX;
     constexpr int A_PLANE = TL::A_PLANE, B_PLANE = TL::B_PLANE, STAGE_BYTES = TL::STAGE_BYTES;
     constexpr int TMEM_COLS = TL::TMEM_COLS;
-    const int mat = blockIdx.y;
+    const int mat = g.mstep ? blockIdx.y * g.mstep + g.moff : blockIdx.y;
     if (g.ictl && g.ictl[(mat >> 1) * 8 + 1]) return;
     const long long t_start = g.dbg_t ? gtimer() : 0;
     int I, J;
-    oz_tile(R, blockIdx.x, I, J);
+    oz_tile(R, g.tiles ? g.tiles[blockIdx.x] : blockIdx.x, I, J);
     const int i0 = I * BM, j0 = J * BN;
     const int ld = g.ld;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1044,7 +1046,7 @@ void launch_oz_gemm(const OzGemm& g0, cudaStream_t st) {
     OzGemm g = g0;
     g.dstore = dstore_mode();
     if (g.Cd && !g.mc) throw Error(kInvalidArgument, "ozaki GEMM: digit output needs its TMA map");
-    if (use_persistent(g.ld, g.nmat) && g.dstore && !g.dbg_t && !g.dbg_mode) {
+    if (use_persistent(g.ld, g.nmat) && g.dstore && !g.dbg_t && !g.dbg_mode && !g.tiles && g.mstep <= 1) {
         const int tpm = tiles_before(PT::R, g.ld / BM);
         cudaLaunchConfig_t cfg{};
         // TPB_OZ_PGRID: SMs left free for concurrent streams (trace SLEM)
@@ -1064,9 +1066,10 @@ void launch_oz_gemm(const OzGemm& g0, cudaStream_t st) {
         TPB_CUDA(cudaLaunchKernelEx(&cfg, oz_gemm_pkernel, g.ma->a, g.mb->bp, g, tpm));
         return;
     }
-    const bool small = use_small_tiles(g.ld, g.nmat);
+    const bool small = use_small_tiles(g.ld, g.nmat) && !g.tiles;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(small ? tiles_before(TileS::R, g.ld / BM) : oz_gemm_tiles(g.ld), g.nmat);
+    cfg.gridDim = dim3(g.tiles ? g.ntiles : small ? tiles_before(TileS::R, g.ld / BM) : oz_gemm_tiles(g.ld),
+                       g.mstep > 1 ? (g.nmat - g.moff + g.mstep - 1) / g.mstep : g.nmat);
     cfg.blockDim = dim3(small ? TileS::THREADS : TileL::THREADS);
     cfg.dynamicSmemBytes = small ? TileS::SMEM_BYTES : TileL::SMEM_BYTES;
     cfg.stream = st;
@@ -1115,10 +1118,46 @@ SignSchedule ozaki_schedule() {
     return s;
 }
 
+std::vector<int> oz_shard_tiles(int ld, int nranks, int rank) {
+    const int NB = ld / BM, R = TileL::R;
+    if (ld % BM || nranks < 1 || NB % nranks || rank < 0 || rank >= nranks)
+        throw Error(kInvalidArgument, "sharded projection: ld/128 must be a multiple of the rank count");
+    const int per = NB / nranks;
+    std::vector<int> t;
+    for (int I = rank * per; I < (rank + 1) * per; ++I) {
+        for (int J = 0; J < R * (I + 1); ++J) t.push_back(tiles_before(R, I) + J);  // rows of block I
+        for (int I2 = I + 1; I2 < NB; ++I2)                                         // mirrors into it
+            for (int J = R * I; J < R * (I + 1); ++J) t.push_back(tiles_before(R, I2) + J);
+    }
+    // a tile below the diagonal inside the rank's rows serves both lists
+    std::sort(t.begin(), t.end());
+    t.erase(std::unique(t.begin(), t.end()), t.end());
+    return t;
+}
+
+namespace {
+// in-place all-gather of the row blocks of every plane of the matrices
+// moff, moff + 2, ... (one NCCL group)
+void shard_allgather(const OzShard& sh, int8_t* planes, int ld, int nmat, int moff, cudaStream_t st) {
+    const size_t count = (size_t)(ld / sh.nranks) * ld;
+    const size_t pstride = (size_t)ld * ld;
+    ncclComm_t comm = static_cast<ncclComm_t>(sh.comm);
+    TPB_NCCL(nccl().group_start());
+    for (int mat = moff; mat < nmat; mat += 2)
+        for (int q = 0; q < KS; ++q) {
+            int8_t* base = planes + ((size_t)mat * KS + q) * pstride;
+            TPB_NCCL(nccl().all_gather(base + (size_t)sh.rank * count, base, count, ncclInt8, comm, st));
+        }
+    TPB_NCCL(nccl().group_end());
+}
+}  // namespace
+
 void enqueue_cone_ozaki(const double* A, double* /*w0*/, double* /*w1*/, double* /*w2*/, const OzWork& oz,
                         int ld, int n, const double* scale, double* C, long long c_stride_b,
                         long long c_stride_w, const int* ictl, int nmat, const SignSchedule& sch,
-                        cudaStream_t st) {
+                        cudaStream_t st, const OzShard* shard) {
+    const bool sharded = shard && shard->nranks > 1;
+    bool ag_pending[2] = {false, false};
     const long long ms = (long long)ld * ld;
     launch_oz_split(A, ms, ld, nmat, scale, kEX0, oz.d[3], ictl, st);
     const double beta = sch.qb / (2.0 * sch.qc);
@@ -1139,7 +1178,26 @@ void enqueue_cone_ozaki(const double* A, double* /*w0*/, double* /*w1*/, double*
         g.Cd = oz.d[od];
         g.mc = &oz.maps[od];
         g.eC = ec;
-        launch_oz_gemm(g, st);
+        if (!sharded) {
+            launch_oz_gemm(g, st);
+            return;
+        }
+        // chain par's product waits for its operands' all-gather only; its
+        // own all-gather then overlaps the other chain's GEMM
+        g.tiles = shard->tiles;
+        g.ntiles = shard->ntiles;
+        g.no_pdl = 1;
+        g.mstep = 2;
+        for (int par = 0; par < 2; ++par) {
+            if (ag_pending[par]) TPB_CUDA(cudaStreamWaitEvent(st, shard->ag_done[par], 0));
+            g.moff = par;
+            launch_oz_gemm(g, st);
+            TPB_CUDA(cudaEventRecord(shard->gemm_done[par], st));
+            TPB_CUDA(cudaStreamWaitEvent(shard->cs, shard->gemm_done[par], 0));
+            shard_allgather(*shard, oz.d[od], ld, nmat, par, shard->cs);
+            TPB_CUDA(cudaEventRecord(shard->ag_done[par], shard->cs));
+            ag_pending[par] = true;
+        }
     };
     int x = 3;  // digit buffer holding X (3: X0)
     auto others = [&](int& f0, int& f1) {
@@ -1183,6 +1241,13 @@ void enqueue_cone_ozaki(const double* A, double* /*w0*/, double* /*w1*/, double*
     g.nvalid = n;
     g.Cd = nullptr;
     g.mc = nullptr;
+    g.tiles = nullptr;  // the FP64 product is replicated
+    g.ntiles = 0;
+    g.mstep = 0;
+    g.moff = 0;
+    g.no_pdl = 0;
+    for (int par = 0; par < 2; ++par)
+        if (ag_pending[par]) TPB_CUDA(cudaStreamWaitEvent(st, shard->ag_done[par], 0));
     launch_oz_gemm(g, st);
 }
 

@@ -15,6 +15,7 @@
 #include <cuda.h>
 
 #include <cstdint>
+#include <vector>
 
 #include "common.cuh"
 
@@ -62,6 +63,10 @@ struct OzGemm {
     int dbg_mode;            // instrumentation: bit 0 skips the MMAs, bit 1 the TMA loads
     int no_pdl;              // launch without programmatic dependent launch
     int dstore;              // digit planes by direct 16-byte global stores (else TMA stores)
+    const int* tiles;        // row-sharded products: this rank's lower-tile indices, or null (all)
+    int ntiles;              // entries of tiles
+    int mstep;               // matrices of this launch: blockIdx.y * mstep + moff (mstep 0 -> 1)
+    int moff;
 };
 
 void launch_oz_gemm(const OzGemm& g, cudaStream_t st);
@@ -76,12 +81,36 @@ struct OzWork {
     OzMaps maps[4];
 };
 
+// Row-sharded projection of one large instance over G ranks:
+// rank k owns the 128-row blocks [k NB/G, (k+1) NB/G) of every iterate. Its
+// tiles are the lower tiles of those row blocks plus the lower tiles whose
+// mirror lands in them, so its rows are complete after its GEMM; an
+// in-place NCCL all-gather of the row blocks of every digit plane then gives
+// every rank the whole iterate. The same kernel computes every tile, so the
+// result is bitwise the single-GPU one. (The final FP64 product is
+// replicated.)
+// The S (even matrices) and T (odd) chains of the sign iteration are
+// independent, so each product runs as two launches and one chain's
+// all-gather (comm stream) overlaps the other chain's GEMM.
+struct OzShard {
+    int rank = 0, nranks = 1;
+    void* comm = nullptr;    // ncclComm_t
+    int* tiles = nullptr;    // device: this rank's tile indices
+    int ntiles = 0;
+    cudaStream_t cs = nullptr;                    // all-gathers
+    cudaEvent_t gemm_done[2] = {nullptr, nullptr};  // per chain
+    cudaEvent_t ag_done[2] = {nullptr, nullptr};
+};
+// Host tile list of `rank` for an ld x ld iterate (ld % 128 == 0, ld/128 % nranks == 0).
+std::vector<int> oz_shard_tiles(int ld, int nranks, int rank);
+
 struct SignSchedule;
 // Ozaki-scheme counterpart of enqueue_cone_tiled (cone_kernels.cuh): the
 // same sign iteration, every product on the int8 tensor cores.
 void enqueue_cone_ozaki(const double* A, double* w0, double* w1, double* w2, const OzWork& oz, int ld,
                         int n, const double* scale, double* C, long long c_stride_b, long long c_stride_w,
-                        const int* ictl, int nmat, const SignSchedule& sch, cudaStream_t st);
+                        const int* ictl, int nmat, const SignSchedule& sch, cudaStream_t st,
+                        const OzShard* shard = nullptr);
 
 // Digit planes of s * A (s = scale[mat] or 1) with exponent e.
 void launch_oz_split(const double* A, long long mstride, int ld, int nmat, const double* scale,

@@ -219,6 +219,14 @@ Solver::~Solver() {
     cudaStreamSynchronize(s0_);
     phase_mark("free");
     if (h_ctl_) pinned_give(h_ctl_, (size_t)B_ * 8 * sizeof(int));
+    if (shard_.cs) {
+        cudaStreamSynchronize(shard_.cs);
+        for (int q = 0; q < 2; ++q) {
+            cudaEventDestroy(shard_.gemm_done[q]);
+            cudaEventDestroy(shard_.ag_done[q]);
+        }
+        cudaStreamDestroy(shard_.cs);
+    }
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_sel_) cudaEventDestroy(ev_sel_);
     if (ev_slem_) cudaEventDestroy(ev_slem_);
@@ -519,11 +527,40 @@ void Solver::enqueue_projection() {
                           2 * B_, sch_, s0_);
     } else if (ozaki_) {
         enqueue_cone_ozaki(d_.A, w0_, w1_, w2_, oz_, ld_, lo_.n, d_.inv_scale, d_.Y + lo_.off_s, cb, cw,
-                           d_.ictl, 2 * B_, sch_, s0_);
+                           d_.ictl, 2 * B_, sch_, s0_, sharded() ? &shard_ : nullptr);
     } else {
         enqueue_cone_tiled(d_.A, w0_, w1_, w2_, ld_, lo_.n, d_.inv_scale, d_.Y + lo_.off_s, cb, cw,
                            d_.ictl, 2 * B_, sch_, s0_, sk_ws_, sk_flags_);
     }
+}
+
+void Solver::set_shard(void* comm, int nranks, int rank) {
+    if (nranks <= 1) {
+        shard_.nranks = 1;
+        shard_.rank = 0;
+        shard_.comm = nullptr;
+    } else {
+        if (!ozaki_) throw Error(kInvalidArgument, "sharded projection: needs the tiled Ozaki path (n > 64)");
+        const std::vector<int> t = oz_shard_tiles(ld_, nranks, rank);
+        shard_.rank = rank;
+        shard_.nranks = nranks;
+        shard_.comm = comm;
+        shard_.ntiles = (int)t.size();
+        if (!shard_.cs) {
+            TPB_CUDA(cudaStreamCreateWithFlags(&shard_.cs, cudaStreamNonBlocking));
+            for (int q = 0; q < 2; ++q) {
+                TPB_CUDA(cudaEventCreateWithFlags(&shard_.gemm_done[q], cudaEventDisableTiming));
+                TPB_CUDA(cudaEventCreateWithFlags(&shard_.ag_done[q], cudaEventDisableTiming));
+            }
+        }
+        shard_.tiles = dalloc<int>(s0_, allocs_, t.size());
+        TPB_CUDA(cudaStreamSynchronize(s0_));
+        h2d(shard_.tiles, t.data(), t.size() * sizeof(int));
+    }
+    // graphs captured before hold the old projection
+    if (g_chunk_) cudaGraphExecDestroy(g_chunk_);
+    if (g_one_) cudaGraphExecDestroy(g_one_);
+    g_chunk_ = g_one_ = nullptr;
 }
 
 void Solver::enqueue_iteration(bool with_slem) {

@@ -101,6 +101,11 @@ class Solver {
     // CG statistics of the last x-step of solve b: iterations, |r|/|h|
     void cg_stats(int b, int* iters, double* rel_res);
     int launches_per_iteration() const;
+    // Row-shard the cone projections of this (replicated) solver over an NCCL
+    // communicator of nranks ranks (OzShard, ozaki_kernels.cuh). Every rank
+    // runs the same solves; results are bitwise the single-GPU ones.
+    void set_shard(void* nccl_comm, int nranks, int rank);
+    bool sharded() const { return shard_.nranks > 1; }
 
    private:
     void alloc();
@@ -140,6 +145,7 @@ class Solver {
     unsigned long long* cap_keys_ = nullptr;
     int *cap_idx_ = nullptr, *cap_load_ = nullptr;
     OzWork oz_;
+    OzShard shard_;
     double* sk_ws_ = nullptr;   // stream-K partial tiles (B == 1, large n)
     int* sk_flags_ = nullptr;
     int *list_ = nullptr, *list_count_ = nullptr;

@@ -632,6 +632,51 @@ def extract_topology(n: int, r: int, g, weight_floor: float = 1e-6):
 
 
 # ---------------------------------------------------------------- batched handle
+COMM_ID_BYTES = 128
+
+
+class Comm:
+    """NCCL communicator of the sharded single-instance projection
+    (tp_comm_*): one process per GPU; rank 0 makes the id, every rank
+    creates the communicator with the same bytes."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(COMM_ID_BYTES)
+        _check(_lib.load().tp_comm_unique_id(buf))
+        return buf.raw
+
+    def __init__(self, uid: bytes, nranks: int, rank: int):
+        h = C.c_void_p()
+        _check(_lib.load().tp_comm_create(uid, nranks, rank, C.byref(h)))
+        self.h, self.nranks, self.rank = h, nranks, rank
+
+    @classmethod
+    def from_torch(cls):
+        """Bootstrap over an initialised torch.distributed process group."""
+        import torch.distributed as dist
+        obj = [cls.unique_id() if dist.get_rank() == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return cls(obj[0], dist.get_world_size(), dist.get_rank())
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.load().tp_comm_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+
+def shard_tiles(ld: int, nranks: int, rank: int) -> np.ndarray:
+    """Lower-tile indices rank `rank` computes in a row-sharded projection
+    (tp_shard_tiles; host logic, no device needed)."""
+    cnt = C.c_int32(0)
+    _check(_lib.load().tp_shard_tiles(ld, nranks, rank, None, C.byref(cnt)))
+    out = np.zeros(max(cnt.value, 1), np.int32)
+    _check(_lib.load().tp_shard_tiles(ld, nranks, rank, _ip(out), C.byref(cnt)))
+    return out[: cnt.value].copy()
+
+
 class BatchSolver:
     """Independent solves of one n in lockstep on the current device
     (tp_solver_*): edge-budget sweeps, bandwidth scenarios, restarts."""
@@ -667,6 +712,11 @@ class BatchSolver:
     def set_warm(self, b: int, edges):
         e = _i32(np.asarray(edges, np.int32).reshape(-1, 2))
         _check(_lib.load().tp_solver_set_warm(self.h, b, _ip(e), len(e)))
+
+    def set_comm(self, comm: "Comm | None"):
+        """Row-shard the cone projections over `comm` (tp_solver_set_comm);
+        call before start(). Every rank runs the same solves."""
+        _check(_lib.load().tp_solver_set_comm(self.h, comm.h if comm is not None else None))
 
     def start(self):
         _check(_lib.load().tp_solver_start(self.h))
