@@ -325,7 +325,10 @@ __global__ void __launch_bounds__(TL::THREADS, TL::MIN_BLOCKS)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const uint32_t tmem = tmem_slot;
     const int KB = ld / BK;
-    const long long plane_rows = (long long)mat * KS * ld;
+    const int rc = g.rc ? g.rc : ld;  // plane layout (OzShard)
+    // plane row of (slice 0, row i): slice s adds s * rc
+    auto prow = [&](int i) { return (long long)mat * KS * ld + (long long)(i / rc) * KS * rc + i % rc; };
+    const long long a_row0 = prow(i0), b_row0 = prow(j0);
 
     if (warp == 0) {
         if (lane == 0) {
@@ -340,10 +343,8 @@ __global__ void __launch_bounds__(TL::THREADS, TL::MIN_BLOCKS)
                 mbar_expect_tx(full_bar(st), STAGE_BYTES);
 #pragma unroll 1
                 for (int s = 0; s < KS; ++s) {
-                    tma_load_2d(a_tile(st, s), &mapA, full_bar(st), kb * BK,
-                                (int)(plane_rows + (long long)s * ld + i0));
-                    tma_load_2d(b_tile(st, s), &mapB, full_bar(st), kb * BK,
-                                (int)(plane_rows + (long long)s * ld + j0));
+                    tma_load_2d(a_tile(st, s), &mapA, full_bar(st), kb * BK, (int)(a_row0 + (long long)s * rc));
+                    tma_load_2d(b_tile(st, s), &mapB, full_bar(st), kb * BK, (int)(b_row0 + (long long)s * rc));
                 }
             }
         }
@@ -479,8 +480,7 @@ __global__ void __launch_bounds__(TL::THREADS, TL::MIN_BLOCKS)
             // then 16-byte stores, four lanes per 64-byte row segment.
             constexpr int NCB = BN / 4;              // column blocks
             const double s28 = ldexp(1.0, 28 - g.eC);
-            int8_t* base = g.Cd + (long long)mat * KS * ld * ld;
-            const long long pstride = (long long)ld * ld;
+            const long long pstride = (long long)rc * ld;  // next slice of the same row
             uint32_t* Dg = reinterpret_cast<uint32_t*>(sgen + TL::CS_BYTES);  // [KS][BM][NCB]
             uint32_t sink = 0;
             const bool nost = (g.dbg_mode & 4) != 0;  // instrumentation: split without the stores
@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(TL::THREADS, TL::MIN_BLOCKS)
                 }
                 if (r0 >= mr0) {
                     // plane-0 address of mirror row j0 + 4 cb, bytes i0 + r0..
-                    int8_t* mp = base + (long long)(j0 + 4 * cb) * ld + i0 + r0;
+                    int8_t* mp = g.Cd + prow(j0 + 4 * cb) * ld + i0 + r0;
 #pragma unroll
                     for (int s2 = 0; s2 < KS; ++s2, mp += pstride) {
                         const uint32_t rows[4] = {w[0][s2], w[1][s2], w[2][s2], w[3][s2]};
@@ -529,7 +529,7 @@ __global__ void __launch_bounds__(TL::THREADS, TL::MIN_BLOCKS)
                 const int f = (rr >> 2) & (NCB - 1);
                 const int k0 = (4 * c4) ^ f, k1 = (4 * c4 + 1) ^ f, k2 = (4 * c4 + 2) ^ f, k3 = (4 * c4 + 3) ^ f;
                 const uint32_t* src = Dg + rr * NCB;
-                int8_t* dp = base + (long long)(i0 + rr) * ld + j0 + 16 * c4;
+                int8_t* dp = g.Cd + prow(i0 + rr) * ld + j0 + 16 * c4;
 #pragma unroll
                 for (int s2 = 0; s2 < KS; ++s2, src += BM * NCB, dp += pstride) {
                     const uint4 v = make_uint4(src[k0], src[k1], src[k2], src[k3]);
@@ -537,7 +537,7 @@ __global__ void __launch_bounds__(TL::THREADS, TL::MIN_BLOCKS)
                     *reinterpret_cast<uint4*>(dp) = v;
                 }
             }
-            if (nost && sink == 0x9E3779B9u) base[0] = 1;  // keep the split live
+            if (nost && sink == 0x9E3779B9u) g.Cd[0] = 1;  // keep the split live
         } else if (g.Cd) {
             // digit planes staged in the TMA-store layout: direct boxes
             // [s][h] (tile rows BB h.., the BN columns) and mirror boxes [s][h]
@@ -908,7 +908,7 @@ __global__ void __maxnreg__(152)
 
 // Digit planes of s A, 4 consecutive row elements per thread.
 __global__ void oz_split_kernel(const double* A, long long mstride, int ld, const double* scale,
-                                int e, int8_t* planes, const int* ictl) {
+                                int e, int8_t* planes, const int* ictl, int rc) {
     const int mat = blockIdx.y;
     if (ictl && ictl[(mat >> 1) * 8 + 1]) return;
     const long long n4 = (long long)ld * ld / 4;
@@ -925,9 +925,11 @@ __global__ void oz_split_kernel(const double* A, long long mstride, int ld, cons
         put_digits(v.y, s, 1, w);
         put_digits(v.z, s, 2, w);
         put_digits(v.w, s, 3, w);
+        const long long e0 = idx * 4;
+        const int i = (int)(e0 / ld), c = (int)(e0 - (long long)i * ld);
+        int8_t* o = out + ((long long)(i / rc) * KS * rc + i % rc) * ld + c;  // slice 0 (OzShard layout)
 #pragma unroll
-        for (int k = 0; k < KS; ++k)
-            reinterpret_cast<uint32_t*>(out + (long long)k * ld * ld)[idx] = w[k];
+        for (int k = 0; k < KS; ++k) *reinterpret_cast<uint32_t*>(o + (long long)k * rc * ld) = w[k];
     }
 }
 
@@ -1045,8 +1047,10 @@ int dstore_mode() {
 void launch_oz_gemm(const OzGemm& g0, cudaStream_t st) {
     OzGemm g = g0;
     g.dstore = dstore_mode();
+    if (g.rc && g.rc != g.ld) g.dstore = 1;  // chunked planes: direct stores only
     if (g.Cd && !g.mc) throw Error(kInvalidArgument, "ozaki GEMM: digit output needs its TMA map");
-    if (use_persistent(g.ld, g.nmat) && g.dstore && !g.dbg_t && !g.dbg_mode && !g.tiles && g.mstep <= 1) {
+    if (use_persistent(g.ld, g.nmat) && g.dstore && !g.dbg_t && !g.dbg_mode && !g.tiles && g.mstep <= 1 &&
+        (!g.rc || g.rc == g.ld)) {
         const int tpm = tiles_before(PT::R, g.ld / BM);
         cudaLaunchConfig_t cfg{};
         // TPB_OZ_PGRID: SMs left free for concurrent streams (trace SLEM)
@@ -1086,10 +1090,10 @@ void launch_oz_gemm(const OzGemm& g0, cudaStream_t st) {
 }
 
 void launch_oz_split(const double* A, long long mstride, int ld, int nmat, const double* scale, int e,
-                     int8_t* planes, const int* ictl, cudaStream_t st) {
+                     int8_t* planes, const int* ictl, cudaStream_t st, int rc) {
     const long long n4 = (long long)ld * ld / 4;
     const int blocks = (int)std::min<long long>((n4 + 255) / 256, 1024);
-    oz_split_kernel<<<dim3(blocks, nmat), 256, 0, st>>>(A, mstride, ld, scale, e, planes, ictl);
+    oz_split_kernel<<<dim3(blocks, nmat), 256, 0, st>>>(A, mstride, ld, scale, e, planes, ictl, rc ? rc : ld);
     TPB_CHECK_LAUNCH();
 }
 
@@ -1139,15 +1143,14 @@ namespace {
 // in-place all-gather of the row blocks of every plane of the matrices
 // moff, moff + 2, ... (one NCCL group)
 void shard_allgather(const OzShard& sh, int8_t* planes, int ld, int nmat, int moff, cudaStream_t st) {
-    const size_t count = (size_t)(ld / sh.nranks) * ld;
-    const size_t pstride = (size_t)ld * ld;
+    // row-chunk-major planes: the rank's rows of all KS planes are one block
+    const size_t count = (size_t)KS * (ld / sh.nranks) * ld;
     ncclComm_t comm = static_cast<ncclComm_t>(sh.comm);
     TPB_NCCL(nccl().group_start());
-    for (int mat = moff; mat < nmat; mat += 2)
-        for (int q = 0; q < KS; ++q) {
-            int8_t* base = planes + ((size_t)mat * KS + q) * pstride;
-            TPB_NCCL(nccl().all_gather(base + (size_t)sh.rank * count, base, count, ncclInt8, comm, st));
-        }
+    for (int mat = moff; mat < nmat; mat += 2) {
+        int8_t* base = planes + (size_t)mat * KS * ld * ld;
+        TPB_NCCL(nccl().all_gather(base + (size_t)sh.rank * count, base, count, ncclInt8, comm, st));
+    }
     TPB_NCCL(nccl().group_end());
 }
 }  // namespace
@@ -1157,9 +1160,10 @@ void enqueue_cone_ozaki(const double* A, double* /*w0*/, double* /*w1*/, double*
                         long long c_stride_w, const int* ictl, int nmat, const SignSchedule& sch,
                         cudaStream_t st, const OzShard* shard) {
     const bool sharded = shard && shard->nranks > 1;
+    const int rc = sharded ? ld / shard->nranks : 0;
     bool ag_pending[2] = {false, false};
     const long long ms = (long long)ld * ld;
-    launch_oz_split(A, ms, ld, nmat, scale, kEX0, oz.d[3], ictl, st);
+    launch_oz_split(A, ms, ld, nmat, scale, kEX0, oz.d[3], ictl, st, rc);
     const double beta = sch.qb / (2.0 * sch.qc);
     const double gamma = sch.qa - sch.qb * sch.qb / (4.0 * sch.qc);
     OzGemm g{};
@@ -1167,6 +1171,7 @@ void enqueue_cone_ozaki(const double* A, double* /*w0*/, double* /*w1*/, double*
     g.nmat = nmat;
     g.scale = scale;
     g.ictl = ictl;
+    g.rc = rc;
     // one product of digit buffers ia, ib into digit buffer od
     auto step = [&](int ia, int ea, int ib, int eb, double al, double shift, int od, int ec) {
         g.ma = &oz.maps[ia];

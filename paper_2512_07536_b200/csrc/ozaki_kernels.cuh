@@ -67,6 +67,7 @@ struct OzGemm {
     int ntiles;              // entries of tiles
     int mstep;               // matrices of this launch: blockIdx.y * mstep + moff (mstep 0 -> 1)
     int moff;
+    int rc;                  // plane layout: rows per chunk (0 -> ld; see OzShard)
 };
 
 void launch_oz_gemm(const OzGemm& g, cudaStream_t st);
@@ -89,6 +90,10 @@ struct OzWork {
 // every rank the whole iterate. The same kernel computes every tile, so the
 // result is bitwise the single-GPU one. (The final FP64 product is
 // replicated.)
+// Sharded runs store each matrix's planes row-chunk-major,
+// [mat][chunk][slice][rc rows][ld] with rc = ld / G (rc = ld is the plain
+// [mat][slice][ld][ld] layout), so a rank's rows of all eight planes are one
+// contiguous block: one all-gather per matrix. Tiles never straddle chunks.
 // The S (even matrices) and T (odd) chains of the sign iteration are
 // independent, so each product runs as two launches and one chain's
 // all-gather (comm stream) overlaps the other chain's GEMM.
@@ -112,8 +117,8 @@ void enqueue_cone_ozaki(const double* A, double* w0, double* w1, double* w2, con
                         const int* ictl, int nmat, const SignSchedule& sch, cudaStream_t st,
                         const OzShard* shard = nullptr);
 
-// Digit planes of s * A (s = scale[mat] or 1) with exponent e.
+// Digit planes of s * A (s = scale[mat] or 1) with exponent e (layout rc as in OzGemm).
 void launch_oz_split(const double* A, long long mstride, int ld, int nmat, const double* scale,
-                     int e, int8_t* planes, const int* ictl, cudaStream_t st);
+                     int e, int8_t* planes, const int* ictl, cudaStream_t st, int rc = 0);
 
 }  // namespace tpb

@@ -403,7 +403,7 @@ void Solver::start() {
     TPB_CUDA(cudaMemcpyAsync(d_.Y, d_.X, B * nx * sizeof(double), cudaMemcpyDeviceToDevice, s0_));
     TPB_CUDA(cudaMemcpyAsync(d_.bestY, d_.X, B * nx * sizeof(double), cudaMemcpyDeviceToDevice, s0_));
     TPB_CUDA(cudaStreamSynchronize(s0_));
-    if (!g_chunk_) build_graphs();
+    if (!g_chunk_ && !eager()) build_graphs();
     phase_mark("graph capture");
     it_enqueued_ = 0;
 }
@@ -547,7 +547,11 @@ void Solver::set_shard(void* comm, int nranks, int rank) {
         shard_.comm = comm;
         shard_.ntiles = (int)t.size();
         if (!shard_.cs) {
-            TPB_CUDA(cudaStreamCreateWithFlags(&shard_.cs, cudaStreamNonBlocking));
+            // highest priority: as GEMM CTAs retire, the SMs go to the
+            // all-gather's CTAs first, so it overlaps the other chain's GEMM
+            int lo = 0, hi = 0;
+            TPB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            TPB_CUDA(cudaStreamCreateWithPriority(&shard_.cs, cudaStreamNonBlocking, hi));
             for (int q = 0; q < 2; ++q) {
                 TPB_CUDA(cudaEventCreateWithFlags(&shard_.gemm_done[q], cudaEventDisableTiming));
                 TPB_CUDA(cudaEventCreateWithFlags(&shard_.ag_done[q], cudaEventDisableTiming));
@@ -621,7 +625,25 @@ void Solver::build_graphs() {
     g_one_ = capture(1, false);
 }
 
+// Sharded solvers launch their iterations eagerly: the all-gathers' stream
+// priority (SMs to the NCCL CTAs first) does not survive graph capture, and
+// at the sizes that shard a launch is ~0.01 % of an iteration. Same
+// iteration sequence as the graphs (TPB_SHARD_GRAPH=1 keeps the graphs).
+bool Solver::eager() const { return sharded() && !std::getenv("TPB_SHARD_GRAPH"); }
+
 void Solver::iterate_async(int k) {
+    if (eager()) {
+        while (k >= chunk_) {
+            for (int j = 0; j < chunk_; ++j) enqueue_iteration(j % cfg_.trace_stride == 0);
+            k -= chunk_;
+            it_enqueued_ += chunk_;
+        }
+        while (k-- > 0) {
+            enqueue_iteration(cfg_.trace_stride == 1);
+            ++it_enqueued_;
+        }
+        return;
+    }
     while (k >= chunk_) {
         TPB_CUDA(cudaGraphLaunch(g_chunk_, s0_));
         k -= chunk_;

@@ -106,6 +106,7 @@ class Solver {
     // runs the same solves; results are bitwise the single-GPU ones.
     void set_shard(void* nccl_comm, int nranks, int rank);
     bool sharded() const { return shard_.nranks > 1; }
+    bool eager() const;  // iterations launched without graphs (sharded)
 
    private:
     void alloc();
