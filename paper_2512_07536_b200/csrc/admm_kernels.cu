@@ -278,7 +278,7 @@ void launch_frob_finalize(const Dev& d, cudaStream_t st) {
 // ---------------------------------------------------------------- x-step A
 // h_g(i,j) = r_g + s (4 - R_ii - R_jj + R_ij + R_ji + v2_i + v2_j) [- s r_nu]
 // with r = Y - (D + c)/rho, R = r_S + r_T, v2 = 1 - r_y.
-__global__ void __launch_bounds__(TB* TY) xstep_a_kernel(Dev d, XConst c) {
+__global__ void __launch_bounds__(TB* TY, 4) xstep_a_kernel(Dev d, XConst c) {
     const int b = blockIdx.y;
     if (solve_done(d, b)) return;
     int bi, bj;
@@ -313,6 +313,22 @@ __global__ void __launch_bounds__(TB* TY) xstep_a_kernel(Dev d, XConst c) {
         for (int k = 0; k < NE; ++k)
             out[k] = ok[k] ? (ys[k] - ds[k] * c.inv_rho) + (yt[k] - dt[k] * c.inv_rho) : 0.0;
     };
+    // diagonals and v2 of both node blocks: issued first, so their latency
+    // overlaps the block loads instead of following them
+    double dgi = 0.0, dgj = 0.0, v2vi = 0.0, v2vj = 0.0;
+    if (ty == 0) {
+        const int i = i0 + tx, j = j0 + tx;
+        if (i < n) {
+            const long long p = (long long)i * n + i;
+            dgi = rS(p) + rT(p);
+            v2vi = 1.0 - (Y[lo.off_y + i] - D[lo.off_y + i] * c.inv_rho);
+        }
+        if (j < n) {
+            const long long p = (long long)j * n + j;
+            dgj = rS(p) + rT(p);
+            v2vj = 1.0 - (Y[lo.off_y + j] - D[lo.off_y + j] * c.inv_rho);
+        }
+    }
     // both orientations' loads are issued before any use: orientation 1
     // R(i, j) at j*n + i, orientation 2 R(j, i) at i*n + j
     long long pos1[NE], pos2[NE];
@@ -351,19 +367,11 @@ __global__ void __launch_bounds__(TB* TY) xstep_a_kernel(Dev d, XConst c) {
     }
 #pragma unroll
     for (int k = 0; k < NE; ++k) Rs[tx][ty + k * TY] = v1[k];
-    // diagonals and v2 for both node blocks
     if (ty == 0) {
-        const int i = i0 + tx, j = j0 + tx;
-        if (i < n) {
-            const long long p = (long long)i * n + i;
-            rd_i[tx] = rS(p) + rT(p);
-            v2_i[tx] = 1.0 - (Y[lo.off_y + i] - D[lo.off_y + i] * c.inv_rho);
-        }
-        if (j < n) {
-            const long long p = (long long)j * n + j;
-            rd_j[tx] = rS(p) + rT(p);
-            v2_j[tx] = 1.0 - (Y[lo.off_y + j] - D[lo.off_y + j] * c.inv_rho);
-        }
+        rd_i[tx] = dgi;
+        v2_i[tx] = v2vi;
+        rd_j[tx] = dgj;
+        v2_j[tx] = v2vj;
     }
     __syncthreads();
     // orientation 2 (loaded above)
@@ -999,7 +1007,7 @@ void launch_xstep_cg(const Dev& d, const XConst& c, cudaStream_t st) {
 }
 
 // ---------------------------------------------------------------- x-step B
-__global__ void __launch_bounds__(TB* TY) xstep_b_kernel(Dev d, XConst c) {
+__global__ void __launch_bounds__(TB* TY, 4) xstep_b_kernel(Dev d, XConst c) {
     const int b = blockIdx.y;
     if (solve_done(d, b)) return;
     int bi, bj;
