@@ -407,38 +407,54 @@ __global__ void __launch_bounds__(TB* TY, 4) xstep_a_kernel(Dev d, XConst c) {
         hh = block_sum_2d(hh, red);
         if (ty == 0 && tx == 0) d.cg_rr[(long long)b * 2 * d.ntile + blockIdx.x] = hh;
     }
-    // node partials: PU[bj][i] (rows of block bi) and PU[bi][j] (cols of block bj)
+    // node partials: PU[bj][i] = row sums of the tile (rows of block bi),
+    // PU[bi][j] = column sums (cols of block bj); on a diagonal tile h sits
+    // in the upper triangle only (zeros elsewhere), so node i's sum there is
+    // row i + column i. All warps reduce: warp ty owns rows ty + k*TY (warp
+    // sum over the lanes), lane tx accumulates column tx over those rows.
+    __shared__ double rowp[2][TB];
+    __shared__ double colp[2][TY][TB + 1];
+    {
+        double cu = 0.0, cz = 0.0;
+#pragma unroll
+        for (int k = 0; k < NE; ++k) {
+            const int il = ty + k * TY;
+            const double hv = Hs[il][tx];
+            cu += hv;
+            const double ru = warp_sum(hv);
+            if (tx == 0) rowp[0][il] = ru;
+            if (d.het) {
+                const double hz = Zs[il][tx];
+                cz += hz;
+                const double rz = warp_sum(hz);
+                if (tx == 0) rowp[1][il] = rz;
+            }
+        }
+        colp[0][ty][tx] = cu;
+        colp[1][ty][tx] = cz;
+    }
+    __syncthreads();
     const int t = ty * TB + tx;
     double* PU = d.PU + (long long)b * d.nb * n;
     double* PZ = d.PZ + (long long)b * d.nb * n;
+    auto colsum = [&](int which, int l) {
+        double s = 0.0;
+#pragma unroll
+        for (int y = 0; y < TY; ++y) s += colp[which][y][l];
+        return s;
+    };
     if (t < TB) {
         const int il = t, i = i0 + il;
         if (i < n) {
-            double su = 0.0, sz = 0.0;
-            for (int jl = 0; jl < TB; ++jl) {
-                if (bi == bj) {
-                    if (jl == il) continue;
-                    const int a = jl > il ? il : jl, bb = jl > il ? jl : il;
-                    su += Hs[a][bb];
-                    if (d.het) sz += Zs[a][bb];
-                } else {
-                    su += Hs[il][jl];
-                    if (d.het) sz += Zs[il][jl];
-                }
-            }
+            const double su = rowp[0][il] + (bi == bj ? colsum(0, il) : 0.0);
             PU[(long long)bj * n + i] = su;
-            if (d.het) PZ[(long long)bj * n + i] = sz;
+            if (d.het) PZ[(long long)bj * n + i] = rowp[1][il] + (bi == bj ? colsum(1, il) : 0.0);
         }
     } else if (t < 2 * TB && bi != bj) {
         const int jl = t - TB, j = j0 + jl;
         if (j < n) {
-            double su = 0.0, sz = 0.0;
-            for (int il = 0; il < TB; ++il) {
-                su += Hs[il][jl];
-                if (d.het) sz += Zs[il][jl];
-            }
-            PU[(long long)bi * n + j] = su;
-            if (d.het) PZ[(long long)bi * n + j] = sz;
+            PU[(long long)bi * n + j] = colsum(0, jl);
+            if (d.het) PZ[(long long)bi * n + j] = colsum(1, jl);
         }
     }
 }
