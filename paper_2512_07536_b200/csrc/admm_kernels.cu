@@ -498,10 +498,15 @@ __global__ void xstep_node_kernel(Dev d, XConst c) {
         su += u;
         sz += z;
     }
-    trS = block_sum(trS, scratch);
-    trT = block_sum(trT, scratch);
-    su = block_sum(su, scratch);
-    sz = block_sum(sz, scratch);
+    {
+        __shared__ double scratch4[4][32];
+        double v4[4] = {trS, trT, su, sz};
+        block_sum4(v4, scratch4);
+        trS = v4[0];
+        trT = v4[1];
+        su = v4[2];
+        sz = v4[3];
+    }
     if (threadIdx.x == 0) {
         const double rl = Y[lo.lambda_ix] - D[lo.lambda_ix] * c.inv_rho + c.inv_rho;  // +1/rho: c = -1 at lambda
         const double hl = rl + c.s * (c.alpha + trS + 2.0 * n - trT);
@@ -1233,6 +1238,9 @@ __global__ void xstep_diag_kernel(Dev d, XConst c) {
     const double lam = d.scal[b * 8 + kLambda];
     __shared__ double scratch[32];
     double res = 0.0;
+    // the thread's first tile residual partial, loaded with the node data
+    const double* rpart = d.res_part + (long long)b * d.ntile;
+    const double rp0 = (int)threadIdx.x < d.ntile ? rpart[threadIdx.x] : 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const double deg = sum_partials(PG, d.nb, n, i);
         const long long p = (long long)i * n + i;
@@ -1253,7 +1261,8 @@ __global__ void xstep_diag_kernel(Dev d, XConst c) {
         res += (xs - ys) * (xs - ys) + (xt - yt) * (xt - yt) + (xy - yy) * (xy - yy);
     }
     // tile partials in fixed order
-    for (int t = threadIdx.x; t < d.ntile; t += blockDim.x) res += d.res_part[(long long)b * d.ntile + t];
+    if ((int)threadIdx.x < d.ntile) res += rp0;
+    for (int t = threadIdx.x + blockDim.x; t < d.ntile; t += blockDim.x) res += rpart[t];
     res = block_sum(res, scratch);
     if (threadIdx.x == 0 && !d.upd_duals) X[lo.lambda_ix] = lam;
     if (threadIdx.x == 0 && d.upd_duals) {

@@ -151,6 +151,26 @@ __device__ inline double warp_sum(double v) {
     return v;
 }
 
+// Four block sums with one pair of barriers; each value follows exactly the
+// reduction tree of block_sum, so the results are bitwise the same.
+__device__ inline void block_sum4(double (&v)[4], double (*scratch)[32]) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = warp_sum(v[q]);
+    __syncthreads();
+    if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) scratch[q][wid] = v[q];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        double t = lane < nw ? scratch[q][lane] : 0.0;
+        v[q] = warp_sum(t);  // every warp reduces the same 32 values
+    }
+}
+
 __device__ inline double block_sum(double v, double* scratch) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int nw = (blockDim.x + 31) >> 5;
