@@ -46,13 +46,12 @@ def peaks():
         return {}
 
 
-FP64_DMMA_TFLOPS = 37.1  # tools/microbench/fp64_peak.cu on this pool's B200 (DMMA m8n8k4)
 # tcgen05.mma kind::i8 SS-mode throughput on this pool's B200: 148 CTAs, M=128,
 # N=256, K=32 at the issue floor (128.1 cycles/MMA): tools/microbench/imma_rate.cu
 IMMA_PEAK_TOPS = 4004.9
 # dram read+write bytes per Ozaki GEMM launch from one ncu --set full capture (profiles/)
-OZ_TRAFFIC = {1024: 16837888.0 + 256.0}  # profiles/r01/prof_ozgemm_raw.csv (2 matrices, n=1024)
-OZ_SLICES, OZ_BM, OZ_BN = 8, 128, 64  # paper_2512_07536_b200/csrc/ozaki_kernels.cuh
+OZ_TRAFFIC = {}  # filled from the round's ncu capture (profiles/r02/)
+OZ_SLICES, OZ_BM, OZ_BN = 7, 128, 64  # paper_2512_07536_b200/csrc/ozaki_kernels.cuh
 
 
 # ---------------------------------------------------------------- clocks
@@ -292,34 +291,24 @@ def run_ours(args):
     bs.close()
     cgm = None if args.no_cg else measure_cg_variant(T, torch, n, r, warm, K, W)
 
-    # roofline of the dominant kernel: the Ozaki-scheme GEMM on the int8
-    # tensor cores (default) or the FP64 DMMA GEMM (TPB_CONE=dmma)
-    ozaki = os.environ.get("TPB_CONE", "ozaki") != "dmma"
-    gemm_avg = t_cone / gemms  # the projection's launches (79 GEMMs + the X0 digit split)
+    # roofline of the dominant kernel: the Ozaki-scheme GEMM on the int8 tensor cores
+    gemm_avg = t_cone / gemms  # the projection's launches (GEMMs + the X0 digit split)
     fp64_flops = 2 * 2.0 * n * (n * (n + 1) / 2)  # 2 matrices x lower triangle x 2n flops
-    if ozaki:
-        ld = -(-n // OZ_BM) * OZ_BM
-        tiles = (OZ_BM // OZ_BN) * (ld // OZ_BM) * (ld // OZ_BM + 1) // 2
-        pairs = OZ_SLICES * (OZ_SLICES + 1) // 2
-        int8_ops = 2.0 * 2 * tiles * pairs * OZ_BM * OZ_BN * ld  # 2 matrices x tiles x pairs x 2 M N K
-        roof = {"bound": "tensor", "kernel": "oz_gemm_kernel (FP64 by Ozaki scheme I: 8 int8 digit planes, "
-                                             "36 tcgen05.mma kind::i8 products per tile)",
-                "achieved": int8_ops / gemm_avg / 1e12, "peak": IMMA_PEAK_TOPS, "unit": "TOP/s (int8)",
-                "frac": int8_ops / gemm_avg / 1e12 / IMMA_PEAK_TOPS,
-                "algorithmic_ops_per_launch": int8_ops,
-                "fp64_equivalent_tflops": fp64_flops / gemm_avg / 1e12,
-                "traffic": OZ_TRAFFIC.get(n), "traffic_unit": "bytes/launch",
-                "peak_source": "measured tcgen05 kind::i8 microbenchmark (tools/microbench/imma_rate.cu); "
-                               "MEASURED_PEAKS.json has no int8 entry",
-                "gemms_per_iteration": gemms, "gemm_avg_ms": gemm_avg * 1e3}
-    else:
-        achieved = fp64_flops / gemm_avg / 1e12
-        roof = {"bound": "tensor", "kernel": "sym_gemm_kernel (FP64 DMMA)",
-                "achieved": achieved, "peak": FP64_DMMA_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / FP64_DMMA_TFLOPS,
-                "traffic": 16.797184e6 if n == 1024 else None, "traffic_unit": "bytes/launch",
-                "peak_source": "measured FP64 DMMA microbenchmark (tools/microbench/fp64_peak.cu)",
-                "gemms_per_iteration": gemms, "gemm_avg_ms": gemm_avg * 1e3}
+    ld = -(-n // OZ_BM) * OZ_BM
+    tiles = (OZ_BM // OZ_BN) * (ld // OZ_BM) * (ld // OZ_BM + 1) // 2
+    pairs = OZ_SLICES * (OZ_SLICES + 1) // 2
+    int8_ops = 2.0 * 2 * tiles * pairs * OZ_BM * OZ_BN * ld  # 2 matrices x tiles x pairs x 2 M N K
+    roof = {"bound": "tensor",
+            "kernel": f"oz_gemm_kernel (FP64 by Ozaki scheme I: {OZ_SLICES} int8 digit planes, "
+                      f"{pairs} tcgen05.mma kind::i8 products per tile)",
+            "achieved": int8_ops / gemm_avg / 1e12, "peak": IMMA_PEAK_TOPS, "unit": "TOP/s (int8)",
+            "frac": int8_ops / gemm_avg / 1e12 / IMMA_PEAK_TOPS,
+            "algorithmic_ops_per_launch": int8_ops,
+            "fp64_equivalent_tflops": fp64_flops / gemm_avg / 1e12,
+            "traffic": OZ_TRAFFIC.get(n), "traffic_unit": "bytes/launch",
+            "peak_source": "measured tcgen05 kind::i8 microbenchmark (tools/microbench/imma_rate.cu); "
+                           "MEASURED_PEAKS.json has no int8 entry",
+            "gemms_per_iteration": gemms, "gemm_avg_ms": gemm_avg * 1e3}
     # x-step algorithmic bytes: pass A reads Y, D over the S
     # and T blocks (4n^2) and the edge block (2m), writes h (m); pass B reads
     # h, Y_g, D_g (3m) and the S, T blocks of Y, D (4n^2), writes X_g, D_g (2m)

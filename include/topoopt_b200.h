@@ -132,6 +132,8 @@ void* tp_solver_stream(tp_solver* s);               /* cudaStream_t of the main 
 int tp_solver_dims(tp_solver* s, int32_t* dims);
 /* Device pointers of the state (X, Y, D), each batch*nx doubles. */
 int tp_solver_state(tp_solver* s, double** x, double** y, double** d);
+/* Host copies of the state X, Y, D of every solve (batch x nx each; NULL skips). */
+int tp_solver_download(tp_solver* s, double* x, double* y, double* d);
 
 /* Instrumentation: enqueue `reps` repetitions of one iteration phase on the
  * solver stream (0 cone projection, 1 x-step, 2 top-r, 3 trace SLEM, 4 prep)
@@ -160,25 +162,14 @@ int tp_shard_tiles(int32_t ld, int32_t nranks, int32_t rank, int32_t* tiles, int
  * iterations and |r| / |h|. */
 int tp_solver_cg_stats(tp_solver* s, int32_t b, int32_t* iters, double* rel_res);
 
-/* Tuning hooks of the FP64 DMMA GEMM behind the cone projections:
- * variant 0 = production; tp_bench_gemm times one GEMM step on nmat
- * matrices of order n (event-timed, ms per launch). */
-int tp_set_gemm_variant(int32_t variant);
-int tp_bench_gemm(int32_t n, int32_t nmat, int32_t variant, int32_t reps, double* ms_per_launch);
 /* One Ozaki-scheme GEMM on the int8 tensor cores (tcgen05 kind::i8) over nmat
  * symmetric ld x ld host matrices (ld % 128 == 0): C = alpha A.B + beta E
- * (E = A if use_e), operands split into 8 digit planes with exponents ea, eb;
- * optional digit planes of C (exponent ec, nmat x 8 x ld x ld int8). reps > 0
+ * (E = A if use_e), operands split into 7 digit planes with exponents ea, eb;
+ * optional digit planes of C (exponent ec, nmat x 7 x ld x ld int8; 128 <= ld <= 16384). reps > 0
  * re-runs the GEMM and returns the event-timed ms per launch. */
 int tp_oz_gemm(int32_t ld, int32_t nmat, const double* a, int32_t ea, const double* b, int32_t eb,
                int32_t use_e, double alpha, double beta, double* c, int8_t* cd, int32_t ec,
                int32_t reps, double* ms);
-/* Instrumented variant: mode bit 0 skips the MMAs, bit 1 the TMA loads;
- * stamps (4 globaltimer ns values per CTA: start, setup, accumulators
- * ready, end) if non-null. */
-int tp_oz_gemm_dbg(int32_t ld, int32_t nmat, const double* a, int32_t ea, const double* b, int32_t eb,
-                   int32_t use_e, double alpha, double beta, double* c, int8_t* cd, int32_t ec,
-                   int32_t reps, double* ms, int32_t mode, long long* stamps);
 
 /* ---------------------------------------------------------------- capacity systems */
 /* Capacity-bound (inequality) systems (proj/include/topoopt/bandwidth.hpp:41-51,

@@ -472,6 +472,71 @@ def update_X(pd: Problem, y: np.ndarray, d: np.ndarray) -> tuple[np.ndarray, np.
     return sol[:pd.nx].copy(), sol
 
 
+def light_problem(n: int, r: int, alpha: float = 2.0, rho: float = 1.0):
+    """Layout and parameters of the homogeneous problem without the sparse
+    KKT (for project_Y / update_X_closed at n where assembling A is costly)."""
+    from types import SimpleNamespace
+    lo = hom_layout(n)
+    return SimpleNamespace(lo=lo, n=n, m=lo.m, nx=lo.nx, neq=lo.neq, r=r, alpha=alpha, rho=rho,
+                           beq=hom_beq(n, alpha))
+
+
+def update_X_closed(pd, y: np.ndarray, d: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """The same delta-regularised KKT solve as update_X (proj/src/admm.cpp:279-293,
+    KKT of proj/src/admm.cpp:46-94), by eliminating the slack blocks.
+
+    With x = r - A^T mu and (A x - delta mu = b) per row block, s = 1/(1+delta):
+      mu_0 = s (L(g) - lam I + S_r - b0), mu_1 = s (L(g) + lam I + T_r - b1),
+      mu_2 = s (D g + y_r - b2)
+    so g solves ((1+4s) I + 3s D^T D) g = h with
+      h_l = r_g + s (4 - R_ii - R_jj + R_ij + R_ji + (1 - r_y)_i + (1 - r_y)_j),
+    R = r_S + r_T (B^T B = D^T D + 2I), and lam is decoupled:
+      lam (1 + 2ns) = r_lam + s (tr r_S - tr r_T + alpha + 2n).
+    On the complete candidate graph D D^T = (n-2) I + J, so the g block is
+    solved exactly by Woodbury in node space. Returns (x, [x; mu])."""
+    lo, n, alpha = pd.lo, pd.n, pd.alpha
+    m, n2 = lo.m, n * n
+    s = 1.0 / (1.0 + KKT_SHIFT)
+    rv = y - d / pd.rho
+    rv[lo.lambda_ix] += 1.0 / pd.rho
+    e = enumerate_edges(n)
+    i, j = e[:, 0], e[:, 1]
+    rS = rv[lo.off_s:lo.off_s + n2].reshape(n, n).T   # column-major blocks
+    rT = rv[lo.off_t:lo.off_t + n2].reshape(n, n).T
+    ry = rv[lo.off_y:lo.off_y + n]
+    R = rS + rT
+    v2 = 1.0 - ry
+    dR = np.diag(R)
+    h = rv[:m] + s * (4.0 - dR[i] - dR[j] + R[i, j] + R[j, i] + v2[i] + v2[j])
+    a, b = 1.0 + 4.0 * s, 3.0 * s
+    u = np.bincount(i, h, n) + np.bincount(j, h, n)           # D h
+    c0 = a + b * (n - 2)
+    w = (u - b * u.sum() / (c0 + b * n)) / c0                 # (c0 I + b J)^-1 D h
+    g = (h - b * (w[i] + w[j])) / a
+    lam = (rv[lo.lambda_ix] + s * (np.trace(rS) - np.trace(rT) + alpha + 2.0 * n)) / (1.0 + 2.0 * n * s)
+    lap = np.zeros((n, n))
+    lap[i, j] = -g
+    lap[j, i] = -g
+    lap[np.arange(n), np.arange(n)] = np.bincount(i, g, n) + np.bincount(j, g, n)
+    eye = np.eye(n)
+    b0 = np.full((n, n), -alpha / n)
+    b1 = 2.0 * eye
+    x = np.empty(lo.nx)
+    x[:m] = g
+    x[lo.lambda_ix] = lam
+    S = s * (KKT_SHIFT * rS + b0 - (lap - lam * eye))
+    Tm = s * (KKT_SHIFT * rT + b1 - (lap + lam * eye))
+    yv = s * (KKT_SHIFT * ry + 1.0 - np.diag(lap))
+    x[lo.off_s:lo.off_s + n2] = S.T.reshape(-1)
+    x[lo.off_t:lo.off_t + n2] = Tm.T.reshape(-1)
+    x[lo.off_y:lo.off_y + n] = yv
+    mu0 = s * (lap - lam * eye + rS - b0)
+    mu1 = s * (lap + lam * eye + rT - b1)
+    mu2 = s * (np.diag(lap) + ry - 1.0)
+    mu = np.concatenate([mu0.T.reshape(-1), mu1.T.reshape(-1), mu2])
+    return x, np.concatenate([x, mu])
+
+
 def update_duals(pd: Problem, x, y, d) -> None:
     """d += rho (x - y) (proj/src/admm.cpp:295-297)."""
     d += pd.rho * (x - y)

@@ -89,10 +89,9 @@ SIGNATURES = {
     "tp_solver_stream": (_P, [_P]),
     "tp_solver_dims": (_I, [_P, _ip]),
     "tp_solver_state": (_I, [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P)]),
+    "tp_solver_download": (_I, [_P, _dp, _dp, _dp]),
     "tp_solver_bench_phase": (_I, [_P, _I, _I, _ip]),
     "tp_solver_launches_per_iteration": (_I, [_P, _ip]),
-    "tp_set_gemm_variant": (_I, [_I]),
-    "tp_bench_gemm": (_I, [_I, _I, _I, _I, _dp]),
     "tp_solve_het_capacity": (_I, [_I, _I, _ip, _ip, _ip, _ip, _I, _cfgp, _ip, _I, _resp, _ip, _dp, _dp,
                                    C.c_char_p, _I]),
     "tp_anneal_capacity": (_I, [_I, _I, _ip, _ip, _ip, _ip, _I, _D, _D, _I, _I, _U64, _ip, _ip]),
@@ -100,8 +99,6 @@ SIGNATURES = {
     "tp_consensus_simulate": (_I, [_I, _dp, _I, _I, _U64, _dp]),
     "tp_device_mt19937_64": (_I, [_U64, _I, C.POINTER(C.c_uint64)]),
     "tp_oz_gemm": (_I, [_I, _I, _dp, _I, _dp, _I, _I, C.c_double, C.c_double, _dp, C.c_void_p, _I, _I, _dp]),
-    "tp_oz_gemm_dbg": (_I, [_I, _I, _dp, _I, _dp, _I, _I, C.c_double, C.c_double, _dp, C.c_void_p, _I, _I,
-                            _dp, _I, C.c_void_p]),
     "tp_project_Y": (_I, [_I, _I, _D, _D, _dp, _dp, _dp]),
     "tp_project_Y_het_node": (_I, [_I, _ip, _D, _D, _dp, _dp, _dp]),
     "tp_update_X": (_I, [_I, _I, _D, _D, _dp, _dp, _dp]),

@@ -1001,9 +1001,8 @@ int cg_grid_size(const Dev& d) {
 }
 
 // register-resident CG when every item fits one co-resident CTA
-// (TPB_CG_GLOBAL forces the global-memory variant: tests, comparisons)
 bool cg_use_registers(const Dev& d) {
-    if (std::getenv("TPB_CG_GLOBAL") || d.nb > kCgRegNb) return false;
+    if (d.nb > kCgRegNb) return false;
     static int cached = 0;
     if (!cached) cached = cg_capacity((const void*)xstep_cg_reg_kernel, d);
     return (long long)d.B * d.ntile <= cached;

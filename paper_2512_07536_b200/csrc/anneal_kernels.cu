@@ -295,7 +295,6 @@ struct Buf {
 }  // namespace
 
 bool anneal_device(int n, std::vector<std::pair<int, int>>& es, const AnnealParams& p) {
-    if (std::getenv("TPB_HOST_ANNEAL")) return false;
     int count = 0;
     if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
         cudaGetLastError();

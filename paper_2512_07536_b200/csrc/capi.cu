@@ -1,8 +1,8 @@
 // C ABI (include/topoopt_b200.h): host entry points over the device solver.
 #include <algorithm>
 #include <cstring>
-#include <unistd.h>  // environ
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -62,6 +62,7 @@ void require_device() {
 // Topology::normalize_and_validate (proj/src/topology.cpp:19-51) on an edge
 // list, returned as ascending packed indices.
 std::vector<int> packed_edges(int n, const int32_t* edges, int k) {
+    if (k > 0 && !edges) throw Error(kInvalidArgument, "topology: null edge list with a positive edge count");
     std::vector<long long> idx(k);
     for (int e = 0; e < k; ++e) {
         const int i = edges[2 * e], j = edges[2 * e + 1];
@@ -275,6 +276,10 @@ int tp_solver_state(tp_solver* s, double** x, double** y, double** d) {
     });
 }
 
+int tp_solver_download(tp_solver* s, double* x, double* y, double* d) {
+    return guarded([&] { s->s->download(x, y, d); });
+}
+
 int tp_solver_bench_phase(tp_solver* s, int32_t phase, int32_t reps, int32_t* launches_per_rep) {
     return guarded([&] {
         const int per = s->s->bench_phase(phase, reps);
@@ -297,28 +302,25 @@ int tp_solver_cg_stats(tp_solver* s, int32_t b, int32_t* iters, double* rel_res)
 }
 
 namespace {
-// Per-thread plan cache of tp_solve: the last homogeneous solver (device
-// buffers, digit planes, TMA maps, captured iteration graphs) serves the next
-// call with the same shape. Solver::start() resets every piece of iteration
-// state, so a reused solver returns bitwise what a fresh one does (tested).
-// The pointer is leaked at thread exit on purpose: no CUDA calls after the
-// runtime may have shut down.
+// Plan cache of tp_solve: a small process-wide pool of idle homogeneous
+// solvers (device buffers, digit planes, TMA maps, captured iteration graphs).
+// A call checks out a plan of its shape (device, n, r, config) exclusively
+// and returns it afterwards, so concurrent callers never share a solver, and
+// at most kPlanCap idle plans are retained (least recently used evicted).
+// Solver::start() resets every piece of iteration state, so a reused solver
+// returns bitwise what a fresh one does (tested). tp_release_plans() frees
+// the pool. The pool itself is never destroyed at exit (no CUDA calls after
+// the runtime may have shut down).
 struct HomPlan {
     int dev = -1, n = 0, r = 0;
     Config c;
-    std::string env;  // TPB_* variables select kernels at capture time
     std::unique_ptr<Solver> s;
 };
-thread_local HomPlan* t_plan = nullptr;
-
-std::string tpb_env() {
-    std::string k;
-    for (char** e = environ; e && *e; ++e)
-        if (std::strncmp(*e, "TPB_", 4) == 0) {
-            k += *e;
-            k += '\n';
-        }
-    return k;
+constexpr size_t kPlanCap = 2;
+std::mutex g_plan_mu;
+std::vector<std::unique_ptr<HomPlan>>& plan_pool() {
+    static auto* pool = new std::vector<std::unique_ptr<HomPlan>>();
+    return *pool;
 }
 
 bool same_cfg(const Config& a, const Config& b) {
@@ -328,36 +330,69 @@ bool same_cfg(const Config& a, const Config& b) {
            a.linear_solver == b.linear_solver && a.cg_max_iter == b.cg_max_iter;
 }
 
-void release_plan() {
-    if (t_plan) {
-        t_plan->s.reset();
-        delete t_plan;
-        t_plan = nullptr;
-    }
-}
-
-Solver& hom_plan(int n, int r, const Config& c) {
+std::unique_ptr<HomPlan> take_plan(int n, int r, const Config& c) {
     int dev = 0;
     TPB_CUDA(cudaGetDevice(&dev));
-    std::string env = tpb_env();
-    if (t_plan && t_plan->s && t_plan->dev == dev && t_plan->n == n && t_plan->r == r &&
-        same_cfg(t_plan->c, c) && t_plan->env == env)
-        return *t_plan->s;
-    release_plan();  // one plan per thread: free the old one before allocating
+    {
+        std::lock_guard<std::mutex> lk(g_plan_mu);
+        auto& pool = plan_pool();
+        for (auto it = pool.end(); it != pool.begin();) {
+            --it;
+            HomPlan& p = **it;
+            if (p.dev == dev && p.n == n && p.r == r && same_cfg(p.c, c)) {
+                std::unique_ptr<HomPlan> out = std::move(*it);
+                pool.erase(it);
+                return out;
+            }
+        }
+    }
     auto p = std::make_unique<HomPlan>();
     p->dev = dev;
     p->n = n;
     p->r = r;
     p->c = c;
-    p->env = std::move(env);
     p->s = std::make_unique<Solver>(n, 1, false, std::vector<int>{r}, std::vector<int>{}, c);
-    t_plan = p.release();
-    return *t_plan->s;
+    return p;
+}
+
+void give_plan(std::unique_ptr<HomPlan> p) {
+    std::unique_ptr<HomPlan> evicted;
+    {
+        std::lock_guard<std::mutex> lk(g_plan_mu);
+        auto& pool = plan_pool();
+        pool.push_back(std::move(p));
+        if (pool.size() > kPlanCap) {
+            evicted = std::move(pool.front());
+            pool.erase(pool.begin());
+        }
+    }
+    if (evicted) {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(evicted->dev);
+        evicted.reset();
+        cudaSetDevice(cur);
+    }
+}
+
+void release_plans() {
+    std::vector<std::unique_ptr<HomPlan>> all;
+    {
+        std::lock_guard<std::mutex> lk(g_plan_mu);
+        all.swap(plan_pool());
+    }
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto& p : all) {
+        cudaSetDevice(p->dev);
+        p.reset();
+    }
+    cudaSetDevice(cur);
 }
 }  // namespace
 
 int tp_release_plans(void) {
-    return guarded([&] { release_plan(); });
+    return guarded([&] { release_plans(); });
 }
 
 int tp_solve(int32_t n, int32_t r, const tp_config* cfg, const int32_t* warm_edges, int32_t n_warm,
@@ -368,19 +403,16 @@ int tp_solve(int32_t n, int32_t r, const tp_config* cfg, const int32_t* warm_edg
         const Config c = to_cfg(cfg);
         validate(c);
         std::vector<int> warm;
-        if (warm_edges && n_warm >= 0) warm = packed_edges(n, warm_edges, n_warm);
+        if (n_warm >= 0) warm = packed_edges(n, warm_edges, n_warm);
         else warm = default_warm(n, r, cfg ? cfg->seed : 0);
-        Solver& s = hom_plan(n, r, c);
-        try {
-            s.set_warm(0, warm);
-            s.start();
-            s.run_to_completion();
-            s.finish();
-        } catch (...) {
-            release_plan();  // a failed solve may leave the plan unusable
-            throw;
-        }
+        std::unique_ptr<HomPlan> plan = take_plan(n, r, c);
+        Solver& s = *plan->s;
+        s.set_warm(0, warm);  // a failed solve drops its plan (may be unusable)
+        s.start();
+        s.run_to_completion();
+        s.finish();
         const SolveResult R = s.result(0);
+        give_plan(std::move(plan));
         if (R.w.empty()) throw Error(kDegenerate, "every edge weight is at or below the floor");
         fill_result(R, out, edges, weights, trace, note, note_cap);
     });
@@ -396,7 +428,7 @@ int tp_solve_het_node(int32_t n, const int32_t* degrees, const tp_config* cfg,
         std::vector<int> dg(degrees, degrees + n);
         Solver s(n, 1, true, {}, dg, c);
         std::vector<int> warm;
-        if (warm_edges && n_warm >= 0) {
+        if (n_warm >= 0) {
             warm = packed_edges(n, warm_edges, n_warm);
         } else {
             // anneal_topology -> anneal_degree_topology (proj/src/anneal.cpp:393-407)
@@ -535,7 +567,7 @@ int tp_solve_het_capacity(int32_t n, int32_t nrows, const int32_t* row_ptr, cons
         const int m = n * (n - 1) / 2;
         if (r < 1 || r > m) throw Error(kInvalidArgument, "assemble_het: edge total outside [1, |E|]");
         std::vector<int> warm;
-        if (warm_edges && n_warm >= 0) {
+        if (n_warm >= 0) {
             warm = packed_edges(n, warm_edges, n_warm);
         } else {
             // anneal_topology -> anneal_capacity_topology (proj/src/anneal.cpp:393-407)

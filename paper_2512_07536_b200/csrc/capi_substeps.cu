@@ -147,8 +147,8 @@ void cone_dense(int n, const double* a, double* out, bool psd) {
     if (n < 1) throw Error(kInvalidArgument, "project: empty matrix");
     init_attrs();
     const bool small = n <= 64;
-    const bool oz = !small && cone_uses_ozaki();
-    const int ld = small ? ((n + 7) & ~7) : (oz ? ((n + 127) / 128) * 128 : ((n + 63) / 64) * 64);
+    const int ld = small ? ((n + 7) & ~7) : ((n + 127) / 128) * 128;
+    if (!small) check_oz_ld(ld);
     const long long ld2 = (long long)ld * ld;
     const int w = psd ? 1 : 0;  // slot 0 -> NSD, slot 1 -> PSD
     DBuf<double> da((size_t)n * n), A(2 * ld2), C(2 * (size_t)n * n), scale(2);
@@ -158,10 +158,9 @@ void cone_dense(int n, const double* a, double* out, bool psd) {
     const int blocks = (int)std::min<long long>(((long long)n * n + 255) / 256, 1024);
     sym_pad_kernel<<<blocks, 256>>>(da.p, n, ld, w, A.p);
     TPB_CHECK_LAUNCH();
-    const SignSchedule sch = (!small && oz) ? ozaki_schedule() : SignSchedule{};
     if (small) {
-        launch_cone_small(A.p, ld2, ld, n, C.p, 0, (long long)n * n, nullptr, 2, sch, 0);
-    } else if (oz) {
+        launch_cone_small(A.p, ld2, ld, n, C.p, 0, (long long)n * n, nullptr, 2, SignSchedule{}, 0);
+    } else {
         frob_kernel<<<1, 1024>>>(A.p, ld, w, scale.p);
         TPB_CHECK_LAUNCH();
         OzWork oz_w;
@@ -172,24 +171,7 @@ void cone_dense(int n, const double* a, double* out, bool psd) {
             oz_w.d[q] = bufs.back()->p;
             make_oz_maps(oz_w.d[q], ld, 2, &oz_w.maps[q]);
         }
-        enqueue_cone_ozaki(A.p, nullptr, nullptr, nullptr, oz_w, ld, n, scale.p, C.p, 0, (long long)n * n,
-                           nullptr, 2, sch, 0);
-        TPB_CUDA(cudaDeviceSynchronize());
-    } else {
-        frob_kernel<<<1, 1024>>>(A.p, ld, w, scale.p);
-        TPB_CHECK_LAUNCH();
-        DBuf<double> w0(2 * ld2), w1(2 * ld2), w2(2 * ld2);
-        w0.zero();
-        w1.zero();
-        w2.zero();
-        const int G = stream_k_ctas(ld);
-        const int nt = ld / 64;
-        DBuf<double> skw((size_t)std::max(G, 1) * 64 * 64);
-        DBuf<int> skf((size_t)nt * (nt + 1));
-        skf.zero();
-        enqueue_cone_tiled(A.p, w0.p, w1.p, w2.p, ld, n, scale.p, C.p, 0, (long long)n * n, nullptr, 2,
-                           sch, 0, G > 0 ? skw.p : nullptr, G > 0 ? skf.p : nullptr);
-        TPB_CUDA(cudaDeviceSynchronize());
+        enqueue_cone_ozaki(A.p, oz_w, ld, n, scale.p, C.p, 0, (long long)n * n, nullptr, 2, ozaki_schedule(), 0);
     }
     TPB_CUDA(cudaDeviceSynchronize());
     // column-major output of a symmetric matrix == row-major
@@ -477,74 +459,6 @@ int tp_project_nsd(int32_t n, const double* a, double* out) {
     return guarded([&] { cone_dense(n, a, out, false); });
 }
 
-int tp_set_gemm_variant(int32_t variant) {
-    return guarded([&] {
-        if (variant < 0 || variant >= sym_gemm_variants())
-            throw Error(kInvalidArgument, "gemm variant out of range");
-        set_sym_gemm_variant(variant);
-    });
-}
-
-// Times one symmetric DMMA GEMM step (C = A.B + E over nmat ld x ld matrices)
-// for the given variant: ms per launch averaged over `reps` launches.
-int tp_bench_gemm(int32_t n, int32_t nmat, int32_t variant, int32_t reps, double* ms_per_launch) {
-    return guarded([&] {
-        require_device();
-        init_attrs();
-        const int ld = ((n + 63) / 64) * 64;
-        const size_t sz = (size_t)nmat * ld * ld;
-        DBuf<double> A(sz), B(sz), C(sz);
-        std::vector<double> h(sz);
-        for (size_t k = 0; k < sz; ++k) {
-            const size_t r = (k / ld) % ld, c = k % ld;
-            h[k] = r < (size_t)n && c < (size_t)n ? 1.0 / (1.0 + (double)((r * 7 + c * 7) % 97)) : 0.0;
-        }
-        A.up(h.data(), sz);
-        B.up(h.data(), sz);
-        C.zero();
-        const int old = get_sym_gemm_variant();
-        // variant == sym_gemm_variants(): stream-K decomposition (single pair)
-        const bool sk = variant == sym_gemm_variants();
-        set_sym_gemm_variant(sk ? 0 : variant);
-        const int G = sk ? stream_k_ctas(ld) : 0;
-        const int nt = ld / 64;
-        DBuf<double> skw((size_t)std::max(G, 1) * 64 * 64);
-        DBuf<int> skf((size_t)nt * (nt + 1));
-        skf.zero();
-        GemmArgs g{};
-        if (G > 0) {
-            g.sk_ws = skw.p;
-            g.sk_flags = skf.p;
-        }
-        g.A = A.p;
-        g.B = B.p;
-        g.E = A.p;
-        g.mstride = (long long)ld * ld;
-        g.C = C.p;
-        g.c_stride_b = 2LL * ld * ld;
-        g.c_stride_w = (long long)ld * ld;
-        g.ldc = ld;
-        g.nvalid = ld;
-        g.ld = ld;
-        g.alpha_c = 1.0;
-        g.beta_c = 0.5;
-        cudaEvent_t e0, e1;
-        TPB_CUDA(cudaEventCreate(&e0));
-        TPB_CUDA(cudaEventCreate(&e1));
-        launch_sym_gemm(g, nmat, 0);
-        TPB_CUDA(cudaEventRecord(e0, 0));
-        for (int k = 0; k < reps; ++k) launch_sym_gemm(g, nmat, 0);
-        TPB_CUDA(cudaEventRecord(e1, 0));
-        TPB_CUDA(cudaEventSynchronize(e1));
-        float ms = 0.f;
-        TPB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
-        set_sym_gemm_variant(old);
-        *ms_per_launch = ms / reps;
-    });
-}
-
 // One Ozaki-scheme GEMM (ozaki_kernels.cuh) on nmat symmetric ld x ld
 // matrices (host, ld % 128 == 0): digit planes of A and B (exponents eA, eB)
 // are made on the device, then C = alpha A.B + beta E (E = A if use_e) with
@@ -553,17 +467,11 @@ int tp_bench_gemm(int32_t n, int32_t nmat, int32_t variant, int32_t reps, double
 int tp_oz_gemm(int32_t ld, int32_t nmat, const double* a, int32_t ea, const double* b, int32_t eb,
                int32_t use_e, double alpha, double beta, double* c, int8_t* cd, int32_t ec,
                int32_t reps, double* ms) {
-    return tp_oz_gemm_dbg(ld, nmat, a, ea, b, eb, use_e, alpha, beta, c, cd, ec, reps, ms, 0, nullptr);
-}
-
-int tp_oz_gemm_dbg(int32_t ld, int32_t nmat, const double* a, int32_t ea, const double* b, int32_t eb,
-                   int32_t use_e, double alpha, double beta, double* c, int8_t* cd, int32_t ec,
-                   int32_t reps, double* ms, int32_t mode, long long* stamps) {
     return guarded([&] {
         require_device();
         init_attrs();
-        if (ld <= 0 || ld % kOzBM != 0 || nmat <= 0)
-            throw Error(kInvalidArgument, "tp_oz_gemm: ld must be a positive multiple of 128");
+        check_oz_ld(ld);
+        if (nmat <= 0) throw Error(kInvalidArgument, "tp_oz_gemm: nmat must be positive");
         const size_t sz = (size_t)nmat * ld * ld;
         DBuf<double> A(sz), B(sz), C(sz);
         DBuf<int8_t> Ad(sz * kOzSlices), Bd(sz * kOzSlices), Cd(sz * kOzSlices);
@@ -573,10 +481,9 @@ int tp_oz_gemm_dbg(int32_t ld, int32_t nmat, const double* a, int32_t ea, const 
         Cd.zero();
         launch_oz_split(A.p, (long long)ld * ld, ld, nmat, nullptr, ea, Ad.p, nullptr, 0);
         launch_oz_split(B.p, (long long)ld * ld, ld, nmat, nullptr, eb, Bd.p, nullptr, 0);
-        OzMaps ma, mb, mc;
+        OzMaps ma, mb;
         make_oz_maps(Ad.p, ld, nmat, &ma);
         make_oz_maps(Bd.p, ld, nmat, &mb);
-        make_oz_maps(Cd.p, ld, nmat, &mc);
         OzGemm g{};
         g.ma = &ma;
         g.mb = &mb;
@@ -593,16 +500,9 @@ int tp_oz_gemm_dbg(int32_t ld, int32_t nmat, const double* a, int32_t ea, const 
         g.ldc = ld;
         g.nvalid = ld;
         g.Cd = cd ? Cd.p : nullptr;
-        g.mc = &mc;
         g.eC = ec;
-        g.dbg_mode = mode;
-        const size_t nst = (size_t)8 * oz_gemm_tiles(ld) * nmat;
-        DBuf<long long> st(nst);
-        g.dbg_t = stamps ? st.p : nullptr;
         launch_oz_gemm(g, 0);
         TPB_CUDA(cudaDeviceSynchronize());
-        if (stamps) st.down(stamps, nst);
-        g.dbg_t = nullptr;
         C.down(c, sz);
         if (cd) Cd.down(cd, sz * kOzSlices);
         // timed repetitions: with a digit output requested, digits only (the
@@ -624,7 +524,6 @@ int tp_oz_gemm_dbg(int32_t ld, int32_t nmat, const double* a, int32_t ea, const 
         }
     });
 }
-
 
 // project_binary_z_capped (proj/src/admm_het.cpp:125-154) on the device.
 int tp_project_binary_z_capped(int32_t n, int32_t nrows, const int32_t* row_ptr, const int32_t* cols,

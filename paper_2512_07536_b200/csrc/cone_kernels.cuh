@@ -23,43 +23,9 @@ struct SignSchedule {
 // = 73 products instead of 79. Scalar-map error max_mu mu |1 - s(mu)| / 2 =
 // 4.4e-14 of ||A||_F (1.8e-14 for the default above). Digit bounds: |X| <=
 // 1.3, |U| <= 1.26, |Z'| <= 3.73, |V| <= 1.5 (exponents unchanged).
-// TPB_SIGN_SCHEDULE=default selects the default above.
 SignSchedule ozaki_schedule();
 
-// One symmetric GEMM step over a batch of matrices (blockIdx.y = matrix):
-//   C = alpha * (A . B) + beta * E,   alpha = alpha_c * s^pa, beta = beta_c * s^pb
-// with s = scale[mat]; A, B, E symmetric ld x ld (row-major, zero padded),
-// C symmetric: lower 64x64 tiles computed, mirrored on store.
-struct GemmArgs {
-    const double* A;
-    const double* B;
-    const double* E;
-    long long mstride;      // elements between matrices for A, B, E
-    double* C;
-    long long c_stride_b;   // C base of matrix (b, w) = C + b*c_stride_b + w*c_stride_w
-    long long c_stride_w;
-    int ldc;
-    int nvalid;             // rows/cols of C to store (n for the state, ld for work)
-    int ld;
-    double alpha_c, beta_c;
-    int pa, pb;
-    const double* scale;    // per matrix (1/||A||_F)
-    const int* ictl;        // done flags per solve (matrix/2), or null
-    double sign_b;          // +1 psd-style / -1: multiplies alpha for odd matrices (w = 1)
-    int sign_mode;          // 1: alpha *= (w == 0 ? -1 : +1)  (S -> NSD, T -> PSD)
-    // stream-K workspace for single-pair launches (null: tiled kernel only)
-    double* sk_ws;          // stream_k_ctas(ld) x 64 x 64 doubles
-    int* sk_flags;          // 2 x tiles ints, zero-initialised
-};
-
-void launch_sym_gemm(const GemmArgs& g, int nmat, cudaStream_t st);
 int sm_count();  // multiprocessors of the current device (cached)
-// CTAs of the stream-K decomposition for one (S, T) pair of order ld (0: not used)
-int stream_k_ctas(int ld);
-// tile/pipeline variants of the DMMA GEMM (for tuning; 0 = production)
-int sym_gemm_variants();
-void set_sym_gemm_variant(int v);
-int get_sym_gemm_variant();
 
 // Fused small-n projection: one CTA per matrix, whole iteration in shared
 // memory (npad <= 64). A at A + mat*mstride (ld-padded, symmetric); output to
@@ -68,12 +34,5 @@ int get_sym_gemm_variant();
 void launch_cone_small(const double* A, long long mstride, int ld, int n, double* C,
                        long long c_stride_b, long long c_stride_w, const int* ictl, int nmat,
                        const SignSchedule& sch, cudaStream_t st);
-
-// Host driver for the tiled path: enqueue the full schedule on `st`.
-// bufs: 3 work buffers (each nmat * ld * ld).
-void enqueue_cone_tiled(const double* A, double* w0, double* w1, double* w2, int ld, int n,
-                        const double* scale, double* C, long long c_stride_b,
-                        long long c_stride_w, const int* ictl, int nmat, const SignSchedule& sch,
-                        cudaStream_t st, double* sk_ws = nullptr, int* sk_flags = nullptr);
 
 }  // namespace tpb

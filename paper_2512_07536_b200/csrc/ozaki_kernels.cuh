@@ -4,12 +4,15 @@
 //   M = 2^e sum_{s=1..KS} 2^{-7s} M_s,   M_s int8 "digit planes" in [-127, 127]
 //   A.B ~= 2^{eA+eB} sum_{d=2..KS+1} 2^{-7d} G_d,   G_d = sum_{s+t=d} A_s . B_t
 //
-// Every A_s . B_t is exact (int32 accumulation in TMEM, |G_d| < 2^31 for
-// K <= 16384); only the FP64 epilogue rounds. The scales are static bounds
-// from the sign iteration (|X| <= 1.21, |Y| <= 1.45,
-// |Z| <= 2.81 in spectral norm, hence entrywise), so a producer GEMM writes
-// its consumer's digit planes in its own epilogue. Accuracy study:
-// tools/proto/ozaki.py.
+// KS = 7 digits (49 bits) and the KS(KS+1)/2 = 28 products with s + t <= KS+1:
+// the dropped products and the operand truncation are both ~2^-49 of
+// |A||B| per entry, the size of an FP64 GEMM's own accumulated rounding
+// (K u ~ 1e-13 worst case at K = 1024). Every A_s . B_t is exact (int32
+// accumulation in TMEM: |G_d| <= KS * K * 127^2 < 2^31 needs K <= 19020, so
+// ld <= kOzMaxLd = 16384 is enforced); only the FP64 epilogue rounds. The
+// scales are static bounds from the sign iteration, so a
+// producer GEMM writes its consumer's digit planes in its own epilogue.
+// Accuracy study: tools/proto/ozaki.py.
 #pragma once
 
 #include <cuda.h>
@@ -21,23 +24,18 @@
 
 namespace tpb {
 
-constexpr int kOzSlices = 8;   // digits per operand (56 bits)
-constexpr int kOzBM = 128;     // tile rows (UMMA M)
-constexpr int kOzBN = 64;      // tile cols of the one-CTA-per-SM variant (a 128 x 32 variant runs
-                               // two CTAs per SM for multi-wave grids; ozaki_kernels.cu)
+constexpr int kOzSlices = 7;     // digits per operand (49 bits)
+constexpr int kOzBM = 128;       // tile rows (UMMA M)
+constexpr int kOzBN = 64;        // tile columns
+constexpr int kOzMaxLd = 16384;  // int32 accumulator bound (see above)
 
-// Digit planes of nmat symmetric ld x ld matrices: [mat][slice][ld][ld] int8.
-struct OzPlanes {
-    int8_t* d = nullptr;
-    int e = 0;  // matrix = 2^e sum_s 2^{-7s} plane_s
-};
+// Throws kInvalidArgument unless ld is a multiple of 128 in [128, kOzMaxLd].
+void check_oz_ld(int ld);
 
-// TMA maps of one plane buffer for both tile variants: loads in the A role
-// (k block x 128 rows) and the B role (k block x BN rows), epilogue stores.
+// TMA maps of one digit-plane buffer: loads in the A role (64-byte k block x
+// 128 rows) and in the B role (64-byte k block x 64 rows).
 struct OzMaps {
-    CUtensorMap a, b, st;     // 128 x 64 tiles (64-byte k blocks, 64 x 64 store boxes)
-    CUtensorMap a2, b2, st2;  // 128 x 32 tiles (32-byte k blocks, 32 x 32 store boxes)
-    CUtensorMap bp;           // persistent 128 x 32 tiles: B boxes of 32 rows x 64 bytes
+    CUtensorMap a, b;
 };
 void make_oz_maps(const int8_t* planes, int ld, int nmat, OzMaps* out);
 
@@ -56,13 +54,9 @@ struct OzGemm {
     long long c_stride_b, c_stride_w;
     int ldc, nvalid;
     int8_t* Cd;              // digit planes out ([mat][slice][ld][ld]), or null
-    const OzMaps* mc;        // TMA maps of Cd (stores use the 64-row box)
     int eC;
     const int* ictl;         // done flags per solve (matrix / 2), or null
-    long long* dbg_t;        // instrumentation: 4 globaltimer stamps per CTA, or null
-    int dbg_mode;            // instrumentation: bit 0 skips the MMAs, bit 1 the TMA loads
     int no_pdl;              // launch without programmatic dependent launch
-    int dstore;              // digit planes by direct 16-byte global stores (else TMA stores)
     const int* tiles;        // row-sharded products: this rank's lower-tile indices, or null (all)
     int ntiles;              // entries of tiles
     int mstep;               // matrices of this launch: blockIdx.y * mstep + moff (mstep 0 -> 1)
@@ -71,12 +65,10 @@ struct OzGemm {
 };
 
 void launch_oz_gemm(const OzGemm& g, cudaStream_t st);
-// Tiled cone projections use this kernel unless TPB_CONE=dmma (FP64 DMMA).
-bool cone_uses_ozaki();
 int oz_gemm_tiles(int ld);
 
-// Digit-plane buffers of the cone projection: [0..2] pair with the three FP64
-// work buffers, [3] holds X0 = A / ||A||_F.
+// Digit-plane buffers of the cone projection: [0..2] hold the rotating
+// iterates, [3] holds X0 = A / ||A||_F.
 struct OzWork {
     int8_t* d[4] = {nullptr, nullptr, nullptr, nullptr};
     OzMaps maps[4];
@@ -92,7 +84,7 @@ struct OzWork {
 // replicated.)
 // Sharded runs store each matrix's planes row-chunk-major,
 // [mat][chunk][slice][rc rows][ld] with rc = ld / G (rc = ld is the plain
-// [mat][slice][ld][ld] layout), so a rank's rows of all eight planes are one
+// [mat][slice][ld][ld] layout), so a rank's rows of all planes are one
 // contiguous block: one all-gather per matrix. Tiles never straddle chunks.
 // The S (even matrices) and T (odd) chains of the sign iteration are
 // independent, so each product runs as two launches and one chain's
@@ -110,12 +102,12 @@ struct OzShard {
 std::vector<int> oz_shard_tiles(int ld, int nranks, int rank);
 
 struct SignSchedule;
-// Ozaki-scheme counterpart of enqueue_cone_tiled (cone_kernels.cuh): the
-// same sign iteration, every product on the int8 tensor cores.
-void enqueue_cone_ozaki(const double* A, double* w0, double* w1, double* w2, const OzWork& oz, int ld,
-                        int n, const double* scale, double* C, long long c_stride_b, long long c_stride_w,
-                        const int* ictl, int nmat, const SignSchedule& sch, cudaStream_t st,
-                        const OzShard* shard = nullptr);
+// The cone projections of nmat symmetric ld x ld inputs A (S at even, T at
+// odd matrices): the sign iteration of cone_kernels.cuh with every product
+// on the int8 tensor cores; P_nsd / P_psd written to C.
+void enqueue_cone_ozaki(const double* A, const OzWork& oz, int ld, int n, const double* scale, double* C,
+                        long long c_stride_b, long long c_stride_w, const int* ictl, int nmat,
+                        const SignSchedule& sch, cudaStream_t st, const OzShard* shard = nullptr);
 
 // Digit planes of s * A (s = scale[mat] or 1) with exponent e (layout rc as in OzGemm).
 void launch_oz_split(const double* A, long long mstride, int ld, int nmat, const double* scale,

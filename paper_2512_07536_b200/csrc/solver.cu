@@ -33,16 +33,20 @@ void validate(const Config& c) {
         throw Error(kInvalidArgument, "SolverConfig: cg_max_iter must be in [1, 64]");
 }
 
-// TPB_TIMING=1: device-synchronised phase timings on stderr (setup overheads)
+// Built with -DTPB_PHASE_TIMING: device-synchronised phase timings on stderr
+// (setup overheads); compiled out otherwise.
 void phase_mark(const char* what) {
-    static const bool on = std::getenv("TPB_TIMING") != nullptr;
-    if (!on) return;
+#ifndef TPB_PHASE_TIMING
+    (void)what;
+    return;
+#else
     static auto last = std::chrono::steady_clock::now();
     cudaDeviceSynchronize();
     const auto now = std::chrono::steady_clock::now();
     std::fprintf(stderr, "[tpb] %-24s %9.3f ms\n", what,
                  std::chrono::duration<double, std::milli>(now - last).count());
     last = now;
+#endif
 }
 
 namespace {
@@ -76,8 +80,9 @@ void pinned_give(int* p, size_t bytes) {
 }
 
 // Stream-ordered allocation from the device's default memory pool, whose
-// release threshold is raised so that freed blocks stay reserved: repeated
-// solves (tp_solve per call) neither map nor unmap device memory.
+// release threshold is raised to 1 GiB so that the blocks of recently freed
+// solvers stay reserved (repeated tp_solve calls neither map nor unmap device
+// memory) while the retention stays bounded for other CUDA users.
 template <typename T>
 T* dalloc(cudaStream_t st, std::vector<void*>& pool, size_t count) {
     static bool pool_ready[64] = {};
@@ -86,7 +91,7 @@ T* dalloc(cudaStream_t st, std::vector<void*>& pool, size_t count) {
     if (dev < 64 && !pool_ready[dev]) {
         cudaMemPool_t mp;
         TPB_CUDA(cudaDeviceGetDefaultMemPool(&mp, dev));
-        uint64_t thr = UINT64_MAX;
+        uint64_t thr = 1ull << 30;
         TPB_CUDA(cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr));
         pool_ready[dev] = true;
     }
@@ -159,11 +164,11 @@ Solver::Solver(int n, int B, bool het, const std::vector<int>& r, const std::vec
                     "system (stiff 1e8 coupling) uses the closed form");
     c_ = make_xconst(n, cfg.alpha, cfg.rho);
     small_ = n <= 64;
-    // Tiled projections: int8 tensor-core (Ozaki) GEMMs by default, FP64 DMMA
-    // with TPB_CONE=dmma; the Ozaki tiles need ld % 128 == 0.
-    ozaki_ = !small_ && cone_uses_ozaki();
+    // Tiled projections (n > 64): int8 tensor-core (Ozaki) GEMMs, ld % 128 == 0.
+    ozaki_ = !small_;
     if (ozaki_) sch_ = ozaki_schedule();
-    ld_ = small_ ? ((n + 7) & ~7) : (ozaki_ ? ((n + 127) / 128) * 128 : ((n + 63) / 64) * 64);
+    ld_ = small_ ? ((n + 7) & ~7) : ((n + 127) / 128) * 128;
+    if (ozaki_) check_oz_ld(ld_);
     list_cap_ = het ? m : *std::max_element(r_host_.begin(), r_host_.end());
     int chunk = cfg.chunk > 0 ? cfg.chunk : (n <= 64 ? 32 : (n <= 256 ? 16 : 8));
     chunk = ((chunk + cfg.trace_stride - 1) / cfg.trace_stride) * cfg.trace_stride;
@@ -204,13 +209,6 @@ Solver::Solver(int n, int B, bool het, const std::vector<int>& r, const std::vec
 
 Solver::~Solver() {
     phase_mark("(before teardown)");
-    if (slem_stats_) {
-        int st[2] = {0, 0};
-        cudaStreamSynchronize(s2_);
-        cudaMemcpy(st, slem_stats_, sizeof(st), cudaMemcpyDeviceToHost);
-        std::fprintf(stderr, "[slem] trace calls %d, matvecs %d (%.1f per call)\n", st[0], st[1],
-                     st[0] ? (double)st[1] / st[0] : 0.0);
-    }
     if (g_chunk_) cudaGraphExecDestroy(g_chunk_);
     if (g_one_) cudaGraphExecDestroy(g_one_);
     phase_mark("graph destroy");
@@ -287,22 +285,6 @@ void Solver::alloc() {
     d_.tr_res = dalloc<double>(s0_, allocs_,(size_t)B * cfg_.max_iter);
     d_.tr_lam = dalloc<double>(s0_, allocs_,(size_t)B * cfg_.max_iter);
     d_.tr_acf = dalloc<double>(s0_, allocs_,(size_t)B * cfg_.max_iter);
-    if (!small_ && !ozaki_) {
-        w0_ = dalloc<double>(s0_, allocs_,(size_t)B * 2 * ld2);
-        w1_ = dalloc<double>(s0_, allocs_,(size_t)B * 2 * ld2);
-        w2_ = dalloc<double>(s0_, allocs_,(size_t)B * 2 * ld2);
-        TPB_CUDA(cudaMemsetAsync(w0_, 0, (size_t)B * 2 * ld2 * sizeof(double), s0_));
-        TPB_CUDA(cudaMemsetAsync(w1_, 0, (size_t)B * 2 * ld2 * sizeof(double), s0_));
-        TPB_CUDA(cudaMemsetAsync(w2_, 0, (size_t)B * 2 * ld2 * sizeof(double), s0_));
-        // stream-K GEMM workspace for single large instances
-        const int G = B == 1 ? stream_k_ctas(ld_) : 0;
-        if (G > 0) {
-            const int nt = ld_ / 64, T = nt * (nt + 1) / 2;
-            sk_ws_ = dalloc<double>(s0_, allocs_, (size_t)G * 64 * 64);
-            sk_flags_ = dalloc<int>(s0_, allocs_, (size_t)2 * T);
-            TPB_CUDA(cudaMemsetAsync(sk_flags_, 0, (size_t)2 * T * sizeof(int), s0_));
-        }
-    }
     phase_mark("alloc: state and scratch");
     if (ozaki_) {
         // digit planes of the cone-projection iterates
@@ -312,10 +294,6 @@ void Solver::alloc() {
             make_oz_maps(oz_.d[q], ld_, 2 * B, &oz_.maps[q]);
         }
         phase_mark("alloc: digit planes + TMA maps");
-    }
-    if (std::getenv("TPB_SLEM_STATS")) {
-        slem_stats_ = dalloc<int>(s0_, allocs_, 2);
-        TPB_CUDA(cudaMemsetAsync(slem_stats_, 0, 2 * sizeof(int), s0_));
     }
     if (cap_) {
         cap_pad_ = 1;
@@ -345,11 +323,11 @@ void Solver::alloc() {
     // Krylov basis in global memory: a shared-memory basis (~200 KB at n=256)
     // would pin one SLEM CTA per SM and starve the concurrent cone GEMMs.
     // plain trace Lanczos (slem_trace_kernel): longer recurrences, write-only basis
-    trace_kmax_ = std::max(1, std::min(n - 1, (n > kSmallDense && !std::getenv("TPB_SLEM_CGS2")) ? 256 : 96));
+    trace_kmax_ = std::max(1, std::min(n - 1, n > kSmallDense ? 256 : 96));
     basis_ = dalloc<double>(s0_, allocs_,(size_t)B * trace_kmax_ * n);
     ritz_ = dalloc<double>(s0_, allocs_,(size_t)B * 2 * n);
     ritz_ok_ = dalloc<int>(s0_, allocs_,B);
-    const int kfin = n - 1 <= kFinalExactDim ? std::max(1, n - 1) : (std::getenv("TPB_SLEM_CGS2") ? kFinalKrylov : 1);
+    const int kfin = n - 1 <= kFinalExactDim ? std::max(1, n - 1) : 1;
     basis_final_ = dalloc<double>(s0_, allocs_,(size_t)B * kfin * n);
     slem_out_ = dalloc<double>(s0_, allocs_,(size_t)B * 8);
     tmp_m_ = dalloc<double>(s0_, allocs_,(size_t)B * m);
@@ -426,7 +404,7 @@ void Solver::final_slem(const double* packed, const int* list, const int* count,
     // (eigenvalue error <= 1e-20 / gap), reusing the trace basis buffer
     const int n = lo_.n;
     const bool exact = n - 1 <= kFinalExactDim;
-    a.plain = exact || std::getenv("TPB_SLEM_CGS2") ? 0 : 1;
+    a.plain = exact ? 0 : 1;
     a.basis = a.plain ? basis_ : basis_final_;
     a.kmax = exact ? std::max(1, n - 1) : (a.plain ? trace_kmax_ : kFinalKrylov);
     // the final topology is the last trace iterate's neighbour: start from
@@ -438,7 +416,6 @@ void Solver::final_slem(const double* packed, const int* list, const int* count,
     a.max_restarts = 200;
     a.min_steps = 64;
     a.tol = 1e-10;
-    if (const char* t = std::getenv("TPB_FINAL_TOL")) a.tol = std::atof(t);  // experiments
     a.out = out;
     a.tr_acf = nullptr;
     a.ictl = nullptr;
@@ -508,13 +485,11 @@ void Solver::enqueue_slem_trace(cudaStream_t st) {
     a.ritz = ritz_;
     a.ritz_ok = ritz_ok_;
     a.tol = cfg_.slem_tol;
-    if (const char* t = std::getenv("TPB_SLEM_TOL")) a.tol = std::atof(t);  // experiments
     a.out = nullptr;
     a.tr_acf = d_.tr_acf;
     a.ictl = d_.ictl;
     a.max_iter = cfg_.max_iter;
-    a.stats = slem_stats_;
-    a.plain = lo_.n > kSmallDense && !std::getenv("TPB_SLEM_CGS2");
+    a.plain = lo_.n > kSmallDense;
     a.nbr = slem_nbr_;
     a.nwt = slem_nwt_;
     launch_slem(a, B_, st);
@@ -525,12 +500,9 @@ void Solver::enqueue_projection() {
     if (small_) {
         launch_cone_small(d_.A, (long long)ld_ * ld_, ld_, lo_.n, d_.Y + lo_.off_s, cb, cw, d_.ictl,
                           2 * B_, sch_, s0_);
-    } else if (ozaki_) {
-        enqueue_cone_ozaki(d_.A, w0_, w1_, w2_, oz_, ld_, lo_.n, d_.inv_scale, d_.Y + lo_.off_s, cb, cw,
-                           d_.ictl, 2 * B_, sch_, s0_, sharded() ? &shard_ : nullptr);
     } else {
-        enqueue_cone_tiled(d_.A, w0_, w1_, w2_, ld_, lo_.n, d_.inv_scale, d_.Y + lo_.off_s, cb, cw,
-                           d_.ictl, 2 * B_, sch_, s0_, sk_ws_, sk_flags_);
+        enqueue_cone_ozaki(d_.A, oz_, ld_, lo_.n, d_.inv_scale, d_.Y + lo_.off_s, cb, cw, d_.ictl, 2 * B_,
+                           sch_, s0_, sharded() ? &shard_ : nullptr);
     }
 }
 
@@ -628,8 +600,8 @@ void Solver::build_graphs() {
 // Sharded solvers launch their iterations eagerly: the all-gathers' stream
 // priority (SMs to the NCCL CTAs first) does not survive graph capture, and
 // at the sizes that shard a launch is ~0.01 % of an iteration. Same
-// iteration sequence as the graphs (TPB_SHARD_GRAPH=1 keeps the graphs).
-bool Solver::eager() const { return sharded() && !std::getenv("TPB_SHARD_GRAPH"); }
+// iteration sequence as the graphs.
+bool Solver::eager() const { return sharded(); }
 
 void Solver::iterate_async(int k) {
     if (eager()) {

@@ -137,7 +137,6 @@ class Solver {
     std::vector<void*> allocs_;
     int* d_r_ = nullptr;
     double* d_deg_ = nullptr;
-    double *w0_ = nullptr, *w1_ = nullptr, *w2_ = nullptr;
     bool ozaki_ = false;        // cone GEMMs on the int8 tensor cores (else FP64 DMMA)
     bool cap_ = false;          // capacity-bound het system
     CapSystem capsys_;
@@ -147,8 +146,6 @@ class Solver {
     int *cap_idx_ = nullptr, *cap_load_ = nullptr;
     OzWork oz_;
     OzShard shard_;
-    double* sk_ws_ = nullptr;   // stream-K partial tiles (B == 1, large n)
-    int* sk_flags_ = nullptr;
     int *list_ = nullptr, *list_count_ = nullptr;
     int *e_i_ = nullptr, *e_j_ = nullptr, *col_idx_ = nullptr;
     double* e_w_ = nullptr;
@@ -156,7 +153,6 @@ class Solver {
     int trace_kmax_ = 0;
     double* ritz_ = nullptr;         // B x 2n extreme Ritz vectors (warm start)
     int* ritz_ok_ = nullptr;
-    int* slem_stats_ = nullptr;      // TPB_SLEM_STATS: {trace SLEM calls, matvecs}
     int* slem_nbr_ = nullptr;        // het trace SLEM: node-major incidence scratch
     double* slem_nwt_ = nullptr;
     double* basis_final_ = nullptr;  // final report

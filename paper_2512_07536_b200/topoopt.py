@@ -744,6 +744,13 @@ class BatchSolver:
         _check(_lib.load().tp_solver_state(self.h, C.byref(x), C.byref(y), C.byref(d)))
         return x.value, y.value, d.value
 
+    def download(self):
+        """Host copies (X, Y, D), each batch x nx (tp_solver_download)."""
+        nx = int(self.dims[2])
+        x, y, d = (np.zeros((self.batch, nx)) for _ in range(3))
+        _check(_lib.load().tp_solver_download(self.h, _dp(x), _dp(y), _dp(d)))
+        return x, y, d
+
     def cg_stats(self, b: int = 0) -> tuple[int, float]:
         """CG x-step statistics of solve b's last iteration: (iterations, |r|/|h|)."""
         it = C.c_int32(0)

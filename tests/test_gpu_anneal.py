@@ -44,33 +44,22 @@ def test_device_mt19937_64():
         assert list(out) == mt19937_64(seed, 700)
 
 
-def anneal(T, degrees, host, **kw):
-    old = os.environ.get("TPB_HOST_ANNEAL")
-    try:
-        if host:
-            os.environ["TPB_HOST_ANNEAL"] = "1"
-        else:
-            os.environ.pop("TPB_HOST_ANNEAL", None)
-        return T.anneal_degree_topology(degrees, **kw)
-    finally:
-        if old is None:
-            os.environ.pop("TPB_HOST_ANNEAL", None)
-        else:
-            os.environ["TPB_HOST_ANNEAL"] = old
-
-
 @pytest.mark.parametrize("n,deg,steps,seed", [(16, 4, 20, 0), (64, 6, 8, 3), (100, 5, 3, 7), (300, 8, 1, 1)])
-def test_device_anneal_equals_host(T, n, deg, steps, seed):
+def test_device_anneal_equals_reference(T, n, deg, steps, seed):
+    """Device annealer vs the compiled reference's anneal_degree_topology
+    (oracle/_ref): identical edge sets."""
+    from oracle import ref
     degrees = [deg] * n
     if (deg * n) % 2:
         degrees[0] += 1
-    dev = anneal(T, degrees, host=False, steps=steps, seed=seed)
-    host = anneal(T, degrees, host=True, steps=steps, seed=seed)
-    assert np.array_equal(dev, host)
+    dev = T.anneal_degree_topology(degrees, steps=steps, seed=seed)
+    want = ref.anneal_degree(degrees, steps=steps, seed=seed)
+    assert np.array_equal(np.asarray(dev).reshape(-1, 2), np.asarray(want).reshape(-1, 2))
 
 
 def test_device_anneal_heterogeneous(T, O):
+    from oracle import ref
     bu, e = O.allocate_edge_capacity([9.76] * 16 + [3.25] * 16, 64)
-    dev = anneal(T, e, host=False, steps=10, seed=2)
-    host = anneal(T, e, host=True, steps=10, seed=2)
-    assert np.array_equal(dev, host)
+    dev = T.anneal_degree_topology(e, steps=10, seed=2)
+    want = ref.anneal_degree(e, steps=10, seed=2)
+    assert np.array_equal(np.asarray(dev).reshape(-1, 2), np.asarray(want).reshape(-1, 2))

@@ -88,8 +88,10 @@ def test_n1024_lockstep_cg_vs_closed_form(T, O):
     b = T.solve(n, r, warm_start=warm, linear_solver=1, **cfg)
     assert a.iterations == b.iterations == 6
     ta, tb = a.trace, b.trace
-    # residuals sum (x - y)^2 of small differences: relative agreement 1e-8
-    assert np.max(np.abs(ta[:, 1] - tb[:, 1]) / np.abs(ta[:, 1])) < 1e-8
+    # residuals sum (x - y)^2 of small differences (|x - y| ~ 1e-3): CG's
+    # 1e-10 relative solve tolerance moves them by ~1e-7 relative; the
+    # north-star tolerance (1e-6 relative) is the bar
+    assert np.max(np.abs(ta[:, 1] - tb[:, 1]) / np.abs(ta[:, 1])) < 1e-6
     assert np.max(np.abs(ta[:, 2] - tb[:, 2])) < 1e-10                     # lambda_tilde
     assert a.edges.tolist() == b.edges.tolist()
     assert np.max(np.abs(a.weights - b.weights)) < 1e-9
@@ -105,33 +107,28 @@ def test_n1024_lockstep_cg_vs_closed_form(T, O):
         sv.close()
 
 
-@pytest.mark.parametrize("n,r", [(16, 32), (65, 300), (1024, 4096)])
-def test_cg_register_variant_bitwise(T, monkeypatch, n, r):
-    """The register-resident CG kernel (every tile's x, r, p held by its own
-    CTA) against the global-memory kernel (TPB_CG_GLOBAL): same arithmetic and
-    reduction order, so x-steps and whole lockstep runs agree bit for bit."""
-    m = n * (n - 1) // 2
-    nx = m + 1 + 2 * n * n + n
-    rng = np.random.default_rng(7 + n)
-    y = rng.standard_normal(nx)
-    d = rng.standard_normal(nx) * 0.3
-
-    def run():
-        x, kkt, its, rel = T.update_X_cg(n, r, y, d, rho=2.5, linear_tol=1e-10)
-        return x, its, rel
-
-    monkeypatch.delenv("TPB_CG_GLOBAL", raising=False)
-    x_r, its_r, rel_r = run()
-    monkeypatch.setenv("TPB_CG_GLOBAL", "1")
-    x_g, its_g, rel_g = run()
-    assert its_r == its_g and rel_r == rel_g
-    assert np.array_equal(x_r, x_g)
-    if n == 1024:
-        bu_e = T.allocate_edge_capacity([1.0] * n, r)
-        warm = T.anneal_degree_topology(bu_e[1], steps=1, moves_per_temp=1, seed=0)
-        cfg = dict(rho=10.0, epsilon=1e-8, max_iter=4, linear_solver=1)
-        g = T.solve(n, r, warm_start=warm, **cfg)
-        monkeypatch.delenv("TPB_CG_GLOBAL")
-        a = T.solve(n, r, warm_start=warm, **cfg)
-        assert np.array_equal(a.trace, g.trace)
-        assert np.array_equal(a.weights, g.weights) and a.edges.tolist() == g.edges.tolist()
+@pytest.mark.parametrize("n,r,B", [(16, 32, 600), (65, 300, 100), (1024, 4096, 2)])
+def test_cg_batched_global_equals_single_register(T, n, r, B):
+    """A single solve's CG x-step runs the register-resident kernel (each of
+    its tiles fits one co-resident CTA); a batch too large for that runs the
+    global-memory kernel. Same arithmetic and reduction order, so every solve
+    of the batch equals the single solve bit for bit (state trace, edges,
+    weights)."""
+    bu_e = T.allocate_edge_capacity([1.0] * n, r)
+    warm = T.anneal_degree_topology(bu_e[1], steps=1, moves_per_temp=1, seed=0)
+    cfg = dict(rho=10.0, epsilon=1e-8, max_iter=4, linear_solver=1)
+    one = T.solve(n, r, warm_start=warm, **cfg)
+    bs = T.BatchSolver(n, r=[r] * B, **cfg)
+    try:
+        for b in range(B):
+            bs.set_warm(b, warm)
+        bs.start()
+        bs.run()
+        bs.finish()
+        for b in sorted({0, B // 2, B - 1}):
+            got = bs.result(b)
+            assert np.array_equal(got.trace, one.trace)
+            assert got.edges.tolist() == one.edges.tolist()
+            assert np.array_equal(got.weights, one.weights)
+    finally:
+        bs.close()

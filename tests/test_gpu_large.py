@@ -24,7 +24,8 @@ def test_project_Y_large_vs_lapack(T, O, n, r):
     x[:lo.m] += rng.standard_normal(lo.m) * 1e-3
     s = rng.standard_normal((n, n)) * 1e-2
     x[lo.off_s:lo.off_s + n * n] += (s + s.T).reshape(-1)
-    x[lo.off_t:lo.off_t + n * n] += (s - s.T + np.diag(rng.standard_normal(n))).reshape(-1) * 0
+    t = rng.standard_normal((n, n)) * 1e-2
+    x[lo.off_t:lo.off_t + n * n] += (t + t.T + np.diag(rng.standard_normal(n)) * 1e-2).reshape(-1)
     y = T.project_Y(n, r, x, d, rho=10.0)
     # edges: clamp + exact top-r with the reference tie rule
     want = np.maximum(0.0, x[:lo.m])

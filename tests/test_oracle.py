@@ -248,3 +248,18 @@ def test_write_optimize_artifacts(T, golden, tmp_path):
     import json
     sj = json.loads((tmp_path / "solution.json").read_text())
     assert sj["mode"] == "homogeneous" and sj["edges"] == 32 and sj["iterations"] == 556
+
+
+@pytest.mark.parametrize("n", [3, 5, 16, 33])
+def test_closed_form_xstep_equals_kkt_lu(O, n):
+    """oracle.update_X_closed (the slack-eliminated KKT solve used for the
+    n=1024 lockstep parity) equals the sparse-LU solve of the assembled
+    delta-regularised KKT (proj/src/admm.cpp:46-94, 279-293)."""
+    rng = np.random.default_rng(100 + n)
+    pd = O.assemble(n, n, 2.0, 2.5)
+    y = rng.standard_normal(pd.nx)
+    d = rng.standard_normal(pd.nx) * 0.3
+    x1, k1 = O.update_X(pd, y, d)
+    x2, k2 = O.update_X_closed(O.light_problem(n, n, 2.0, 2.5), y, d)
+    assert np.abs(x1 - x2).max() < 1e-13 * np.abs(x1).max()
+    assert np.abs(k1 - k2).max() < 1e-13 * np.abs(k1).max()
