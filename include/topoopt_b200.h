@@ -187,6 +187,11 @@ int tp_anneal_capacity(int32_t n, int32_t nrows, const int32_t* row_ptr, const i
                        const int32_t* allowed, int32_t r, double t0, double cooling, int32_t steps,
                        int32_t moves_per_temp, uint64_t seed, int32_t* edges, int32_t* n_edges);
 /* project_binary_z_capped (proj/src/admm_het.cpp:125-154), v and z of n(n-1)/2. */
+/* project_Y_het (proj/src/admm_het.cpp:156-171) for a capacity-bound system:
+ * clamps, cones, z by project_binary_z_capped with edge total r, nu clamp. */
+int tp_project_Y_het_capacity(int32_t n, int32_t nrows, const int32_t* row_ptr, const int32_t* cols,
+                              const int32_t* caps, const int32_t* allowed, int32_t r, double alpha, double rho,
+                              const double* x, const double* d, double* y);
 int tp_project_binary_z_capped(int32_t n, int32_t nrows, const int32_t* row_ptr, const int32_t* cols,
                                const int32_t* caps, const int32_t* allowed, const double* v, int32_t r,
                                double* z);
@@ -243,6 +248,10 @@ int tp_spectral_report(int32_t n, const double* w, double* out4);
 int tp_spectral_edges(int32_t n, const int32_t* edges, const double* weights, int32_t k,
                       double* out4);
 /* project_psd / project_nsd (proj/src/eig.cpp:174-176), row-major n x n. */
+/* sym_eig (proj/src/eig.cpp:149-172) on the device: one-sided Jacobi on the
+ * shifted matrix (eig_kernels.cu). values ascending; vectors row-major, column k
+ * the eigenvector of values[k]. */
+int tp_sym_eig(int32_t n, const double* a, double* values, double* vectors);
 int tp_project_psd(int32_t n, const double* a, double* out);
 int tp_project_nsd(int32_t n, const double* a, double* out);
 

@@ -96,6 +96,7 @@ SIGNATURES = {
                                    C.c_char_p, _I]),
     "tp_anneal_capacity": (_I, [_I, _I, _ip, _ip, _ip, _ip, _I, _D, _D, _I, _I, _U64, _ip, _ip]),
     "tp_project_binary_z_capped": (_I, [_I, _I, _ip, _ip, _ip, _ip, _dp, _I, _dp]),
+    "tp_project_Y_het_capacity": (_I, [_I, _I, _ip, _ip, _ip, _ip, _I, C.c_double, C.c_double, _dp, _dp, _dp]),
     "tp_consensus_simulate": (_I, [_I, _dp, _I, _I, _U64, _dp]),
     "tp_device_mt19937_64": (_I, [_U64, _I, C.POINTER(C.c_uint64)]),
     "tp_oz_gemm": (_I, [_I, _I, _dp, _I, _dp, _I, _I, C.c_double, C.c_double, _dp, C.c_void_p, _I, _I, _dp]),
@@ -113,6 +114,7 @@ SIGNATURES = {
     "tp_spectral_report": (_I, [_I, _dp, _dp]),
     "tp_spectral_edges": (_I, [_I, _ip, _dp, _I, _dp]),
     "tp_project_psd": (_I, [_I, _dp, _dp]),
+    "tp_sym_eig": (_I, [_I, _dp, _dp, _dp]),
     "tp_project_nsd": (_I, [_I, _dp, _dp]),
 }
 

@@ -196,6 +196,22 @@ __global__ void __launch_bounds__(TB* TY) prep_kernel(Dev d, XConst c) {
             }
         }
         __syncthreads();
+        // |A| row-sum partials (for ||A||_inf): rows of block bi over the
+        // columns of block bj and, off the diagonal, rows of bj over bi;
+        // fixed-order sums (lanes: warp tree; rows: ascending)
+        {
+            double* rp = d.row_part + ((long long)b * 2 + which) * d.nb * n;
+            for (int cc = ty; cc < TB; cc += TY) {  // row i0 + cc over columns j0 + tx
+                const double v = warp_sum(fabs(Vs[tx][cc]));
+                if (tx == 0 && i0 + cc < n) rp[(long long)bj * n + i0 + cc] = v;
+            }
+            if (bi != bj && ty == 0) {  // row j0 + tx over columns i0 + cc
+                double v = 0.0;
+                for (int cc = 0; cc < TB; ++cc) v += fabs(Vs[tx][cc]);
+                if (j0 + tx < n) rp[(long long)bi * n + j0 + tx] = v;
+            }
+        }
+        __syncthreads();
         if (bi != bj) {
             for (int cc = ty; cc < TB; cc += TY) {
                 const int i = i0 + tx, j = j0 + cc;
@@ -248,18 +264,31 @@ __global__ void __launch_bounds__(TB* TY) prep_kernel(Dev d, XConst c) {
     }
 }
 
+// Scale of the sign iteration's start X0 = A / c: c = min(||A||_F, ||A||_inf),
+// both upper bounds of the spectral radius (the spectrum of X0 stays in
+// [-1, 1]); the tighter one leaves small eigenvalues relatively larger, so the
+// fixed inflation schedule reaches a smaller error.
 __global__ void frob_finalize_kernel(Dev d) {
     const int b = blockIdx.x;
     if (solve_done(d, b)) return;
     __shared__ double scratch[32];
+    const int n = d.lo.n;
     for (int which = 0; which < 2; ++which) {
         const double* part = d.frob_part + ((long long)b * 2 + which) * d.ntile;
         double v = 0.0;
         for (int t = threadIdx.x; t < d.ntile; t += blockDim.x) v += part[t];
         v = block_sum(v, scratch);
+        const double* rp = d.row_part + ((long long)b * 2 + which) * d.nb * n;
+        double inf = 0.0;
+        for (int r = threadIdx.x; r < n; r += blockDim.x) {
+            double rs = 0.0;
+            for (int cb = 0; cb < d.nb; ++cb) rs += rp[(long long)cb * n + r];
+            inf = fmax(inf, rs);
+        }
+        inf = block_max(inf, scratch);
         if (threadIdx.x == 0) {
-            const double f = sqrt(v);
-            d.inv_scale[b * 2 + which] = f > 0.0 ? 1.0 / f : 0.0;
+            const double c = fmin(sqrt(v), inf);
+            d.inv_scale[b * 2 + which] = c > 0.0 ? 1.0 / c : 0.0;
         }
     }
 }

@@ -38,7 +38,8 @@ struct Dev {
     // projection
     double* A;         // B x 2 x ld x ld  (S, T inputs, symmetrized)
     double* frob_part; // B x 2 x ntile
-    double* inv_scale; // B x 2   (1/||A||_F)
+    double* inv_scale; // B x 2   (1 / min(||A||_F, ||A||_inf))
+    double* row_part;  // B x 2 x nb x n: |A| row sums of row r over column block C at [C][r]
     // x-step scratch
     double* h;         // B x m
     double* PU;        // B x nb x n  (row partials of h)

@@ -585,6 +585,23 @@ int tp_solve_het_capacity(int32_t n, int32_t nrows, const int32_t* row_ptr, cons
     });
 }
 
+int tp_project_Y_het_capacity(int32_t n, int32_t nrows, const int32_t* row_ptr, const int32_t* cols,
+                              const int32_t* caps, const int32_t* allowed, int32_t r, double alpha, double rho,
+                              const double* x, const double* d, double* y) {
+    return guarded([&] {
+        require_device();
+        const CapSystem sys = cap_system(n, nrows, row_ptr, cols, caps, allowed);
+        Config c;
+        c.alpha = alpha;
+        c.rho = rho;
+        c.max_iter = 1;
+        Solver s(n, 1, true, {r}, {}, c, &sys);
+        s.upload(x, nullptr, d);
+        s.project_only();
+        s.download(nullptr, y, nullptr);
+    });
+}
+
 int tp_anneal_capacity(int32_t n, int32_t nrows, const int32_t* row_ptr, const int32_t* cols, const int32_t* caps,
                        const int32_t* allowed, int32_t r, double t0, double cooling, int32_t steps,
                        int32_t moves_per_temp, uint64_t seed, int32_t* edges, int32_t* n_edges) {

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "../../include/topoopt_b200.h"
+#include "eig_kernels.cuh"
 #include "ozaki_kernels.cuh"
 #include "solver.cuh"
 
@@ -100,16 +101,24 @@ __global__ void sym_pad_kernel(const double* a, int n, int ld, int w, double* A)
     }
 }
 
+// 1 / min(||A||_F, ||A||_inf) of matrix w (the solver's frob_finalize_kernel)
 __global__ void frob_kernel(const double* A, int ld, int w, double* scale) {
     __shared__ double scratch[32];
     const double* src = A + (long long)w * ld * ld;
-    double s = 0.0;
+    double s = 0.0, inf = 0.0;
     for (long long p = threadIdx.x; p < (long long)ld * ld; p += blockDim.x) s += src[p] * src[p];
+    for (int r = threadIdx.x; r < ld; r += blockDim.x) {
+        double rs = 0.0;
+        for (int c = 0; c < ld; ++c) rs += fabs(src[(long long)r * ld + c]);
+        inf = fmax(inf, rs);
+    }
     s = block_sum(s, scratch);
+    inf = block_max(inf, scratch);
     if (threadIdx.x == 0) {
         scale[0] = 0.0;
         scale[1] = 0.0;
-        scale[w] = s > 0.0 ? 1.0 / sqrt(s) : 0.0;
+        const double c = fmin(sqrt(s), inf);
+        scale[w] = c > 0.0 ? 1.0 / c : 0.0;
     }
 }
 
@@ -228,6 +237,13 @@ int tp_project_Y(int32_t n, int32_t r, double alpha, double rho, const double* x
         s.upload(x, nullptr, d);
         s.project_only();
         s.download(nullptr, y, nullptr);
+    });
+}
+
+int tp_sym_eig(int32_t n, const double* a, double* values, double* vectors) {
+    return guarded([&] {
+        require_device();
+        sym_eig_device(n, a, values, vectors);
     });
 }
 

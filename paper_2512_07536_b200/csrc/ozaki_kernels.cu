@@ -568,7 +568,7 @@ constexpr int kEX = 2, kEU = 2, kEZ = 3, kEV = 2, kEX0 = 2;
 
 SignSchedule ozaki_schedule() {
     SignSchedule s;
-    s.k1 = 20;
+    s.k1 = 18;
     s.k2 = 6;
     s.qa = 3.73052;
     s.qb = -5.13486;

@@ -13,6 +13,12 @@
 // list of kept nonzero edges consumed by the SLEM kernel.
 #include "select_kernels.cuh"
 
+#include <cooperative_groups.h>
+
+namespace cg = cooperative_groups;
+
+#include <algorithm>
+
 namespace tpb {
 
 namespace {
@@ -208,6 +214,208 @@ void launch_topr(const SelectArgs& a, int B, cudaStream_t st) {
     const int smem = kCap * sizeof(unsigned long long);
     topr_kernel<<<B, kThreads, smem, st>>>(a);
     TPB_CHECK_LAUNCH();
+}
+
+// ---------------------------------------------------------------------------
+// keep_top_r of ONE large solve across the whole GPU (hom thinning, B = 1):
+// a cooperative grid of G CTAs, CTA g owning the contiguous index range g of
+// the packed weights. Radix select MSB first with 11-bit digits (64-bit keys:
+// 53, 42, 31, 20, 9, 0): per round every CTA histograms the keys of its
+// range that match the prefix so far into shared memory and adds the bins
+// into a global histogram with integer atomics (order-independent, so
+// deterministic); after a grid barrier every CTA reads the same histogram and
+// derives the same next digit. The final pass counts ties (== K*) and
+// keys > K* per CTA; after one more barrier each CTA knows its exclusive
+// prefix over lower CTAs, so ties go to the lowest indices exactly as the
+// reference's comparator (v desc, index asc) orders them
+// (proj/src/admm.cpp:114-121), and the ascending kept-edge list for the
+// SLEM is written without a further pass. Small register and shared-memory
+// footprint (256 threads x 32 registers) so its CTAs co-reside with the
+// concurrent cone-projection GEMM CTAs (one per SM).
+namespace {
+constexpr int kGThreads = 256;
+constexpr int kGBins = 2048;
+constexpr int kGRounds = 6;
+__device__ __forceinline__ int g_shift(int round) { return round < 5 ? 53 - 11 * round : 0; }
+__device__ __forceinline__ int g_bits(int round) { return round < 5 ? 11 : 9; }
+}  // namespace
+
+__global__ void __launch_bounds__(kGThreads, 8) topr_grid_kernel(SelectArgs a, int* gh, int* cnt) {
+    cg::grid_group grid = cg::this_grid();
+    if (a.done && a.done[1]) return;  // uniform across the grid
+    const long long m = a.m;
+    double* v = a.base;
+    const long long r = a.r[0];
+    const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
+    const long long per = (m + G - 1) / G;
+    const long long lo = (long long)g * per, hi = lo + per < m ? lo + per : m;
+    __shared__ int sh[kGBins];
+    __shared__ int scan_scratch[32];
+    __shared__ int s_sel[4];  // digit, need after, bucket population, count above
+
+    // zero the global histograms (grid-strided), then the first barrier
+    for (int k = g * kGThreads + tid; k < kGRounds * kGBins; k += G * kGThreads) gh[k] = 0;
+    int mode;  // 0 keep all, 1 key >= thresh, 2 key > thresh + first need ties, 3 keep none
+    unsigned long long prefix = 0, pmask = 0;
+    long long need = r;
+    if (r >= m) {
+        mode = 0;
+    } else if (r <= 0) {
+        mode = 3;
+    } else {
+        mode = 2;
+        grid.sync();
+        for (int round = 0; round < kGRounds; ++round) {
+            const int shift = g_shift(round), nb = 1 << g_bits(round);
+            for (int k = tid; k < nb; k += kGThreads) sh[k] = 0;
+            __syncthreads();
+            for (long long k = lo + tid; k < hi; k += kGThreads) {
+                const unsigned long long key = (unsigned long long)__double_as_longlong(v[k] + 0.0);
+                if ((key & pmask) == prefix) atomicAdd(&sh[(key >> shift) & (nb - 1)], 1);
+            }
+            __syncthreads();
+            int* ghr = gh + round * kGBins;
+            for (int k = tid; k < nb; k += kGThreads)
+                if (sh[k]) atomicAdd(&ghr[k], sh[k]);
+            grid.sync();
+            // every CTA: bucket of the need-th largest key (suffix scan, 8 bins per thread)
+            const int per_t = nb / kGThreads;  // 8 (or 2 in the last round)
+            int own = 0;
+            for (int q = 0; q < per_t; ++q) {
+                const int bin = nb - 1 - (tid * per_t + q);  // descending order
+                own += __ldcg(&ghr[bin]);
+            }
+            int tot;
+            const int before = block_exclusive_scan(own, scan_scratch, &tot);
+            if (before < need && before + own >= need) {
+                long long cum = before;
+                for (int q = 0; q < per_t; ++q) {
+                    const int bin = nb - 1 - (tid * per_t + q);
+                    const int h = __ldcg(&ghr[bin]);
+                    if (cum + h >= need) {
+                        s_sel[0] = bin;
+                        s_sel[1] = (int)(need - cum);
+                        s_sel[2] = h;
+                        break;
+                    }
+                    cum += h;
+                }
+            }
+            __syncthreads();
+            prefix |= (unsigned long long)s_sel[0] << shift;
+            pmask |= (unsigned long long)(nb - 1) << shift;
+            need = s_sel[1];
+            const bool fin = s_sel[2] == need;  // whole bucket kept
+            __syncthreads();
+            if (fin) {
+                mode = 1;
+                break;
+            }
+        }
+    }
+    const unsigned long long thresh = prefix;
+    // final pass 1: ties and kept-nonzero keys above the threshold, per CTA
+    int t_own = 0, k_own = 0;
+    for (long long k = lo + tid; k < hi; k += kGThreads) {
+        const double x = v[k];
+        const unsigned long long key = (unsigned long long)__double_as_longlong(x + 0.0);
+        bool keep = mode == 0 || (mode == 1 && key >= thresh) || (mode == 2 && key > thresh);
+        if (mode == 2 && key == thresh) ++t_own;
+        k_own += keep && x != 0.0;
+    }
+    int ttot, ktot;
+    block_exclusive_scan(t_own, scan_scratch, &ttot);
+    block_exclusive_scan(k_own, scan_scratch, &ktot);
+    if (tid == 0) {
+        cnt[2 * g] = ttot;
+        cnt[2 * g + 1] = ktot;
+    }
+    grid.sync();
+    // exclusive prefixes over the lower CTAs (index order)
+    long long tie_off = 0, list_off = 0;
+    for (int q = tid; q < g; q += kGThreads) {
+        tie_off += __ldcg(&cnt[2 * q]);
+        list_off += __ldcg(&cnt[2 * q + 1]);
+    }
+    __shared__ long long red[2][kGThreads / 32];
+    {
+        long long a0 = tie_off, a1 = list_off;
+        for (int o = 16; o > 0; o >>= 1) {
+            a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+            a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+        }
+        if ((tid & 31) == 0) {
+            red[0][tid >> 5] = a0;
+            red[1][tid >> 5] = a1;
+        }
+        __syncthreads();
+        tie_off = list_off = 0;
+        for (int w = 0; w < kGThreads / 32; ++w) {
+            tie_off += red[0][w];
+            list_off += red[1][w];
+        }
+    }
+    // kept ties precede the list entries of later CTAs: add the ties kept by
+    // lower CTAs (thresh > 0: ties are nonzero) to the list offset
+    const long long need_eq = mode == 2 ? need : 0;
+    const bool tie_nonzero = thresh != 0ull;
+    {
+        const long long kept_before = tie_off < need_eq ? tie_off : need_eq;
+        if (tie_nonzero) list_off += kept_before;
+    }
+    // final pass 2: in index order, chunks of kGThreads with block scans
+    long long tie_run = tie_off, pos_run = list_off;
+    for (long long base = lo; base < hi; base += kGThreads) {
+        const long long k = base + tid;
+        double x = 0.0;
+        bool keep = false, tie = false;
+        if (k < hi) {
+            x = v[k];
+            const unsigned long long key = (unsigned long long)__double_as_longlong(x + 0.0);
+            keep = mode == 0 || (mode == 1 && key >= thresh) || (mode == 2 && key > thresh);
+            tie = mode == 2 && key == thresh;
+        }
+        int tt;
+        const int tex = block_exclusive_scan(tie ? 1 : 0, scan_scratch, &tt);
+        if (tie) keep = tie_run + tex < need_eq;
+        tie_run += tt;
+        const int nz = (keep && x != 0.0) ? 1 : 0;
+        int kt;
+        const int kex = block_exclusive_scan(nz, scan_scratch, &kt);
+        if (k < hi) {
+            if (!keep) v[k] = 0.0;
+            if (nz && a.list && pos_run + kex < a.list_cap) a.list[pos_run + kex] = (int)k;
+        }
+        pos_run += kt;
+    }
+    if (a.list && g == G - 1 && tid == 0) a.list_count[0] = (int)pos_run;
+}
+
+int topr_grid_ctas(long long m) {
+    static int cap[64] = {};
+    int dev = 0;
+    TPB_CUDA(cudaGetDevice(&dev));
+    if (dev >= 64) dev = 63;
+    if (!cap[dev]) {
+        int sms = 0, per_sm = 0;
+        TPB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        TPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, topr_grid_kernel, kGThreads, 0));
+        cap[dev] = std::max(1, sms * std::min(per_sm, 1));  // one CTA per SM
+    }
+    return (int)std::max<long long>(1, std::min<long long>(cap[dev], (m + 2047) / 2048));
+}
+
+void launch_topr_grid(const SelectArgs& a, int* gh, int* cnt, cudaStream_t st) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(topr_grid_ctas(a.m));
+    cfg.blockDim = dim3(kGThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    TPB_CUDA(cudaLaunchKernelEx(&cfg, topr_grid_kernel, a, gh, cnt));
 }
 
 // Compaction of the nonzero entries of a packed vector into an ascending list

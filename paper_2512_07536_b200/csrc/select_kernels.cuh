@@ -18,6 +18,11 @@ struct SelectArgs {
 };
 
 void launch_topr(const SelectArgs& a, int B, cudaStream_t st);
+// keep_top_r of one large solve (B = 1, hom) over a cooperative grid:
+// gh >= kTopRGridHist ints, cnt >= 2 x topr_grid_ctas(m) ints (scratch).
+constexpr int kTopRGridHist = 6 * 2048;
+int topr_grid_ctas(long long m);
+void launch_topr_grid(const SelectArgs& a, int* gh, int* cnt, cudaStream_t st);
 
 // project_binary_z_capped (proj/src/admm_het.cpp:125-154): ones taken in the
 // order (v desc, index asc) while every capacity row through the column has

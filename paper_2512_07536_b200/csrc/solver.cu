@@ -259,6 +259,7 @@ void Solver::alloc() {
     TPB_CUDA(cudaMemsetAsync(d_.A, 0, (size_t)B * 2 * ld2 * sizeof(double), s0_));
     d_.frob_part = dalloc<double>(s0_, allocs_,(size_t)B * 2 * d_.ntile);
     d_.inv_scale = dalloc<double>(s0_, allocs_,(size_t)B * 2);
+    d_.row_part = dalloc<double>(s0_, allocs_, (size_t)B * 2 * d_.nb * n);
     d_.h = dalloc<double>(s0_, allocs_,B * m);
     if (cfg_.linear_solver == 1) {
         d_.cg = 1;
@@ -311,6 +312,10 @@ void Solver::alloc() {
         // node-major incidence of dense het supports for the trace SLEM
         slem_nbr_ = dalloc<int>(s0_, allocs_, (size_t)B * 2 * list_cap_);
         slem_nwt_ = dalloc<double>(s0_, allocs_, (size_t)B * 2 * list_cap_);
+    }
+    if (!het_ && !cap_ && B == 1 && m >= kTopRGridMin) {
+        topr_gh_ = dalloc<int>(s0_, allocs_, kTopRGridHist);
+        topr_cnt_ = dalloc<int>(s0_, allocs_, 2 * (size_t)topr_grid_ctas(m));
     }
     list_ = dalloc<int>(s0_, allocs_,(size_t)B * list_cap_);
     list_count_ = dalloc<int>(s0_, allocs_,B);
@@ -460,6 +465,10 @@ void Solver::enqueue_select(cudaStream_t st) {
         a.base = d_.Y;
         a.gbase = nullptr;
         a.binary = 0;
+    }
+    if (topr_gh_) {
+        launch_topr_grid(a, topr_gh_, topr_cnt_, st);  // one large solve: the whole GPU
+        return;
     }
     launch_topr(a, B_, st);
 }

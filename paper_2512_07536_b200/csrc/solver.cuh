@@ -44,6 +44,9 @@ void phase_mark(const char* what);
 // space up to this dimension, restarted Lanczos with this basis beyond.
 constexpr int kFinalExactDim = 256;
 constexpr int kFinalKrylov = 128;
+// single homogeneous solves with at least this many candidate edges select
+// top-r over the whole GPU (select_kernels.cu::topr_grid_kernel)
+constexpr long long kTopRGridMin = 65536;
 
 struct SolveResult {
     int iterations = 0;
@@ -136,6 +139,8 @@ class Solver {
     // device buffers
     std::vector<void*> allocs_;
     int* d_r_ = nullptr;
+    int* topr_gh_ = nullptr;   // grid top-r scratch (single large hom solve)
+    int* topr_cnt_ = nullptr;
     double* d_deg_ = nullptr;
     bool ozaki_ = false;        // cone GEMMs on the int8 tensor cores (else FP64 DMMA)
     bool cap_ = false;          // capacity-bound het system

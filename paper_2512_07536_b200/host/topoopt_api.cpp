@@ -12,11 +12,21 @@
 #include <cctype>
 #include <numeric>
 #include <limits>
+#include <map>
 #include <set>
 
 #include "topoopt_b200.h"
+#include "json_lite.hpp"
+
+#include <deque>
+#include <functional>
+#include <variant>
 
 namespace topoopt {
+
+namespace detail {
+SparseMatrix build_kkt(int n, int q, bool het, const std::vector<std::vector<int>>& degree_rows);
+}
 
 namespace {
 
@@ -238,6 +248,53 @@ int edge_index(int n, int i, int j) {
     if (i > j) std::swap(i, j);
     if (i < 0 || j >= n) throw std::invalid_argument("edge_index: endpoint out of range");
     return i * n - i * (i + 1) / 2 + (j - i - 1);
+}
+
+Matrix incidence_matrix(const Topology& t) {
+    // proj/include/topoopt/topology.hpp:36-38: column per edge, +1 at the
+    // lower endpoint, -1 at the higher one
+    t.validate();
+    Matrix a(t.n, (int)t.edges.size());
+    for (size_t c = 0; c < t.edges.size(); ++c) {
+        a(t.edges[c].first, (int)c) = 1.0;
+        a(t.edges[c].second, (int)c) = -1.0;
+    }
+    return a;
+}
+
+double aspl(const Topology& t) {
+    // mean hop distance over unordered pairs (BFS from every node);
+    // +infinity when disconnected (proj/include/topoopt/topology.hpp:60-62)
+    t.validate();
+    const int n = t.n;
+    if (n < 2) return 0.0;
+    std::vector<std::vector<int>> adj(n);
+    for (const auto& [i, j] : t.edges) {
+        adj[i].push_back(j);
+        adj[j].push_back(i);
+    }
+    long long total = 0;
+    std::vector<int> dist(n);
+    std::deque<int> q;
+    for (int s0 = 0; s0 < n; ++s0) {
+        std::fill(dist.begin(), dist.end(), -1);
+        dist[s0] = 0;
+        q.assign(1, s0);
+        int seen = 1;
+        while (!q.empty()) {
+            const int u = q.front();
+            q.pop_front();
+            for (int v : adj[u])
+                if (dist[v] < 0) {
+                    dist[v] = dist[u] + 1;
+                    total += dist[v];
+                    ++seen;
+                    q.push_back(v);
+                }
+        }
+        if (seen < n) return std::numeric_limits<double>::infinity();
+    }
+    return (double)total / ((double)n * (n - 1));  // each pair counted twice
 }
 
 Matrix laplacian(const Topology& t) {
@@ -583,6 +640,17 @@ static Matrix cone(const Matrix& s, bool psd) {
     return out;
 }
 Matrix project_nsd(const Matrix& s) { return cone(s, false); }
+
+EigDecomposition sym_eig(const Matrix& s) {
+    if (s.rows() != s.cols()) throw std::invalid_argument("sym_eig: matrix not square");
+    const int n = s.rows();
+    EigDecomposition d;
+    d.values.assign(n, 0.0);
+    d.vectors = Matrix(n, n);
+    if (n == 0) return d;
+    raise(tp_sym_eig(n, s.data().data(), d.values.data(), d.vectors.data().data()));
+    return d;
+}
 Matrix project_psd(const Matrix& s) { return cone(s, true); }
 
 // ------------------------------------------------------------------ bandwidth
@@ -614,6 +682,13 @@ int CapacitySystem::implied_edge_total() const {
     for (const auto& row : rows) s += row.capacity;
     if (s % 2) throw std::invalid_argument("CapacitySystem: capacity sum is odd, no edge total");
     return (int)(s / 2);
+}
+
+SparseMatrix CapacitySystem::row_matrix() const {
+    std::vector<Triplet> t;
+    for (size_t k = 0; k < rows.size(); ++k)
+        for (int c : rows[k].edge_cols) t.push_back({(int)k, c, 1.0});
+    return SparseMatrix::from_triplets((int)rows.size(), num_edges, t);
 }
 
 CapacitySystem node_level_constraints(int n, const std::vector<int>& degrees) {
@@ -706,12 +781,17 @@ Topology anneal_topology(const CapacitySystem& sys, std::optional<int> r, const 
         return anneal_degree_topology(std::vector<int>(deg.begin(), deg.end()), cfg);
     }
     if (!r) throw std::invalid_argument("anneal_topology: capacity mode needs an explicit r");
+    return anneal_capacity_topology(sys, *r, cfg);
+}
+
+Topology anneal_capacity_topology(const CapacitySystem& sys, int r, const AnnealConfig& cfg) {
+    // proj/src/anneal.cpp:275-391
     cfg.validate();
     const FlatRows f = flat_rows(sys);
-    std::vector<int32_t> e(2 * (size_t)std::max(*r, 1));
+    std::vector<int32_t> e(2 * (size_t)std::max(r, 1));
     int32_t k = 0;
     raise(tp_anneal_capacity(sys.n, (int32_t)sys.rows.size(), f.row_ptr.data(), f.cols.data(), f.caps.data(),
-                             f.allowed.data(), *r, cfg.t0, cfg.cooling, cfg.steps, cfg.moves_per_temp, cfg.seed,
+                             f.allowed.data(), r, cfg.t0, cfg.cooling, cfg.steps, cfg.moves_per_temp, cfg.seed,
                              e.data(), &k));
     Topology t;
     t.n = sys.n;
@@ -823,9 +903,177 @@ CapacitySystem bcube_constraints(const BCubeSpec& spec) {
     return sys;
 }
 
-std::vector<UtilizationRow> utilization(const CapacitySystem& sys, const Topology& t) {
-    // proj/src/admm_het.cpp:371-392
+// ------------------------------------------------------------------ time model
+// The reference's evaluation-side wall-clock model (proj/include/topoopt/
+// bandwidth.hpp:85-128): per-edge bandwidth when every node / link splits its
+// capacity over the edges mapped to it, the iteration/epoch times built on the
+// bottleneck, and the scenario JSON. Outside the solver's hot path.
+namespace {
+
+std::vector<double> node_split(const Topology& t, const std::vector<double>& node_bw) {
+    const auto deg = t.degrees();
+    std::vector<double> out;
+    out.reserve(t.edges.size());
+    for (const auto& [i, j] : t.edges) out.push_back(std::min(node_bw[i] / deg[i], node_bw[j] / deg[j]));
+    return out;
+}
+
+std::vector<double> resource_split(const Topology& t, const CapacitySystem& sys, const std::vector<double>& row_bw) {
+    std::vector<char> sel(sys.num_edges, 0);
+    for (const auto& [i, j] : t.edges) {
+        const int c = edge_index(sys.n, i, j);
+        if (!sys.allowed[c])
+            throw std::invalid_argument("edge {" + std::to_string(i) + "," + std::to_string(j) +
+                                        "} is not carried by any resource");
+        sel[c] = 1;
+    }
+    const auto load = sys.loads(sel);
+    std::vector<double> best(sys.num_edges, std::numeric_limits<double>::infinity());
+    for (size_t k = 0; k < sys.rows.size(); ++k) {
+        if (load[k] == 0) continue;
+        const double share = row_bw[k] / load[k];
+        for (int c : sys.rows[k].edge_cols) best[c] = std::min(best[c], share);
+    }
+    std::vector<double> out;
+    out.reserve(t.edges.size());
+    for (const auto& [i, j] : t.edges) out.push_back(best[edge_index(sys.n, i, j)]);
+    return out;
+}
+
+struct EdgeBandwidth {
+    const Topology& t;
+    std::vector<double> operator()(const HomogeneousScenario& h) const {
+        if (!(h.bandwidth > 0.0)) throw std::invalid_argument("homogeneous bandwidth must be positive");
+        return node_split(t, std::vector<double>(t.n, h.bandwidth));
+    }
+    std::vector<double> operator()(const NodeScenario& ns) const {
+        if ((int)ns.bandwidths.size() != t.n) throw std::invalid_argument("node bandwidth list size mismatch");
+        for (double b : ns.bandwidths)
+            if (!(b > 0.0)) throw std::invalid_argument("node bandwidths must be positive");
+        return node_split(t, ns.bandwidths);
+    }
+    std::vector<double> operator()(const IntraScenario& is) const {
+        const CapacitySystem sys = intra_server_constraints(is.tree);
+        if (t.n != sys.n) throw std::invalid_argument("topology size mismatch with server");
+        std::vector<double> bw;
+        for (const auto& link : is.tree.links) bw.push_back(link.bandwidth);
+        return resource_split(t, sys, bw);
+    }
+    std::vector<double> operator()(const BCubeScenario& bs) const {
+        const CapacitySystem sys = bcube_constraints(bs.spec);
+        if (t.n != sys.n) throw std::invalid_argument("topology size mismatch with bcube");
+        std::vector<double> bw(sys.rows.size());
+        for (int layer = 0; layer < bs.spec.k; ++layer) {
+            const double b = bs.spec.layer_bandwidths.empty() ? kDefaultBandwidth : bs.spec.layer_bandwidths[layer];
+            if (!(b > 0.0)) throw std::invalid_argument("layer bandwidths must be positive");
+            std::fill(bw.begin() + (size_t)layer * sys.n, bw.begin() + (size_t)(layer + 1) * sys.n, b);
+        }
+        return resource_split(t, sys, bw);
+    }
+    std::vector<double> operator()(const FixedScenario&) const {
+        throw std::invalid_argument("fixed-time scenario carries no bandwidth model");
+    }
+};
+
+ServerTree tree_from_json(const json_lite::Value& j) {
+    if (j.contains("preset")) {
+        const std::string& preset = j.at("preset").as_string("preset");
+        if (preset != "tiered8") throw std::invalid_argument("unknown server preset: " + preset);
+        auto num = [&](const char* k, double dflt) { return j.contains(k) ? j.at(k).as_double(k) : dflt; };
+        return tiered8_tree(num("leaf_bandwidth", kDefaultBandwidth / 2.0), num("group_bandwidth", kDefaultBandwidth / 2.0),
+                            num("root_bandwidth", kDefaultBandwidth));
+    }
+    if (!j.contains("devices") || !j.contains("links") || !j.contains("routes"))
+        throw std::invalid_argument("server tree config needs devices, links, routes");
+    ServerTree tree;
+    tree.n_devices = (int)j.at("devices").as_int("devices");
+    std::map<std::string, int> index;
+    for (const auto& lj : j.at("links").items) {
+        ServerLink link{lj.at("name").as_string("name"), lj.at("bandwidth").as_double("bandwidth"),
+                        (int)lj.at("capacity").as_int("capacity")};
+        if (!index.emplace(link.name, (int)tree.links.size()).second)
+            throw std::invalid_argument("duplicate link name: " + link.name);
+        tree.links.push_back(link);
+    }
+    tree.routes.assign(tree.n_devices * (tree.n_devices - 1) / 2, {});
+    for (const auto& rj : j.at("routes").items) {
+        const auto& pair = rj.at("pair");
+        if (!pair.is_array() || pair.items.size() != 2) throw std::invalid_argument("route pair must be [i, j]");
+        const int col = edge_index(tree.n_devices, (int)pair.items[0].as_int("pair"), (int)pair.items[1].as_int("pair"));
+        if (!tree.routes[col].empty()) throw std::invalid_argument("duplicate route for one device pair");
+        for (const auto& name : rj.at("links").items) {
+            auto it = index.find(name.as_string("link"));
+            if (it == index.end()) throw std::invalid_argument("route references unknown link: " + name.text);
+            tree.routes[col].push_back(it->second);
+        }
+    }
+    tree.validate();
+    return tree;
+}
+
+}  // namespace
+
+std::vector<double> edge_bandwidths(const Topology& t, const Scenario& s) {
     t.validate();
+    return std::visit(EdgeBandwidth{t}, s);
+}
+
+double min_edge_bandwidth(const Topology& t, const Scenario& s) {
+    if (t.edges.empty()) throw std::invalid_argument("min_edge_bandwidth: topology has no edges");
+    const auto bw = edge_bandwidths(t, s);
+    return *std::min_element(bw.begin(), bw.end());
+}
+
+double iter_time(double b_avail, double b_min, double t_comm) {
+    if (!(b_avail > 0.0) || !(b_min > 0.0) || !(t_comm > 0.0))
+        throw std::invalid_argument("iter_time: arguments must be positive");
+    return (b_avail / b_min) * t_comm;
+}
+
+double epoch_time(double b_avail, double b_min, double t_comm, double t_comp, int c_iter) {
+    if (t_comp < 0.0) throw std::invalid_argument("epoch_time: negative compute time");
+    if (c_iter < 1) throw std::invalid_argument("epoch_time: need at least one step per epoch");
+    return (iter_time(b_avail, b_min, t_comm) + t_comp) * c_iter;
+}
+
+double iter_time(const TimeModel& m, double b_min) { return iter_time(m.b_avail, b_min, m.t_comm); }
+double epoch_time(const TimeModel& m, double b_min) {
+    return epoch_time(m.b_avail, b_min, m.t_comm, m.t_comp, m.c_iter);
+}
+
+Scenario scenario_from_json(const std::string& text) {
+    const json_lite::Value j = json_lite::parse(text);
+    if (!j.is_object() || !j.contains("mode")) throw std::invalid_argument("scenario config needs a mode");
+    const std::string& mode = j.at("mode").as_string("mode");
+    if (mode == "homogeneous")
+        return HomogeneousScenario{j.contains("bandwidth") ? j.at("bandwidth").as_double("bandwidth") : kDefaultBandwidth};
+    if (mode == "node") {
+        if (!j.contains("bandwidths")) throw std::invalid_argument("node scenario needs bandwidths");
+        return NodeScenario{j.at("bandwidths").as_doubles("bandwidths")};
+    }
+    if (mode == "intra") {
+        if (!j.contains("tree")) throw std::invalid_argument("intra scenario needs a tree");
+        return IntraScenario{tree_from_json(j.at("tree"))};
+    }
+    if (mode == "bcube") {
+        BCubeSpec spec;
+        spec.p = j.contains("p") ? (int)j.at("p").as_int("p") : 0;
+        spec.k = j.contains("k") ? (int)j.at("k").as_int("k") : 0;
+        if (j.contains("layer_bandwidths")) spec.layer_bandwidths = j.at("layer_bandwidths").as_doubles("layer_bandwidths");
+        spec.n_servers();  // validates p, k
+        return BCubeScenario{spec};
+    }
+    if (mode == "fixed") {
+        if (!j.contains("t_iter_ms")) throw std::invalid_argument("fixed scenario needs t_iter_ms");
+        FixedScenario f{j.at("t_iter_ms").as_double("t_iter_ms")};
+        if (!(f.t_iter_ms > 0.0)) throw std::invalid_argument("t_iter_ms must be positive");
+        return f;
+    }
+    throw std::invalid_argument("unknown scenario mode: " + mode);
+}
+
+std::vector<UtilizationRow> utilization(const CapacitySystem& sys, const Topology& t) {
+    // proj/src/admm_het.cpp:371-392 (edges need not be sorted)
     if (t.n != sys.n) throw std::invalid_argument("utilization: node count mismatch");
     std::vector<char> sel(sys.num_edges, 0);
     for (const auto& [i, j] : t.edges) sel[edge_index(t.n, i, j)] = 1;
@@ -845,6 +1093,26 @@ std::string utilization_csv(const std::vector<UtilizationRow>& rows) {
 void SolverConfig::validate() const {
     const tp_config c = to_c(*this);
     raise(tp_config_validate(&c));
+}
+
+SolverConfig solver_config_from_json(const std::string& text) {
+    // proj/src/admm.cpp:197-221: any subset of the fields, unknown keys and
+    // non-objects rejected, then validate()
+    const json_lite::Value j = json_lite::parse(text);
+    if (!j.is_object()) throw std::invalid_argument("solver config must be a JSON object");
+    SolverConfig cfg;
+    for (const auto& [key, v] : j.members) {
+        if (key == "rho") cfg.rho = v.as_double("rho");
+        else if (key == "epsilon") cfg.epsilon = v.as_double("epsilon");
+        else if (key == "max_iter") cfg.max_iter = (int)v.as_int("max_iter");
+        else if (key == "alpha") cfg.alpha = v.as_double("alpha");
+        else if (key == "weight_floor") cfg.weight_floor = v.as_double("weight_floor");
+        else if (key == "seed") cfg.seed = v.as_u64("seed");
+        else if (key == "linear_tol") cfg.linear_tol = v.as_double("linear_tol");
+        else throw std::invalid_argument("solver config: unknown field " + key);
+    }
+    cfg.validate();
+    return cfg;
 }
 
 std::string Solution::trace_csv() const {
@@ -881,6 +1149,8 @@ ProblemData assemble(int n, int r, double alpha, double rho) {
     for (int c = 0; c < n; ++c)
         for (int rr = 0; rr < n; ++rr) pd.beq.push_back(rr == c ? 2.0 : 0.0);
     pd.beq.insert(pd.beq.end(), n, 1.0);
+    pd.kkt = KktMatrix(pd.nx + pd.neq, [n] { return detail::build_kkt(n, 0, false, {}); });
+    pd.ilu = KktIlu(pd.kkt);
     return pd;
 }
 
@@ -975,36 +1245,56 @@ Solution solve(int n, int r, const SolverConfig& cfg, const std::optional<Topolo
 
 // ------------------------------------------------------------------ admm_het
 ProblemDataHet assemble_het(const CapacitySystem& sys, std::optional<int> r, double alpha, double rho) {
-    std::vector<int32_t> deg;
-    if (!node_level_degrees(sys, deg))
-        throw std::invalid_argument("assemble_het: only node-level equality systems are supported");
+    // proj/src/admm_het.cpp:20-114: node-level (equality) systems carry their
+    // degree rows in the KKT and imply r; capacity-bound systems need r in
+    // [1, |E|] and keep their rows out of the equality block (q = 0)
+    if (sys.n < 2) throw std::invalid_argument("assemble_het: need at least 2 nodes");
+    if (sys.num_edges != sys.n * (sys.n - 1) / 2 || (int)sys.allowed.size() != sys.num_edges)
+        throw std::invalid_argument("assemble_het: capacity system columns differ from the pair set");
+    for (const auto& row : sys.rows)
+        for (int c : row.edge_cols)
+            if (c < 0 || c >= sys.num_edges)
+                throw std::invalid_argument("assemble_het: a row references a column outside [0, |E|)");
     if (!(alpha > 0.0)) throw std::invalid_argument("assemble_het: alpha must be positive");
     if (!(rho > 0.0)) throw std::invalid_argument("assemble_het: rho must be positive");
-    long long total = 0;
-    for (int d : deg) total += d;
-    if (total % 2) throw InfeasibleError("degree sum " + std::to_string(total) + " is odd");
-    if (r && *r != total / 2) throw std::invalid_argument("edge total conflicts with the degree rows");
-    const ProblemData base = assemble(sys.n, std::max(1, (int)(total / 2)), alpha, rho);
+    int total = 0, q = 0;
+    std::vector<std::vector<int>> degree_rows;
+    if (sys.equality) {
+        const int implied = sys.implied_edge_total();
+        if (r && *r != implied) throw std::invalid_argument("edge total conflicts with the degree rows");
+        total = implied;
+        q = (int)sys.rows.size();
+        for (const auto& row : sys.rows) degree_rows.push_back(row.edge_cols);
+    } else {
+        if (!r) throw std::invalid_argument("capacity-bound system needs an explicit edge total");
+        total = *r;
+    }
+    const int m = sys.num_edges;
+    if (total < 1 || total > m) throw std::invalid_argument("assemble_het: edge total outside [1, |E|]");
+    const ProblemData base = assemble(sys.n, total, alpha, rho);
     ProblemDataHet pd;
     pd.n = base.n;
     pd.m = base.m;
-    pd.r = (int)(total / 2);
+    pd.r = total;
     pd.alpha = alpha;
     pd.rho = rho;
-    pd.q = sys.n;
+    pd.q = q;
     pd.lambda_ix = base.lambda_ix;
     pd.off_s = base.off_s;
     pd.off_y = base.off_y;
     pd.off_t = base.off_t;
     pd.off_z = base.nx;
-    pd.off_nu = base.nx + base.m;
-    pd.nx = base.nx + 2 * base.m;
-    pd.neq = base.neq + pd.q + base.m;
+    pd.off_nu = base.nx + m;
+    pd.nx = base.nx + 2 * m;
+    pd.neq = base.neq + q + m;
     pd.pairs = base.pairs;
     pd.sys = sys;
     pd.beq = base.beq;
-    for (int d : deg) pd.beq.push_back((double)d);
-    pd.beq.insert(pd.beq.end(), base.m, 0.0);
+    for (int k = 0; k < q; ++k) pd.beq.push_back((double)sys.rows[k].capacity);
+    pd.beq.insert(pd.beq.end(), m, 0.0);
+    const int n = sys.n;
+    pd.kkt = KktMatrix(pd.nx + pd.neq, [n, q, degree_rows] { return detail::build_kkt(n, q, true, degree_rows); });
+    pd.ilu = KktIlu(pd.kkt);
     return pd;
 }
 
@@ -1014,12 +1304,32 @@ Vec project_binary_z(const Vec& v, int r) {
     return z;
 }
 
+Vec project_binary_z_capped(const Vec& v, int r, const CapacitySystem& sys) {
+    // proj/src/admm_het.cpp:125-154 on the device (select_kernels.cu::capped_z_kernel)
+    if ((int)v.size() != sys.num_edges)
+        throw std::invalid_argument("project_binary_z_capped: score length differs from |E|");
+    const FlatRows f = flat_rows(sys);
+    Vec z(v.size());
+    raise(tp_project_binary_z_capped(sys.n, (int32_t)sys.rows.size(), f.row_ptr.data(), f.cols.data(),
+                                     f.caps.data(), f.allowed.data(), v.data(), r, z.data()));
+    return z;
+}
+
 Vec project_Y_het(const ProblemDataHet& pd, const Vec& x, const Vec& d) {
-    std::vector<int32_t> deg;
-    if (!node_level_degrees(pd.sys, deg))
-        throw std::invalid_argument("project_Y_het: only node-level equality systems are supported");
+    if ((int)x.size() != pd.nx || (int)d.size() != pd.nx)
+        throw std::invalid_argument("project_Y_het: state length differs from nx");
     Vec y(pd.nx);
-    raise(tp_project_Y_het_node(pd.n, deg.data(), pd.alpha, pd.rho, x.data(), d.data(), y.data()));
+    std::vector<int32_t> deg;
+    if (pd.sys.equality && node_level_degrees(pd.sys, deg)) {
+        raise(tp_project_Y_het_node(pd.n, deg.data(), pd.alpha, pd.rho, x.data(), d.data(), y.data()));
+        return y;
+    }
+    if (pd.sys.equality)
+        throw std::invalid_argument("project_Y_het: equality systems must be one degree row per node");
+    const FlatRows f = flat_rows(pd.sys);
+    raise(tp_project_Y_het_capacity(pd.n, (int32_t)pd.sys.rows.size(), f.row_ptr.data(), f.cols.data(),
+                                    f.caps.data(), f.allowed.data(), pd.r, pd.alpha, pd.rho, x.data(), d.data(),
+                                    y.data()));
     return y;
 }
 

@@ -8,6 +8,7 @@
 #include <string>
 
 #include "topoopt/admm.hpp"
+#include "topoopt/consensus.hpp"
 #include "topoopt/admm_het.hpp"
 #include "topoopt/bandwidth.hpp"
 #include "topoopt/eig.hpp"

@@ -11,30 +11,8 @@ import numpy as np
 sys.path.insert(0, ".")
 from paper_2512_07536_b200 import _lib  # noqa: E402
 
-KS = 8
-
-
-def planes(M, e):
-    u = M * 2.0 ** (-e)
-    out = []
-    for _ in range(KS):
-        u = u * 128.0
-        d = np.trunc(u)
-        out.append(d)
-        u = u - d
-    return out
-
-
-def emulate(A, eA, B, eB):
-    As, Bs = planes(A, eA), planes(B, eB)
-    acc = np.zeros_like(A)
-    for d in range(KS + 1, 1, -1):
-        g = np.zeros_like(A)
-        for s in range(max(1, d - KS), min(KS, d - 1) + 1):
-            g += As[s - 1] @ Bs[d - s - 1]
-        acc += g * 2.0 ** (-7 * d)
-    acc *= 2.0 ** (eA + eB)
-    return np.tril(acc) + np.tril(acc, -1).T
+sys.path.insert(0, "tests")
+from test_gpu_ozaki import KS, emulate  # noqa: E402  (balanced base-256 digit emulation)
 
 
 def sym_matrix(rng, n, bound):
@@ -53,21 +31,21 @@ def run(ld, nmat=2, reps=20, use_e=0, beta=0.0):
     Cd = np.zeros((nmat, KS, ld, ld), dtype=np.int8)
     ms = C.c_double(0)
     dp = C.POINTER(C.c_double)
-    rc = lib.tp_oz_gemm(ld, nmat, A.ctypes.data_as(dp), 1, B.ctypes.data_as(dp), 1, use_e, 1.0, beta,
-                        Cg.ctypes.data_as(dp), Cd.ctypes.data_as(C.c_void_p), 2, reps, C.byref(ms))
+    rc = lib.tp_oz_gemm(ld, nmat, A.ctypes.data_as(dp), 2, B.ctypes.data_as(dp), 2, use_e, 1.0, beta,
+                        Cg.ctypes.data_as(dp), Cd.ctypes.data_as(C.c_void_p), 3, reps, C.byref(ms))
     if rc != 0:
         raise RuntimeError(lib.tp_last_error_message().decode() if hasattr(lib, "tp_last_error_message") else rc)
     worst_emu = worst_fp = worst_dig = 0.0
     for m in range(nmat if not os.environ.get("OZ_NOEMU") else 0):
-        emu = emulate(A[m], 1, B[m], 1) + (beta * A[m] if use_e else 0.0)
+        emu = emulate(A[m], 2, B[m], 2) + (beta * A[m] if use_e else 0.0)
         ex = A[m] @ B[m]
         ex = np.tril(ex) + np.tril(ex, -1).T + (beta * A[m] if use_e else 0.0)
         sc = np.abs(ex).max()
         worst_emu = max(worst_emu, np.abs(Cg[m] - emu).max() / sc)
         worst_fp = max(worst_fp, np.abs(Cg[m] - ex).max() / sc)
-        rec = sum(Cd[m, s].astype(np.float64) * 2.0 ** (-7 * (s + 1)) for s in range(KS)) * 4.0
+        rec = sum(Cd[m, s].astype(np.float64) * 2.0 ** (-8 * (s + 1)) for s in range(KS)) * 8.0
         worst_dig = max(worst_dig, np.abs(rec - Cg[m]).max())
-    tiles = 2 * (ld // 128) * (ld // 128 + 1) // 2
+    tiles = 2 * (ld // 128) * (ld // 128 + 1) // 2  # 128 x 64 lower tiles
     ops = 2.0 * 128 * 64 * ld * (KS * (KS + 1) // 2) * tiles * nmat  # int8 MACs x 2
     print(f"ld={ld:5d} nmat={nmat} |C-emu|/max={worst_emu:.2e} |C-fp64|/max={worst_fp:.2e} "
           f"|digits-C|={worst_dig:.2e}  {ms.value * 1e3:8.1f} us/launch  "

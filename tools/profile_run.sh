@@ -16,4 +16,6 @@ ncu --set full --clock-control none --import-source on -k regex:xstep_a -s 5 -c 
     -o gpurun_out/prof_xstep_a -f python bench.py $LITE > gpurun_out/ncu_xa.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:xstep_cg -s 2 -c 1 \
     -o gpurun_out/prof_cg -f python tools/cg_probe.py > gpurun_out/ncu_cg.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:topr -s 5 -c 1 \
+    -o gpurun_out/prof_topr -f python bench.py $LITE > gpurun_out/ncu_topr.log 2>&1
 echo profile-done
