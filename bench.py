@@ -113,6 +113,24 @@ def dist_env():
     return ws, rank, local
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def config_n1024(n=N_NODES, r=R_EDGES):
+    """The workload dict both arms report (same_config)."""
+    return {"workload": "n1024_single_instance_per_gpu", "n": n, "r": r, "m_edge_vars": n * (n - 1) // 2,
+            **CFG, "warm_start": "anneal_degree_topology(Alg.1 unit bandwidth, steps=1, moves=1, seed=rank)",
+            "l2": "state+work buffers ~170 MB > 126 MB L2 per iteration"}
+
+
 def warm_start(T, n, r, seed):
     bu, e = T.allocate_edge_capacity([1.0] * n, r)
     return T.anneal_degree_topology(e, steps=1, moves_per_temp=1, seed=seed)
@@ -130,7 +148,18 @@ def cpu_reference_sample(n, r, warm):
 
 
 # ---------------------------------------------------------------- reference arm
+REF_MAX_TIMED = 2  # reference iterations timed (~38 s each on one core at n=1024)
+
+
 def run_reference(args):
+    """The reference's own ADMM loop (proj/src/admm.cpp:360-401), unmodified
+    functions, run sequentially on one core (the reference is
+    single-threaded) on the same n=1024 workload: assemble + feasible start,
+    one untimed iteration, then min(--steps, 2) timed iterations (each ~38 s,
+    so the whole run stays near two minutes; --steps/--warmup are capped and
+    the line says so). The x-step uses the reference's kkt_rhs + ILU(0)
+    BiCGSTAB restarted every 10 iterations, as SURVEY §8d sanctions
+    (un-restarted it stagnates at n=1024)."""
     ws, rank, local = dist_env()
     if rank != 0:
         return
@@ -138,34 +167,30 @@ def run_reference(args):
     if not ref.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
-    sys.path.insert(0, HERE)
     # warm start from the reference's own annealer (steps=1, moves=1), SURVEY §8(d)
     bu, e = ref.allocate([1.0] * N_NODES, R_EDGES)
     warm = ref.anneal_degree(e, steps=1, moves_per_temp=1, seed=0)
-    samples, details = [], []
-    t_start = time.time()
-    budget_s = 150.0
-    for k in range(max(1, args.steps)):
-        per_iter, s, wall = cpu_reference_sample(N_NODES, R_EDGES, warm)
-        samples.append(per_iter)
-        details.append(s)
-        if time.time() - t_start > budget_s:
-            break
-    per = statistics.median(samples)
+    timed = max(1, min(args.steps, REF_MAX_TIMED))
+    t0 = time.time()
+    run = ref.admm_run(N_NODES, R_EDGES, warm, iters=1 + timed, rho=CFG["rho"], chunk=10)
+    wall = time.time() - t0
+    per = statistics.mean(run["iter_s"][1:])
     value = 1.0 / per
-    cores = os.cpu_count()
     line = {
         "impl": "reference", "metric": "admm_iter_per_s_n1024", "value": value, "unit": "iter/s",
-        "n_gpus": args.gpus, "steps": len(samples), "warmup": 0, "ms_per_step": per * 1e3,
+        "n_gpus": args.gpus, "steps": timed, "warmup": 1, "steps_requested": args.steps,
+        "warmup_requested": args.warmup, "ms_per_step": per * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": "n1024_single_instance", "n": N_NODES, "r": R_EDGES, **CFG},
+        "data": "synthetic", "config": config_n1024(),
         "cpu_baseline": {"value": value, "unit": "iter/s", "cores": 1, "kind": "reference",
-                         "host_cores": cores,
-                         "sample": f"{len(samples)} reference ADMM iteration(s) at n=1024: project_nsd, "
-                                   "project_psd, kkt_rhs+BiCGSTAB/ILU (restarted every 10), acf_of_g; "
-                                   "substeps timed concurrently on separate cores, summed per iteration",
-                         "substeps_s": details[-1]},
+                         "cpu_model": cpu_model(), "host_cores": os.cpu_count(),
+                         "sample": f"reference ADMM loop (proj/src/admm.cpp:384-406) sequential on one core: "
+                                   f"assemble + feasible start ({run['setup_s']:.1f} s), 1 untimed iteration, "
+                                   f"{timed} timed iteration(s) of project_Y, kkt_rhs + ILU(0) BiCGSTAB "
+                                   "(restarted every 10), update_duals, residual, acf_of_g; --steps capped at "
+                                   f"{REF_MAX_TIMED} to keep the run within minutes",
+                         "iteration_s": run["iter_s"], "setup_s": run["setup_s"],
+                         "bicgstab_iters": run["bicgstab_iters"], "wall_s": wall},
         "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -363,6 +388,7 @@ def run_ours(args):
             if ref.available():
                 per_iter, s, wall = cpu_reference_sample(n, r, warm)
                 cpu = {"value": 1.0 / per_iter, "unit": "iter/s", "cores": 1, "kind": "reference",
+                       "cpu_model": cpu_model(),
                        "sample": "one reference ADMM iteration at n=1024 (project_nsd, project_psd, "
                                  "restarted BiCGSTAB x-step, acf_of_g), substeps timed concurrently, "
                                  f"summed: {per_iter:.2f} s/iter (wall {wall:.1f} s)",
@@ -376,16 +402,14 @@ def run_ours(args):
         # the reference's KKT assembly + ILU setup (stated as extrapolated)
         setup = (cpu.get("substeps_s") or {}).get("setup_s", 0.0)
         cpu["time_to_topology_s_extrapolated"] = ttt["iterations"] / cpu["value"] + setup
+    sweep = None if args.no_sweep else sweep_phase(args, ws, rank, local, torch, tdist)
     if rank == 0:
         pk = peaks()
         line = {
             "metric": "admm_iter_per_s_n1024", "value": value, "unit": "iter/s", "n_gpus": ws,
             "steps": K, "warmup": W, "ms_per_step": dt / K * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "n1024_single_instance_per_gpu", "n": n, "r": r,
-                       "m_edge_vars": m, **CFG,
-                       "warm_start": "anneal_degree_topology(Alg.1 unit bandwidth, steps=1, moves=1, seed=rank)",
-                       "l2": "state+work buffers ~170 MB > 126 MB L2 per iteration"},
+            "config": config_n1024(n, r),
             "roofline": roof,
             "phases_ms": {"cone_projection": t_cone * 1e3, "xstep": t_x * 1e3, "topr": t_sel * 1e3,
                           "trace_slem": t_slem * 1e3, "prep": t_prep * 1e3},
@@ -412,26 +436,77 @@ def run_ours(args):
             "gpu_launches": launches_per_iter * K,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
+            "sweep": sweep,
         }
         print(json.dumps(line), flush=True)
     if ws > 1:
         tdist.destroy_process_group()
 
 
-def run_sweep(args):
-    """Config 5: n=256 x 64 budgets x 4 bandwidth scenarios = 256 independent
-    solves, sharded round-robin across ranks (no data-path collective)."""
-    import torch
-    import torch.distributed as tdist
+def cpu_sweep_baseline(rows, n=256):
+    """Config-5 CPU baseline: the reference's own
+    ADMM loops (oracle/_ref: ref_admm_run / ref_admm_het_run -- admm.cpp /
+    admm_het.cpp with BiCGSTAB restarted every 10, since the un-restarted
+    solve stalls on some of these n=256 instances) on all host cores, one
+    solve per core, on a fixed subset -- every scenario x 4 budgets spread
+    over the sweep -- 5 iterations each: setup and per-iteration seconds
+    (mean of iterations 2-5). The whole sweep is extrapolated with the GPU
+    run's per-job iteration counts (same algorithm, same iteration counts:
+    parity tests)."""
+    import concurrent.futures as cf
 
-    ws, rank, local = dist_env()
-    if ws > 1:
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
-    from paper_2512_07536_b200 import _lib
+    from oracle import ref
+    from paper_2512_07536_b200.sweep import SCENARIOS, scenario_bandwidths
+    budgets = sorted({r.r for r in rows})
+    step = max(1, len(budgets) // 4)
+    pick = budgets[::step][:4]
+    samples = [(sc, rb) for sc in SCENARIOS for rb in pick]
+
+    def one(sc, rb):
+        if sc == "homogeneous":
+            bu, e = ref.allocate([1.0] * n, rb)
+        else:
+            try:
+                bu, e = ref.allocate(scenario_bandwidths(sc, n), rb)
+            except Exception:
+                return sc, rb, None
+        warm = ref.anneal_degree(e, steps=1, moves_per_temp=1, seed=0)
+        if sc == "homogeneous":
+            run = ref.admm_run(n, rb, warm, iters=5, rho=10.0, chunk=10)
+        else:
+            run = ref.admm_het_run(e, warm, iters=5, rho=10.0, chunk=10)
+        return sc, rb, (statistics.mean(run["iter_s"][1:]), run["setup_s"])
+
+    cores = os.cpu_count() or 1
+    t0 = time.time()
+    with cf.ThreadPoolExecutor(max_workers=min(len(samples), cores)) as ex:
+        res = list(ex.map(lambda p: one(*p), samples))
+    wall = time.time() - t0
+    model = {}
+    for sc, rb, v in res:
+        if v is not None:
+            model.setdefault(sc, []).append((rb, v))
+    total = 0.0
+    for row in rows:
+        if row.status != "ok" or row.scenario not in model:
+            continue
+        rb, (per, fixed) = min(model[row.scenario], key=lambda q: abs(q[0] - row.r))
+        total += fixed + row.iterations * per
+    value = len(rows) / (total / cores) if total > 0 else None
+    return {"value": value, "unit": "solves/s", "cores": cores, "kind": "reference", "cpu_model": cpu_model(),
+            "sample": f"{len(samples)} reference ADMM loops (4 scenarios x budgets {pick}), 5 iterations each, one "
+                      f"per core concurrently ({wall:.1f} s wall); the sweep's CPU seconds extrapolated from the "
+                      "per-iteration and setup costs with the GPU run's iteration counts, divided over all cores",
+            "cpu_seconds_total_extrapolated": total,
+            "per_iteration_s": {sc: {str(rb): round(v[0], 4) for rb, v in lst} for sc, lst in model.items()}}
+
+
+def sweep_phase(args, ws, rank, local, torch, tdist, cpu=True):
+    """Config 5: n=256 x 64 budgets x 4 bandwidth scenarios = 256 independent
+    solves, sharded across ranks (no data-path collective). Returns the
+    sweep dict on rank 0 (None elsewhere)."""
     from paper_2512_07536_b200.sweep import gather, partition, run_jobs, sweep_jobs
 
-    _lib.load().tp_set_device(local)
     jobs = sweep_jobs(n=256, n_budgets=args.sweep_budgets, dr=32 * (64 // args.sweep_budgets))
     mine = partition(jobs, ws, rank)
     if ws > 1:
@@ -447,23 +522,48 @@ def run_sweep(args):
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         wall = float(t.item())
     allrows = gather(rows)
+    if rank != 0:
+        return None
+    ok = [r for r in allrows if r.status == "ok"]
+    out = {
+        "metric": "batched_solves_per_s_n256_sweep", "value": len(jobs) / wall, "unit": "solves/s",
+        "n_gpus": ws, "jobs": len(jobs), "scaling": "strong", "higher_is_better": True,
+        "config": {"workload": "sweep_n256_budgets_x_scenarios", "n": 256,
+                   "budgets": [min(j.r for j in jobs), max(j.r for j in jobs), len({j.r for j in jobs})],
+                   "scenarios": sorted({j.scenario for j in jobs}), "rho": 10.0, "epsilon": 1e-8,
+                   "max_iter": args.sweep_max_iter, "warm_start": "anneal_degree_topology(Alg.1, steps=1, moves=1)"},
+        "solved": len(ok), "infeasible": len(allrows) - len(ok), "converged": sum(r.converged for r in ok),
+        "iterations_total": sum(r.iterations for r in ok),
+        "iterations_max": max((r.iterations for r in ok), default=0),
+        "wall_s": wall, "clocks": clk.summary(),
+    }
+    if cpu and ws == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle import ref
+            if ref.available():
+                out["cpu_baseline"] = cpu_sweep_baseline(allrows)
+        except Exception as exc:  # reported, not required
+            out["cpu_baseline"] = {"value": None, "sample": f"failed: {exc}"}
+    return out
+
+
+def run_sweep(args):
+    """--workload sweep: the config-5 sweep alone, as its own JSON line."""
+    import torch
+    import torch.distributed as tdist
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    from paper_2512_07536_b200 import _lib
+
+    _lib.load().tp_set_device(local)
+    out = sweep_phase(args, ws, rank, local, torch, tdist)
     if rank == 0:
-        ok = [r for r in allrows if r.status == "ok"]
-        line = {
-            "metric": "batched_solves_per_s_n256_sweep", "value": len(jobs) / wall, "unit": "solves/s",
-            "n_gpus": ws, "steps": len(jobs), "warmup": 0, "ms_per_step": wall / len(jobs) * 1e3,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic",
-            "config": {"workload": "sweep_n256_budgets_x_scenarios", "n": 256,
-                       "budgets": sorted({j.r for j in jobs}), "scenarios": list({j.scenario for j in jobs}),
-                       "rho": 10.0, "epsilon": 1e-8, "max_iter": args.sweep_max_iter,
-                       "warm_start": "anneal_degree_topology(Alg.1, steps=1, moves=1)"},
-            "solved": len(ok), "infeasible": len(allrows) - len(ok),
-            "converged": sum(r.converged for r in ok),
-            "iterations_total": sum(r.iterations for r in ok),
-            "iterations_max": max((r.iterations for r in ok), default=0),
-            "wall_s": wall, "clocks": clk.summary(),
-        }
+        line = dict(out)
+        line.update({"steps": out["jobs"], "warmup": 0, "ms_per_step": out["wall_s"] / out["jobs"] * 1e3,
+                     "vs_baseline": None, "dtype": "f64", "data": "synthetic"})
         print(json.dumps(line), flush=True)
     if ws > 1:
         tdist.destroy_process_group()
@@ -553,6 +653,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-topology solve")
     ap.add_argument("--no-cg", action="store_true", help="skip the CG x-step variant measurement")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the config-5 sweep sub-object")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

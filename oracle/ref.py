@@ -94,6 +94,8 @@ def lib():
         L.ref_extract_topology.argtypes = [I, I, dp, D, ip, dp, ip]
         L.ref_project_binary_z.argtypes = [dp, I, I, dp]
         L.ref_iteration_sample.argtypes = [I, I, ip, I, D, I, dp]
+        L.ref_admm_run.argtypes = [I, I, ip, I, D, I, I, dp]
+        L.ref_admm_het_run.argtypes = [I, ip, ip, I, D, I, I, dp]
         _lib = L
     return _lib
 
@@ -409,3 +411,24 @@ def iteration_sample(n, r, warm_edges, rho=10.0, chunk=10):
     _check(lib().ref_iteration_sample(n, r, _ip(we), len(we), rho, chunk, _dp(t)))
     return {"project_nsd_s": t[0], "project_psd_s": t[1], "xstep_s": t[2], "acf_s": t[3],
             "setup_s": t[4], "bicgstab_iters": int(t[5])}
+
+
+def admm_run(n, r, warm_edges, iters, rho=10.0, chunk=10):
+    """The reference's own ADMM loop, sequential on this thread (see
+    ref_shim.cpp::ref_admm_run): setup seconds, per-iteration seconds."""
+    we = np.ascontiguousarray(np.asarray(warm_edges, np.int32).reshape(-1, 2))
+    out = np.zeros(iters + 3)
+    _check(lib().ref_admm_run(n, r, _ip(we), len(we), rho, iters, chunk, _dp(out)))
+    return {"setup_s": float(out[0]), "iter_s": out[1:iters + 1].tolist(),
+            "residual": float(out[iters + 1]), "bicgstab_iters": int(out[iters + 2])}
+
+
+def admm_het_run(degrees, warm_edges, iters, rho=10.0, chunk=10):
+    """The reference's node-level heterogeneous ADMM loop, sequential on this
+    thread (ref_shim.cpp::ref_admm_het_run)."""
+    deg = np.ascontiguousarray(np.asarray(degrees, np.int32))
+    we = np.ascontiguousarray(np.asarray(warm_edges, np.int32).reshape(-1, 2))
+    out = np.zeros(iters + 3)
+    _check(lib().ref_admm_het_run(len(deg), _ip(deg), _ip(we), len(we), rho, iters, chunk, _dp(out)))
+    return {"setup_s": float(out[0]), "iter_s": out[1:iters + 1].tolist(),
+            "residual": float(out[iters + 1]), "bicgstab_iters": int(out[iters + 2])}

@@ -15,6 +15,7 @@
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <limits>
 #include <memory>
 #include <optional>
 #include <stdexcept>
@@ -619,6 +620,123 @@ int ref_iteration_sample(int n, int r, const int* warm_edges, int n_warm, double
         times[2] = tx;
         times[3] = ta;
         times[5] = iters;
+    });
+}
+
+// The reference's homogeneous ADMM loop (proj/src/admm.cpp:360-401) run
+// sequentially on the calling thread for `iters` iterations, with the one
+// sanctioned change: the x-step solves its KKT system with the
+// reference's own kkt_rhs + ILU(0) BiCGSTAB restarted every `chunk`
+// iterations (update_X's un-restarted BiCGSTAB stagnates at n = 1024,
+// SURVEY §6). Every other call is the reference's: assemble,
+// feasible_start, project_Y, update_duals, the residual, acf_of_g, the
+// best-iterate copy. out = {setup_s, iter_1_s, ..., iter_k_s, residual_k,
+// bicgstab_iterations_total}.
+int ref_admm_run(int n, int r, const int* warm_edges, int n_warm, double rho, int iters, int chunk,
+                 double* out) {
+    return guarded([&] {
+        using clk = std::chrono::steady_clock;
+        auto sec = [](clk::time_point a, clk::time_point b) {
+            return std::chrono::duration<double>(b - a).count();
+        };
+        const auto t0 = clk::now();
+        ProblemData pd = assemble(n, r, 2.0, rho);
+        const auto lo = detail::hom_layout(n);
+        Topology warm = make_topo(n, warm_edges, nullptr, n_warm);
+        Vec x_state = detail::feasible_start(lo, warm, 2.0);
+        Vec y_state = x_state;
+        Vec duals(pd.nx, 0.0);
+        Vec kkt_warm(pd.nx + pd.neq, 0.0);
+        std::copy(x_state.begin(), x_state.end(), kkt_warm.begin());
+        double best_res = std::numeric_limits<double>::infinity();
+        Vec best_y = y_state;
+        out[0] = sec(t0, clk::now());
+        double res = 0.0;
+        long long bicg = 0;
+        for (int it = 1; it <= iters; ++it) {
+            const auto a = clk::now();
+            y_state = project_Y(pd, x_state, duals);
+            const Vec rhs = detail::kkt_rhs(lo, y_state, duals, pd.beq, pd.rho);
+            for (int round = 0; round < 100000; ++round) {
+                SolveReport rep = bicgstab(pd.kkt, rhs, kkt_warm, &pd.ilu, 1e-10, chunk);
+                bicg += rep.iterations;
+                if (rep.converged) break;
+            }
+            x_state.assign(kkt_warm.begin(), kkt_warm.begin() + pd.nx);
+            update_duals(pd, x_state, y_state, duals);
+            res = 0.0;
+            for (int k = 0; k < pd.nx; ++k) {
+                const double d = x_state[k] - y_state[k];
+                res += d * d;
+            }
+            volatile double acf = detail::acf_of_g(n, pd.pairs, y_state.data());
+            (void)acf;
+            if (res < best_res) {
+                best_res = res;
+                best_y = y_state;
+            }
+            out[it] = sec(a, clk::now());
+        }
+        out[iters + 1] = res;
+        out[iters + 2] = (double)bicg;
+    });
+}
+
+// The reference's node-level heterogeneous ADMM loop (proj/src/admm_het.cpp:
+// 235-297) sequential on the calling thread, the x-step's BiCGSTAB restarted
+// every `chunk` iterations (as ref_admm_run). out as ref_admm_run.
+int ref_admm_het_run(int n, const int* degrees, const int* warm_edges, int n_warm, double rho, int iters,
+                     int chunk, double* out) {
+    return guarded([&] {
+        using clk = std::chrono::steady_clock;
+        auto sec = [](clk::time_point a, clk::time_point b) {
+            return std::chrono::duration<double>(b - a).count();
+        };
+        const auto t0 = clk::now();
+        CapacitySystem sys = node_level_constraints(n, std::vector<int>(degrees, degrees + n));
+        ProblemDataHet pd = assemble_het(sys, std::nullopt, 2.0, rho);
+        const auto lo = detail::het_layout(pd.n, pd.q);
+        const int m = pd.m;
+        Topology warm = make_topo(n, warm_edges, nullptr, n_warm);
+        Vec x_state = detail::feasible_start(lo, warm, 2.0);
+        for (const auto& [i, j] : warm.edges) x_state[pd.off_z + edge_index(n, i, j)] = 1.0;
+        for (int l = 0; l < m; ++l) x_state[pd.off_nu + l] = std::max(0.0, x_state[pd.off_z + l] - x_state[l]);
+        Vec y_state = x_state;
+        Vec duals(pd.nx, 0.0);
+        Vec kkt_warm(pd.nx + pd.neq, 0.0);
+        std::copy(x_state.begin(), x_state.end(), kkt_warm.begin());
+        double best_res = std::numeric_limits<double>::infinity();
+        Vec best_y = y_state, best_score(m, 0.0);
+        out[0] = sec(t0, clk::now());
+        double res = 0.0;
+        long long bicg = 0;
+        for (int it = 1; it <= iters; ++it) {
+            const auto a = clk::now();
+            y_state = project_Y_het(pd, x_state, duals);
+            const Vec rhs = detail::kkt_rhs(lo, y_state, duals, pd.beq, pd.rho);
+            for (int round = 0; round < 100000; ++round) {
+                SolveReport rep = bicgstab(pd.kkt, rhs, kkt_warm, &pd.ilu, 1e-10, chunk);
+                bicg += rep.iterations;
+                if (rep.converged) break;
+            }
+            x_state.assign(kkt_warm.begin(), kkt_warm.begin() + pd.nx);
+            for (int k = 0; k < pd.nx; ++k) duals[k] += pd.rho * (x_state[k] - y_state[k]);
+            res = 0.0;
+            for (int k = 0; k < pd.nx; ++k) {
+                const double d = x_state[k] - y_state[k];
+                res += d * d;
+            }
+            volatile double acf = detail::acf_of_g(n, pd.pairs, y_state.data());
+            (void)acf;
+            if (res < best_res) {
+                best_res = res;
+                best_y = y_state;
+                for (int l = 0; l < m; ++l) best_score[l] = x_state[pd.off_z + l] + duals[pd.off_z + l] / pd.rho;
+            }
+            out[it] = sec(a, clk::now());
+        }
+        out[iters + 1] = res;
+        out[iters + 2] = (double)bicg;
     });
 }
 

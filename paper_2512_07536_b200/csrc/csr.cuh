@@ -6,14 +6,14 @@
 namespace tpb {
 
 // Builds, for the ascending packed edge list `list[0..ne)`:
-//   ei/ej/ew   endpoints and weights g[list[e]]
+//   ei/ej/ew   endpoints and weights g[list[e]] (aligned: g[e])
 //   rowptr     edges e with ei[e] == v are rowptr[v]..rowptr[v+1] (ascending e)
 //   colptr/cidx edges with ej[e] == v, cidx[colptr[v]..colptr[v+1]) ascending e
 // so "column part then row part" visits a node's incident edges in ascending
 // edge index — the accumulation order of the reference's loops over pairs.
 // rowptr/colptr/cur live in shared memory (n+1, n+1, n ints).
-__device__ inline void build_csr(int n, int ne, const int* list, const double* g, int* ei, int* ej,
-                                 double* ew, int* rowptr, int* colptr, int* cur, int* cidx,
+__device__ inline void build_csr(int n, int ne, const int* list, const double* g, bool aligned, int* ei,
+                                 int* ej, double* ew, int* rowptr, int* colptr, int* cur, int* cidx,
                                  int* iscr) {
     const int tid = threadIdx.x, nthr = blockDim.x;
     for (int e = tid; e < ne; e += nthr) {
@@ -21,7 +21,7 @@ __device__ inline void build_csr(int n, int ne, const int* list, const double* g
         edge_pair(n, list[e], i, j);
         ei[e] = i;
         ej[e] = j;
-        ew[e] = g[list[e]];
+        ew[e] = aligned ? g[e] : g[list[e]];
     }
     for (int v = tid; v < n; v += nthr) {
         rowptr[v] = 0;

@@ -226,7 +226,7 @@ __global__ void extract_kernel(int n, long long m, const double* gall, long long
     int* cidx = cidx_all + (long long)b * list_cap;
     __shared__ int iscr[32];
     __shared__ double scratch[32];
-    build_csr(n, ne, list, g, ei, ej, ew, rowptr, colptr, cur, cidx, iscr);
+    build_csr(n, ne, list, g, false, ei, ej, ew, rowptr, colptr, cur, cidx, iscr);
     double worst = -INFINITY;
     for (int v = threadIdx.x; v < n; v += blockDim.x) {
         double s = 0.0;  // ascending edge index: (u, v) u < v first, then (v, j)

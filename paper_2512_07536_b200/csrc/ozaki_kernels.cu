@@ -130,6 +130,20 @@ __device__ __forceinline__ double i32_to_f64(uint32_t x) {
     return __hiloint2double(0x43300000, (int)(x ^ 0x80000000u)) - 4503601774854144.0;
 }
 
+#ifdef OZ_STAMPS
+// instrumentation build only (make STAMPS=1): globaltimer stamps per CTA
+__device__ long long* g_oz_stamps = nullptr;
+__device__ __forceinline__ void stamp(int slot) {
+    if (!g_oz_stamps) return;
+    long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    g_oz_stamps[8LL * (blockIdx.y * gridDim.x + blockIdx.x) + slot] = t;
+}
+#define OZ_STAMP(slot) stamp(slot)
+#else
+#define OZ_STAMP(slot) ((void)0)
+#endif
+
 __device__ __forceinline__ double spow(double s, int p) {
     return p == 0 ? 1.0 : (p == 1 ? s : (p == 2 ? s * s : (p == -1 ? 1.0 / s : 1.0)));
 }
@@ -250,6 +264,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t tmem = tmem_slot;
     const int KB = ld / BK;
     const int rc = g.rc ? g.rc : ld;  // plane layout (OzShard)
+    if (threadIdx.x == 0) OZ_STAMP(0);
     // plane row of (slice 0, row i): slice s adds s * rc
     auto prow = [&](int i) { return (long long)mat * KS * ld + (long long)(i / rc) * KS * rc + i % rc; };
     const long long a_row0 = prow(i0), b_row0 = prow(j0);
@@ -296,6 +311,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 tc_commit(empty_bar(st));
             }
             tc_commit(tfull_bar);
+            OZ_STAMP(1);
         }
     } else {
         // ---------------- epilogue: warps 2..17; thread <-> (tile row = TMEM
@@ -307,6 +323,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
         mbar_wait(tfull_bar, 0);
         tc_fence_after();
+        if (threadIdx.x == 64) OZ_STAMP(2);
         double acc[HN];
 #pragma unroll
         for (int j = 0; j < HN; ++j) acc[j] = 0.0;
@@ -348,6 +365,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         // themselves and their mirror; in the diagonal 128-row block the tile
         // t = J - R I owns rows BN t.. (its BN x BN diagonal sub-block
         // symmetrised) and mirrors rows BN (t+1).. into the tiles to its right.
+        if (threadIdx.x == 64) OZ_STAMP(3);
         const int tdiag = J - R * I;
         const int dr0 = tdiag < 0 ? 0 : BN * tdiag;          // first directly owned tile row
         const int mr0 = tdiag < 0 ? 0 : BN * (tdiag + 1);    // first mirrored tile row
@@ -442,6 +460,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
     }
+    if (threadIdx.x == 64) OZ_STAMP(4);
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
@@ -507,6 +526,13 @@ void encode(CUtensorMap* m, const int8_t* base, int ld, long long rows, int box_
 }
 
 }  // namespace
+
+#ifdef OZ_STAMPS
+// instrumentation build: stamps[8 * cta + slot] (ns) of every following launch
+extern "C" int tp_oz_set_stamps(void* dev_ptr) {
+    return cudaMemcpyToSymbol(g_oz_stamps, &dev_ptr, sizeof(void*)) == cudaSuccess ? 0 : 7;
+}
+#endif
 
 void check_oz_ld(int ld) {
     if (ld < BM || ld % BM != 0 || ld > kOzMaxLd)

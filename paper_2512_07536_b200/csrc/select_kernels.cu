@@ -39,7 +39,11 @@ __device__ inline unsigned long long key_of(double v, int binary) {
 // compaction of the nonzero clamped Y_g.
 __global__ void __launch_bounds__(kThreads) topr_kernel(SelectArgs a) {
     const int b = blockIdx.x;
-    if (a.done && a.done[b * 8 + 1]) return;
+    if (a.done && a.done[b * 8 + 1]) {
+        if (a.it_snap && threadIdx.x == 0) a.it_snap[b] = -1;
+        return;
+    }
+    if (a.it_snap && threadIdx.x == 0) a.it_snap[b] = a.done ? a.done[b * 8] : 0;
     const long long m = a.m;
     double* v = a.base + (long long)b * a.stride;
     const long long r = a.r[b];
@@ -177,8 +181,10 @@ __global__ void __launch_bounds__(kThreads) topr_kernel(SelectArgs a) {
 #pragma unroll
             for (int q = 0; q < kItems; ++q) {
                 const long long k = base + (long long)tid * kItems + q;
-                if (k < m && keep[q] && val[q] != 0.0 && pos < a.list_cap)
+                if (k < m && keep[q] && val[q] != 0.0 && pos < a.list_cap) {
+                    if (a.list_w) a.list_w[(long long)b * a.list_cap + pos] = val[q];
                     a.list[(long long)b * a.list_cap + pos++] = (int)k;
+                }
             }
             kept_run += tot;
         }
@@ -201,8 +207,10 @@ __global__ void __launch_bounds__(kThreads) topr_kernel(SelectArgs a) {
 #pragma unroll
             for (int q = 0; q < kItems; ++q) {
                 const long long k = base + (long long)tid * kItems + q;
-                if (k < m && g[k] != 0.0 && pos < a.list_cap)
+                if (k < m && g[k] != 0.0 && pos < a.list_cap) {
+                    if (a.list_w) a.list_w[(long long)b * a.list_cap + pos] = g[k];
                     a.list[(long long)b * a.list_cap + pos++] = (int)k;
+                }
             }
             run += tot;
         }
@@ -242,7 +250,11 @@ __device__ __forceinline__ int g_bits(int round) { return round < 5 ? 11 : 9; }
 
 __global__ void __launch_bounds__(kGThreads, 8) topr_grid_kernel(SelectArgs a, int* gh, int* cnt) {
     cg::grid_group grid = cg::this_grid();
-    if (a.done && a.done[1]) return;  // uniform across the grid
+    if (a.done && a.done[1]) {  // uniform across the grid
+        if (a.it_snap && blockIdx.x == 0 && threadIdx.x == 0) a.it_snap[0] = -1;
+        return;
+    }
+    if (a.it_snap && blockIdx.x == 0 && threadIdx.x == 0) a.it_snap[0] = a.done ? a.done[0] : 0;
     const long long m = a.m;
     double* v = a.base;
     const long long r = a.r[0];
@@ -384,7 +396,10 @@ __global__ void __launch_bounds__(kGThreads, 8) topr_grid_kernel(SelectArgs a, i
         const int kex = block_exclusive_scan(nz, scan_scratch, &kt);
         if (k < hi) {
             if (!keep) v[k] = 0.0;
-            if (nz && a.list && pos_run + kex < a.list_cap) a.list[pos_run + kex] = (int)k;
+            if (nz && a.list && pos_run + kex < a.list_cap) {
+                a.list[pos_run + kex] = (int)k;
+                if (a.list_w) a.list_w[pos_run + kex] = x;
+            }
         }
         pos_run += kt;
     }
@@ -421,8 +436,14 @@ void launch_topr_grid(const SelectArgs& a, int* gh, int* cnt, cudaStream_t st) {
 // Compaction of the nonzero entries of a packed vector into an ascending list
 // (used when no selection runs, e.g. the SLEM of an arbitrary weight vector).
 __global__ void __launch_bounds__(kThreads) compact_kernel(const double* g, long long stride, long long m,
-                                                          int* list, int* count, int cap) {
+                                                          int* list, int* count, int cap, double* list_w,
+                                                          int* it_snap, const int* done) {
     const int b = blockIdx.x;
+    if (done && done[b * 8 + 1]) {
+        if (it_snap && threadIdx.x == 0) it_snap[b] = -1;
+        return;
+    }
+    if (it_snap && threadIdx.x == 0) it_snap[b] = done ? done[b * 8] : 0;
     g += (long long)b * stride;
     __shared__ int scan_scratch[32];
     int run = 0;
@@ -438,7 +459,10 @@ __global__ void __launch_bounds__(kThreads) compact_kernel(const double* g, long
 #pragma unroll
         for (int q = 0; q < kItems; ++q) {
             const long long k = base + (long long)threadIdx.x * kItems + q;
-            if (k < m && g[k] != 0.0 && pos < cap) list[(long long)b * cap + pos++] = (int)k;
+            if (k < m && g[k] != 0.0 && pos < cap) {
+                if (list_w) list_w[(long long)b * cap + pos] = g[k];
+                list[(long long)b * cap + pos++] = (int)k;
+            }
         }
         run += tot;
     }
@@ -446,8 +470,8 @@ __global__ void __launch_bounds__(kThreads) compact_kernel(const double* g, long
 }
 
 void launch_compact(const double* g, long long stride, long long m, int* list, int* count, int cap,
-                    int B, cudaStream_t st) {
-    compact_kernel<<<B, kThreads, 0, st>>>(g, stride, m, list, count, cap);
+                    int B, cudaStream_t st, double* list_w, int* it_snap, const int* done) {
+    compact_kernel<<<B, kThreads, 0, st>>>(g, stride, m, list, count, cap, list_w, it_snap, done);
     TPB_CHECK_LAUNCH();
 }
 

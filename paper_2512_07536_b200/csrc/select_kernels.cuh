@@ -14,7 +14,9 @@ struct SelectArgs {
     int* list;           // per-solve ascending list of kept nonzero edges
     int* list_count;
     int list_cap;
-    const int* done;     // ictl (done flag at [b*8+1]) or null
+    double* list_w;      // weights aligned with the list (per solve at b*list_cap), or null
+    int* it_snap;        // per solve: iteration counter ictl[b*8] at selection, -1 if done (or null)
+    const int* done;     // ictl (done flag at [b*8+1], iteration counter at [b*8]) or null
 };
 
 void launch_topr(const SelectArgs& a, int B, cudaStream_t st);
@@ -45,8 +47,10 @@ struct CappedArgs {
     const int* done;           // ictl or null
 };
 void launch_capped_z(const CappedArgs& a, int B, cudaStream_t st);
+// ascending nonzero entries of g (+ aligned weights / iteration snapshot as in SelectArgs)
 void launch_compact(const double* g, long long stride, long long m, int* list, int* count, int cap,
-                    int B, cudaStream_t st);
+                    int B, cudaStream_t st, double* list_w = nullptr, int* it_snap = nullptr,
+                    const int* done = nullptr);
 
 // Once-per-device opt-in for > 48 KB dynamic shared memory.
 template <typename K>

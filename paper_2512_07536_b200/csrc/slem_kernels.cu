@@ -220,14 +220,22 @@ __device__ inline void cgs2(const double* Q, int n, int ldq, int k, double* w, d
     }
 }
 
+// Trace mode: the iteration a report belongs to, or -1 when the solve is done.
+__device__ inline int slem_iter(const SlemArgs& a, int b) {
+    if (a.it_snap) return a.it_snap[b];
+    if (a.ictl) return a.ictl[b * 8 + 1] ? -1 : a.ictl[b * 8];
+    return 0;
+}
+
 __global__ void __launch_bounds__(kThreads) slem_kernel(SlemArgs a) {
     const int b = blockIdx.x;
-    if (a.ictl && a.ictl[b * 8 + 1]) return;  // solve already finished
+    const int it_rec = slem_iter(a, b);
+    if (it_rec < 0) return;  // solve already finished
     const int n = a.n;
     const int tid = threadIdx.x, nthr = blockDim.x, wid = tid >> 5;
     const int ne = min(a.count[b], a.list_cap);
     const int* list = a.list + (long long)b * a.list_cap;
-    const double* g = a.g + (long long)b * a.stride;
+    const double* g = a.gw ? a.gw + (long long)b * a.list_cap : a.g + (long long)b * a.stride;
     int* ei = a.e_i + (long long)b * a.list_cap;
     int* ej = a.e_j + (long long)b * a.list_cap;
     double* ew = a.e_w + (long long)b * a.list_cap;
@@ -258,7 +266,7 @@ __global__ void __launch_bounds__(kThreads) slem_kernel(SlemArgs a) {
     __shared__ int s_flag;  // bit0 stop, bit1 converged
     __shared__ double s_th[2];
 
-    build_csr(n, ne, list, g, ei, ej, ew, rowptr, colptr, cur, cidx, iscr);
+    build_csr(n, ne, list, g, a.gw != nullptr, ei, ej, ew, rowptr, colptr, cur, cidx, iscr);
 
     // Exact mode (Krylov dimension covers 1-perp): run to completion, no early
     // stop, so the extreme Ritz values are eigenvalues up to rounding.
@@ -390,14 +398,10 @@ __global__ void __launch_bounds__(kThreads) slem_kernel(SlemArgs a) {
         if (converged) break;
     }
     if (tid == 0) {
-        if (a.stats) {
-            atomicAdd(a.stats, 1);
-            atomicAdd(a.stats + 1, steps);
-        }
         if (a.ritz_ok) a.ritz_ok[b] = 1;
         const double l2 = 1.0 - th_min, ln = 1.0 - th_max;
         const double acf = fmax(fabs(l2), fabs(ln));
-        if (a.tr_acf) a.tr_acf[(long long)b * a.max_iter + a.ictl[b * 8]] = acf;
+        if (a.tr_acf) a.tr_acf[(long long)b * a.max_iter + it_rec] = acf;
         if (a.out) {
             double* o = a.out + b * 8;
             o[0] = acf;
@@ -424,12 +428,13 @@ size_t slem_smem_bytes(int n, int kmax, bool basis_in_smem) {
 // the reference's Householder + QL (eig.cpp:18-129), without iterating.
 __global__ void __launch_bounds__(256) slem_small_kernel(SlemArgs a) {
     const int b = blockIdx.x;
-    if (a.ictl && a.ictl[b * 8 + 1]) return;
+    const int it_rec = slem_iter(a, b);
+    if (it_rec < 0) return;
     const int n = a.n, ld = n + 1;
     const int tid = threadIdx.x, nthr = blockDim.x, wid = tid >> 5;
     const int ne = min(a.count[b], a.list_cap);
     const int* list = a.list + (long long)b * a.list_cap;
-    const double* g = a.g + (long long)b * a.stride;
+    const double* g = a.gw ? a.gw + (long long)b * a.list_cap : a.g + (long long)b * a.stride;
     extern __shared__ double sh[];
     double* A = sh;              // n x ld
     double* v = A + n * ld;      // n
@@ -438,14 +443,14 @@ __global__ void __launch_bounds__(256) slem_small_kernel(SlemArgs a) {
     double* e = d + n;           // n
     __shared__ double scratch[32];
     __shared__ int s_it;
-    if (tid == 0 && a.ictl) s_it = a.ictl[b * 8];
+    if (tid == 0) s_it = it_rec;
     // W: off-diagonals +g, diagonal 1 - (sum of incident g, ascending edges)
     for (int k = tid; k < n * ld; k += nthr) A[k] = 0.0;
     __syncthreads();
     for (int t = tid; t < ne; t += nthr) {
         int i, j;
         edge_pair(n, list[t], i, j);
-        const double w = g[list[t]];
+        const double w = a.gw ? g[t] : g[list[t]];
         A[i * ld + j] = w;
         A[j * ld + i] = w;
     }
@@ -542,12 +547,13 @@ constexpr int kTraceThreads = 1024;
 
 __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
     const int b = blockIdx.x;
-    if (a.ictl && a.ictl[b * 8 + 1]) return;  // solve already finished
+    const int it_rec = slem_iter(a, b);
+    if (it_rec < 0) return;  // solve already finished
     const int n = a.n;
     const int tid = threadIdx.x, nthr = blockDim.x, wid = tid >> 5;
     const int ne = min(a.count[b], a.list_cap);
     const int* list = a.list + (long long)b * a.list_cap;
-    const double* g = a.g + (long long)b * a.stride;
+    const double* g = a.gw ? a.gw + (long long)b * a.list_cap : a.g + (long long)b * a.stride;
     int* ei = a.e_i + (long long)b * a.list_cap;
     int* ej = a.e_j + (long long)b * a.list_cap;
     double* ew = a.e_w + (long long)b * a.list_cap;
@@ -573,7 +579,7 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
     __shared__ int s_flag;  // bit0 stop, bit1 converged
     __shared__ double s_th[2];
 
-    build_csr(n, ne, list, g, ei, ej, ew, rowptr, colptr, cur, cidx, iscr);
+    build_csr(n, ne, list, g, a.gw != nullptr, ei, ej, ew, rowptr, colptr, cur, cidx, iscr);
     // dense supports (het trace: every positive g): node-major incidence
     // (column part then row part, i.e. ascending edge order) for a warp-per-
     // node SpMV with coalesced loads
@@ -735,14 +741,10 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
         deflate_normalize(q, n, scratch);
     }
     if (tid == 0) {
-        if (a.stats) {
-            atomicAdd(a.stats, 1);
-            atomicAdd(a.stats + 1, steps);
-        }
         if (a.ritz_ok) a.ritz_ok[b] = 1;
         const double l2 = 1.0 - th_min, ln = 1.0 - th_max;
         const double acf = fmax(fabs(l2), fabs(ln));
-        if (a.tr_acf) a.tr_acf[(long long)b * a.max_iter + a.ictl[b * 8]] = acf;
+        if (a.tr_acf) a.tr_acf[(long long)b * a.max_iter + it_rec] = acf;
         if (a.out) {
             double* o = a.out + b * 8;
             o[0] = acf;

@@ -30,11 +30,14 @@ struct SlemArgs {
     int* ritz_ok;
     // outputs: out[b*8 + {0:acf, 1:lambda2, 2:lambda_n, 3:connected, 4:steps, 5:converged}]
     double* out;
-    // trace mode: acf -> tr_acf[b*max_iter + ictl[b*8]] ; skipped when done
+    // trace mode: acf -> tr_acf[b*max_iter + it], it = it_snap[b] (the
+    // iteration recorded by the select kernel; < 0 skips the solve) or, without
+    // it_snap, ictl[b*8] (skipped when ictl[b*8+1] marks the solve done)
     double* tr_acf;
     const int* ictl;
+    const int* it_snap;
+    const double* gw;      // weights aligned with the list (gw + b*list_cap), or null: g[list[e]]
     int max_iter;
-    int* stats;            // instrumentation: {calls, matvecs} accumulated, or null
     int plain;             // trace mode: plain Lanczos (no reorthogonalisation), basis write-only
     int* nbr;              // plain mode, dense supports: node-major incidence scratch (2 list_cap per solve)
     double* nwt;

@@ -171,8 +171,10 @@ Solver::Solver(int n, int B, bool het, const std::vector<int>& r, const std::vec
     if (ozaki_) check_oz_ld(ld_);
     list_cap_ = het ? m : *std::max_element(r_host_.begin(), r_host_.end());
     int chunk = cfg.chunk > 0 ? cfg.chunk : (n <= 64 ? 32 : (n <= 256 ? 16 : 8));
-    chunk = ((chunk + cfg.trace_stride - 1) / cfg.trace_stride) * cfg.trace_stride;
-    chunk_ = chunk;
+    // a multiple of the trace stride (the SLEM pattern repeats per chunk) and
+    // even (chunks start and end at selection parity 0)
+    const int unit = cfg.trace_stride % 2 ? 2 * cfg.trace_stride : cfg.trace_stride;
+    chunk_ = ((chunk + unit - 1) / unit) * unit;
     init_attrs();
     phase_mark("solver init_attrs");
     TPB_CUDA(cudaStreamCreateWithFlags(&s0_, cudaStreamNonBlocking));
@@ -181,6 +183,7 @@ Solver::Solver(int n, int B, bool het, const std::vector<int>& r, const std::vec
     TPB_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     TPB_CUDA(cudaEventCreateWithFlags(&ev_sel_, cudaEventDisableTiming));
     TPB_CUDA(cudaEventCreateWithFlags(&ev_slem_, cudaEventDisableTiming));
+    for (int q = 0; q < 2; ++q) TPB_CUDA(cudaEventCreateWithFlags(&ev_slem_p_[q], cudaEventDisableTiming));
     phase_mark("solver streams");
     alloc();
     if (het && !cap_) {
@@ -210,7 +213,8 @@ Solver::Solver(int n, int B, bool het, const std::vector<int>& r, const std::vec
 Solver::~Solver() {
     phase_mark("(before teardown)");
     if (g_chunk_) cudaGraphExecDestroy(g_chunk_);
-    if (g_one_) cudaGraphExecDestroy(g_one_);
+    for (auto& g1 : g_one_)
+        if (g1) cudaGraphExecDestroy(g1);
     phase_mark("graph destroy");
     // stream-ordered frees return the blocks to the device pool (no unmap)
     for (void* p : allocs_) cudaFreeAsync(p, s0_);
@@ -228,6 +232,8 @@ Solver::~Solver() {
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_sel_) cudaEventDestroy(ev_sel_);
     if (ev_slem_) cudaEventDestroy(ev_slem_);
+    for (auto& e : ev_slem_p_)
+        if (e) cudaEventDestroy(e);
     if (s0_) cudaStreamDestroy(s0_);
     if (s1_) cudaStreamDestroy(s1_);
     if (s2_) cudaStreamDestroy(s2_);
@@ -319,6 +325,14 @@ void Solver::alloc() {
     }
     list_ = dalloc<int>(s0_, allocs_,(size_t)B * list_cap_);
     list_count_ = dalloc<int>(s0_, allocs_,B);
+    tlist_[0] = list_;
+    tcount_[0] = list_count_;
+    tlist_[1] = dalloc<int>(s0_, allocs_, (size_t)B * list_cap_);
+    tcount_[1] = dalloc<int>(s0_, allocs_, B);
+    for (int q = 0; q < 2; ++q) {
+        tlw_[q] = dalloc<double>(s0_, allocs_, (size_t)B * list_cap_);
+        tsnap_[q] = dalloc<int>(s0_, allocs_, B);
+    }
     e_i_ = dalloc<int>(s0_, allocs_,(size_t)B * list_cap_);
     e_j_ = dalloc<int>(s0_, allocs_,(size_t)B * list_cap_);
     col_idx_ = dalloc<int>(s0_, allocs_,(size_t)B * list_cap_);
@@ -427,14 +441,16 @@ void Solver::final_slem(const double* packed, const int* list, const int* count,
     launch_slem(a, B_, s0_);
 }
 
-void Solver::enqueue_select(cudaStream_t st) {
+void Solver::enqueue_select(cudaStream_t st, int parity) {
     SelectArgs a{};
     a.stride = lo_.nx;
     a.m = lo_.m;
     a.r = d_r_;
-    a.list = list_;
-    a.list_count = list_count_;
+    a.list = tlist_[parity];
+    a.list_count = tcount_[parity];
     a.list_cap = list_cap_;
+    a.list_w = tlw_[parity];
+    a.it_snap = tsnap_[parity];
     a.done = d_.ictl;
     if (cap_) {
         // project_binary_z_capped on the z block, then the g support for the SLEM
@@ -454,7 +470,8 @@ void Solver::enqueue_select(cudaStream_t st) {
         c.pad = cap_pad_;
         c.done = d_.ictl;
         launch_capped_z(c, B_, st);
-        launch_compact(d_.Y, lo_.nx, lo_.m, list_, list_count_, list_cap_, B_, st);
+        launch_compact(d_.Y, lo_.nx, lo_.m, tlist_[parity], tcount_[parity], list_cap_, B_, st, tlw_[parity],
+                       tsnap_[parity], d_.ictl);
         return;
     }
     if (het_) {
@@ -473,14 +490,16 @@ void Solver::enqueue_select(cudaStream_t st) {
     launch_topr(a, B_, st);
 }
 
-void Solver::enqueue_slem_trace(cudaStream_t st) {
+void Solver::enqueue_slem_trace(cudaStream_t st, int parity) {
     SlemArgs a{};
     a.n = lo_.n;
     a.m = lo_.m;
     a.g = d_.Y;
+    a.gw = tlw_[parity];  // weights captured by the select kernel (Y moves on)
+    a.it_snap = tsnap_[parity];
     a.stride = lo_.nx;
-    a.list = list_;
-    a.count = list_count_;
+    a.list = tlist_[parity];
+    a.count = tcount_[parity];
     a.list_cap = list_cap_;
     a.e_i = e_i_;
     a.e_j = e_j_;
@@ -544,28 +563,47 @@ void Solver::set_shard(void* comm, int nranks, int rank) {
     }
     // graphs captured before hold the old projection
     if (g_chunk_) cudaGraphExecDestroy(g_chunk_);
-    if (g_one_) cudaGraphExecDestroy(g_one_);
-    g_chunk_ = g_one_ = nullptr;
+    for (auto& g1 : g_one_) {
+        if (g1) cudaGraphExecDestroy(g1);
+        g1 = nullptr;
+    }
+    g_chunk_ = nullptr;
 }
 
-void Solver::enqueue_iteration(bool with_slem) {
+// One ADMM iteration on three streams: prep on s0, then the
+// selection (top-r / binary z) on s1 beside the cone projections on s0; the
+// x-step joins the selection. The trace SLEM of this iteration runs on s2 from
+// the selection's parity buffers and is joined by nobody in the iteration: it
+// overlaps the next iteration, whose successor's selection (same parity)
+// waits for it. Stream capture and eager chunks end with join_slem().
+void Solver::enqueue_iteration(bool with_slem, int parity) {
     launch_prep(d_, c_, s0_);
     if (!small_) launch_frob_finalize(d_, s0_);
     TPB_CUDA(cudaEventRecord(ev_fork_, s0_));
     TPB_CUDA(cudaStreamWaitEvent(s1_, ev_fork_, 0));
-    enqueue_select(s1_);
+    if (slem_pending_[parity]) TPB_CUDA(cudaStreamWaitEvent(s1_, ev_slem_p_[parity], 0));
+    enqueue_select(s1_, parity);
     TPB_CUDA(cudaEventRecord(ev_sel_, s1_));
+    slem_pending_[parity] = false;
     if (with_slem) {
         TPB_CUDA(cudaStreamWaitEvent(s2_, ev_sel_, 0));
-        enqueue_slem_trace(s2_);
-        TPB_CUDA(cudaEventRecord(ev_slem_, s2_));
+        enqueue_slem_trace(s2_, parity);
+        TPB_CUDA(cudaEventRecord(ev_slem_p_[parity], s2_));
+        slem_pending_[parity] = true;
+        slem_any_ = true;
+        slem_last_ = parity;
     }
     enqueue_projection();
     TPB_CUDA(cudaStreamWaitEvent(s0_, ev_sel_, 0));
     enqueue_xstep(d_);
-    if (with_slem) TPB_CUDA(cudaStreamWaitEvent(s0_, ev_slem_, 0));
     launch_xstep_diag(d_, c_, s0_);
     launch_best_copy(d_, c_, s0_);
+}
+
+void Solver::join_slem(cudaStream_t st) {
+    if (slem_any_) TPB_CUDA(cudaStreamWaitEvent(st, ev_slem_p_[slem_last_], 0));
+    slem_any_ = false;
+    slem_pending_[0] = slem_pending_[1] = false;
 }
 
 void Solver::enqueue_xstep(const Dev& d) {
@@ -589,21 +627,27 @@ void Solver::cg_stats(int b, int* iters, double* rel_res) {
 }
 
 void Solver::build_graphs() {
-    auto capture = [&](int iters, bool stride_aligned) {
+    // chunk_ is even: a chunk starts and ends at parity 0; single-iteration
+    // graphs exist for both parities
+    auto capture = [&](int iters, int parity0, bool stride_aligned) {
         cudaGraph_t g;
+        slem_pending_[0] = slem_pending_[1] = false;  // earlier graphs have completed
+        slem_any_ = false;
         TPB_CUDA(cudaStreamBeginCapture(s0_, cudaStreamCaptureModeThreadLocal));
         for (int j = 0; j < iters; ++j) {
             const bool slem = stride_aligned ? (j % cfg_.trace_stride == 0) : (cfg_.trace_stride == 1);
-            enqueue_iteration(slem);
+            enqueue_iteration(slem, (parity0 + j) & 1);
         }
+        join_slem(s0_);
         TPB_CUDA(cudaStreamEndCapture(s0_, &g));
         cudaGraphExec_t ex;
         TPB_CUDA(cudaGraphInstantiate(&ex, g, 0));
         TPB_CUDA(cudaGraphDestroy(g));
         return ex;
     };
-    g_chunk_ = capture(chunk_, true);
-    g_one_ = capture(1, false);
+    g_chunk_ = capture(chunk_, 0, true);
+    g_one_[0] = capture(1, 0, false);
+    g_one_[1] = capture(1, 1, false);
 }
 
 // Sharded solvers launch their iterations eagerly: the all-gathers' stream
@@ -614,25 +658,28 @@ bool Solver::eager() const { return sharded(); }
 
 void Solver::iterate_async(int k) {
     if (eager()) {
-        while (k >= chunk_) {
-            for (int j = 0; j < chunk_; ++j) enqueue_iteration(j % cfg_.trace_stride == 0);
-            k -= chunk_;
-            it_enqueued_ += chunk_;
-        }
-        while (k-- > 0) {
-            enqueue_iteration(cfg_.trace_stride == 1);
-            ++it_enqueued_;
+        while (k > 0) {
+            const int run = (it_enqueued_ % 2 == 0 && k >= chunk_) ? chunk_ : 1;
+            for (int j = 0; j < run; ++j) {
+                const bool slem = run == chunk_ ? (j % cfg_.trace_stride == 0) : (cfg_.trace_stride == 1);
+                enqueue_iteration(slem, (it_enqueued_ + j) & 1);
+            }
+            join_slem(s0_);
+            k -= run;
+            it_enqueued_ += run;
         }
         return;
     }
-    while (k >= chunk_) {
-        TPB_CUDA(cudaGraphLaunch(g_chunk_, s0_));
-        k -= chunk_;
-        it_enqueued_ += chunk_;
-    }
-    while (k-- > 0) {
-        TPB_CUDA(cudaGraphLaunch(g_one_, s0_));
-        ++it_enqueued_;
+    while (k > 0) {
+        if (it_enqueued_ % 2 == 0 && k >= chunk_) {
+            TPB_CUDA(cudaGraphLaunch(g_chunk_, s0_));
+            k -= chunk_;
+            it_enqueued_ += chunk_;
+        } else {
+            TPB_CUDA(cudaGraphLaunch(g_one_[it_enqueued_ & 1], s0_));
+            --k;
+            ++it_enqueued_;
+        }
     }
 }
 

@@ -113,11 +113,12 @@ class Solver {
 
    private:
     void alloc();
-    void enqueue_iteration(bool with_slem);
+    void enqueue_iteration(bool with_slem, int parity);
     void enqueue_xstep(const Dev& d);  // pass A, node, [CG], pass B
     void enqueue_projection();
-    void enqueue_select(cudaStream_t st);
-    void enqueue_slem_trace(cudaStream_t st);
+    void enqueue_select(cudaStream_t st, int parity = 0);
+    void enqueue_slem_trace(cudaStream_t st, int parity = 0);
+    void join_slem(cudaStream_t st);  // st waits for the last enqueued trace SLEM
     void build_graphs();
     void epilogue_hom();
     void epilogue_het();
@@ -152,6 +153,18 @@ class Solver {
     OzWork oz_;
     OzShard shard_;
     int *list_ = nullptr, *list_count_ = nullptr;
+    // Per-iteration selection output for the trace SLEM, double-buffered by
+    // iteration parity (set 0 aliases list_/list_count_): the SLEM of
+    // iteration k reads set k % 2 while iteration k + 1 runs, and the select
+    // of iteration k + 2 waits for it
+    int* tlist_[2] = {nullptr, nullptr};
+    int* tcount_[2] = {nullptr, nullptr};
+    double* tlw_[2] = {nullptr, nullptr};
+    int* tsnap_[2] = {nullptr, nullptr};
+    cudaEvent_t ev_slem_p_[2] = {nullptr, nullptr};
+    bool slem_pending_[2] = {false, false};
+    bool slem_any_ = false;
+    int slem_last_ = 0;
     int *e_i_ = nullptr, *e_j_ = nullptr, *col_idx_ = nullptr;
     double* e_w_ = nullptr;
     double* basis_ = nullptr;        // trace Lanczos basis (B x kmax x n)
@@ -170,7 +183,7 @@ class Solver {
     // streams / graphs
     cudaStream_t s0_ = nullptr, s1_ = nullptr, s2_ = nullptr;
     cudaEvent_t ev_fork_ = nullptr, ev_sel_ = nullptr, ev_slem_ = nullptr;
-    cudaGraphExec_t g_chunk_ = nullptr, g_one_ = nullptr;
+    cudaGraphExec_t g_chunk_ = nullptr, g_one_[2] = {nullptr, nullptr};
     int it_enqueued_ = 0;
     // results
     std::vector<SolveResult> res_;
