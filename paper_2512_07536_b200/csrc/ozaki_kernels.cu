@@ -328,25 +328,39 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int j = 0; j < HN; ++j) acc[j] = 0.0;
         // groups d = KS+1 .. 2 at TMEM columns (d - 2) BN, smallest
-        // contributions first, up to two groups per wait
-#pragma unroll
-        for (int d = KS + 1; d >= 2; d -= 2) {
-            const int ng = d - 1 >= 2 ? 2 : 1;
-            uint32_t v[2][HN];
+        // contributions first (the emulation's order), two groups per TMEM
+        // load batch; the next batch's loads are in flight while the current
+        // one is converted and accumulated
+        static_assert(KS == 7, "drain schedule: batches (8,7) (6,5) (4,3) (2)");
+        uint32_t va[2][HN], vb[2][HN];
+        auto load2 = [&](int d, int ng, uint32_t (&v)[2][HN]) {
 #pragma unroll
             for (int q2 = 0; q2 < ng; ++q2)
 #pragma unroll
                 for (int c = 0; c < HN / 16; ++c)
                     tmem_ld16(taddr + (uint32_t)((d - q2 - 2) * BN + c * 16),
                               *reinterpret_cast<uint32_t(*)[16]>(&v[q2][c * 16]));
-            tmem_wait_ld();
+        };
+        auto use2 = [&](int d, int ng, const uint32_t (&v)[2][HN]) {
 #pragma unroll
             for (int q2 = 0; q2 < ng; ++q2) {
                 const double sc = ldexp(1.0, -8 * (d - q2));
 #pragma unroll
                 for (int j = 0; j < HN; ++j) acc[j] = fma(i32_to_f64(v[q2][j]), sc, acc[j]);
             }
-        }
+        };
+        load2(8, 2, va);
+        tmem_wait_ld();
+        load2(6, 2, vb);
+        use2(8, 2, va);
+        tmem_wait_ld();
+        load2(4, 2, va);
+        use2(6, 2, vb);
+        tmem_wait_ld();
+        load2(2, 1, vb);
+        use2(4, 2, va);
+        tmem_wait_ld();
+        use2(2, 1, vb);
         const double s = g.scale ? g.scale[mat] : 1.0;
         double alpha = g.alpha_c * spow(s, g.pa) * ldexp(1.0, g.eA + g.eB);
         const double beta = g.beta_c * spow(s, g.pb);
@@ -403,6 +417,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
             }
         }
+        if (threadIdx.x == 64) OZ_STAMP(5);
         if (g.Cd) {
             // Each thread splits one 4 x 4 block (rows 4 rb.., columns 4 cb..)
             // into digits once. Mirror rows: a 4 x 4 byte transpose per plane
@@ -446,6 +461,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
             }
             asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");
+            if (threadIdx.x == 64) OZ_STAMP(6);
             constexpr int NC4 = BN / 16;             // 16-byte chunks per row segment
             static_assert(EPI_THREADS % NC4 == 0, "read-back mapping");
             for (int rr = dr0 + et / NC4; rr < BM; rr += EPI_THREADS / NC4) {

@@ -25,16 +25,19 @@ Cd = np.zeros((2, 7, ld, ld), np.int8)
 dp = C.POINTER(C.c_double)
 ms = C.c_double(0)
 for it in range(3):
+    # reps=2: the timed repetitions write digit planes only (the cone
+    # iteration's intermediate products); the stamps are the last one's
     rc = lib.tp_oz_gemm(ld, 2, A.ctypes.data_as(dp), 2, A.ctypes.data_as(dp), 2, 0, 1.0, 0.0,
-                        Cg.ctypes.data_as(dp), Cd.ctypes.data_as(C.c_void_p), 3, 0, C.byref(ms))
+                        Cg.ctypes.data_as(dp), Cd.ctypes.data_as(C.c_void_p), 3, 2, C.byref(ms))
     assert rc == 0
     torch.cuda.synchronize()
-    st = buf.view(-1, 8).cpu().numpy()[:, :5].astype(np.float64)
+    st = buf.view(-1, 8).cpu().numpy()[:, :7].astype(np.float64)
     t0 = st[:, 0].min()
     rel = (st - t0) / 1e3  # us
     print(f"ld={ld} run {it}: CTAs {len(st)}  start spread {rel[:, 0].max():.2f} us")
     for name, a, b in (("main loop (start -> last MMA commit)", 0, 1), ("commit -> epilogue sees TMEM", 1, 2),
-                       ("TMEM drain + FP64", 2, 3), ("stores (FP64 / digits)", 3, 4), ("start -> end", 0, 4)):
+                       ("TMEM drain + FP64", 2, 3), ("staging + symmetrise (smem)", 3, 5), ("digit split + mirror stores", 5, 6),
+                       ("direct-row stores", 6, 4), ("start -> end", 0, 4)):
         d = rel[:, b] - rel[:, a]
         print(f"  {name:40s} mean {d.mean():7.2f}  min {d.min():7.2f}  max {d.max():7.2f} us")
     print(f"  last CTA end {rel[:, 4].max():.2f} us")
