@@ -43,13 +43,18 @@ __device__ int sturm_count(const double* al, const double* be, int k, double x) 
         prev_neg = neg;
         pm = p;
         p = pn;
-        const double mx = fmax(fabs(p), fabs(pm));
-        if (mx > 0x1p400) {
-            p *= 0x1p-400;
-            pm *= 0x1p-400;
-        } else if (mx < 0x1p-400 && mx > 0.0) {
-            p *= 0x1p400;
-            pm *= 0x1p400;
+        // rescale every 8 steps (|p| grows by < 2^5 per step with the spectra
+        // bounded by Gershgorin here, far inside the 2^400 margin): keeps the
+        // dependent chain per step at two FMAs
+        if ((i & 7) == 7) {
+            const double mx = fmax(fabs(p), fabs(pm));
+            if (mx > 0x1p400) {
+                p *= 0x1p-400;
+                pm *= 0x1p-400;
+            } else if (mx < 0x1p-400 && mx > 0.0) {
+                p *= 0x1p400;
+                pm *= 0x1p400;
+            }
         }
     }
     return cnt;
@@ -219,6 +224,30 @@ __device__ inline void cgs2(const double* Q, int n, int ldq, int k, double* w, d
         __syncthreads();
     }
 }
+
+#ifdef OZ_STAMPS
+// instrumentation build only (make STAMPS=1): per-kernel {calls, steps} of the
+// Lanczos SLEM kernels, slot 0 trace reports, slot 1 one-off reports
+__device__ unsigned long long g_slem_stats[8];
+extern "C" int tp_slem_stats(unsigned long long* out, int reset) {
+    if (cudaMemcpyFromSymbol(out, g_slem_stats, sizeof(g_slem_stats)) != cudaSuccess) return 7;
+    if (reset) {
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        cudaMemcpyToSymbol(g_slem_stats, z, sizeof(z));
+    }
+    return 0;
+}
+#define SLEM_STAT(oneoff, steps)                                   \
+    do {                                                           \
+        atomicAdd(&g_slem_stats[(oneoff) ? 2 : 0], 1ull);          \
+        atomicAdd(&g_slem_stats[(oneoff) ? 3 : 1], (unsigned long long)(steps)); \
+    } while (0)
+#define SLEM_CLK(slot, t0) \
+    if (threadIdx.x == 0) atomicAdd(&g_slem_stats[slot], (unsigned long long)(clock64() - (t0)))
+#else
+#define SLEM_STAT(oneoff, steps) ((void)0)
+#define SLEM_CLK(slot, t0) ((void)0)
+#endif
 
 // Trace mode: the iteration a report belongs to, or -1 when the solve is done.
 __device__ inline int slem_iter(const SlemArgs& a, int b) {
@@ -402,6 +431,7 @@ __global__ void __launch_bounds__(kThreads) slem_kernel(SlemArgs a) {
         const double l2 = 1.0 - th_min, ln = 1.0 - th_max;
         const double acf = fmax(fabs(l2), fabs(ln));
         if (a.tr_acf) a.tr_acf[(long long)b * a.max_iter + it_rec] = acf;
+        SLEM_STAT(a.out != nullptr, steps);
         if (a.out) {
             double* o = a.out + b * 8;
             o[0] = acf;
@@ -569,8 +599,8 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
     double* be = al + kcap;           // kcap
     double* smin = be + kcap;         // kcap
     double* smax = smin + kcap;       // kcap
-    double* wk = smax + kcap;         // 2 kcap
-    int* rowptr = (int*)(wk + 2 * kcap);  // n+1
+    double* wk = smax + kcap;         // 4 kcap (two inverse-iteration work arrays)
+    int* rowptr = (int*)(wk + 4 * kcap);  // n+1
     int* colptr = rowptr + (n + 1);       // n+1
     int* cur = colptr + (n + 1);          // n
     double* Q = a.basis + (long long)b * a.kmax * n;
@@ -578,16 +608,23 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
     __shared__ int iscr[32];
     __shared__ int s_flag;  // bit0 stop, bit1 converged
     __shared__ double s_th[2];
+    __shared__ double s_res[2];
 
     build_csr(n, ne, list, g, a.gw != nullptr, ei, ej, ew, rowptr, colptr, cur, cidx, iscr);
     // dense supports (het trace: every positive g): node-major incidence
     // (column part then row part, i.e. ascending edge order) for a warp-per-
     // node SpMV with coalesced loads
+    // Sparse supports whose node-major incidence fits the shared memory the
+    // launch reserved (a.smem_nm entries) keep it there: the matvec then
+    // reads no global memory (thread per node, same ascending edge order).
     const bool dense = a.nbr && 2 * ne >= 32 * n;
+    const bool snm = !dense && 2 * ne <= a.smem_nm;
     int* nptr = cur;  // n+1 ints: reuses the counting-sort cursor
-    int* nbr = a.nbr ? a.nbr + (long long)b * 2 * a.list_cap : nullptr;
-    double* nwt = a.nwt ? a.nwt + (long long)b * 2 * a.list_cap : nullptr;
-    if (dense) {
+    double* snwt = reinterpret_cast<double*>(((uintptr_t)(cur + n + 1) + 15) & ~(uintptr_t)15);
+    int* snbr = reinterpret_cast<int*>(snwt + a.smem_nm);
+    int* nbr = snm ? snbr : (a.nbr ? a.nbr + (long long)b * 2 * a.list_cap : nullptr);
+    double* nwt = snm ? snwt : (a.nwt ? a.nwt + (long long)b * 2 * a.list_cap : nullptr);
+    if (dense || snm) {
         __syncthreads();
         if (tid == 0) nptr[0] = 0;
         for (int v = tid; v < n; v += nthr)
@@ -611,6 +648,9 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
         __syncthreads();
     }
 
+#ifdef OZ_STAMPS
+    const long long tk0 = clock64();
+#endif
     const bool warm = a.ritz && a.ritz_ok && a.ritz_ok[b];
     double* rz = a.ritz ? a.ritz + (long long)b * 2 * n : nullptr;
     for (int v = tid; v < n; v += nthr) q[v] = warm ? rz[v] + rz[n + v] : hash_unit(v);
@@ -644,6 +684,16 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
                         w[v] = acc;
                         pa += qv * acc;
                     }
+                }
+            } else if (snm) {
+                for (int v = tid; v < n; v += nthr) {
+                    const double qv = q[v];
+                    Q[(long long)k * n + v] = qv;
+                    double acc = 0.0;
+                    for (int p = nptr[v]; p < nptr[v + 1]; ++p) acc += nwt[p] * (qv - q[nbr[p]]);
+                    acc -= beta_prev * qp[v];
+                    w[v] = acc;
+                    pa += qv * acc;
                 }
             } else {
                 for (int v = tid; v < n; v += nthr) {
@@ -679,27 +729,36 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
             kk = k + 1;
             ++steps;
             const bool breakdown = !(beta > 1e-13 * fmax(fabs(alpha), fabs(c_max)) + 1e-300);
-            const bool want_check = breakdown || kk == kcap || (steps >= a.min_steps && check_step(kk));
+            // residual tests (two Sturm multisections + two inverse iterations
+            // on T_k, ~100 us at k = 256) only every check_every steps: a
+            // matvec costs ~1 us, a test up to 100x more
+            const int every = a.check_every > 0 ? a.check_every : 16;
+            const bool want_check = breakdown || kk == kcap || (steps >= a.min_steps && kk % every == 0);
+#ifdef OZ_STAMPS
+            const long long tck = clock64();
+#endif
             if (want_check) {
                 __syncthreads();
-                if (wid == 0) {
+                // warp 0: smallest Ritz pair, warp 1: largest, concurrently
+                if (wid < 2) {
                     double lo, hi;
                     gershgorin(al, be, kk, lo, hi);
-                    const double tmin = tri_eig(al, be, kk, 0, lo, hi);
-                    const double tmax = tri_eig(al, be, kk, kk - 1, lo, hi);
-                    if (tid == 0) {
-                        const double r1 = beta * tri_vec(al, be, kk, tmin, wk, smin);
-                        const double r2 = beta * tri_vec(al, be, kk, tmax, wk, smax);
-                        const double sc = fmax(fabs(tmax), 1e-300);
-                        const bool conv = !breakdown && r1 <= a.tol * sc && r2 <= a.tol * sc;
-                        s_th[0] = tmin;
-                        s_th[1] = tmax;
-                        s_flag = (conv || breakdown || kk == kcap) ? (1 | (conv ? 2 : 0) | (breakdown ? 4 : 0)) : 0;
+                    const double t = tri_eig(al, be, kk, wid == 0 ? 0 : kk - 1, lo, hi);
+                    if ((tid & 31) == 0) {
+                        s_th[wid] = t;
+                        s_res[wid] = beta * tri_vec(al, be, kk, t, wk + 2 * kcap * wid, wid == 0 ? smin : smax);
                     }
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    const double sc = fmax(fabs(s_th[1]), 1e-300);
+                    const bool conv = !breakdown && s_res[0] <= a.tol * sc && s_res[1] <= a.tol * sc;
+                    s_flag = (conv || breakdown || kk == kcap) ? (1 | (conv ? 2 : 0) | (breakdown ? 4 : 0)) : 0;
                 }
                 __syncthreads();
                 c_min = s_th[0];
                 c_max = s_th[1];
+                SLEM_CLK(a.out ? 5 : 4, tck);
                 if (s_flag & 1) {
                     converged = (s_flag >> 1) & 1;
                     broke = (s_flag >> 2) & 1;
@@ -745,6 +804,8 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
         const double l2 = 1.0 - th_min, ln = 1.0 - th_max;
         const double acf = fmax(fabs(l2), fabs(ln));
         if (a.tr_acf) a.tr_acf[(long long)b * a.max_iter + it_rec] = acf;
+        SLEM_CLK(a.out ? 7 : 6, tk0);
+        SLEM_STAT(a.out != nullptr, steps);
         if (a.out) {
             double* o = a.out + b * 8;
             o[0] = acf;
@@ -759,7 +820,7 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
 
 size_t slem_trace_smem_bytes(int n, int kmax) {
     const int kcap = std::max(2, std::min(kmax, n - 1));
-    return (3 * (size_t)n + 6 * (size_t)kcap) * sizeof(double) + (3 * (size_t)n + 3) * sizeof(int);
+    return (3 * (size_t)n + 8 * (size_t)kcap) * sizeof(double) + (3 * (size_t)n + 3) * sizeof(int);
 }
 
 void launch_slem(const SlemArgs& a, int B, cudaStream_t st) {
@@ -771,8 +832,28 @@ void launch_slem(const SlemArgs& a, int B, cudaStream_t st) {
         return;
     }
     if (a.plain) {
+        // (batched het solves keep n-sized CTAs: several fit an SM between the
+        // concurrent GEMM waves, measured faster for the config-5 sweep than
+        // one 1024-thread CTA per SM)
         const int threads = std::min(kTraceThreads, std::max(128, ((n + 31) / 32) * 32));
-        slem_trace_kernel<<<B, threads, slem_trace_smem_bytes(n, a.kmax), st>>>(a);
+        // single solves: the node-major incidence of up to list_cap edges in
+        // shared memory when it fits (batches keep the small CTAs)
+        size_t smem = slem_trace_smem_bytes(n, a.kmax);
+        SlemArgs b = a;
+        b.smem_nm = 0;
+        const size_t nm = 2 * (size_t)a.list_cap;
+        static int optin = 0;
+        if (!optin) {
+            int dev = 0;
+            TPB_CUDA(cudaGetDevice(&dev));
+            TPB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        }
+        const size_t extra = 16 + nm * (sizeof(double) + sizeof(int));
+        if (B == 1 && smem + extra + 2048 <= (size_t)optin) {
+            b.smem_nm = (int)nm;
+            smem += extra;
+        }
+        slem_trace_kernel<<<B, threads, smem, st>>>(b);
         TPB_CHECK_LAUNCH();
         return;
     }

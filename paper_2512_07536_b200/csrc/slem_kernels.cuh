@@ -23,6 +23,7 @@ struct SlemArgs {
     int kmax;              // Krylov dimension per cycle (<= n-1); >= n-1: exact mode
     int max_restarts;      // explicit restarts from the extreme Ritz vectors
     int min_steps;         // restarted mode: matvecs before the first residual test
+    int check_every;       // plain (trace) Lanczos: residual tests every this many steps of a cycle (0: 16)
     double noise;          // warm start: weight of the fixed random component
     double tol;            // residual tolerance relative to the spectral scale
     // optional warm start: ritz[b*2n ..] = previous (v_min, v_max); ritz_ok[b]
@@ -41,6 +42,7 @@ struct SlemArgs {
     int plain;             // trace mode: plain Lanczos (no reorthogonalisation), basis write-only
     int* nbr;              // plain mode, dense supports: node-major incidence scratch (2 list_cap per solve)
     double* nwt;
+    int smem_nm;           // plain mode: entries of a node-major incidence kept in shared memory (set by launch_slem)
 };
 
 // n <= kSmallDense: dense Householder tridiagonalisation in shared memory

@@ -434,6 +434,7 @@ void Solver::final_slem(const double* packed, const int* list, const int* count,
     }
     a.max_restarts = 200;
     a.min_steps = 64;
+    a.check_every = 64;
     a.tol = 1e-10;
     a.out = out;
     a.tr_acf = nullptr;
@@ -509,6 +510,7 @@ void Solver::enqueue_slem_trace(cudaStream_t st, int parity) {
     a.kmax = trace_kmax_;
     a.max_restarts = 40;
     a.min_steps = 8;
+    a.check_every = 24;
     a.noise = 0.0;
     a.ritz = ritz_;
     a.ritz_ok = ritz_ok_;
