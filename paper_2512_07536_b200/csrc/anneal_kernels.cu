@@ -97,7 +97,41 @@ struct Args {
     int* bad;                  // G "some source did not reach every node" flags
     int* cmd;                  // master -> all: [0] kind, [1] i1, [2] i2, [3..6] n1, n2, [8] decision
     double* energy_out;
+    // capacity veto (anneal_capacity_topology, proj/src/anneal.cpp:357-385);
+    // allowed == nullptr: unconstrained. Only the master touches these.
+    const int* allowed;  // per packed column
+    const int* cr_ptr;   // column -> rows CSR
+    const int* cr;
+    const int* caps;     // per row
+    int* load;           // per row, current edge count (master-owned)
 };
+
+// Row-load change of the swap (r1, r2) -> (a1, a2) at `row`.
+__device__ inline int row_delta(const Args& a, const long long c[4], int row) {
+    int d = 0;
+    for (int k = 0; k < 4; ++k)
+        for (int q = a.cr_ptr[c[k]]; q < a.cr_ptr[c[k] + 1]; ++q)
+            if (a.cr[q] == row) d += k < 2 ? -1 : 1;
+    return d;
+}
+
+// The reference's feasible(): both new columns allowed and every row the
+// swap touches within capacity. Rows only losing load cannot overflow, so
+// only the rows of the added columns are checked.
+__device__ bool cap_feasible(const Args& a, const long long c[4]) {
+    if (!a.allowed[c[2]] || !a.allowed[c[3]]) return false;
+    for (int k = 2; k < 4; ++k)
+        for (int q = a.cr_ptr[c[k]]; q < a.cr_ptr[c[k] + 1]; ++q) {
+            const int row = a.cr[q];
+            if (a.load[row] + row_delta(a, c, row) > a.caps[row]) return false;
+        }
+    return true;
+}
+
+__device__ void cap_apply(const Args& a, const long long c[4]) {
+    for (int k = 0; k < 4; ++k)
+        for (int q = a.cr_ptr[c[k]]; q < a.cr_ptr[c[k] + 1]; ++q) a.load[a.cr[q]] += k < 2 ? -1 : 1;
+}
 
 // Sum of hop distances from this CTA's sources (lane groups of GS lanes; a
 // group's lane w < W holds word w of the frontier / visited bitsets).
@@ -218,6 +252,11 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_kernel(Args a) {
                 const int2 n1 = ordered2(e1.x, cross ? e2.y : e2.x);
                 const int2 n2 = ordered2(e1.y, cross ? e2.x : e2.y);
                 if (has_edge(adj, W, n1) || has_edge(adj, W, n2)) continue;
+                if (a.allowed) {
+                    const long long c[4] = {edge_idx(n, e1.x, e1.y), edge_idx(n, e2.x, e2.y),
+                                            edge_idx(n, n1.x, n1.y), edge_idx(n, n2.x, n2.y)};
+                    if (!cap_feasible(a, c)) continue;
+                }
                 kind = 1;
                 cmd[1] = (int)i1;
                 cmd[2] = (int)i2;
@@ -253,6 +292,12 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_kernel(Args a) {
             if (!take && isfinite(delta)) take = unit(*rng) < exp(-delta / temp);
             int improved = 0;
             if (take) {
+                if (a.allowed) {
+                    const int2 o1 = s_old[0], o2 = s_old[1];
+                    const long long c[4] = {edge_idx(n, o1.x, o1.y), edge_idx(n, o2.x, o2.y),
+                                            edge_idx(n, n1.x, n1.y), edge_idx(n, n2.x, n2.y)};
+                    cap_apply(a, c);
+                }
                 energy = cand;
                 if (energy < best_e) {
                     best_e = energy;
@@ -294,7 +339,7 @@ struct Buf {
 
 }  // namespace
 
-bool anneal_device(int n, std::vector<std::pair<int, int>>& es, const AnnealParams& p) {
+bool anneal_device(int n, std::vector<std::pair<int, int>>& es, const AnnealParams& p, const CapVeto* veto) {
     int count = 0;
     if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
         cudaGetLastError();
@@ -344,6 +389,22 @@ bool anneal_device(int n, std::vector<std::pair<int, int>>& es, const AnnealPara
     a.bad = d_bad.p;
     a.cmd = d_cmd.p;
     a.energy_out = d_energy.p;
+    const CapVeto empty{};
+    const CapVeto& v = veto ? *veto : empty;
+    Buf<int> d_allowed(v.allowed.size()), d_crp(v.cr_ptr.size()), d_cr(v.cr.size()), d_caps(v.caps.size()),
+        d_load(v.load.size());
+    if (veto) {
+        h2d(d_allowed.p, v.allowed.data(), v.allowed.size() * sizeof(int));
+        h2d(d_crp.p, v.cr_ptr.data(), v.cr_ptr.size() * sizeof(int));
+        if (!v.cr.empty()) h2d(d_cr.p, v.cr.data(), v.cr.size() * sizeof(int));
+        if (!v.caps.empty()) h2d(d_caps.p, v.caps.data(), v.caps.size() * sizeof(int));
+        if (!v.load.empty()) h2d(d_load.p, v.load.data(), v.load.size() * sizeof(int));
+        a.allowed = d_allowed.p;
+        a.cr_ptr = d_crp.p;
+        a.cr = d_cr.p;
+        a.caps = d_caps.p;
+        a.load = d_load.p;
+    }
     void* args[] = {&a};
     TPB_CUDA(cudaLaunchCooperativeKernel((const void*)anneal_kernel, dim3(G), dim3(kThreads), args, smem, 0));
     TPB_CUDA(cudaDeviceSynchronize());

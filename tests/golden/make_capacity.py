@@ -43,7 +43,8 @@ def main():
             out["capped"].append({"spec": spec, "r": r, "v": v.tolist(),
                                   "z": ref.project_binary_z_capped(tuple(spec), v, r).tolist()})
     for spec, r, steps, seed in [(T8, 12, 200, 0), (T8, 10, 200, 0), (["bcube", 4, 2], 24, 50, 1),
-                                 (["bcube", 3, 2], 12, 30, 2)]:
+                                 (["bcube", 3, 2], 12, 30, 2), (["bcube", 4, 3], 100, 200, 3),
+                                 (["bcube", 3, 3], 40, 200, 4)]:
         out["anneal"].append({"spec": spec, "r": r, "steps": steps, "seed": seed,
                               "edges": ref.anneal_capacity(tuple(spec), r, steps=steps, seed=seed).tolist()})
     # solves (proj/tests/test_admm_het.cpp:171-229, acceptance.cpp:238-268)
