@@ -35,21 +35,6 @@ __device__ inline void tile_of(int t, int& bi, int& bj) {
 
 __device__ inline bool solve_done(const Dev& d, int b) { return d.ictl[b * 8 + kDone] != 0; }
 
-// sum_k P[k*stride + i] in k order, loads batched so their latencies overlap
-__device__ inline double sum_partials(const double* P, int nb, long long stride, int i) {
-    double s = 0.0;
-    int k = 0;
-    for (; k + 8 <= nb; k += 8) {
-        double v[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = P[(long long)(k + q) * stride + i];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) s += v[q];
-    }
-    for (; k < nb; ++k) s += P[(long long)k * stride + i];
-    return s;
-}
-
 // 2-D block (TB x TY) deterministic sum; every thread receives the result.
 __device__ inline double block_sum_2d(double v, double* scratch) {
     const int t = threadIdx.y * TB + threadIdx.x;
@@ -102,6 +87,116 @@ __device__ inline double warp_sum_partials(const double* P, int cnt, int lane) {
     return warp_sum(v);
 }
 
+// Arrival of a finished tile at the node blocks it touches (bi and bj):
+// after a CTA barrier thread 0 fences (release, cumulative over the CTA's
+// stores) and adds one arrival per block.
+// Returns the blocks whose last tile this CTA was (bit 0: bi, bit 1: bj);
+// the completer resets the counter for the next launch.
+__device__ inline int arrive_blocks(int* cnt, int nb, int bi, int bj, int* s_flag) {
+    __syncthreads();  // the CTA's stores precede thread 0's release fence (cumulative)
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+        __threadfence();
+        int fin = 0;
+        if (atomicAdd(cnt + bi, 1) == nb - 1) {
+            atomicExch(cnt + bi, 0);
+            fin |= 1;
+        }
+        if (bi != bj && atomicAdd(cnt + bj, 1) == nb - 1) {
+            atomicExch(cnt + bj, 0);
+            fin |= 2;
+        }
+        *s_flag = fin;
+    }
+    __syncthreads();
+    const int fin = *s_flag;
+    if (fin) __threadfence();
+    return fin;
+}
+
+// Arrival of a completed node block at the solve counter: true in the CTA
+// that completed the solve's last block (all nb of them).
+__device__ inline bool arrive_solve(int* cnt, int nb, int* s_flag) {
+    __syncthreads();
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+        __threadfence();
+        const bool last = atomicAdd(cnt, 1) == nb - 1;
+        if (last) atomicExch(cnt, 0);
+        *s_flag = last ? 1 : 0;
+    }
+    __syncthreads();
+    const bool last = *s_flag != 0;
+    if (last) __threadfence();
+    return last;
+}
+
+// Node sums over the nb tile partials P[q][k n + i] (K arrays) for the 32
+// nodes of block `blk`: warp w sums k = w, w + TY, ... in k order (all
+// loads of a batch in flight together), warp 0 adds the TY warp partials in
+// warp order. Valid in warp 0 (0 for i >= n). `pre` runs between the loads
+// and the barrier (warp 0 can issue its own independent loads there).
+template <int K, class Pre>
+__device__ inline void node_sum(const double* const (&P)[K], int nb, int n, int blk, double (*sm)[TY][TB + 1],
+                                double (&out)[K], Pre pre) {
+    const int tx = threadIdx.x, ty = threadIdx.y, i = blk * TB + tx;
+    double v[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) v[q] = 0.0;
+    if (i < n) {
+        constexpr int NQ = 8 / K;
+        int k = ty;
+        for (; k + (NQ - 1) * TY < nb; k += NQ * TY) {
+            double x[K][NQ];
+#pragma unroll
+            for (int q = 0; q < K; ++q)
+#pragma unroll
+                for (int u = 0; u < NQ; ++u) x[q][u] = __ldcg(P[q] + (long long)(k + u * TY) * n + i);
+#pragma unroll
+            for (int q = 0; q < K; ++q)
+#pragma unroll
+                for (int u = 0; u < NQ; ++u) v[q] += x[q][u];
+        }
+        for (; k < nb; k += TY)
+#pragma unroll
+            for (int q = 0; q < K; ++q) v[q] += __ldcg(P[q] + (long long)k * n + i);
+    }
+    pre();
+#pragma unroll
+    for (int q = 0; q < K; ++q) sm[q][ty][tx] = v[q];
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+        double s = 0.0;
+        if (ty == 0) {
+#pragma unroll
+            for (int y = 0; y < TY; ++y) s += sm[q][y][tx];
+        }
+        out[q] = s;
+    }
+    __syncthreads();
+}
+
+// Fixed-order sums of two values over the CTA (warp trees, then warps in
+// order); every thread receives them.
+__device__ inline void block_sum2_2d(double& a, double& b, double (*scratch)[2]) {
+    const int t = threadIdx.y * TB + threadIdx.x;
+    const int lane = t & 31, wid = t >> 5;
+    a = warp_sum(a);
+    b = warp_sum(b);
+    __syncthreads();
+    if (lane == 0) {
+        scratch[wid][0] = a;
+        scratch[wid][1] = b;
+    }
+    __syncthreads();
+    a = b = 0.0;
+#pragma unroll
+    for (int w = 0; w < TB * TY / 32; ++w) {
+        a += scratch[w][0];
+        b += scratch[w][1];
+    }
+    __syncthreads();
+}
+
 }  // namespace
 
 XConst make_xconst(int n, double alpha, double rho) {
@@ -149,7 +244,7 @@ XConst make_xconst(int n, double alpha, double rho) {
 // Block (bi <= bj) of node pairs. Writes A_S/A_T = sym(v) in both triangles of
 // the ld-padded buffers, clamps the packed edge blocks for pairs in the tile,
 // and the per-node blocks (lambda, y) from tile 0.
-__global__ void __launch_bounds__(TB* TY) prep_kernel(Dev d, XConst c) {
+__global__ void __launch_bounds__(TB* TY, 4) prep_kernel(Dev d, XConst c) {
     const int b = blockIdx.y;
     if (solve_done(d, b)) return;
     int bi, bj;
@@ -262,34 +357,49 @@ __global__ void __launch_bounds__(TB* TY) prep_kernel(Dev d, XConst c) {
         }
         __syncthreads();
     }
-}
-
-// Scale of the sign iteration's start X0 = A / c: c = min(||A||_F, ||A||_inf),
-// both upper bounds of the spectral radius (the spectrum of X0 stays in
-// [-1, 1]); the tighter one leaves small eigenvalues relatively larger, so the
-// fixed inflation schedule reaches a smaller error.
-__global__ void frob_finalize_kernel(Dev d) {
-    const int b = blockIdx.x;
-    if (solve_done(d, b)) return;
-    __shared__ double scratch[32];
-    const int n = d.lo.n;
-    for (int which = 0; which < 2; ++which) {
-        const double* part = d.frob_part + ((long long)b * 2 + which) * d.ntile;
-        double v = 0.0;
-        for (int t = threadIdx.x; t < d.ntile; t += blockDim.x) v += part[t];
-        v = block_sum(v, scratch);
-        const double* rp = d.row_part + ((long long)b * 2 + which) * d.nb * n;
-        double inf = 0.0;
-        for (int r = threadIdx.x; r < n; r += blockDim.x) {
-            double rs = 0.0;
-            for (int cb = 0; cb < d.nb; ++cb) rs += rp[(long long)cb * n + r];
-            inf = fmax(inf, rs);
+    // the last tile of a node block: max |A| row sum of the block's rows; the
+    // last block of the solve: 1 / min(||A||_F, ||A||_inf) per matrix
+    __shared__ int s_fin;
+    __shared__ double sm8[2][TY][TB + 1];
+    int* cnt = d.cnt + (long long)b * d.cnt_stride;
+    const int fin = arrive_blocks(cnt + kCntP * d.nb, d.nb, bi, bj, &s_fin);
+    if (!fin) return;
+    bool last = false;
+    for (int q = 0; q < 2; ++q) {
+        if (!(fin >> q & 1)) continue;
+        const int k = q == 0 ? bi : bj;
+        const double* const rp[2] = {d.row_part + (long long)b * 2 * d.nb * n,
+                                     d.row_part + ((long long)b * 2 + 1) * d.nb * n};
+        double rs[2];
+        node_sum<2>(rp, d.nb, n, k, sm8, rs, [] {});
+        if (ty == 0) {
+            const double m0 = warp_max(rs[0]), m1 = warp_max(rs[1]);
+            if (tx == 0) {
+                d.blk_inf[(long long)b * 2 * d.nb + k] = m0;
+                d.blk_inf[((long long)b * 2 + 1) * d.nb + k] = m1;
+            }
         }
-        inf = block_max(inf, scratch);
-        if (threadIdx.x == 0) {
-            const double c = fmin(sqrt(v), inf);
-            d.inv_scale[b * 2 + which] = c > 0.0 ? 1.0 / c : 0.0;
+        last |= arrive_solve(cnt + 2 * d.nb + kCntP, d.nb, &s_fin);
+    }
+    if (!last) return;
+    const int t = ty * TB + tx;
+    double f0 = 0.0, f1 = 0.0, inf = 0.0;
+    {
+        const double* p0 = d.frob_part + (long long)b * 2 * d.ntile;
+        for (int k = t; k < d.ntile; k += TB * TY) {
+            f0 += __ldcg(p0 + k);
+            f1 += __ldcg(p0 + d.ntile + k);
         }
+        if (ty < 2) {
+            const double* bm = d.blk_inf + ((long long)b * 2 + ty) * d.nb;
+            for (int k = tx; k < d.nb; k += TB) inf = fmax(inf, __ldcg(bm + k));
+            inf = warp_max(inf);
+        }
+    }
+    block_sum2_2d(f0, f1, reinterpret_cast<double (*)[2]>(&sm8[0][0]));
+    if (ty < 2 && tx == 0) {
+        const double cc = fmin(sqrt(ty == 0 ? f0 : f1), inf);
+        d.inv_scale[b * 2 + ty] = cc > 0.0 ? 1.0 / cc : 0.0;
     }
 }
 
@@ -299,10 +409,6 @@ void launch_prep(const Dev& d, const XConst& c, cudaStream_t st) {
     TPB_CHECK_LAUNCH();
 }
 
-void launch_frob_finalize(const Dev& d, cudaStream_t st) {
-    frob_finalize_kernel<<<d.B, 256, 0, st>>>(d);
-    TPB_CHECK_LAUNCH();
-}
 
 // ---------------------------------------------------------------- x-step A
 // h_g(i,j) = r_g + s (4 - R_ii - R_jj + R_ij + R_ji + v2_i + v2_j) [- s r_nu]
@@ -344,12 +450,14 @@ __global__ void __launch_bounds__(TB* TY, 4) xstep_a_kernel(Dev d, XConst c) {
     };
     // diagonals and v2 of both node blocks: issued first, so their latency
     // overlaps the block loads instead of following them
-    double dgi = 0.0, dgj = 0.0, v2vi = 0.0, v2vj = 0.0;
+    double dgi = 0.0, dgj = 0.0, v2vi = 0.0, v2vj = 0.0, rsi = 0.0, rti = 0.0;
     if (ty == 0) {
         const int i = i0 + tx, j = j0 + tx;
         if (i < n) {
             const long long p = (long long)i * n + i;
-            dgi = rS(p) + rT(p);
+            rsi = rS(p);
+            rti = rT(p);
+            dgi = rsi + rti;
             v2vi = 1.0 - (Y[lo.off_y + i] - D[lo.off_y + i] * c.inv_rho);
         }
         if (j < n) {
@@ -472,19 +580,51 @@ __global__ void __launch_bounds__(TB* TY, 4) xstep_a_kernel(Dev d, XConst c) {
         for (int y = 0; y < TY; ++y) s += colp[which][y][l];
         return s;
     };
+    // node partials, and their tile totals (sum u = 2 sum h) for pass B's
+    // node-space solve: warp 0 the rows, warp 1 the columns
+    double pu = 0.0, pz = 0.0;
     if (t < TB) {
         const int il = t, i = i0 + il;
         if (i < n) {
-            const double su = rowp[0][il] + (bi == bj ? colsum(0, il) : 0.0);
-            PU[(long long)bj * n + i] = su;
-            if (d.het) PZ[(long long)bj * n + i] = rowp[1][il] + (bi == bj ? colsum(1, il) : 0.0);
+            pu = rowp[0][il] + (bi == bj ? colsum(0, il) : 0.0);
+            PU[(long long)bj * n + i] = pu;
+            if (d.het) {
+                pz = rowp[1][il] + (bi == bj ? colsum(1, il) : 0.0);
+                PZ[(long long)bj * n + i] = pz;
+            }
         }
     } else if (t < 2 * TB && bi != bj) {
         const int jl = t - TB, j = j0 + jl;
         if (j < n) {
-            PU[(long long)bi * n + j] = colsum(0, jl);
-            if (d.het) PZ[(long long)bi * n + j] = colsum(1, jl);
+            pu = colsum(0, jl);
+            PU[(long long)bi * n + j] = pu;
+            if (d.het) {
+                pz = colsum(1, jl);
+                PZ[(long long)bi * n + j] = pz;
+            }
         }
+    }
+    __shared__ double s_tot[2][2];
+    if (ty < 2) {
+        const double a0 = warp_sum(pu), a1 = warp_sum(pz);
+        if (tx == 0) {
+            s_tot[ty][0] = a0;
+            s_tot[ty][1] = a1;
+        }
+    }
+    // diagonal tiles: tr r_S, tr r_T and the degree targets over the block
+    double4 bk = make_double4(0.0, 0.0, 0.0, 0.0);
+    if (bi == bj && ty == 0) {
+        const int i = i0 + tx;
+        const double dg = d.het && i < n ? d.deg[(long long)b * n + i] : 0.0;
+        bk = make_double4(warp_sum(rsi), warp_sum(rti), warp_sum(dg), 0.0);
+    }
+    __syncthreads();
+    if (t == 0) {
+        double* ta = d.tile_aux + ((long long)b * d.ntile + blockIdx.x) * 2;
+        ta[0] = s_tot[0][0] + s_tot[1][0];
+        ta[1] = s_tot[0][1] + s_tot[1][1];
+        if (bi == bj) reinterpret_cast<double4*>(d.blk)[(long long)b * d.nb + bi] = bk;
     }
 }
 
@@ -494,119 +634,13 @@ void launch_xstep_a(const Dev& d, const XConst& c, cudaStream_t st) {
     TPB_CHECK_LAUNCH();
 }
 
-// ---------------------------------------------------------------- node solve
-// One CTA per solve: node sums u = D h, lambda, and the node-space vectors of
-// the closed form. node[0..n) = t (hom) / t_g (het); node[n..2n) = t_z;
-// node[2n..3n) = mu_d. scal[kLambda] = lambda.
-__global__ void xstep_node_kernel(Dev d, XConst c) {
-    const int b = blockIdx.x;
-    if (solve_done(d, b)) return;
-    const Layout& lo = d.lo;
-    const int n = lo.n;
-    const double* Y = d.Y + (long long)b * d.nx;
-    const double* D = d.D + (long long)b * d.nx;
-    const double* PU = d.PU + (long long)b * d.nb * n;
-    const double* PZ = d.PZ + (long long)b * d.nb * n;
-    double* node = d.node + (long long)b * 4 * n;
-    __shared__ double scratch[32];
-    extern __shared__ double sh[];  // 3n doubles: ug, uz, tmp
-    double* ug = sh;
-    double* uz = sh + n;
-    double* tmp = sh + 2 * n;
-
-    // traces of r_S, r_T for lambda
-    double trS = 0.0, trT = 0.0, su = 0.0, sz = 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const long long p = (long long)i * n + i;
-        trS += Y[lo.off_s + p] - D[lo.off_s + p] * c.inv_rho;
-        trT += Y[lo.off_t + p] - D[lo.off_t + p] * c.inv_rho;
-        const double u = sum_partials(PU, d.nb, n, i);
-        const double z = d.het ? sum_partials(PZ, d.nb, n, i) : 0.0;
-        ug[i] = u;
-        uz[i] = z;
-        su += u;
-        sz += z;
-    }
-    {
-        __shared__ double scratch4[4][32];
-        double v4[4] = {trS, trT, su, sz};
-        block_sum4(v4, scratch4);
-        trS = v4[0];
-        trT = v4[1];
-        su = v4[2];
-        sz = v4[3];
-    }
-    if (threadIdx.x == 0) {
-        const double rl = Y[lo.lambda_ix] - D[lo.lambda_ix] * c.inv_rho + c.inv_rho;  // +1/rho: c = -1 at lambda
-        const double hl = rl + c.s * (c.alpha + trS + 2.0 * n - trT);
-        d.scal[b * 8 + kLambda] = hl / c.lam_den;
-    }
-    const double ubar = su / n;
-    if (!d.het) {
-        for (int i = threadIdx.x; i < n; i += blockDim.x)
-            node[i] = c.c1 * (ug[i] - ubar) + c.c2 * ubar;
-        return;
-    }
-    const double zbar = sz / n;
-    if (d.cap) {
-        // capacity-bound rows are not in the KKT (q = 0): the commuting 2x2
-        // block G(K) alone, no degree multipliers
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            const double pg = ug[i] - ubar, pz = uz[i] - zbar;
-            node[i] = c.c1_11 * pg + c.c2_11 * ubar + c.c1_12 * pz + c.c2_12 * zbar;
-            node[n + i] = c.c1_12 * pg + c.c2_12 * ubar + c.c1_22 * pz + c.c2_22 * zbar;
-            node[2 * n + i] = 0.0;
-        }
-        return;
-    }
-    // het: rhs_d = G21(Q) u_g + G22(Q) u_z - e ; Q = (n-2) I + J
-    double srhs = 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const double rhs = c.g12_p * (ug[i] - ubar) + c.g12_1 * ubar + c.g22_p * (uz[i] - zbar) +
-                           c.g22_1 * zbar - d.deg[(long long)b * n + i];
-        tmp[i] = rhs;
-        srhs += rhs;
-    }
-    srhs = block_sum(srhs, scratch);
-    const double rbar = srhs / n;
-    double smu = 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const double mu = (tmp[i] - rbar) / c.mu_den_p + rbar / c.mu_den_1;
-        tmp[i] = mu;
-        node[2 * n + i] = mu;
-        smu += mu;
-    }
-    smu = block_sum(smu, scratch);
-    // u_z'' = u_z - Q mu = u_z - (n-2) mu - (sum mu) 1
-    double sz2 = 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const double v = uz[i] - (n - 2.0) * tmp[i] - smu;
-        uz[i] = v;
-        sz2 += v;
-    }
-    sz2 = block_sum(sz2, scratch);
-    const double z2bar = sz2 / n;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const double pg = ug[i] - ubar, pz = uz[i] - z2bar;
-        node[i] = c.c1_11 * pg + c.c2_11 * ubar + c.c1_12 * pz + c.c2_12 * z2bar;
-        node[n + i] = c.c1_12 * pg + c.c2_12 * ubar + c.c1_22 * pz + c.c2_22 * z2bar;
-    }
-}
-
-void launch_xstep_node(const Dev& d, const XConst& c, cudaStream_t st) {
-    // one thread per node (latency-bound single-CTA pass)
-    const int threads = std::min(1024, std::max(128, ((d.lo.n + 31) / 32) * 32));
-    xstep_node_kernel<<<d.B, threads, 3 * d.lo.n * sizeof(double), st>>>(d, c);
-    TPB_CHECK_LAUNCH();
-}
-
 // ---------------------------------------------------------------- CG x-step
 // The paper's linear substep as matrix-free CG on the g block of the reduced
 // KKT system: H_gg = (1 + 4s) I + 3s D^T D, applied as one
 // node-sum scatter (u = D p, fixed-order tile partials) and one per-edge
 // gather (u_i + u_j). On the complete candidate graph H_gg has three
 // eigenvalues, so CG stops after three iterations at ~1e-15; the closed form
-// (launch_xstep_node + pass B) is the default and this path is its
+// (pass B's node-space prologue) is the default and this path is its
 // operator-level cross-check and the general-graph formulation.
 
 namespace {
@@ -700,6 +734,9 @@ __global__ void __launch_bounds__(TB* TY, 4) xstep_cg_kernel(Dev d, XConst c) {
                         if (blockIdx.x == 0) {
                             d.ictl[b * 8 + kCgIters] = k;
                             d.scal[b * 8 + kCgRes] = rr0 > 0.0 ? sqrt(rr1 / rr0) : 0.0;
+                            // the reference's guard after its linear solve (admm.cpp:287):
+                            // sticky, raised by the host after the chunk
+                            if (rr0 > 0.0 && !(rr1 <= 1e-16 * rr0)) d.ictl[b * 8 + kCgFail] = 1;
                         }
                     }
                     s_beta[b] = k == 0 ? 0.0 : rr1 / s_rrk[b];
@@ -927,6 +964,9 @@ __global__ void __launch_bounds__(TB* TY, 4) xstep_cg_reg_kernel(Dev d, XConst c
                         if (blockIdx.x == 0) {
                             d.ictl[bb * 8 + kCgIters] = k;
                             d.scal[bb * 8 + kCgRes] = rr0 > 0.0 ? sqrt(rr1 / rr0) : 0.0;
+                            // the reference's guard after its linear solve (admm.cpp:287):
+                            // sticky, raised by the host after the chunk
+                            if (rr0 > 0.0 && !(rr1 <= 1e-16 * rr0)) d.ictl[bb * 8 + kCgFail] = 1;
                         }
                     }
                     s_beta[bb] = k == 0 ? 0.0 : rr1 / s_rrk[bb];
@@ -1023,24 +1063,19 @@ int cg_capacity(const void* kernel, const Dev& d) {
 }
 }  // namespace
 
-int cg_grid_size(const Dev& d) {
-    static int cached = 0;
-    if (!cached) cached = cg_capacity((const void*)xstep_cg_kernel, d);
-    return std::max(1, std::min(cached, d.B * d.ntile));
-}
-
-// register-resident CG when every item fits one co-resident CTA
-bool cg_use_registers(const Dev& d) {
-    if (d.nb > kCgRegNb) return false;
-    static int cached = 0;
-    if (!cached) cached = cg_capacity((const void*)xstep_cg_reg_kernel, d);
-    return (long long)d.B * d.ntile <= cached;
+// Launch shape of the CG x-step for this solver's device and batch (set once
+// per solver in Dev::cg_grid; 0 ... register-resident kernel, one CTA per
+// (solve, tile) item, when every item fits one co-resident CTA).
+int cg_launch_grid(const Dev& d) {
+    if (d.nb <= kCgRegNb && (long long)d.B * d.ntile <= cg_capacity((const void*)xstep_cg_reg_kernel, d))
+        return -d.B * d.ntile;  // negative: register kernel
+    return std::max(1, std::min(cg_capacity((const void*)xstep_cg_kernel, d), d.B * d.ntile));
 }
 
 void launch_xstep_cg(const Dev& d, const XConst& c, cudaStream_t st) {
-    const bool reg = cg_use_registers(d);
+    const bool reg = d.cg_grid < 0;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(reg ? d.B * d.ntile : cg_grid_size(d));
+    cfg.gridDim = dim3(reg ? -d.cg_grid : d.cg_grid);
     cfg.blockDim = dim3(TB, TY);
     cfg.stream = st;
     cfg.dynamicSmemBytes = cg_dyn_smem(d);
@@ -1056,6 +1091,111 @@ void launch_xstep_cg(const Dev& d, const XConst& c, cudaStream_t st) {
 }
 
 // ---------------------------------------------------------------- x-step B
+// Node-space part of the closed form for node blocks bi and bj (DESIGN.md
+// §3.3/§3.4), formed by every pass-B CTA from pass A's partials: the totals
+// of u = D h (and u_z) from the per-tile sums, the traces and degree totals
+// from the diagonal tiles (fixed order, identical in every CTA), u_i from
+// the nb node partials (four k-strided groups, added in group order).
+//   hom: t = c1 (u - ubar) + c2 ubar
+//   het: rhs = G21(Q) u_g + G22(Q) u_z - e with Q = (n-2) I + J, whose mean
+//        is g12(2n-2) ubar + g22(2n-2) zbar - mean(e), so mean(mu_d) =
+//        mean(rhs) / mu_den_1 and u_z'' = u_z - Q mu_d in closed form.
+// Leaves nv[q][0..2][lane] (t_g, t_z, mu_d of block q) and, in thread 0,
+// returns lambda. Ends with a CTA barrier.
+__device__ double node_space(const Dev& d, const XConst& c, int b, int bi, int bj, double (*nv)[3][TB],
+                             double (*sp)[2][4][TB], double (*scr)[2]) {
+    const Layout& lo = d.lo;
+    const int n = lo.n;
+    const int tx = threadIdx.x, ty = threadIdx.y, t = ty * TB + tx;
+    // per-tile totals (thread-strided, then the CTA tree)
+    double su = 0.0, sz = 0.0;
+    const double* ta = d.tile_aux + (long long)b * d.ntile * 2;
+    for (int k = t; k < d.ntile; k += TB * TY) {
+        su += ta[2 * k];
+        sz += ta[2 * k + 1];
+    }
+    // node partials of the two blocks: warp w takes block w & 1, partials
+    // k = w >> 1, (w >> 1) + 4, ...
+    const int q = ty & 1, g = ty >> 1;
+    const int i = (q ? bj : bi) * TB + tx;
+    double pu = 0.0, pz = 0.0;
+    if (i < n) {
+        const double* PU = d.PU + (long long)b * d.nb * n;
+        const double* PZ = d.PZ + (long long)b * d.nb * n;
+        for (int k = g; k < d.nb; k += 4) {
+            pu += PU[(long long)k * n + i];
+            if (d.het) pz += PZ[(long long)k * n + i];
+        }
+    }
+    // traces and degree totals of the diagonal tiles (warps 0 and 1 alike)
+    double trS = 0.0, trT = 0.0, sdeg = 0.0;
+    if (ty < 2) {
+        const double4* bk = reinterpret_cast<const double4*>(d.blk) + (long long)b * d.nb;
+        for (int k = tx; k < d.nb; k += TB) {
+            const double4 v = bk[k];
+            trS += v.x;
+            trT += v.y;
+            sdeg += v.z;
+        }
+        trS = warp_sum(trS);
+        trT = warp_sum(trT);
+        sdeg = warp_sum(sdeg);
+    }
+    sp[q][0][g][tx] = pu;
+    sp[q][1][g][tx] = pz;
+    block_sum2_2d(su, sz, scr);  // barriers: sp is visible after
+    double lam = 0.0;
+    if (t == 0) {
+        const double rl = d.Y[(long long)b * d.nx + lo.lambda_ix] - d.D[(long long)b * d.nx + lo.lambda_ix] * c.inv_rho +
+                          c.inv_rho;  // +1/rho: c = -1 at lambda
+        lam = (rl + c.s * (c.alpha + trS + 2.0 * n - trT)) / c.lam_den;
+    }
+    if (ty < 2) {
+        const double ubar = su / n;
+        double u = 0.0, uz = 0.0;
+#pragma unroll
+        for (int gg = 0; gg < 4; ++gg) {
+            u += sp[ty][0][gg][tx];
+            uz += sp[ty][1][gg][tx];
+        }
+        double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+        const double pg = u - ubar;
+        if (!d.het) {
+            v0 = c.c1 * pg + c.c2 * ubar;
+        } else {
+            const double zbar = sz / n;
+            double z2bar = zbar, uz2 = uz;
+            if (!d.cap && i < n) {
+                const double rbar = c.g12_1 * ubar + c.g22_1 * zbar - sdeg / n;
+                const double mbar = rbar / c.mu_den_1, smu = n * mbar;
+                const double rhs = c.g12_p * pg + c.g12_1 * ubar + c.g22_p * (uz - zbar) + c.g22_1 * zbar -
+                                   d.deg[(long long)b * n + i];
+                v2 = (rhs - rbar) / c.mu_den_p + mbar;
+                uz2 = uz - (n - 2.0) * v2 - smu;
+                z2bar = zbar - (n - 2.0) * mbar - smu;
+            }
+            const double pz = uz2 - z2bar;
+            v0 = c.c1_11 * pg + c.c2_11 * ubar + c.c1_12 * pz + c.c2_12 * z2bar;
+            v1 = c.c1_12 * pg + c.c2_12 * ubar + c.c1_22 * pz + c.c2_22 * z2bar;
+        }
+        if (i >= n) v0 = v1 = v2 = 0.0;
+        nv[ty][0][tx] = v0;
+        nv[ty][1][tx] = v1;
+        nv[ty][2][tx] = v2;
+        if (bi == bj && ty == 0 && i < n) {
+            // the node-space vector itself (substep API: mu_d)
+            double* node = d.node + (long long)b * 4 * n;
+            node[i] = v0;
+            if (d.het) {
+                node[n + i] = v1;
+                node[2 * n + i] = v2;
+            }
+        }
+    }
+    __syncthreads();
+    return lam;
+}
+
 __global__ void __launch_bounds__(TB* TY, 4) xstep_b_kernel(Dev d, XConst c) {
     const int b = blockIdx.y;
     if (solve_done(d, b)) return;
@@ -1066,20 +1206,23 @@ __global__ void __launch_bounds__(TB* TY, 4) xstep_b_kernel(Dev d, XConst c) {
     const double* Y = d.Y + (long long)b * d.nx;
     double* X = d.X + (long long)b * d.nx;
     double* D = d.D + (long long)b * d.nx;
-    const double* node = d.node + (long long)b * 4 * n;
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int i0 = bi * TB, j0 = bj * TB;
     __shared__ double Gs[TB][TB + 1];  // g(i, j) of the tile's pairs
     __shared__ double red[TB * TY / 32];
+    __shared__ double nv[2][3][TB];    // node vectors of blocks bi (0) and bj (1)
     double res = 0.0;
 
-    // edge blocks (hom: batched loads of h, Y_g, D_g for the thread's rows)
-    const int cg_it = d.cg ? d.ictl[b * 8 + kCgIters] : 0;
+    __shared__ double sp[2][2][4][TB];
+    __shared__ double scr2[TB * TY / 32][2];
+    const double lam = node_space(d, c, b, bi, bj, nv, sp, scr2);  // thread 0
+
+    // edge loads of the thread's rows (hom), batched
+    constexpr int NR = TB / TY;
+    long long l[NR];
+    bool ok[NR];
+    double hv[NR], yg[NR], dg[NR];
     if (!d.het) {
-        constexpr int NR = TB / TY;
-        long long l[NR];
-        bool ok[NR];
-        double hv[NR], yg[NR], dg[NR];
 #pragma unroll
         for (int k = 0; k < NR; ++k) {
             const int i = i0 + ty + k * TY, j = j0 + tx;
@@ -1091,14 +1234,17 @@ __global__ void __launch_bounds__(TB* TY, 4) xstep_b_kernel(Dev d, XConst c) {
                 dg[k] = D[l[k]];
             }
         }
+    }
+    const int cg_it = d.cg ? d.ictl[b * 8 + kCgIters] : 0;
+    if (!d.het) {
 #pragma unroll
         for (int k = 0; k < NR; ++k) {
-            const int il = ty + k * TY, i = i0 + il, j = j0 + tx;
+            const int il = ty + k * TY;
             double g = 0.0;
             if (ok[k]) {
                 // CG: zero iterations means h = 0 and g = 0
                 g = d.cg ? (cg_it > 0 ? d.cg_x[(long long)b * lo.m + l[k]] : 0.0)
-                         : c.f0 * hv[k] + node[i] + node[j];
+                         : c.f0 * hv[k] + nv[0][0][il] + nv[1][0][tx];
                 const double e = g - yg[k];
                 X[l[k]] = g;
                 if (d.upd_duals) D[l[k]] = dg[k] + c.rho * e;
@@ -1117,9 +1263,9 @@ __global__ void __launch_bounds__(TB* TY, 4) xstep_b_kernel(Dev d, XConst c) {
                 const long long lz = lo.off_z + l, lv = lo.off_nu + l;
                 const double rz = Y[lz] - D[lz] * c.inv_rho;
                 const double rnu = Y[lv] - D[lv] * c.inv_rho;
-                const double hz2 = rz + c.s * rnu - node[2 * n + i] - node[2 * n + j];
-                g = c.g11_0 * hv + c.g12_0 * hz2 + node[i] + node[j];
-                const double z = c.g12_0 * hv + c.g22_0 * hz2 + node[n + i] + node[n + j];
+                const double hz2 = rz + c.s * rnu - nv[0][2][il] - nv[1][2][jl];
+                g = c.g11_0 * hv + c.g12_0 * hz2 + nv[0][0][il] + nv[1][0][jl];
+                const double z = c.g12_0 * hv + c.g22_0 * hz2 + nv[0][1][il] + nv[1][1][jl];
                 // nu = s (delta r_nu - (g - z))   (slack of g - z + nu = 0)
                 const double nu = c.s * (c.delta * rnu - (g - z));
                 const double dz = z - Y[lz], dnu = nu - Y[lv];
@@ -1131,10 +1277,10 @@ __global__ void __launch_bounds__(TB* TY, 4) xstep_b_kernel(Dev d, XConst c) {
                 }
                 res += dz * dz + dnu * dnu;
             }
-            const double dg = g - Y[l];
+            const double dgv = g - Y[l];
             X[l] = g;
-            if (d.upd_duals) D[l] += c.rho * dg;
-            res += dg * dg;
+            if (d.upd_duals) D[l] += c.rho * dgv;
+            res += dgv * dgv;
         }
         Gs[il][jl] = g;
     }
@@ -1145,11 +1291,11 @@ __global__ void __launch_bounds__(TB* TY, 4) xstep_b_kernel(Dev d, XConst c) {
     // batch: all loads first (independent, in flight together), then the
     // arithmetic and the stores (X/D may alias Y in the compiler's view).
     constexpr int NE = TB / TY;
-    auto upd_batch = [&](const long long (&pos)[NE], const double (&gv)[NE], const bool (&ok)[NE]) {
+    auto upd_batch = [&](const long long (&pos)[NE], const double (&gv)[NE], const bool (&okb)[NE]) {
         double ys[NE], yt[NE], ds[NE], dt[NE];
 #pragma unroll
         for (int k = 0; k < NE; ++k) {
-            if (!ok[k]) continue;
+            if (!okb[k]) continue;
             ys[k] = Y[lo.off_s + pos[k]];
             yt[k] = Y[lo.off_t + pos[k]];
             ds[k] = D[lo.off_s + pos[k]];
@@ -1157,7 +1303,7 @@ __global__ void __launch_bounds__(TB* TY, 4) xstep_b_kernel(Dev d, XConst c) {
         }
 #pragma unroll
         for (int k = 0; k < NE; ++k) {
-            if (!ok[k]) continue;
+            if (!okb[k]) continue;
             const double rs = ys[k] - ds[k] * c.inv_rho, rt = yt[k] - dt[k] * c.inv_rho;
             const double xs = c.s * (c.delta * rs - c.alpha_over_n + gv[k]);
             const double xt = c.s * (c.delta * rt + gv[k]);
@@ -1174,32 +1320,32 @@ __global__ void __launch_bounds__(TB* TY, 4) xstep_b_kernel(Dev d, XConst c) {
         // orientation 1: entries (i, j), address j*n + i
         long long pos[NE];
         double gv[NE];
-        bool ok[NE];
+        bool okb[NE];
 #pragma unroll
         for (int k = 0; k < NE; ++k) {
             const int cc = ty + k * TY;
             const int i = i0 + tx, j = j0 + cc;
-            ok[k] = i < n && j < n && i != j;
+            okb[k] = i < n && j < n && i != j;
             pos[k] = (long long)j * n + i;
             // diagonal tiles hold each pair once: entry (i, j) with either order
             gv[k] = (bi == bj && i > j) ? Gs[cc][tx] : Gs[tx][cc];
         }
-        upd_batch(pos, gv, ok);
+        upd_batch(pos, gv, okb);
     }
     if (bi != bj) {
         // orientation 2: entries (j, i), address i*n + j
         long long pos[NE];
         double gv[NE];
-        bool ok[NE];
+        bool okb[NE];
 #pragma unroll
         for (int k = 0; k < NE; ++k) {
             const int cc = ty + k * TY;
             const int j = j0 + tx, i = i0 + cc;
-            ok[k] = i < n && j < n;
+            okb[k] = i < n && j < n;
             pos[k] = (long long)i * n + j;
             gv[k] = Gs[cc][tx];
         }
-        upd_batch(pos, gv, ok);
+        upd_batch(pos, gv, okb);
     }
     // node partials of g (deg = L_ii)
     const int t = ty * TB + tx;
@@ -1239,87 +1385,106 @@ __global__ void __launch_bounds__(TB* TY, 4) xstep_b_kernel(Dev d, XConst c) {
             d.res_part[(long long)b * d.ntile + blockIdx.x] = s;
         }
     }
+
+    // ---- tail: the last tile of a node block writes the block's diagonal
+    // entries (deg_i = L_ii = node sums of g):
+    //   S_ii = s (delta r_S,ii - alpha/n - deg_i + lambda)
+    //   T_ii = s (delta r_T,ii + 2 - deg_i - lambda)
+    //   y_i  = s (delta r_y,i + 1 - deg_i)
+    // and the CTA completing the solve's last block adds the residual (the
+    // reduction tree of a node_threads(n)-thread pass: node terms, then the
+    // tile partials), the trace row, the best iterate and the stop flags.
+    int* cnt = d.cnt + (long long)b * d.cnt_stride;
+    __shared__ int s_fin;
+    __shared__ double s_lam;
+    if (t == 0) s_lam = lam;
+    const int fin = arrive_blocks(cnt + kCntB * d.nb, d.nb, bi, bj, &s_fin);
+    if (!fin) return;
+    double* rnode = d.res_node + (long long)b * n;
+    bool last = false;
+    for (int q = 0; q < 2; ++q) {
+        if (!(fin >> q & 1)) continue;
+        const int k = q == 0 ? bi : bj;
+        const int i = k * TB + tx;
+        const long long p = (long long)i * n + i;
+        const long long ps = lo.off_s + p, pt = lo.off_t + p, py = lo.off_y + i;
+        double ys = 0.0, yt = 0.0, yy = 0.0, ds = 0.0, dt = 0.0, dy = 0.0;
+        const double* const pg1[1] = {PG};
+        double degv[1];
+        node_sum<1>(pg1, d.nb, n, k, reinterpret_cast<double (*)[TY][TB + 1]>(&Gs[0][0]), degv, [&] {
+            if (ty == 0 && i < n) {  // the diagonal entries' loads overlap the partial sums
+                ys = Y[ps];
+                yt = Y[pt];
+                yy = Y[py];
+                ds = D[ps];
+                dt = D[pt];
+                dy = D[py];
+            }
+        });
+        const double deg = degv[0];
+        if (ty == 0 && i < n) {
+            const double rs = ys - ds * c.inv_rho, rt = yt - dt * c.inv_rho, ry = yy - dy * c.inv_rho;
+            const double xs = c.s * (c.delta * rs - c.alpha_over_n - deg + s_lam);
+            const double xt = c.s * (c.delta * rt + 2.0 - deg - s_lam);
+            const double xy = c.s * (c.delta * ry + 1.0 - deg);
+            X[ps] = xs;
+            X[pt] = xt;
+            X[py] = xy;
+            if (d.upd_duals) {
+                D[ps] = ds + c.rho * (xs - ys);
+                D[pt] = dt + c.rho * (xt - yt);
+                D[py] = dy + c.rho * (xy - yy);
+            }
+            rnode[i] = (xs - ys) * (xs - ys) + (xt - yt) * (xt - yt) + (xy - yy) * (xy - yy);
+        }
+        last |= arrive_solve(cnt + 2 * d.nb + kCntB, d.nb, &s_fin);
+    }
+    if (!last) return;
+    int* ctl = d.ictl + b * 8;
+    double yl = 0.0, dl = 0.0, best = 0.0;
+    int it = 0;
+    if (t == 0) {  // independent of the reduction: in flight alongside it
+        yl = Y[lo.lambda_ix];
+        dl = D[lo.lambda_ix];
+        best = d.scal[b * 8 + kBestRes];
+        it = ctl[kIter];
+    }
+    double rsum = 0.0, dummy = 0.0;
+    {
+        const double* rp = d.res_part + (long long)b * d.ntile;
+        for (int k = t; k < n; k += TB * TY) rsum += __ldcg(rnode + k);
+        for (int k = t; k < d.ntile; k += TB * TY) rsum += __ldcg(rp + k);
+    }
+    block_sum2_2d(rsum, dummy, scr2);
+    if (t != 0) return;
+    const double lamv = s_lam;
+    d.scal[b * 8 + kLambda] = lamv;
+    X[lo.lambda_ix] = lamv;
+    if (!d.upd_duals) return;
+    D[lo.lambda_ix] = dl + c.rho * (lamv - yl);
+    rsum += (lamv - yl) * (lamv - yl);
+    if (!d.bookkeep) return;
+    // it: 0-based index of this iteration
+    d.tr_res[(long long)b * d.max_iter + it] = rsum;
+    d.tr_lam[(long long)b * d.max_iter + it] = yl;
+    d.scal[b * 8 + kRes] = rsum;
+    ctl[kIter] = it + 1;
+    if (d.track_best && rsum < best) {
+        d.scal[b * 8 + kBestRes] = rsum;
+        ctl[kBestIter] = it + 1;
+        ctl[kImproved] = 1;
+    }
+    if (rsum <= d.epsilon) {
+        ctl[kDone] = 1;
+        ctl[4] = 1;  // converged
+    } else if (it + 1 >= d.max_iter) {
+        ctl[kDone] = 1;
+    }
 }
 
 void launch_xstep_b(const Dev& d, const XConst& c, cudaStream_t st) {
     dim3 grid(d.ntile, d.B), block(TB, TY);
     xstep_b_kernel<<<grid, block, 0, st>>>(d, c);
-    TPB_CHECK_LAUNCH();
-}
-
-// ---------------------------------------------------------------- diag + tail
-// deg_i = L_ii = sum of node partials of g. Diagonal entries:
-//   S_ii = s (delta r_S,ii - alpha/n - deg_i + lambda)
-//   T_ii = s (delta r_T,ii + 2 - deg_i - lambda)
-//   y_i  = s (delta r_y,i + 1 - deg_i)
-// then residual, trace row, best iterate flag and the stop test.
-__global__ void xstep_diag_kernel(Dev d, XConst c) {
-    const int b = blockIdx.x;
-    int* ctl = d.ictl + b * 8;
-    if (ctl[kDone]) return;
-    const Layout& lo = d.lo;
-    const int n = lo.n;
-    const double* Y = d.Y + (long long)b * d.nx;
-    double* X = d.X + (long long)b * d.nx;
-    double* D = d.D + (long long)b * d.nx;
-    const double* PG = d.PG + (long long)b * d.nb * n;
-    const double lam = d.scal[b * 8 + kLambda];
-    __shared__ double scratch[32];
-    double res = 0.0;
-    // the thread's first tile residual partial, loaded with the node data
-    const double* rpart = d.res_part + (long long)b * d.ntile;
-    const double rp0 = (int)threadIdx.x < d.ntile ? rpart[threadIdx.x] : 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const double deg = sum_partials(PG, d.nb, n, i);
-        const long long p = (long long)i * n + i;
-        const long long ps = lo.off_s + p, pt = lo.off_t + p, py = lo.off_y + i;
-        const double ys = Y[ps], yt = Y[pt], yy = Y[py];
-        const double rs = ys - D[ps] * c.inv_rho, rt = yt - D[pt] * c.inv_rho, ry = yy - D[py] * c.inv_rho;
-        const double xs = c.s * (c.delta * rs - c.alpha_over_n - deg + lam);
-        const double xt = c.s * (c.delta * rt + 2.0 - deg - lam);
-        const double xy = c.s * (c.delta * ry + 1.0 - deg);
-        X[ps] = xs;
-        X[pt] = xt;
-        X[py] = xy;
-        if (d.upd_duals) {
-            D[ps] += c.rho * (xs - ys);
-            D[pt] += c.rho * (xt - yt);
-            D[py] += c.rho * (xy - yy);
-        }
-        res += (xs - ys) * (xs - ys) + (xt - yt) * (xt - yt) + (xy - yy) * (xy - yy);
-    }
-    // tile partials in fixed order
-    if ((int)threadIdx.x < d.ntile) res += rp0;
-    for (int t = threadIdx.x + blockDim.x; t < d.ntile; t += blockDim.x) res += rpart[t];
-    res = block_sum(res, scratch);
-    if (threadIdx.x == 0 && !d.upd_duals) X[lo.lambda_ix] = lam;
-    if (threadIdx.x == 0 && d.upd_duals) {
-        const double yl = Y[lo.lambda_ix];
-        X[lo.lambda_ix] = lam;
-        D[lo.lambda_ix] += c.rho * (lam - yl);
-        res += (lam - yl) * (lam - yl);
-        const int it = ctl[kIter];  // 0-based index of this iteration
-        d.tr_res[(long long)b * d.max_iter + it] = res;
-        d.tr_lam[(long long)b * d.max_iter + it] = yl;
-        d.scal[b * 8 + kRes] = res;
-        ctl[kIter] = it + 1;
-        if (d.track_best && res < d.scal[b * 8 + kBestRes]) {
-            d.scal[b * 8 + kBestRes] = res;
-            ctl[kBestIter] = it + 1;
-            ctl[kImproved] = 1;
-        }
-        if (res <= d.epsilon) {
-            ctl[kDone] = 1;
-            ctl[4] = 1;  // converged
-        } else if (it + 1 >= d.max_iter) {
-            ctl[kDone] = 1;
-        }
-    }
-}
-
-void launch_xstep_diag(const Dev& d, const XConst& c, cudaStream_t st) {
-    const int threads = std::min(1024, std::max(128, ((d.lo.n + 31) / 32) * 32));
-    xstep_diag_kernel<<<d.B, threads, 0, st>>>(d, c);
     TPB_CHECK_LAUNCH();
 }
 
@@ -1356,8 +1521,6 @@ void launch_best_copy(const Dev& d, const XConst& c, cudaStream_t st) {
     TPB_CHECK_LAUNCH();
 }
 
-void init_attrs_admm() {
-    set_max_dyn_smem(xstep_node_kernel);
-}
+void init_attrs_admm() {}
 
 }  // namespace tpb

@@ -101,7 +101,7 @@ __global__ void sym_pad_kernel(const double* a, int n, int ld, int w, double* A)
     }
 }
 
-// 1 / min(||A||_F, ||A||_inf) of matrix w (the solver's frob_finalize_kernel)
+// 1 / min(||A||_F, ||A||_inf) of matrix w (as the solver's prep tail)
 __global__ void frob_kernel(const double* A, int ld, int w, double* scale) {
     __shared__ double scratch[32];
     const double* src = A + (long long)w * ld * ld;
@@ -191,7 +191,8 @@ void slem_edges(int n, const std::vector<int>& packed, const std::vector<double>
     const long long m = (long long)n * (n - 1) / 2;
     const int k = (int)packed.size();
     init_attrs();
-    const int kfin = n - 1 <= kFinalExactDim ? std::max(1, n - 1) : kFinalKrylov;
+    const bool exact = n - 1 <= kFinalExactDim;
+    const int kfin = exact ? std::max(1, n - 1) : slem_oneoff_kmax(n);
     DBuf<double> g(m), out(8), basis((size_t)kfin * n), ew(std::max(1, k));
     DBuf<int> list(std::max(1, k)), count(1), ei(std::max(1, k)), ej(std::max(1, k)), ci(std::max(1, k));
     g.zero();
@@ -214,8 +215,10 @@ void slem_edges(int n, const std::vector<int>& packed, const std::vector<double>
     a.col_idx = ci.p;
     a.basis = basis.p;
     a.kmax = kfin;
+    a.plain = exact ? 0 : 1;  // as the solver's one-off reports (Solver::final_slem)
     a.max_restarts = 200;
     a.min_steps = 64;
+    a.check_every = 128;
     a.tol = 1e-10;
     a.out = out.p;
     launch_slem(a, 1, 0);

@@ -21,7 +21,7 @@ struct SignSchedule {
 // guaranteed growth on [0, 0.55] that keeps [0.55, 1.3] invariant (an LP over
 // the coefficients, tools/proto/sign_schedule.py), 18 steps + 6 Newton-Schulz
 // = 67 products. X0 = A / c with c = min(||A||_F, ||A||_inf) (both bound the
-// spectral radius; frob_finalize_kernel): scalar-map error
+// spectral radius; prep_kernel tail): scalar-map error
 // max_mu mu |1 - s(mu)| / 2 = 6.1e-13 of c <= 6.1e-13 ||A||_F (the slack
 // blocks have c ~ ||A||_F / 5 at n = 1024, so ~1e-13 of ||A||_F there).
 // Digit bounds: |X| <= 1.3, |U| <= 1.26, |Z'| <= 3.73, |V| <= 1.5.

@@ -187,6 +187,38 @@ __device__ inline void block_sum2(double& a, double& b, double* scratch) {
     b = y;
 }
 
+// One-barrier variants for the Lanczos step: the same reduction trees as
+// block_sum / block_sum2 (bitwise the same results), with the leading and
+// trailing barriers dropped. The caller alternates scratch buffers so that a
+// buffer is rewritten only after a barrier that follows its last read.
+__device__ inline double allreduce1(double v, double* scratch) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nw = (blockDim.x + 31) >> 5;
+    v = warp_sum(v);
+    if (lane == 0) scratch[wid] = v;
+    __syncthreads();
+    return warp_sum(lane < nw ? scratch[lane] : 0.0);
+}
+
+__device__ inline void allreduce2(double& a, double& b, double* scratch) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nw = (blockDim.x + 31) >> 5;
+    a = warp_sum(a);
+    b = warp_sum(b);
+    if (lane == 0) {
+        scratch[wid] = a;
+        scratch[32 + wid] = b;
+    }
+    __syncthreads();
+    double x = 0.0, y = 0.0;
+    for (int k = 0; k < nw; ++k) {
+        x += scratch[k];
+        y += scratch[32 + k];
+    }
+    a = x;
+    b = y;
+}
+
 // w <- w - sum_{j<=k} (Q_j . w) Q_j, twice (CGS2); cf[j] receives the first
 // pass coefficients (cf[k] = alpha when q_k is the current Lanczos vector).
 __device__ inline void cgs2(const double* Q, int n, int ldq, int k, double* w, double* cf,
@@ -605,6 +637,7 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
     int* cur = colptr + (n + 1);          // n
     double* Q = a.basis + (long long)b * a.kmax * n;
     __shared__ double scratch[64];
+    __shared__ double red1[32], red2[64];  // Lanczos step reductions (alternating with each other)
     __shared__ int iscr[32];
     __shared__ int s_flag;  // bit0 stop, bit1 converged
     __shared__ double s_th[2];
@@ -665,6 +698,14 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
         double beta_prev = 0.0;
         double c_min = 0.0, c_max = 0.0;
         bool broke = false;
+        // residual tests: the first after min_steps (rounded up to a multiple
+        // of check_every), then where the residual's decay rate since the
+        // previous test predicts convergence (at least 8, at most
+        // check_every steps ahead); identical in every thread
+        const int every = a.check_every > 0 ? a.check_every : 16;
+        int next_check = ((max(a.min_steps - steps, 1) + every - 1) / every) * every;
+        int prev_k = 0;
+        double prev_r = 0.0;
         __syncthreads();
         for (int k = 0; k < kcap; ++k) {
             // w = L q - beta_{k-1} q_{k-1} (gather, ascending edge order); alpha = q.w
@@ -672,11 +713,27 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
             if (dense) {
                 // warp per node over the node-major incidence (coalesced), fixed
                 // lane/tree order: deterministic
+                // The first 8 entries of each lane are loaded before any is
+                // used (same summation order): the L2 latency of the
+                // incidence overlaps instead of serialising per entry.
                 const int lane = tid & 31, nw = nthr >> 5;
+                constexpr int NB = 8;
                 for (int v = wid; v < n; v += nw) {
                     const double qv = q[v];
+                    const int p0 = nptr[v] + lane, p1 = nptr[v + 1];
+                    double wb[NB];
+                    int jb[NB];
+#pragma unroll
+                    for (int u = 0; u < NB; ++u) {
+                        const int p = p0 + 32 * u;
+                        wb[u] = p < p1 ? nwt[p] : 0.0;  // written above in this kernel: no __ldg
+                        jb[u] = p < p1 ? nbr[p] : v;
+                    }
                     double acc = 0.0;
-                    for (int p = nptr[v] + lane; p < nptr[v + 1]; p += 32) acc += nwt[p] * (qv - q[nbr[p]]);
+#pragma unroll
+                    for (int u = 0; u < NB; ++u)
+                        if (p0 + 32 * u < p1) acc += wb[u] * (qv - q[jb[u]]);
+                    for (int p = p0 + 32 * NB; p < p1; p += 32) acc += nwt[p] * (qv - q[nbr[p]]);
                     acc = warp_sum(acc);
                     if (lane == 0) {
                         Q[(long long)k * n + v] = qv;
@@ -686,32 +743,64 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
                     }
                 }
             } else if (snm) {
-                for (int v = tid; v < n; v += nthr) {
-                    const double qv = q[v];
-                    Q[(long long)k * n + v] = qv;
-                    double acc = 0.0;
-                    for (int p = nptr[v]; p < nptr[v + 1]; ++p) acc += nwt[p] * (qv - q[nbr[p]]);
-                    acc -= beta_prev * qp[v];
-                    w[v] = acc;
-                    pa += qv * acc;
+                // eight lanes per node over its incidence (consecutive
+                // entries: no shared-memory bank conflicts; a thread per
+                // node strode the node-major arrays by the degree), fixed
+                // lane/tree order: deterministic
+                constexpr int SG = 8;
+                const int sub = tid / SG, sl = tid % SG, nsub = nthr / SG;
+                for (int v0 = 0; v0 < n; v0 += nsub) {
+                    const int v = v0 + sub;
+                    double acc = 0.0, qv = 0.0;
+                    if (v < n) {
+                        qv = q[v];
+                        for (int p = nptr[v] + sl; p < nptr[v + 1]; p += SG) acc += nwt[p] * (qv - q[nbr[p]]);
+                    }
+                    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+                    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+                    acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+                    if (sl == 0 && v < n) {
+                        Q[(long long)k * n + v] = qv;
+                        acc -= beta_prev * qp[v];
+                        w[v] = acc;
+                        pa += qv * acc;
+                    }
                 }
             } else {
-                for (int v = tid; v < n; v += nthr) {
-                    const double qv = q[v];
-                    Q[(long long)k * n + v] = qv;
-                    double acc = 0.0;
-                    for (int p = colptr[v]; p < colptr[v + 1]; ++p) {
-                        const int e = __ldg(cidx + p);
-                        acc += __ldg(ew + e) * (qv - q[__ldg(ei + e)]);
+                // the same eight-lane split and entry order as the shared-
+                // memory incidence above (column part, then row part), so a
+                // batch gives the single solve's values bit for bit
+                constexpr int SG = 8;
+                const int sub = tid / SG, sl = tid % SG, nsub = nthr / SG;
+                for (int v0 = 0; v0 < n; v0 += nsub) {
+                    const int v = v0 + sub;
+                    double acc = 0.0, qv = 0.0;
+                    if (v < n) {
+                        qv = q[v];
+                        const int c0 = colptr[v], nc = colptr[v + 1] - c0, r0 = rowptr[v];
+                        const int deg = nc + rowptr[v + 1] - r0;
+                        for (int t = sl; t < deg; t += SG) {
+                            if (t < nc) {
+                                const int e = cidx[c0 + t];
+                                acc += ew[e] * (qv - q[ei[e]]);
+                            } else {
+                                const int e = r0 + t - nc;
+                                acc += ew[e] * (qv - q[ej[e]]);
+                            }
+                        }
                     }
-                    for (int e = rowptr[v]; e < rowptr[v + 1]; ++e)
-                        acc += __ldg(ew + e) * (qv - q[__ldg(ej + e)]);
-                    acc -= beta_prev * qp[v];
-                    w[v] = acc;
-                    pa += qv * acc;
+                    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+                    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+                    acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+                    if (sl == 0 && v < n) {
+                        Q[(long long)k * n + v] = qv;
+                        acc -= beta_prev * qp[v];
+                        w[v] = acc;
+                        pa += qv * acc;
+                    }
                 }
             }
-            const double alpha = block_sum(pa, scratch);
+            const double alpha = allreduce1(pa, red1);
             double s = 0.0, s2 = 0.0;
             for (int v = tid; v < n; v += nthr) {
                 const double x = w[v] - alpha * q[v];
@@ -719,7 +808,7 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
                 s += x;
                 s2 += x * x;
             }
-            block_sum2(s, s2, scratch);
+            allreduce2(s, s2, red2);
             const double mean = s / n;
             const double beta = sqrt(fmax(s2 - n * mean * mean, 0.0));
             if (tid == 0) {
@@ -732,8 +821,7 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
             // residual tests (two Sturm multisections + two inverse iterations
             // on T_k, ~100 us at k = 256) only every check_every steps: a
             // matvec costs ~1 us, a test up to 100x more
-            const int every = a.check_every > 0 ? a.check_every : 16;
-            const bool want_check = breakdown || kk == kcap || (steps >= a.min_steps && kk % every == 0);
+            const bool want_check = breakdown || kk == kcap || kk >= next_check;
 #ifdef OZ_STAMPS
             const long long tck = clock64();
 #endif
@@ -758,6 +846,18 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
                 __syncthreads();
                 c_min = s_th[0];
                 c_max = s_th[1];
+                {
+                    const double r = fmax(s_res[0], s_res[1]) / fmax(fabs(s_th[1]), 1e-300);
+                    int ahead = every;
+                    if (prev_k > 0 && r < prev_r && r > 0.0) {
+                        const double rate = log(r / prev_r) / (kk - prev_k);  // < 0
+                        const double need = log(a.tol / r) / rate;
+                        ahead = (int)fmin((double)every, fmax(8.0, ceil(1.1 * need)));
+                    }
+                    prev_k = kk;
+                    prev_r = r;
+                    next_check = kk + ahead;
+                }
                 SLEM_CLK(a.out ? 5 : 4, tck);
                 if (s_flag & 1) {
                     converged = (s_flag >> 1) & 1;
@@ -821,6 +921,15 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
 size_t slem_trace_smem_bytes(int n, int kmax) {
     const int kcap = std::max(2, std::min(kmax, n - 1));
     return (3 * (size_t)n + 8 * (size_t)kcap) * sizeof(double) + (3 * (size_t)n + 3) * sizeof(int);
+}
+
+int slem_oneoff_kmax(int n) {
+    int dev = 0, optin = 0;
+    TPB_CUDA(cudaGetDevice(&dev));
+    TPB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    int k = std::max(2, std::min(n - 1, kOneOffKrylov));
+    while (k > 64 && slem_trace_smem_bytes(n, k) + 2048 > (size_t)optin) k -= 64;
+    return k;
 }
 
 void launch_slem(const SlemArgs& a, int B, cudaStream_t st) {

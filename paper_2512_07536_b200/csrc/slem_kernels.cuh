@@ -49,6 +49,12 @@ struct SlemArgs {
 // (exact, no iteration); larger n: Lanczos (exact or restarted, see SlemArgs).
 constexpr int kSmallDense = 128;
 void launch_slem(const SlemArgs& a, int B, cudaStream_t st);
+// Krylov dimension of a one-off plain-Lanczos report at n > kFinalExactDim:
+// up to kOneOffKrylov steps in one cycle (no restart in the usual case: a
+// restart from two Ritz vectors discards the recurrence), capped so the
+// trace kernel's shared memory fits.
+constexpr int kOneOffKrylov = 1024;
+int slem_oneoff_kmax(int n);
 // dynamic shared memory of launch_slem (basis_in_smem: a.basis == null)
 size_t slem_smem_bytes(int n, int kmax, bool basis_in_smem);
 

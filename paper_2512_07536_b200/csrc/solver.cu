@@ -277,11 +277,19 @@ void Solver::alloc() {
         d_.cg_rr = dalloc<double>(s0_, allocs_, (size_t)B * 2 * d_.ntile);
         d_.cg_nr = dalloc<double>(s0_, allocs_, (size_t)B * d_.nb * n);
         d_.cg_u = dalloc<double>(s0_, allocs_, (size_t)B * 2 * n);
+        d_.cg_grid = cg_launch_grid(d_);
     }
     d_.PU = dalloc<double>(s0_, allocs_,(size_t)B * d_.nb * n);
     d_.PZ = dalloc<double>(s0_, allocs_,(size_t)B * d_.nb * n);
     d_.PG = dalloc<double>(s0_, allocs_,(size_t)B * d_.nb * n);
     d_.node = dalloc<double>(s0_, allocs_,(size_t)B * 4 * n);
+    d_.tile_aux = dalloc<double>(s0_, allocs_, (size_t)B * d_.ntile * 2);
+    d_.blk = dalloc<double>(s0_, allocs_, (size_t)B * d_.nb * 4);
+    d_.res_node = dalloc<double>(s0_, allocs_, (size_t)B * n);
+    d_.blk_inf = dalloc<double>(s0_, allocs_, (size_t)B * 2 * d_.nb);
+    d_.cnt_stride = 2 * d_.nb + 2;
+    d_.cnt = dalloc<int>(s0_, allocs_, (size_t)B * d_.cnt_stride);
+    TPB_CUDA(cudaMemsetAsync(d_.cnt, 0, (size_t)B * d_.cnt_stride * sizeof(int), s0_));
     d_.res_part = dalloc<double>(s0_, allocs_,(size_t)B * d_.ntile);
     d_.scal = dalloc<double>(s0_, allocs_,(size_t)B * 8);
     d_.ictl = dalloc<int>(s0_, allocs_,(size_t)B * 8);
@@ -346,8 +354,10 @@ void Solver::alloc() {
     basis_ = dalloc<double>(s0_, allocs_,(size_t)B * trace_kmax_ * n);
     ritz_ = dalloc<double>(s0_, allocs_,(size_t)B * 2 * n);
     ritz_ok_ = dalloc<int>(s0_, allocs_,B);
-    const int kfin = n - 1 <= kFinalExactDim ? std::max(1, n - 1) : 1;
-    basis_final_ = dalloc<double>(s0_, allocs_,(size_t)B * kfin * n);
+    // one-off reports: complete space up to kFinalExactDim, else one long
+    // plain-Lanczos cycle
+    kfin_ = n - 1 <= kFinalExactDim ? std::max(1, n - 1) : slem_oneoff_kmax(n);
+    basis_final_ = dalloc<double>(s0_, allocs_, (size_t)B * kfin_ * n);
     slem_out_ = dalloc<double>(s0_, allocs_,(size_t)B * 8);
     tmp_m_ = dalloc<double>(s0_, allocs_,(size_t)B * m);
     tmp_m2_ = dalloc<double>(s0_, allocs_,(size_t)B * m);
@@ -420,12 +430,12 @@ void Solver::final_slem(const double* packed, const int* list, const int* count,
     a.col_idx = col_idx_;
     // exact (complete Krylov space, CGS2) up to n = 257; beyond, the plain
     // Lanczos recurrence of the trace kernel at residual tolerance 1e-10
-    // (eigenvalue error <= 1e-20 / gap), reusing the trace basis buffer
+    // (eigenvalue error <= 1e-20 / gap) in one cycle of up to kfin_ steps
     const int n = lo_.n;
     const bool exact = n - 1 <= kFinalExactDim;
     a.plain = exact ? 0 : 1;
-    a.basis = a.plain ? basis_ : basis_final_;
-    a.kmax = exact ? std::max(1, n - 1) : (a.plain ? trace_kmax_ : kFinalKrylov);
+    a.basis = basis_final_;
+    a.kmax = kfin_;
     // the final topology is the last trace iterate's neighbour: start from
     // the trace's extreme Ritz vectors (tolerance unchanged)
     if (a.plain) {
@@ -434,7 +444,7 @@ void Solver::final_slem(const double* packed, const int* list, const int* count,
     }
     a.max_restarts = 200;
     a.min_steps = 64;
-    a.check_every = 64;
+    a.check_every = 128;
     a.tol = 1e-10;
     a.out = out;
     a.tr_acf = nullptr;
@@ -580,7 +590,6 @@ void Solver::set_shard(void* comm, int nranks, int rank) {
 // waits for it. Stream capture and eager chunks end with join_slem().
 void Solver::enqueue_iteration(bool with_slem, int parity) {
     launch_prep(d_, c_, s0_);
-    if (!small_) launch_frob_finalize(d_, s0_);
     TPB_CUDA(cudaEventRecord(ev_fork_, s0_));
     TPB_CUDA(cudaStreamWaitEvent(s1_, ev_fork_, 0));
     if (slem_pending_[parity]) TPB_CUDA(cudaStreamWaitEvent(s1_, ev_slem_p_[parity], 0));
@@ -598,7 +607,6 @@ void Solver::enqueue_iteration(bool with_slem, int parity) {
     enqueue_projection();
     TPB_CUDA(cudaStreamWaitEvent(s0_, ev_sel_, 0));
     enqueue_xstep(d_);
-    launch_xstep_diag(d_, c_, s0_);
     launch_best_copy(d_, c_, s0_);
 }
 
@@ -610,7 +618,6 @@ void Solver::join_slem(cudaStream_t st) {
 
 void Solver::enqueue_xstep(const Dev& d) {
     launch_xstep_a(d, c_, s0_);
-    launch_xstep_node(d, c_, s0_);
     if (d.cg) launch_xstep_cg(d, c_, s0_);
     launch_xstep_b(d, c_, s0_);
 }
@@ -688,6 +695,10 @@ void Solver::iterate_async(int k) {
 bool Solver::all_done() {
     TPB_CUDA(cudaMemcpyAsync(h_ctl_, d_.ictl, (size_t)B_ * 8 * sizeof(int), cudaMemcpyDeviceToHost, s0_));
     TPB_CUDA(cudaStreamSynchronize(s0_));
+    for (int b = 0; b < B_; ++b)
+        if (d_.cg && h_ctl_[b * 8 + kCgFail])
+            throw Error(kLinearSolve, "update_X: CG relative residual above 1e-8 (solve " + std::to_string(b) +
+                                          "; raise cg_max_iter)");
     for (int b = 0; b < B_; ++b)
         if (!h_ctl_[b * 8 + kDone]) return false;
     return true;
@@ -946,7 +957,6 @@ void Solver::download(double* X, double* Y, double* D) {
 void Solver::project_only() {
     TPB_CUDA(cudaMemsetAsync(d_.ictl, 0, (size_t)B_ * 8 * sizeof(int), s0_));
     launch_prep(d_, c_, s0_);
-    if (!small_) launch_frob_finalize(d_, s0_);
     enqueue_select(s0_);
     enqueue_projection();
     TPB_CUDA(cudaStreamSynchronize(s0_));
@@ -958,7 +968,6 @@ void Solver::xstep_only(bool update_duals) {
     d.upd_duals = update_duals ? 1 : 0;
     d.track_best = 0;
     enqueue_xstep(d);
-    launch_xstep_diag(d, c_, s0_);
     TPB_CUDA(cudaStreamSynchronize(s0_));
     // keep the CG statistics for cg_stats(); clear the iteration control words
     std::vector<int> keep(B_ * 8, 0);
@@ -972,7 +981,7 @@ void Solver::xstep_only(bool update_duals) {
 
 int Solver::launches_per_iteration() const {
     const int cone = small_ ? 1 : sch_.gemms();
-    return 1 + (small_ ? 0 : 1) + 1 + 1 + cone + 4 + 2 + (d_.cg ? 1 : 0);
+    return 1 + 1 + 1 + cone + 2 + 2 + (d_.cg ? 1 : 0);
 }
 
 int Solver::bench_phase(int phase, int reps) {
@@ -984,14 +993,13 @@ int Solver::bench_phase(int phase, int reps) {
                 per = small_ ? 1 : sch_.gemms();
                 break;
             case 1: {
-                // as in the iteration (dual update on); the diag pass without
-                // the O(n) dual update so the iteration counter is untouched
+                // as in the iteration (dual update on), without the iteration
+                // counter, trace row and stop flags
                 Dev d = d_;
                 d.track_best = 0;
+                d.bookkeep = 0;
                 enqueue_xstep(d);
-                d.upd_duals = 0;
-                launch_xstep_diag(d, c_, s0_);
-                per = 4 + (d.cg ? 1 : 0);
+                per = 2 + (d.cg ? 1 : 0);
                 break;
             }
             case 7: {
@@ -1010,6 +1018,7 @@ int Solver::bench_phase(int phase, int reps) {
             case 6: {
                 Dev d = d_;                   // pass B alone (dual update on)
                 d.track_best = 0;
+                d.bookkeep = 0;
                 launch_xstep_b(d, c_, s0_);
                 per = 1;
                 break;

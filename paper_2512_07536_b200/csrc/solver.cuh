@@ -43,7 +43,6 @@ void phase_mark(const char* what);
 // One-off spectral reports (feasible start, final topology): complete Krylov
 // space up to this dimension, restarted Lanczos with this basis beyond.
 constexpr int kFinalExactDim = 256;
-constexpr int kFinalKrylov = 128;
 // single homogeneous solves with at least this many candidate edges select
 // top-r over the whole GPU (select_kernels.cu::topr_grid_kernel)
 constexpr long long kTopRGridMin = 65536;
@@ -169,6 +168,7 @@ class Solver {
     double* e_w_ = nullptr;
     double* basis_ = nullptr;        // trace Lanczos basis (B x kmax x n)
     int trace_kmax_ = 0;
+    int kfin_ = 1;  // Krylov dimension of the one-off reports
     double* ritz_ = nullptr;         // B x 2n extreme Ritz vectors (warm start)
     int* ritz_ok_ = nullptr;
     int* slem_nbr_ = nullptr;        // het trace SLEM: node-major incidence scratch

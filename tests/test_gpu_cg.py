@@ -132,3 +132,11 @@ def test_cg_batched_global_equals_single_register(T, n, r, B):
             assert np.array_equal(got.weights, one.weights)
     finally:
         bs.close()
+
+
+def test_solve_raises_linear_solve_error_like_the_reference(T):
+    """update_X throws LinearSolveError when the linear solve misses 1e-8
+    relative (proj/src/admm.cpp:287); solve() propagates it. One CG
+    iteration per x-step cannot reach it on a generic iterate."""
+    with pytest.raises(T.LinearSolveError):
+        T.solve(16, 32, linear_solver=1, cg_max_iter=1, max_iter=50)
