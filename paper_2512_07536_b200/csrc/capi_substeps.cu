@@ -216,6 +216,7 @@ void slem_edges(int n, const std::vector<int>& packed, const std::vector<double>
     a.basis = basis.p;
     a.kmax = kfin;
     a.plain = exact ? 0 : 1;  // as the solver's one-off reports (Solver::final_slem)
+    a.cluster = kOneOffCluster;
     a.max_restarts = 200;
     a.min_steps = 64;
     a.check_every = 128;

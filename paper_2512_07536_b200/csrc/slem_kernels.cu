@@ -17,9 +17,13 @@
 //  * Extreme Ritz values by warp multisection on Sturm counts; convergence by
 //    the residual bound beta_k |s_k| (s from inverse iteration on T_k).
 #include "slem_kernels.cuh"
+
+#include <cooperative_groups.h>
 #include "csr.cuh"
 
 namespace tpb {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -608,11 +612,18 @@ __global__ void __launch_bounds__(256) slem_small_kernel(SlemArgs a) {
 constexpr int kTraceThreads = 1024;
 
 __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
-    const int b = blockIdx.x;
+    // a cluster of C CTAs per solve (one-off reports of one large solve) or
+    // one CTA (C = 1): CTA `rank` owns nodes [v_lo, v_hi) of every
+    // node-indexed pass; q is kept whole in every CTA, and each step's new
+    // slice is pushed to the others through distributed shared memory
+    cg::cluster_group cl = cg::this_cluster();
+    const int C = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+    const int b = blockIdx.x / C;
     const int it_rec = slem_iter(a, b);
-    if (it_rec < 0) return;  // solve already finished
+    if (it_rec < 0) return;  // solve already finished (uniform over the cluster)
     const int n = a.n;
     const int tid = threadIdx.x, nthr = blockDim.x, wid = tid >> 5;
+    const int per = (n + C - 1) / C, v_lo = min(n, rank * per), v_hi = min(n, v_lo + per);
     const int ne = min(a.count[b], a.list_cap);
     const int* list = a.list + (long long)b * a.list_cap;
     const double* g = a.gw ? a.gw + (long long)b * a.list_cap : a.g + (long long)b * a.stride;
@@ -642,8 +653,43 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
     __shared__ int s_flag;  // bit0 stop, bit1 converged
     __shared__ double s_th[2];
     __shared__ double s_res[2];
+    __shared__ double xch[2][16][2];  // cluster partials (two alternating buffers)
+    auto csync = [&] {
+        if (C > 1)
+            cl.sync();
+        else
+            __syncthreads();
+    };
+    // cluster-wide sum of a CTA value pair (CTA partials in rank order)
+    auto cluster_sum2 = [&](double& x, double& y, int buf) {
+        if (C == 1) return;
+        if (tid == 0)
+            for (int r = 0; r < C; ++r) {
+                double* dst = cl.map_shared_rank(&xch[buf][rank][0], r);
+                dst[0] = x;
+                dst[1] = y;
+            }
+        cl.sync();
+        double sx = 0.0, sy = 0.0;
+        for (int r = 0; r < C; ++r) {
+            sx += xch[buf][r][0];
+            sy += xch[buf][r][1];
+        }
+        x = sx;
+        y = sy;
+    };
 
-    build_csr(n, ne, list, g, a.gw != nullptr, ei, ej, ew, rowptr, colptr, cur, cidx, iscr);
+    // the incidence: built once (CTA 0 writes the global edge arrays), the
+    // cluster's other CTAs take rowptr / colptr from CTA 0's shared memory
+    if (rank == 0) build_csr(n, ne, list, g, a.gw != nullptr, ei, ej, ew, rowptr, colptr, cur, cidx, iscr);
+    if (C > 1) {
+        cl.sync();
+        if (rank != 0) {
+            const int* r0 = cl.map_shared_rank(rowptr, 0);
+            for (int v = tid; v < 2 * (n + 1); v += nthr) rowptr[v] = r0[v];  // rowptr, colptr adjacent
+        }
+        cl.sync();
+    }
     // dense supports (het trace: every positive g): node-major incidence
     // (column part then row part, i.e. ascending edge order) for a warp-per-
     // node SpMV with coalesced loads
@@ -694,7 +740,7 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
     int steps = 0, converged = 0, kk = 0;
     for (int cycle = 0; cycle <= a.max_restarts; ++cycle) {
         if (tid == 0) s_flag = 0;
-        for (int v = tid; v < n; v += nthr) qp[v] = 0.0;
+        for (int v = v_lo + tid; v < v_hi; v += nthr) qp[v] = 0.0;
         double beta_prev = 0.0;
         double c_min = 0.0, c_max = 0.0;
         bool broke = false;
@@ -718,7 +764,7 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
                 // incidence overlaps instead of serialising per entry.
                 const int lane = tid & 31, nw = nthr >> 5;
                 constexpr int NB = 8;
-                for (int v = wid; v < n; v += nw) {
+                for (int v = v_lo + wid; v < v_hi; v += nw) {
                     const double qv = q[v];
                     const int p0 = nptr[v] + lane, p1 = nptr[v + 1];
                     double wb[NB];
@@ -749,17 +795,17 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
                 // lane/tree order: deterministic
                 constexpr int SG = 8;
                 const int sub = tid / SG, sl = tid % SG, nsub = nthr / SG;
-                for (int v0 = 0; v0 < n; v0 += nsub) {
+                for (int v0 = v_lo; v0 < v_hi; v0 += nsub) {
                     const int v = v0 + sub;
                     double acc = 0.0, qv = 0.0;
-                    if (v < n) {
+                    if (v < v_hi) {
                         qv = q[v];
                         for (int p = nptr[v] + sl; p < nptr[v + 1]; p += SG) acc += nwt[p] * (qv - q[nbr[p]]);
                     }
                     acc += __shfl_xor_sync(0xffffffffu, acc, 1);
                     acc += __shfl_xor_sync(0xffffffffu, acc, 2);
                     acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-                    if (sl == 0 && v < n) {
+                    if (sl == 0 && v < v_hi) {
                         Q[(long long)k * n + v] = qv;
                         acc -= beta_prev * qp[v];
                         w[v] = acc;
@@ -772,10 +818,10 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
                 // batch gives the single solve's values bit for bit
                 constexpr int SG = 8;
                 const int sub = tid / SG, sl = tid % SG, nsub = nthr / SG;
-                for (int v0 = 0; v0 < n; v0 += nsub) {
+                for (int v0 = v_lo; v0 < v_hi; v0 += nsub) {
                     const int v = v0 + sub;
                     double acc = 0.0, qv = 0.0;
-                    if (v < n) {
+                    if (v < v_hi) {
                         qv = q[v];
                         const int c0 = colptr[v], nc = colptr[v + 1] - c0, r0 = rowptr[v];
                         const int deg = nc + rowptr[v + 1] - r0;
@@ -792,7 +838,7 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
                     acc += __shfl_xor_sync(0xffffffffu, acc, 1);
                     acc += __shfl_xor_sync(0xffffffffu, acc, 2);
                     acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-                    if (sl == 0 && v < n) {
+                    if (sl == 0 && v < v_hi) {
                         Q[(long long)k * n + v] = qv;
                         acc -= beta_prev * qp[v];
                         w[v] = acc;
@@ -800,15 +846,20 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
                     }
                 }
             }
-            const double alpha = allreduce1(pa, red1);
+            double alpha = allreduce1(pa, red1);
+            {
+                double dummy = 0.0;
+                cluster_sum2(alpha, dummy, 0);
+            }
             double s = 0.0, s2 = 0.0;
-            for (int v = tid; v < n; v += nthr) {
+            for (int v = v_lo + tid; v < v_hi; v += nthr) {
                 const double x = w[v] - alpha * q[v];
                 w[v] = x;
                 s += x;
                 s2 += x * x;
             }
             allreduce2(s, s2, red2);
+            cluster_sum2(s, s2, 1);
             const double mean = s / n;
             const double beta = sqrt(fmax(s2 - n * mean * mean, 0.0));
             if (tid == 0) {
@@ -866,17 +917,21 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
                 }
             }
             const double inv = beta > 0.0 ? 1.0 / beta : 0.0;
-            for (int v = tid; v < n; v += nthr) {
+            for (int v = v_lo + tid; v < v_hi; v += nthr) {
                 qp[v] = q[v];
-                q[v] = (w[v] - mean) * inv;
+                const double qn = (w[v] - mean) * inv;
+                q[v] = qn;
+                for (int r = 0; r < C; ++r)
+                    if (r != rank) *cl.map_shared_rank(q + v, r) = qn;
             }
             beta_prev = beta;
-            __syncthreads();
+            csync();
         }
         th_min = fmin(th_min, c_min);
         th_max = fmax(th_max, c_max);
-        // Ritz vectors y = Q s of both extremes (restart vector / next warm start)
-        for (int v = tid; v < n; v += nthr) {
+        // Ritz vectors y = Q s of both extremes (restart vector / next warm
+        // start), this CTA's nodes
+        for (int v = v_lo + tid; v < v_hi; v += nthr) {
             double y1 = 0.0, y2 = 0.0;
             for (int j = 0; j < kk; ++j) {
                 const double qj = Q[(long long)j * n + v];
@@ -888,18 +943,24 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
         }
         __syncthreads();
         if (rz && !broke) {
-            for (int v = tid; v < n; v += nthr) {
+            for (int v = v_lo + tid; v < v_hi; v += nthr) {
                 rz[v] = w[v];
                 rz[n + v] = q[v];
             }
         }
         if (converged) break;
-        // restart from the Ritz pair (a fresh random direction after a breakdown)
-        for (int v = tid; v < n; v += nthr) q[v] = broke ? hash_unit(v * 7 + 13 * cycle + 1) : q[v] + w[v];
-        __syncthreads();
+        // restart from the Ritz pair (a fresh random direction after a
+        // breakdown); the whole vector in every CTA of the cluster
+        for (int v = v_lo + tid; v < v_hi; v += nthr) {
+            const double qn = broke ? hash_unit(v * 7 + 13 * cycle + 1) : q[v] + w[v];
+            q[v] = qn;
+            for (int r = 0; r < C; ++r)
+                if (r != rank) *cl.map_shared_rank(q + v, r) = qn;
+        }
+        csync();
         deflate_normalize(q, n, scratch);
     }
-    if (tid == 0) {
+    if (tid == 0 && rank == 0) {
         if (a.ritz_ok) a.ritz_ok[b] = 1;
         const double l2 = 1.0 - th_min, ln = 1.0 - th_max;
         const double acf = fmax(fabs(l2), fabs(ln));
@@ -962,8 +1023,25 @@ void launch_slem(const SlemArgs& a, int B, cudaStream_t st) {
             b.smem_nm = (int)nm;
             smem += extra;
         }
-        slem_trace_kernel<<<B, threads, smem, st>>>(b);
-        TPB_CHECK_LAUNCH();
+        const int C = std::max(1, std::min(a.cluster, 8));
+        if (C == 1) {
+            slem_trace_kernel<<<B, threads, smem, st>>>(b);
+            TPB_CHECK_LAUNCH();
+            return;
+        }
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(B * C);
+        cfg.blockDim = dim3(threads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = C;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        TPB_CUDA(cudaLaunchKernelEx(&cfg, slem_trace_kernel, b));
         return;
     }
     const size_t smem = slem_smem_bytes(n, a.kmax, a.basis == nullptr);

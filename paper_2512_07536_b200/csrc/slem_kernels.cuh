@@ -43,6 +43,7 @@ struct SlemArgs {
     int* nbr;              // plain mode, dense supports: node-major incidence scratch (2 list_cap per solve)
     double* nwt;
     int smem_nm;           // plain mode: entries of a node-major incidence kept in shared memory (set by launch_slem)
+    int cluster;           // plain mode: CTAs per solve (a thread-block cluster; 0/1: one CTA)
 };
 
 // n <= kSmallDense: dense Householder tridiagonalisation in shared memory
@@ -54,6 +55,9 @@ void launch_slem(const SlemArgs& a, int B, cudaStream_t st);
 // restart from two Ritz vectors discards the recurrence), capped so the
 // trace kernel's shared memory fits.
 constexpr int kOneOffKrylov = 1024;
+// CTAs of the thread-block cluster that runs a one-off report of one solve
+// (slem_trace_kernel: node slices per CTA, q exchanged through DSMEM)
+constexpr int kOneOffCluster = 8;
 int slem_oneoff_kmax(int n);
 // dynamic shared memory of launch_slem (basis_in_smem: a.basis == null)
 size_t slem_smem_bytes(int n, int kmax, bool basis_in_smem);

@@ -436,6 +436,10 @@ void Solver::final_slem(const double* packed, const int* list, const int* count,
     a.plain = exact ? 0 : 1;
     a.basis = basis_final_;
     a.kmax = kfin_;
+    // the report's Lanczos spread over a cluster of CTAs per solve (node
+    // slices, q shared through distributed shared memory); for every batch
+    // size, so a batch reproduces the single solve bit for bit
+    a.cluster = kOneOffCluster;
     // the final topology is the last trace iterate's neighbour: start from
     // the trace's extreme Ritz vectors (tolerance unchanged)
     if (a.plain) {
