@@ -191,8 +191,8 @@ __device__ inline void block_sum2(double& a, double& b, double* scratch) {
     b = y;
 }
 
-// One-barrier variants for the Lanczos step: the same reduction trees as
-// block_sum / block_sum2 (bitwise the same results), with the leading and
+// One-barrier reductions for the Lanczos step (block_sum's trees: warp
+// sums, then every warp reduces the warp partials), with the leading and
 // trailing barriers dropped. The caller alternates scratch buffers so that a
 // buffer is rewritten only after a barrier that follows its last read.
 __device__ inline double allreduce1(double v, double* scratch) {
@@ -214,13 +214,8 @@ __device__ inline void allreduce2(double& a, double& b, double* scratch) {
         scratch[32 + wid] = b;
     }
     __syncthreads();
-    double x = 0.0, y = 0.0;
-    for (int k = 0; k < nw; ++k) {
-        x += scratch[k];
-        y += scratch[32 + k];
-    }
-    a = x;
-    b = y;
+    a = warp_sum(lane < nw ? scratch[lane] : 0.0);
+    b = warp_sum(lane < nw ? scratch[32 + lane] : 0.0);
 }
 
 // w <- w - sum_{j<=k} (Q_j . w) Q_j, twice (CGS2); cf[j] receives the first
@@ -851,15 +846,21 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
                 double dummy = 0.0;
                 cluster_sum2(alpha, dummy, 0);
             }
+            // x = w - alpha q on this CTA's nodes, pushed with the partial sums
+            // to the other CTAs: one cluster barrier, then every CTA forms the
+            // whole next q itself
             double s = 0.0, s2 = 0.0;
             for (int v = v_lo + tid; v < v_hi; v += nthr) {
                 const double x = w[v] - alpha * q[v];
                 w[v] = x;
+                qp[v] = q[v];
+                for (int r = 0; r < C; ++r)
+                    if (r != rank) *cl.map_shared_rank(w + v, r) = x;
                 s += x;
                 s2 += x * x;
             }
             allreduce2(s, s2, red2);
-            cluster_sum2(s, s2, 1);
+            cluster_sum2(s, s2, 1);  // (C = 1: allreduce2's barrier orders w)
             const double mean = s / n;
             const double beta = sqrt(fmax(s2 - n * mean * mean, 0.0));
             if (tid == 0) {
@@ -917,15 +918,9 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
                 }
             }
             const double inv = beta > 0.0 ? 1.0 / beta : 0.0;
-            for (int v = v_lo + tid; v < v_hi; v += nthr) {
-                qp[v] = q[v];
-                const double qn = (w[v] - mean) * inv;
-                q[v] = qn;
-                for (int r = 0; r < C; ++r)
-                    if (r != rank) *cl.map_shared_rank(q + v, r) = qn;
-            }
+            for (int v = tid; v < n; v += nthr) q[v] = (w[v] - mean) * inv;
             beta_prev = beta;
-            csync();
+            __syncthreads();
         }
         th_min = fmin(th_min, c_min);
         th_max = fmax(th_max, c_max);

@@ -172,18 +172,19 @@ Solver::Solver(int n, int B, bool het, const std::vector<int>& r, const std::vec
     list_cap_ = het ? m : *std::max_element(r_host_.begin(), r_host_.end());
     int chunk = cfg.chunk > 0 ? cfg.chunk : (n <= 64 ? 32 : (n <= 256 ? 16 : 8));
     // a multiple of the trace stride (the SLEM pattern repeats per chunk) and
-    // even (chunks start and end at selection parity 0)
-    const int unit = cfg.trace_stride % 2 ? 2 * cfg.trace_stride : cfg.trace_stride;
+    // a multiple of kSets (chunks start and end at selection set 0)
+    int unit = cfg.trace_stride;
+    while (unit % kSets) unit += cfg.trace_stride;
     chunk_ = ((chunk + unit - 1) / unit) * unit;
     init_attrs();
     phase_mark("solver init_attrs");
     TPB_CUDA(cudaStreamCreateWithFlags(&s0_, cudaStreamNonBlocking));
     TPB_CUDA(cudaStreamCreateWithFlags(&s1_, cudaStreamNonBlocking));
-    TPB_CUDA(cudaStreamCreateWithFlags(&s2_, cudaStreamNonBlocking));
+    for (auto& st : s2_) TPB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     TPB_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     TPB_CUDA(cudaEventCreateWithFlags(&ev_sel_, cudaEventDisableTiming));
     TPB_CUDA(cudaEventCreateWithFlags(&ev_slem_, cudaEventDisableTiming));
-    for (int q = 0; q < 2; ++q) TPB_CUDA(cudaEventCreateWithFlags(&ev_slem_p_[q], cudaEventDisableTiming));
+    for (auto& e : ev_slem_p_) TPB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     phase_mark("solver streams");
     alloc();
     if (het && !cap_) {
@@ -236,7 +237,8 @@ Solver::~Solver() {
         if (e) cudaEventDestroy(e);
     if (s0_) cudaStreamDestroy(s0_);
     if (s1_) cudaStreamDestroy(s1_);
-    if (s2_) cudaStreamDestroy(s2_);
+    for (auto& st : s2_)
+        if (st) cudaStreamDestroy(st);
 }
 
 void Solver::alloc() {
@@ -324,8 +326,10 @@ void Solver::alloc() {
     }
     if (het_ && n > kSmallDense) {
         // node-major incidence of dense het supports for the trace SLEM
-        slem_nbr_ = dalloc<int>(s0_, allocs_, (size_t)B * 2 * list_cap_);
-        slem_nwt_ = dalloc<double>(s0_, allocs_, (size_t)B * 2 * list_cap_);
+        for (int L = 0; L < kLanes; ++L) {
+            slem_nbr_[L] = dalloc<int>(s0_, allocs_, (size_t)B * 2 * list_cap_);
+            slem_nwt_[L] = dalloc<double>(s0_, allocs_, (size_t)B * 2 * list_cap_);
+        }
     }
     if (!het_ && !cap_ && B == 1 && m >= kTopRGridMin) {
         topr_gh_ = dalloc<int>(s0_, allocs_, kTopRGridHist);
@@ -335,25 +339,31 @@ void Solver::alloc() {
     list_count_ = dalloc<int>(s0_, allocs_,B);
     tlist_[0] = list_;
     tcount_[0] = list_count_;
-    tlist_[1] = dalloc<int>(s0_, allocs_, (size_t)B * list_cap_);
-    tcount_[1] = dalloc<int>(s0_, allocs_, B);
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < kSets; ++q) {
+        if (q > 0) {
+            tlist_[q] = dalloc<int>(s0_, allocs_, (size_t)B * list_cap_);
+            tcount_[q] = dalloc<int>(s0_, allocs_, B);
+        }
         tlw_[q] = dalloc<double>(s0_, allocs_, (size_t)B * list_cap_);
         tsnap_[q] = dalloc<int>(s0_, allocs_, B);
     }
-    e_i_ = dalloc<int>(s0_, allocs_,(size_t)B * list_cap_);
-    e_j_ = dalloc<int>(s0_, allocs_,(size_t)B * list_cap_);
-    col_idx_ = dalloc<int>(s0_, allocs_,(size_t)B * list_cap_);
-    e_w_ = dalloc<double>(s0_, allocs_,(size_t)B * list_cap_);
+    for (int L = 0; L < kLanes; ++L) {
+        e_i_[L] = dalloc<int>(s0_, allocs_, (size_t)B * list_cap_);
+        e_j_[L] = dalloc<int>(s0_, allocs_, (size_t)B * list_cap_);
+        col_idx_[L] = dalloc<int>(s0_, allocs_, (size_t)B * list_cap_);
+        e_w_[L] = dalloc<double>(s0_, allocs_, (size_t)B * list_cap_);
+    }
     // trace Lanczos: exact for n <= 97, else restarted and warm-started from
     // the previous Ritz vectors; basis in shared memory when it fits
     // Krylov basis in global memory: a shared-memory basis (~200 KB at n=256)
     // would pin one SLEM CTA per SM and starve the concurrent cone GEMMs.
     // plain trace Lanczos (slem_trace_kernel): longer recurrences, write-only basis
     trace_kmax_ = std::max(1, std::min(n - 1, n > kSmallDense ? 256 : 96));
-    basis_ = dalloc<double>(s0_, allocs_,(size_t)B * trace_kmax_ * n);
-    ritz_ = dalloc<double>(s0_, allocs_,(size_t)B * 2 * n);
-    ritz_ok_ = dalloc<int>(s0_, allocs_,B);
+    for (int L = 0; L < kLanes; ++L) {
+        basis_[L] = dalloc<double>(s0_, allocs_, (size_t)B * trace_kmax_ * n);
+        ritz_[L] = dalloc<double>(s0_, allocs_, (size_t)B * 2 * n);
+        ritz_ok_[L] = dalloc<int>(s0_, allocs_, B);
+    }
     // one-off reports: complete space up to kFinalExactDim, else one long
     // plain-Lanczos cycle
     kfin_ = n - 1 <= kFinalExactDim ? std::max(1, n - 1) : slem_oneoff_kmax(n);
@@ -384,7 +394,7 @@ void Solver::start() {
     TPB_CUDA(cudaMemsetAsync(d_.X, 0, B * nx * sizeof(double), s0_));
     TPB_CUDA(cudaMemsetAsync(d_.D, 0, B * nx * sizeof(double), s0_));
     TPB_CUDA(cudaMemsetAsync(d_.ictl, 0, (size_t)B * 8 * sizeof(int), s0_));
-    TPB_CUDA(cudaMemsetAsync(ritz_ok_, 0, (size_t)B * sizeof(int), s0_));
+    for (auto* r : ritz_ok_) TPB_CUDA(cudaMemsetAsync(r, 0, (size_t)B * sizeof(int), s0_));
     if (het_) TPB_CUDA(cudaMemsetAsync(d_.bestScore, 0, (size_t)B * lo_.m * sizeof(double), s0_));
     {
         std::vector<double> sc((size_t)B * 8, 0.0);
@@ -424,10 +434,10 @@ void Solver::final_slem(const double* packed, const int* list, const int* count,
     a.list = list;
     a.count = count;
     a.list_cap = list_cap_;
-    a.e_i = e_i_;
-    a.e_j = e_j_;
-    a.e_w = e_w_;
-    a.col_idx = col_idx_;
+    a.e_i = e_i_[0];
+    a.e_j = e_j_[0];
+    a.e_w = e_w_[0];
+    a.col_idx = col_idx_[0];
     // exact (complete Krylov space, CGS2) up to n = 257; beyond, the plain
     // Lanczos recurrence of the trace kernel at residual tolerance 1e-10
     // (eigenvalue error <= 1e-20 / gap) in one cycle of up to kfin_ steps
@@ -443,8 +453,8 @@ void Solver::final_slem(const double* packed, const int* list, const int* count,
     // the final topology is the last trace iterate's neighbour: start from
     // the trace's extreme Ritz vectors (tolerance unchanged)
     if (a.plain) {
-        a.ritz = ritz_;
-        a.ritz_ok = ritz_ok_;
+        a.ritz = ritz_[0];
+        a.ritz_ok = ritz_ok_[0];
     }
     a.max_restarts = 200;
     a.min_steps = 64;
@@ -516,26 +526,27 @@ void Solver::enqueue_slem_trace(cudaStream_t st, int parity) {
     a.list = tlist_[parity];
     a.count = tcount_[parity];
     a.list_cap = list_cap_;
-    a.e_i = e_i_;
-    a.e_j = e_j_;
-    a.e_w = e_w_;
-    a.col_idx = col_idx_;
-    a.basis = basis_;  // null: Krylov basis in shared memory
+    const int L = parity % kLanes;
+    a.e_i = e_i_[L];
+    a.e_j = e_j_[L];
+    a.e_w = e_w_[L];
+    a.col_idx = col_idx_[L];
+    a.basis = basis_[L];
     a.kmax = trace_kmax_;
     a.max_restarts = 40;
     a.min_steps = 8;
     a.check_every = 24;
     a.noise = 0.0;
-    a.ritz = ritz_;
-    a.ritz_ok = ritz_ok_;
+    a.ritz = ritz_[L];
+    a.ritz_ok = ritz_ok_[L];
     a.tol = cfg_.slem_tol;
     a.out = nullptr;
     a.tr_acf = d_.tr_acf;
     a.ictl = d_.ictl;
     a.max_iter = cfg_.max_iter;
     a.plain = lo_.n > kSmallDense;
-    a.nbr = slem_nbr_;
-    a.nwt = slem_nwt_;
+    a.nbr = slem_nbr_[L];
+    a.nwt = slem_nwt_[L];
     launch_slem(a, B_, st);
 }
 
@@ -601,12 +612,13 @@ void Solver::enqueue_iteration(bool with_slem, int parity) {
     TPB_CUDA(cudaEventRecord(ev_sel_, s1_));
     slem_pending_[parity] = false;
     if (with_slem) {
-        TPB_CUDA(cudaStreamWaitEvent(s2_, ev_sel_, 0));
-        enqueue_slem_trace(s2_, parity);
-        TPB_CUDA(cudaEventRecord(ev_slem_p_[parity], s2_));
+        const int L = parity % kLanes;
+        TPB_CUDA(cudaStreamWaitEvent(s2_[L], ev_sel_, 0));
+        enqueue_slem_trace(s2_[L], parity);
+        TPB_CUDA(cudaEventRecord(ev_slem_p_[parity], s2_[L]));
         slem_pending_[parity] = true;
-        slem_any_ = true;
-        slem_last_ = parity;
+        slem_any_[L] = true;
+        slem_last_[L] = parity;
     }
     enqueue_projection();
     TPB_CUDA(cudaStreamWaitEvent(s0_, ev_sel_, 0));
@@ -615,9 +627,11 @@ void Solver::enqueue_iteration(bool with_slem, int parity) {
 }
 
 void Solver::join_slem(cudaStream_t st) {
-    if (slem_any_) TPB_CUDA(cudaStreamWaitEvent(st, ev_slem_p_[slem_last_], 0));
-    slem_any_ = false;
-    slem_pending_[0] = slem_pending_[1] = false;
+    for (int L = 0; L < kLanes; ++L) {
+        if (slem_any_[L]) TPB_CUDA(cudaStreamWaitEvent(st, ev_slem_p_[slem_last_[L]], 0));
+        slem_any_[L] = false;
+    }
+    for (auto& p : slem_pending_) p = false;
 }
 
 void Solver::enqueue_xstep(const Dev& d) {
@@ -640,16 +654,16 @@ void Solver::cg_stats(int b, int* iters, double* rel_res) {
 }
 
 void Solver::build_graphs() {
-    // chunk_ is even: a chunk starts and ends at parity 0; single-iteration
-    // graphs exist for both parities
+    // chunk_ is a multiple of kSets: a chunk starts and ends at set 0;
+    // single-iteration graphs exist for every set
     auto capture = [&](int iters, int parity0, bool stride_aligned) {
         cudaGraph_t g;
-        slem_pending_[0] = slem_pending_[1] = false;  // earlier graphs have completed
-        slem_any_ = false;
+        for (auto& p : slem_pending_) p = false;  // earlier graphs have completed
+        for (auto& a : slem_any_) a = false;
         TPB_CUDA(cudaStreamBeginCapture(s0_, cudaStreamCaptureModeThreadLocal));
         for (int j = 0; j < iters; ++j) {
             const bool slem = stride_aligned ? (j % cfg_.trace_stride == 0) : (cfg_.trace_stride == 1);
-            enqueue_iteration(slem, (parity0 + j) & 1);
+            enqueue_iteration(slem, (parity0 + j) % kSets);
         }
         join_slem(s0_);
         TPB_CUDA(cudaStreamEndCapture(s0_, &g));
@@ -659,8 +673,7 @@ void Solver::build_graphs() {
         return ex;
     };
     g_chunk_ = capture(chunk_, 0, true);
-    g_one_[0] = capture(1, 0, false);
-    g_one_[1] = capture(1, 1, false);
+    for (int q = 0; q < kSets; ++q) g_one_[q] = capture(1, q, false);
 }
 
 // Sharded solvers launch their iterations eagerly: the all-gathers' stream
@@ -672,10 +685,10 @@ bool Solver::eager() const { return sharded(); }
 void Solver::iterate_async(int k) {
     if (eager()) {
         while (k > 0) {
-            const int run = (it_enqueued_ % 2 == 0 && k >= chunk_) ? chunk_ : 1;
+            const int run = (it_enqueued_ % kSets == 0 && k >= chunk_) ? chunk_ : 1;
             for (int j = 0; j < run; ++j) {
                 const bool slem = run == chunk_ ? (j % cfg_.trace_stride == 0) : (cfg_.trace_stride == 1);
-                enqueue_iteration(slem, (it_enqueued_ + j) & 1);
+                enqueue_iteration(slem, (it_enqueued_ + j) % kSets);
             }
             join_slem(s0_);
             k -= run;
@@ -684,12 +697,12 @@ void Solver::iterate_async(int k) {
         return;
     }
     while (k > 0) {
-        if (it_enqueued_ % 2 == 0 && k >= chunk_) {
+        if (it_enqueued_ % kSets == 0 && k >= chunk_) {
             TPB_CUDA(cudaGraphLaunch(g_chunk_, s0_));
             k -= chunk_;
             it_enqueued_ += chunk_;
         } else {
-            TPB_CUDA(cudaGraphLaunch(g_one_[it_enqueued_ & 1], s0_));
+            TPB_CUDA(cudaGraphLaunch(g_one_[it_enqueued_ % kSets], s0_));
             --k;
             ++it_enqueued_;
         }
@@ -762,16 +775,16 @@ void Solver::epilogue_hom() {
     a.done = nullptr;
     launch_topr(a, B_, s0_);
     TPB_CUDA(cudaMemsetAsync(tmp_m_, 0, (size_t)B_ * m * sizeof(double), s0_));
-    launch_extract(lo_.n, m, tmp_m2_, m, list_, list_count_, list_cap_, e_i_, e_j_, e_w_, tmp_m_, worst_,
-                   col_idx_, B_, s0_);
+    launch_extract(lo_.n, m, tmp_m2_, m, list_, list_count_, list_cap_, e_i_[0], e_j_[0], e_w_[0], tmp_m_, worst_,
+                   col_idx_[0], B_, s0_);
     std::vector<int> counts(B_);
     TPB_CUDA(cudaMemcpyAsync(counts.data(), list_count_, B_ * sizeof(int), cudaMemcpyDeviceToHost, s0_));
     TPB_CUDA(cudaStreamSynchronize(s0_));
     std::vector<int> ei((size_t)B_ * list_cap_), ej((size_t)B_ * list_cap_);
     std::vector<double> ew((size_t)B_ * list_cap_);
-    TPB_CUDA(cudaMemcpy(ei.data(), e_i_, ei.size() * sizeof(int), cudaMemcpyDeviceToHost));
-    TPB_CUDA(cudaMemcpy(ej.data(), e_j_, ej.size() * sizeof(int), cudaMemcpyDeviceToHost));
-    TPB_CUDA(cudaMemcpy(ew.data(), e_w_, ew.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    TPB_CUDA(cudaMemcpy(ei.data(), e_i_[0], ei.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    TPB_CUDA(cudaMemcpy(ej.data(), e_j_[0], ej.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    TPB_CUDA(cudaMemcpy(ew.data(), e_w_[0], ew.size() * sizeof(double), cudaMemcpyDeviceToHost));
     final_slem(tmp_m_, list_, list_count_, slem_out_);
     std::vector<double> so((size_t)B_ * 8);
     TPB_CUDA(cudaMemcpyAsync(so.data(), slem_out_, so.size() * sizeof(double), cudaMemcpyDeviceToHost, s0_));

@@ -152,27 +152,31 @@ class Solver {
     OzWork oz_;
     OzShard shard_;
     int *list_ = nullptr, *list_count_ = nullptr;
-    // Per-iteration selection output for the trace SLEM, double-buffered by
-    // iteration parity (set 0 aliases list_/list_count_): the SLEM of
-    // iteration k reads set k % 2 while iteration k + 1 runs, and the select
-    // of iteration k + 2 waits for it
-    int* tlist_[2] = {nullptr, nullptr};
-    int* tcount_[2] = {nullptr, nullptr};
-    double* tlw_[2] = {nullptr, nullptr};
-    int* tsnap_[2] = {nullptr, nullptr};
-    cudaEvent_t ev_slem_p_[2] = {nullptr, nullptr};
-    bool slem_pending_[2] = {false, false};
-    bool slem_any_ = false;
-    int slem_last_ = 0;
-    int *e_i_ = nullptr, *e_j_ = nullptr, *col_idx_ = nullptr;
-    double* e_w_ = nullptr;
-    double* basis_ = nullptr;        // trace Lanczos basis (B x kmax x n)
+    // Per-iteration selection output for the trace SLEM in kSets buffer sets
+    // (iteration k uses set k % kSets; set 0 aliases list_/list_count_). The
+    // trace SLEMs run on kLanes streams (iteration k on lane k % kLanes, each
+    // lane warm-starting from its own previous report's Ritz vectors), so two
+    // reports can be in flight beside the projections; the select of
+    // iteration k + kSets waits for the SLEM of iteration k
+    static constexpr int kSets = 4, kLanes = 2;
+    int* tlist_[kSets] = {};
+    int* tcount_[kSets] = {};
+    double* tlw_[kSets] = {};
+    int* tsnap_[kSets] = {};
+    cudaEvent_t ev_slem_p_[kSets] = {};
+    bool slem_pending_[kSets] = {};
+    bool slem_any_[kLanes] = {};
+    int slem_last_[kLanes] = {};
+    // per-lane SLEM scratch (lane 0 also serves extraction and the one-offs)
+    int *e_i_[kLanes] = {}, *e_j_[kLanes] = {}, *col_idx_[kLanes] = {};
+    double* e_w_[kLanes] = {};
+    double* basis_[kLanes] = {};     // trace Lanczos basis (B x kmax x n)
     int trace_kmax_ = 0;
     int kfin_ = 1;  // Krylov dimension of the one-off reports
-    double* ritz_ = nullptr;         // B x 2n extreme Ritz vectors (warm start)
-    int* ritz_ok_ = nullptr;
-    int* slem_nbr_ = nullptr;        // het trace SLEM: node-major incidence scratch
-    double* slem_nwt_ = nullptr;
+    double* ritz_[kLanes] = {};      // B x 2n extreme Ritz vectors (warm start)
+    int* ritz_ok_[kLanes] = {};
+    int* slem_nbr_[kLanes] = {};     // het trace SLEM: node-major incidence scratch
+    double* slem_nwt_[kLanes] = {};
     double* basis_final_ = nullptr;  // final report
     double* slem_out_ = nullptr;     // B x 8
     double* tmp_m_ = nullptr;        // B x m
@@ -181,9 +185,9 @@ class Solver {
     double* fs_scal_ = nullptr;      // B x 2
     int* h_ctl_ = nullptr;           // pinned B x 8
     // streams / graphs
-    cudaStream_t s0_ = nullptr, s1_ = nullptr, s2_ = nullptr;
+    cudaStream_t s0_ = nullptr, s1_ = nullptr, s2_[kLanes] = {};
     cudaEvent_t ev_fork_ = nullptr, ev_sel_ = nullptr, ev_slem_ = nullptr;
-    cudaGraphExec_t g_chunk_ = nullptr, g_one_[2] = {nullptr, nullptr};
+    cudaGraphExec_t g_chunk_ = nullptr, g_one_[kSets] = {};
     int it_enqueued_ = 0;
     // results
     std::vector<SolveResult> res_;
