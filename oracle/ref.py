@@ -96,6 +96,7 @@ def lib():
         L.ref_iteration_sample.argtypes = [I, I, ip, I, D, I, dp]
         L.ref_admm_run.argtypes = [I, I, ip, I, D, I, I, dp]
         L.ref_admm_het_run.argtypes = [I, ip, ip, I, D, I, I, dp]
+        L.ref_admm_het_trace.argtypes = [I, ip, ip, I, D, I, I, dp]
         _lib = L
     return _lib
 
@@ -421,6 +422,16 @@ def admm_run(n, r, warm_edges, iters, rho=10.0, chunk=10):
     _check(lib().ref_admm_run(n, r, _ip(we), len(we), rho, iters, chunk, _dp(out)))
     return {"setup_s": float(out[0]), "iter_s": out[1:iters + 1].tolist(),
             "residual": float(out[iters + 1]), "bicgstab_iters": int(out[iters + 2])}
+
+
+def admm_het_trace(degrees, warm_edges, iters, rho=10.0, chunk=10):
+    """Per-iteration (residual, lambda, acf) of the reference's node-level het
+    ADMM loop (ref_shim.cpp::ref_admm_het_trace), iters x 3."""
+    deg = np.ascontiguousarray(np.asarray(degrees, np.int32))
+    we = np.ascontiguousarray(np.asarray(warm_edges, np.int32).reshape(-1, 2))
+    out = np.zeros(3 * iters)
+    _check(lib().ref_admm_het_trace(len(deg), _ip(deg), _ip(we), len(we), rho, iters, chunk, _dp(out)))
+    return out.reshape(iters, 3)
 
 
 def admm_het_run(degrees, warm_edges, iters, rho=10.0, chunk=10):

@@ -740,4 +740,46 @@ int ref_admm_het_run(int n, const int* degrees, const int* warm_edges, int n_war
     });
 }
 
+
+// The same loop as ref_admm_het_run, recording the trace row of every
+// iteration (residual, lambda of the projected iterate, acf_of_g) for a
+// lockstep golden at n = 256 (tests/golden/make_config5.py): the reference's
+// solve_het loop (proj/src/admm_het.cpp:266-301) with BiCGSTAB restarted in
+// chunks until it meets its 1e-10 tolerance.
+int ref_admm_het_trace(int n, const int* degrees, const int* warm_edges, int n_warm, double rho, int iters,
+                       int chunk, double* trace) {
+    return guarded([&] {
+        CapacitySystem sys = node_level_constraints(n, std::vector<int>(degrees, degrees + n));
+        ProblemDataHet pd = assemble_het(sys, std::nullopt, 2.0, rho);
+        const auto lo = detail::het_layout(pd.n, pd.q);
+        const int m = pd.m;
+        Topology warm = make_topo(n, warm_edges, nullptr, n_warm);
+        Vec x_state = detail::feasible_start(lo, warm, 2.0);
+        for (const auto& [i, j] : warm.edges) x_state[pd.off_z + edge_index(n, i, j)] = 1.0;
+        for (int l = 0; l < m; ++l) x_state[pd.off_nu + l] = std::max(0.0, x_state[pd.off_z + l] - x_state[l]);
+        Vec y_state = x_state;
+        Vec duals(pd.nx, 0.0);
+        Vec kkt_warm(pd.nx + pd.neq, 0.0);
+        std::copy(x_state.begin(), x_state.end(), kkt_warm.begin());
+        for (int it = 1; it <= iters; ++it) {
+            y_state = project_Y_het(pd, x_state, duals);
+            const Vec rhs = detail::kkt_rhs(lo, y_state, duals, pd.beq, pd.rho);
+            for (int round = 0; round < 100000; ++round) {
+                SolveReport rep = bicgstab(pd.kkt, rhs, kkt_warm, &pd.ilu, 1e-10, chunk);
+                if (rep.converged) break;
+            }
+            x_state.assign(kkt_warm.begin(), kkt_warm.begin() + pd.nx);
+            for (int k = 0; k < pd.nx; ++k) duals[k] += pd.rho * (x_state[k] - y_state[k]);
+            double res = 0.0;
+            for (int k = 0; k < pd.nx; ++k) {
+                const double d = x_state[k] - y_state[k];
+                res += d * d;
+            }
+            trace[3 * (it - 1)] = res;
+            trace[3 * (it - 1) + 1] = y_state[lo.lambda_ix];
+            trace[3 * (it - 1) + 2] = detail::acf_of_g(n, pd.pairs, y_state.data());
+        }
+    });
+}
+
 }  // extern "C"
