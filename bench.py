@@ -50,7 +50,12 @@ def peaks():
 # N=256, K=32 at the issue floor (128.1 cycles/MMA): tools/microbench/imma_rate.cu
 IMMA_PEAK_TOPS = 4004.9
 # dram read+write bytes per Ozaki GEMM launch from one ncu --set full capture (profiles/)
-OZ_TRAFFIC = {}  # filled from the round's ncu capture (profiles/r02/)
+# dram__bytes_read.sum + dram__bytes_write.sum of one oz_gemm_kernel launch
+# at n=1024 (ncu --set full, cold replay; profiles/r02/ncu_oz_gemm.txt):
+# 38.84 MB read + 0.37 MB written (writes land in L2). The two operands'
+# digit planes are 2 x 7 x 1024^2 = 14.7 MB; the rest is the epilogue's FP64
+# reads and the cold-cache replay re-reading planes across the 144 CTAs
+OZ_TRAFFIC = {1024: 38844672 + 368384}
 OZ_SLICES, OZ_BM, OZ_BN = 7, 128, 64  # paper_2512_07536_b200/csrc/ozaki_kernels.cuh
 
 
