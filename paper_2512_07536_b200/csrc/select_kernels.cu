@@ -244,6 +244,7 @@ namespace {
 constexpr int kGThreads = 256;
 constexpr int kGBins = 2048;
 constexpr int kGRounds = 6;
+constexpr int kTopRCacheBytes = 32 * 1024;
 __device__ __forceinline__ int g_shift(int round) { return round < 5 ? 53 - 11 * round : 0; }
 __device__ __forceinline__ int g_bits(int round) { return round < 5 ? 11 : 9; }
 }  // namespace
@@ -264,6 +265,28 @@ __global__ void __launch_bounds__(kGThreads, 8) topr_grid_kernel(SelectArgs a, i
     __shared__ int sh[kGBins];
     __shared__ int scan_scratch[32];
     __shared__ int s_sel[4];  // digit, need after, bucket population, count above
+    // the CTA's range of values, read from HBM once and kept in shared
+    // memory for every later pass when the launch reserved room for it
+    extern __shared__ double sv[];
+    const bool cached = a.topr_cache >= hi - lo;
+    if (cached) {
+        // all of a thread's loads in flight before the first store
+        constexpr int NL = 8;
+        for (long long k0 = lo + tid; k0 < hi; k0 += NL * kGThreads) {
+            double t[NL];
+#pragma unroll
+            for (int u = 0; u < NL; ++u) {
+                const long long k = k0 + (long long)u * kGThreads;
+                t[u] = k < hi ? v[k] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < NL; ++u) {
+                const long long k = k0 + (long long)u * kGThreads;
+                if (k < hi) sv[k - lo] = t[u];
+            }
+        }
+    }
+    auto val = [&](long long k) { return cached ? sv[k - lo] : v[k]; };
 
     // zero the global histograms (grid-strided), then the first barrier
     for (int k = g * kGThreads + tid; k < kGRounds * kGBins; k += G * kGThreads) gh[k] = 0;
@@ -282,7 +305,7 @@ __global__ void __launch_bounds__(kGThreads, 8) topr_grid_kernel(SelectArgs a, i
             for (int k = tid; k < nb; k += kGThreads) sh[k] = 0;
             __syncthreads();
             for (long long k = lo + tid; k < hi; k += kGThreads) {
-                const unsigned long long key = (unsigned long long)__double_as_longlong(v[k] + 0.0);
+                const unsigned long long key = (unsigned long long)__double_as_longlong(val(k) + 0.0);
                 if ((key & pmask) == prefix) atomicAdd(&sh[(key >> shift) & (nb - 1)], 1);
             }
             __syncthreads();
@@ -329,7 +352,7 @@ __global__ void __launch_bounds__(kGThreads, 8) topr_grid_kernel(SelectArgs a, i
     // final pass 1: ties and kept-nonzero keys above the threshold, per CTA
     int t_own = 0, k_own = 0;
     for (long long k = lo + tid; k < hi; k += kGThreads) {
-        const double x = v[k];
+        const double x = val(k);
         const unsigned long long key = (unsigned long long)__double_as_longlong(x + 0.0);
         bool keep = mode == 0 || (mode == 1 && key >= thresh) || (mode == 2 && key > thresh);
         if (mode == 2 && key == thresh) ++t_own;
@@ -375,6 +398,59 @@ __global__ void __launch_bounds__(kGThreads, 8) topr_grid_kernel(SelectArgs a, i
         const long long kept_before = tie_off < need_eq ? tie_off : need_eq;
         if (tie_nonzero) list_off += kept_before;
     }
+    if (cached) {
+        // final pass 2 over the shared-memory copy: each thread a contiguous
+        // run of the CTA's range (index order), two block scans in all
+        const long long L = (hi - lo + kGThreads - 1) / kGThreads;
+        const long long r0 = lo + tid * L < hi ? lo + tid * L : hi, r1 = r0 + L < hi ? r0 + L : hi;
+        auto classify = [&](long long k, bool& keep, bool& tie, double& x) {
+            x = sv[k - lo];
+            const unsigned long long key = (unsigned long long)__double_as_longlong(x + 0.0);
+            keep = mode == 0 || (mode == 1 && key >= thresh) || (mode == 2 && key > thresh);
+            tie = mode == 2 && key == thresh;
+        };
+        int nt = 0;
+        for (long long k = r0; k < r1; ++k) {
+            bool keep, tie;
+            double x;
+            classify(k, keep, tie, x);
+            nt += tie;
+        }
+        int tt;
+        const long long tie0 = tie_off + block_exclusive_scan(nt, scan_scratch, &tt);
+        int nk = 0;
+        {
+            long long tr = tie0;
+            for (long long k = r0; k < r1; ++k) {
+                bool keep, tie;
+                double x;
+                classify(k, keep, tie, x);
+                if (tie) keep = tr++ < need_eq;
+                nk += keep && x != 0.0;
+            }
+        }
+        int kt;
+        const long long pos0 = list_off + block_exclusive_scan(nk, scan_scratch, &kt);
+        {
+            long long tr = tie0, pos = pos0;
+            for (long long k = r0; k < r1; ++k) {
+                bool keep, tie;
+                double x;
+                classify(k, keep, tie, x);
+                if (tie) keep = tr++ < need_eq;
+                if (!keep) v[k] = 0.0;
+                if (keep && x != 0.0) {
+                    if (a.list && pos < a.list_cap) {
+                        a.list[pos] = (int)k;
+                        if (a.list_w) a.list_w[pos] = x;
+                    }
+                    ++pos;
+                }
+            }
+        }
+        if (a.list && g == G - 1 && tid == 0) a.list_count[0] = (int)(list_off + kt);
+        return;
+    }
     // final pass 2: in index order, chunks of kGThreads with block scans
     long long tie_run = tie_off, pos_run = list_off;
     for (long long base = lo; base < hi; base += kGThreads) {
@@ -382,7 +458,7 @@ __global__ void __launch_bounds__(kGThreads, 8) topr_grid_kernel(SelectArgs a, i
         double x = 0.0;
         bool keep = false, tie = false;
         if (k < hi) {
-            x = v[k];
+            x = val(k);
             const unsigned long long key = (unsigned long long)__double_as_longlong(x + 0.0);
             keep = mode == 0 || (mode == 1 && key >= thresh) || (mode == 2 && key > thresh);
             tie = mode == 2 && key == thresh;
@@ -422,15 +498,21 @@ int topr_grid_ctas(long long m) {
 
 void launch_topr_grid(const SelectArgs& a, int* gh, int* cnt, cudaStream_t st) {
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(topr_grid_ctas(a.m));
+    const int G = topr_grid_ctas(a.m);
+    const long long per = (a.m + G - 1) / G;
+    SelectArgs b = a;
+    // the range cache fits beside a cone-GEMM CTA (173 KB) on the same SM
+    b.topr_cache = per * (long long)sizeof(double) <= kTopRCacheBytes ? (int)per : 0;
+    cfg.gridDim = dim3(G);
     cfg.blockDim = dim3(kGThreads);
+    cfg.dynamicSmemBytes = b.topr_cache * sizeof(double);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    TPB_CUDA(cudaLaunchKernelEx(&cfg, topr_grid_kernel, a, gh, cnt));
+    TPB_CUDA(cudaLaunchKernelEx(&cfg, topr_grid_kernel, b, gh, cnt));
 }
 
 // Compaction of the nonzero entries of a packed vector into an ascending list

@@ -17,6 +17,7 @@ struct SelectArgs {
     double* list_w;      // weights aligned with the list (per solve at b*list_cap), or null
     int* it_snap;        // per solve: iteration counter ictl[b*8] at selection, -1 if done (or null)
     const int* done;     // ictl (done flag at [b*8+1], iteration counter at [b*8]) or null
+    int topr_cache = 0;  // grid top-r: values per CTA kept in shared memory (set by launch_topr_grid)
 };
 
 void launch_topr(const SelectArgs& a, int B, cudaStream_t st);
