@@ -65,6 +65,8 @@ def lib():
         L.ref_capacity_system_sizes.argtypes = [I, D, D, D, I, ip]
         L.ref_topology_to_json.argtypes = [I, ip, dp, I, C.c_char_p, I]
         L.ref_matrix_to_csv.argtypes = [I, dp, C.c_char_p, I]
+        L.ref_allocation_json.argtypes = [D, ip, I, C.c_char_p, I]
+        L.ref_solution_json.argtypes = [C.c_char_p, D, D, I, I, I, I, D, I, C.c_char_p, C.c_char_p, I]
         L.ref_solution_trace_csv.argtypes = [P, C.c_char_p, I]
         L.ref_capacity_system.argtypes = [I, D, D, D, I, ip, ip, ip, ip]
         L.ref_project_binary_z_capped.argtypes = [I, D, D, D, I, dp, I, dp]
@@ -295,6 +297,26 @@ def topology_to_json(n, edges, weights) -> str:
         _check(7)
     buf = C.create_string_buffer(k + 1)
     lib().ref_topology_to_json(n, _ip(e), _dp(w), len(e), buf, k + 1)
+    return buf.value.decode()
+
+
+def allocation_json(b_unit, e) -> str:
+    """allocation.json of `topoopt optimize` (proj/tools/topoopt.cpp:244-246)."""
+    e = np.ascontiguousarray(np.asarray(e, np.int32))
+    k = lib().ref_allocation_json(float(b_unit), _ip(e), len(e), None, 0)
+    buf = C.create_string_buffer(k + 1)
+    lib().ref_allocation_json(float(b_unit), _ip(e), len(e), buf, k + 1)
+    return buf.value.decode()
+
+
+def solution_json(mode, acf, lambda_tilde, converged, connected, repaired, iterations, residual, n_edges,
+                  note) -> str:
+    """solution.json of `topoopt optimize` (proj/tools/topoopt.cpp:285-296)."""
+    args = [mode.encode(), float(acf), float(lambda_tilde), int(converged), int(connected), int(repaired),
+            int(iterations), float(residual), int(n_edges), note.encode()]
+    k = lib().ref_solution_json(*args, None, 0)
+    buf = C.create_string_buffer(k + 1)
+    lib().ref_solution_json(*args, buf, k + 1)
     return buf.value.decode()
 
 

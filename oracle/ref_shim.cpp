@@ -23,6 +23,8 @@
 #include <thread>
 #include <vector>
 
+#include <nlohmann/json.hpp>
+
 #include "admm_shared.hpp"  // proj/src: detail::feasible_start / kkt_rhs / acf_of_g
 #include "topoopt/admm.hpp"
 #include "topoopt/admm_het.hpp"
@@ -244,6 +246,42 @@ static int copy_out(const std::string& text, char* buf, int cap) {
 int ref_topology_to_json(int n, const int* edges, const double* weights, int ne, char* buf, int cap) {
     int len = 0;
     const int st = guarded([&] { len = copy_out(topology_to_json(make_topo(n, edges, weights, ne)), buf, cap); });
+    return st != 0 ? -1 : len;
+}
+
+// The `topoopt optimize` artefacts the CLI builds itself
+// (proj/tools/topoopt.cpp:244-246, 285-296): allocation.json and
+// solution.json, nlohmann objects dumped with indent 2 (restated here, test
+// infrastructure: the CLI is not built).
+int ref_allocation_json(double b_unit, const int* e, int n, char* buf, int cap) {
+    int len = 0;
+    const int st = guarded([&] {
+        nlohmann::json aj;
+        aj["b_unit"] = b_unit;
+        aj["e"] = std::vector<int>(e, e + n);
+        len = copy_out(aj.dump(2) + "\n", buf, cap);
+    });
+    return st != 0 ? -1 : len;
+}
+
+int ref_solution_json(const char* mode, double acf, double lambda_tilde, int converged, int connected,
+                      int repaired, int iterations, double residual, int n_edges, const char* note, char* buf,
+                      int cap) {
+    int len = 0;
+    const int st = guarded([&] {
+        nlohmann::json sj;
+        sj["mode"] = std::string(mode);
+        sj["acf"] = acf;
+        sj["lambda_tilde"] = lambda_tilde;
+        sj["converged"] = converged != 0;
+        sj["connected"] = connected != 0;
+        sj["repaired"] = repaired != 0;
+        sj["iterations"] = iterations;
+        sj["residual"] = residual;
+        sj["edges"] = (size_t)n_edges;
+        sj["note"] = std::string(note);
+        len = copy_out(sj.dump(2) + "\n", buf, cap);
+    });
     return st != 0 ? -1 : len;
 }
 

@@ -1,6 +1,9 @@
 """On-disk format goldens (§8f row 4: proj/src/topology.cpp:283-324,
-proj/src/admm.cpp:223-236, proj/include/topoopt/textio.hpp:10-14): the
-reference's own serializations of topologies, gossip matrices and traces.
+proj/src/admm.cpp:223-236, proj/include/topoopt/textio.hpp:10-14,
+proj/tools/topoopt.cpp:244-296): the reference's own serializations of
+topologies, gossip matrices, traces and the optimize command's
+solution.json / allocation.json, byte for byte (the oracle build's nlohmann
+prints as stock 3.11.3, oracle/Makefile).
 Run in the development container: ``python tests/golden/make_formats.py``."""
 from __future__ import annotations
 
@@ -24,7 +27,18 @@ def main():
     s = ref.solve(16, 32, warm_edges=np.array(c1["warm"]), **c1["cfg"])
     cases.append({"label": "config1", "n": 16, "edges": s.edges.tolist(), "weights": s.weights.tolist(),
                   "topology_json": ref.topology_to_json(16, s.edges, s.weights),
-                  "w_csv": ref.matrix_to_csv(s.w), "trace_csv": s.trace_csv})
+                  "w_csv": ref.matrix_to_csv(s.w), "trace_csv": s.trace_csv,
+                  # the CLI's own objects (proj/tools/topoopt.cpp:244-246, 285-296)
+                  "solution": {"acf": s.acf, "lambda_tilde": s.lambda_tilde, "converged": bool(s.converged),
+                               "connected": bool(s.connected), "repaired": bool(s.repaired),
+                               "iterations": int(s.iterations), "residual": s.residual,
+                               "note": s.note},
+                  "solution_json": ref.solution_json("homogeneous", s.acf, s.lambda_tilde, s.converged,
+                                                     s.connected, s.repaired, s.iterations, s.residual,
+                                                     len(s.edges), s.note)})
+    c2 = json.load(open(os.path.join(OUT, "config2.json")))
+    cases[0]["allocation"] = {"b_unit": c2["b_unit"], "e": c2["degrees"]}
+    cases[0]["allocation_json"] = ref.allocation_json(c2["b_unit"], c2["degrees"])
     for kind, n in [("ring", 8), ("exponential", 16), ("grid2d", 9)]:
         e, w = ref.generate_benchmark(kind, n)
         cases.append({"label": f"{kind}_{n}", "n": n, "edges": e.tolist(), "weights": w.tolist(),
