@@ -35,7 +35,7 @@ int sm_count() {
 // ---------------------------------------------------------------- small n
 // One CTA per matrix; all iterates in shared memory (npad <= 64).
 namespace {
-constexpr int ST = 256;  // 8 warps
+constexpr int ST = 512;  // 16 warps
 }
 
 __global__ void __launch_bounds__(ST) cone_small_kernel(const double* Ag, long long mstride, int ld, int n,
@@ -75,12 +75,22 @@ __global__ void __launch_bounds__(ST) cone_small_kernel(const double* Ag, long l
             while ((fi + 1) * (fi + 2) / 2 <= f) ++fi;
             while (fi * (fi + 1) / 2 > f) --fi;
             const int fj = f - fi * (fi + 1) / 2;
-            double d0 = 0.0, d1 = 0.0;
-            for (int k = 0; k < np; k += 4) {
-                const double av = a[(fi * 8 + (lane >> 2)) * P + k + (lane & 3)];
-                const double bv = b[(fj * 8 + (lane >> 2)) * P + k + (lane & 3)];
-                dmma(d0, d1, av, bv);
+            // four independent accumulator pairs over k (the DMMA chain is
+            // latency-bound), added pairwise at the end
+            const double* ar = a + (fi * 8 + (lane >> 2)) * P + (lane & 3);
+            const double* br = b + (fj * 8 + (lane >> 2)) * P + (lane & 3);
+            double e0[4] = {0.0, 0.0, 0.0, 0.0}, e1[4] = {0.0, 0.0, 0.0, 0.0};
+            int k = 0;
+            for (; k + 16 <= np; k += 16) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) dmma(e0[q], e1[q], ar[k + 4 * q], br[k + 4 * q]);
             }
+            if (k < np) {  // np % 16 == 8: two more k steps
+                dmma(e0[0], e1[0], ar[k], br[k]);
+                dmma(e0[1], e1[1], ar[k + 4], br[k + 4]);
+            }
+            const double d0 = (e0[0] + e0[1]) + (e0[2] + e0[3]);
+            const double d1 = (e1[0] + e1[1]) + (e1[2] + e1[3]);
             const int r = fi * 8 + (lane >> 2);
             const int c = fj * 8 + (lane & 3) * 2;
             double v0 = alpha * d0, v1 = alpha * d1;

@@ -502,7 +502,7 @@ __global__ void __launch_bounds__(256) slem_small_kernel(SlemArgs a) {
     double* p = v + n;           // n
     double* d = p + n;           // n
     double* e = d + n;           // n
-    __shared__ double scratch[32];
+    __shared__ double red1[32], red2[32];  // one-barrier reductions, alternating
     __shared__ int s_it;
     if (tid == 0) s_it = it_rec;
     // W: off-diagonals +g, diagonal 1 - (sum of incident g, ascending edges)
@@ -527,7 +527,7 @@ __global__ void __launch_bounds__(256) slem_small_kernel(SlemArgs a) {
         const int m0 = k + 1, len = n - m0;
         double nn = 0.0;
         for (int i = m0 + tid; i < n; i += nthr) nn += A[i * ld + k] * A[i * ld + k];
-        nn = block_sum(nn, scratch);
+        nn = allreduce1(nn, red1);
         const double a0 = A[m0 * ld + k];
         if (nn == 0.0) {
             if (tid == 0) {
@@ -542,16 +542,21 @@ __global__ void __launch_bounds__(256) slem_small_kernel(SlemArgs a) {
         const double beta = 1.0 / (s * (s + fabs(a0)));
         for (int i = m0 + tid; i < n; i += nthr) v[i] = A[i * ld + k] + (i == m0 ? sg * s : 0.0);
         __syncthreads();
-        // p = beta A[m0:, m0:] v
-        for (int i = m0 + tid; i < n; i += nthr) {
+        // p = beta A[m0:, m0:] v: four lanes per row (interleaved columns,
+        // then two xor shuffles; fixed order)
+        for (int i0 = m0; i0 < n; i0 += nthr / 4) {
+            const int i = i0 + (tid >> 2), part = tid & 3;
             double acc = 0.0;
-            for (int j = m0; j < n; ++j) acc += A[i * ld + j] * v[j];
-            p[i] = beta * acc;
+            if (i < n)
+                for (int j = m0 + part; j < n; j += 4) acc += A[i * ld + j] * v[j];
+            acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+            acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+            if (part == 0 && i < n) p[i] = beta * acc;
         }
         __syncthreads();
         double pv = 0.0;
         for (int i = m0 + tid; i < n; i += nthr) pv += p[i] * v[i];
-        pv = block_sum(pv, scratch);
+        pv = allreduce1(pv, red2);
         const double K = 0.5 * beta * pv;
         for (int i = m0 + tid; i < n; i += nthr) p[i] -= K * v[i];  // w
         __syncthreads();
