@@ -13,7 +13,8 @@ the data path; the barrier and the max-over-ranks timing use torch.distributed.
 
 `--workload sweep`: config 5 (256 independent n=256 solves, sharded across
 ranks). `--workload sharded`: one n=4096 instance whose cone projections are
-row-sharded over the ranks (NCCL all-gather; strong scaling).
+sharded over the ranks (tiles dealt round-robin; each GEMM epilogue stores
+its tiles into every rank's buffers over NVLink; strong scaling).
 
 `--impl reference` times the reference's own CPU implementation (compiled
 from /root/reference into oracle/_ref) on the host cores, rank 0 only.
@@ -576,9 +577,10 @@ def run_sweep(args):
 
 def run_sharded(args):
     """One large instance (default n=4096, r=4n) with its cone
-    projections row-sharded over the N ranks (tp_solver_set_comm: NCCL
-    all-gather of each product's row blocks, overlapped with the other
-    chain's GEMM); everything else replicated. Strong scaling: value = ADMM
+    projections sharded over the N ranks (tp_solver_set_comm: each rank
+    computes 1/N of every product's tiles and its GEMM epilogue stores them
+    into every rank's digit buffers over NVLink; per-product flags between
+    the ranks); everything else replicated. Strong scaling: value = ADMM
     iterations/s of the one instance."""
     import torch
     import torch.distributed as tdist

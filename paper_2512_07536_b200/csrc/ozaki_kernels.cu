@@ -15,8 +15,6 @@
 // The KS accumulator groups (KS x 64 int32 columns) sit in TMEM's 512 columns.
 #include "ozaki_kernels.cuh"
 
-#include "nccl_shim.hpp"
-
 #include "cone_kernels.cuh"
 
 #include <algorithm>
@@ -106,6 +104,25 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&v)[16]) {
           "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
           "=r"(v[14]), "=r"(v[15])
         : "r"(addr));
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// sharded product: this CTA is done (its stores, local and remote, precede the
+// release); the launch's last CTA publishes the product to every rank
+__device__ inline void shard_arrive(const OzGemm& g) {
+    if (g.nranks <= 1 || threadIdx.x != 0) return;
+    const int total = gridDim.x * gridDim.y;
+    if (atomicAdd(g.done, 1) == total - 1) {
+        atomicExch(g.done, 0);
+        __threadfence_system();
+        for (int r = 0; r < g.nranks; ++r) st_release_sys(g.peer_flags[r] + g.rank, g.epoch + 1);
+    }
 }
 __device__ __forceinline__ void tmem_wait_ld() {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -219,7 +236,10 @@ __device__ inline void oz_tile(int t, int& I, int& J) {
 __global__ void __launch_bounds__(THREADS, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, OzGemm g) {
     const int mat = g.mstep ? blockIdx.y * g.mstep + g.moff : blockIdx.y;
-    if (g.ictl && g.ictl[(mat >> 1) * 8 + 1]) return;
+    if (g.ictl && g.ictl[(mat >> 1) * 8 + 1]) {
+        shard_arrive(g);
+        return;
+    }
     int I, J;
     oz_tile(g.tiles ? g.tiles[blockIdx.x] : blockIdx.x, I, J);
     const int i0 = I * BM, j0 = J * BN;
@@ -261,6 +281,26 @@ __global__ void __launch_bounds__(THREADS, 1)
     // may then be scheduled as SMs free up.
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (g.nranks > 1) {
+        // every rank has finished the previous product (its stores into our
+        // operand buffers are visible); bounded wait (no hang on a lost peer)
+        if (threadIdx.x == 0) {
+            const long long t0 = clock64();
+            for (int r = 0; r < g.nranks; ++r) {
+                if (r == g.rank) continue;
+                while (ld_acquire_sys(g.flags + r) < g.epoch) {
+                    if (clock64() - t0 > 8000000000LL) {
+                        atomicExch(g.err, 1);
+                        break;
+                    }
+                    __nanosleep(64);
+                }
+            }
+            // the operands arrive through the async proxy (TMA)
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        __syncthreads();
+    }
     const uint32_t tmem = tmem_slot;
     const int KB = ld / BK;
     const int rc = g.rc ? g.rc : ld;  // plane layout (OzShard)
@@ -457,6 +497,13 @@ __global__ void __launch_bounds__(THREADS, 1)
                         transpose4x4(rows, cols);
 #pragma unroll
                         for (int c = 0; c < 4; ++c) *reinterpret_cast<uint32_t*>(mp + c * ld) = cols[c];
+                        // sharded: the same bytes into every peer's copy (NVLink)
+                        for (int pr = 0; pr < g.nranks; ++pr) {
+                            if (pr == g.rank) continue;
+                            int8_t* pp = g.peer_cd[pr] + (mp - g.Cd);
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) *reinterpret_cast<uint32_t*>(pp + c * ld) = cols[c];
+                        }
                     }
                 }
             }
@@ -471,14 +518,20 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const uint32_t* src = Dg + rr * NCB;
                 int8_t* dp = g.Cd + prow(i0 + rr) * ld + j0 + 16 * c4;
 #pragma unroll
-                for (int s2 = 0; s2 < KS; ++s2, src += BM * NCB, dp += pstride)
-                    *reinterpret_cast<uint4*>(dp) = make_uint4(src[k0], src[k1], src[k2], src[k3]);
+                for (int s2 = 0; s2 < KS; ++s2, src += BM * NCB, dp += pstride) {
+                    const uint4 v4 = make_uint4(src[k0], src[k1], src[k2], src[k3]);
+                    *reinterpret_cast<uint4*>(dp) = v4;
+                    for (int pr = 0; pr < g.nranks; ++pr)
+                        if (pr != g.rank) *reinterpret_cast<uint4*>(g.peer_cd[pr] + (dp - g.Cd)) = v4;
+                }
             }
         }
     }
     if (threadIdx.x == 64) OZ_STAMP(4);
+    if (g.nranks > 1) __threadfence_system();  // this thread's peer stores precede the release
     tc_fence_before();
     __syncthreads();
+    shard_arrive(g);
     if (warp == 1) {
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS)
                      : "memory");
@@ -619,46 +672,20 @@ SignSchedule ozaki_schedule() {
 }
 
 std::vector<int> oz_shard_tiles(int ld, int nranks, int rank) {
-    const int NB = ld / BM;
-    if (ld % BM || nranks < 1 || NB % nranks || rank < 0 || rank >= nranks)
-        throw Error(kInvalidArgument, "sharded projection: ld/128 must be a multiple of the rank count");
-    const int per = NB / nranks;
+    if (ld % BM || nranks < 1 || nranks > kOzMaxRanks || rank < 0 || rank >= nranks)
+        throw Error(kInvalidArgument, "sharded projection: bad rank / size (ld % 128, at most 8 ranks)");
     std::vector<int> t;
-    for (int I = rank * per; I < (rank + 1) * per; ++I) {
-        for (int J = 0; J < R * (I + 1); ++J) t.push_back(tiles_before(I) + J);  // rows of block I
-        for (int I2 = I + 1; I2 < NB; ++I2)                                      // mirrors into it
-            for (int J = R * I; J < R * (I + 1); ++J) t.push_back(tiles_before(I2) + J);
-    }
-    // a tile below the diagonal inside the rank's rows serves both lists
-    std::sort(t.begin(), t.end());
-    t.erase(std::unique(t.begin(), t.end()), t.end());
+    const int all = tiles_before(ld / BM);
+    for (int k = rank; k < all; k += nranks) t.push_back(k);
     return t;
 }
 
-namespace {
-// in-place all-gather of the row blocks of every plane of the matrices
-// moff, moff + 2, ... (one NCCL group)
-void shard_allgather(const OzShard& sh, int8_t* planes, int ld, int nmat, int moff, cudaStream_t st) {
-    // row-chunk-major planes: the rank's rows of all KS planes are one block
-    const size_t count = (size_t)KS * (ld / sh.nranks) * ld;
-    ncclComm_t comm = static_cast<ncclComm_t>(sh.comm);
-    TPB_NCCL(nccl().group_start());
-    for (int mat = moff; mat < nmat; mat += 2) {
-        int8_t* base = planes + (size_t)mat * KS * ld * ld;
-        TPB_NCCL(nccl().all_gather(base + (size_t)sh.rank * count, base, count, ncclInt8, comm, st));
-    }
-    TPB_NCCL(nccl().group_end());
-}
-}  // namespace
-
 void enqueue_cone_ozaki(const double* A, const OzWork& oz, int ld, int n, const double* scale, double* C,
                         long long c_stride_b, long long c_stride_w, const int* ictl, int nmat,
-                        const SignSchedule& sch, cudaStream_t st, const OzShard* shard) {
+                        const SignSchedule& sch, cudaStream_t st, OzShard* shard) {
     const bool sharded = shard && shard->nranks > 1;
-    const int rc = sharded ? ld / shard->nranks : 0;
-    bool ag_pending[2] = {false, false};
     const long long ms = (long long)ld * ld;
-    launch_oz_split(A, ms, ld, nmat, scale, kEX0, oz.d[3], ictl, st, rc);
+    launch_oz_split(A, ms, ld, nmat, scale, kEX0, oz.d[3], ictl, st, 0);
     const double beta = sch.qb / (2.0 * sch.qc);
     const double gamma = sch.qa - sch.qb * sch.qb / (4.0 * sch.qc);
     OzGemm g{};
@@ -666,7 +693,25 @@ void enqueue_cone_ozaki(const double* A, const OzWork& oz, int ld, int n, const 
     g.nmat = nmat;
     g.scale = scale;
     g.ictl = ictl;
-    g.rc = rc;
+    g.rc = 0;
+    if (sharded) {
+        g.nranks = shard->nranks;
+        g.rank = shard->rank;
+        g.flags = shard->flags;
+        for (int r = 0; r < shard->nranks; ++r) g.peer_flags[r] = shard->peer_flags[r];
+        g.done = shard->done;
+        g.err = shard->err;
+        g.no_pdl = 1;
+    }
+    // every product of a sharded solve waits for the previous one on every
+    // rank and publishes its own (the final FP64 product included)
+    auto launch = [&](int od) {
+        if (sharded) {
+            for (int r = 0; r < shard->nranks; ++r) g.peer_cd[r] = od >= 0 ? shard->peer_d[od][r] : nullptr;
+            g.epoch = shard->epoch++;
+        }
+        launch_oz_gemm(g, st);
+    };
     // one product of digit buffers ia, ib into digit buffer od
     auto step = [&](int ia, int ea, int ib, int eb, double al, double shift, int od, int ec) {
         g.ma = &oz.maps[ia];
@@ -677,26 +722,11 @@ void enqueue_cone_ozaki(const double* A, const OzWork& oz, int ld, int n, const 
         g.dshift = shift;
         g.Cd = oz.d[od];
         g.eC = ec;
-        if (!sharded) {
-            launch_oz_gemm(g, st);
-            return;
+        if (sharded) {
+            g.tiles = shard->tiles;  // this rank's tiles, stored to every rank
+            g.ntiles = shard->ntiles;
         }
-        // chain par's product waits for its operands' all-gather only; its
-        // own all-gather then overlaps the other chain's GEMM
-        g.tiles = shard->tiles;
-        g.ntiles = shard->ntiles;
-        g.no_pdl = 1;
-        g.mstep = 2;
-        for (int par = 0; par < 2; ++par) {
-            if (ag_pending[par]) TPB_CUDA(cudaStreamWaitEvent(st, shard->ag_done[par], 0));
-            g.moff = par;
-            launch_oz_gemm(g, st);
-            TPB_CUDA(cudaEventRecord(shard->gemm_done[par], st));
-            TPB_CUDA(cudaStreamWaitEvent(shard->cs, shard->gemm_done[par], 0));
-            shard_allgather(*shard, oz.d[od], ld, nmat, par, shard->cs);
-            TPB_CUDA(cudaEventRecord(shard->ag_done[par], shard->cs));
-            ag_pending[par] = true;
-        }
+        launch(od);
     };
     int x = 3;  // digit buffer holding X (3: X0)
     auto others = [&](int& f0, int& f1) {
@@ -739,14 +769,12 @@ void enqueue_cone_ozaki(const double* A, const OzWork& oz, int ld, int n, const 
     g.ldc = n;
     g.nvalid = n;
     g.Cd = nullptr;
-    g.tiles = nullptr;  // the FP64 product is replicated
+    g.tiles = nullptr;  // the FP64 product is replicated (every tile on every rank)
     g.ntiles = 0;
     g.mstep = 0;
     g.moff = 0;
-    g.no_pdl = 0;
-    for (int par = 0; par < 2; ++par)
-        if (ag_pending[par]) TPB_CUDA(cudaStreamWaitEvent(st, shard->ag_done[par], 0));
-    launch_oz_gemm(g, st);
+    g.no_pdl = sharded ? 1 : 0;
+    launch(-1);
 }
 
 }  // namespace tpb

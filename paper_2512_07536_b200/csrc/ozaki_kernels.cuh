@@ -28,6 +28,7 @@ constexpr int kOzSlices = 7;     // digits per operand (49 bits)
 constexpr int kOzBM = 128;       // tile rows (UMMA M)
 constexpr int kOzBN = 64;        // tile columns
 constexpr int kOzMaxLd = 16384;  // int32 accumulator bound (see above)
+constexpr int kOzMaxRanks = 8;   // GPUs of one NVLink/NVSwitch domain sharing a projection
 
 // Throws kInvalidArgument unless ld is a multiple of 128 in [128, kOzMaxLd].
 void check_oz_ld(int ld);
@@ -62,6 +63,16 @@ struct OzGemm {
     int mstep;               // matrices of this launch: blockIdx.y * mstep + moff (mstep 0 -> 1)
     int moff;
     int rc;                  // plane layout: rows per chunk (0 -> ld; see OzShard)
+    // sharded product over nranks GPUs (nranks > 1): the epilogue stores every
+    // digit-plane tile into all ranks' output buffers over NVLink, and the
+    // launch waits for / publishes per-rank product counters (OzShard)
+    int nranks, rank;
+    int8_t* peer_cd[kOzMaxRanks];                 // rank r's output digit buffer (slot rank: Cd)
+    unsigned long long* flags;                    // local [kOzMaxRanks]: products completed by rank r
+    unsigned long long* peer_flags[kOzMaxRanks];  // rank r's flag array
+    int* done;                                    // local arrival counter of the launch's CTAs
+    int* err;                                     // wait timeout (results invalid)
+    unsigned long long epoch;                     // products every rank completed before this one
 };
 
 void launch_oz_gemm(const OzGemm& g, cudaStream_t st);
@@ -74,31 +85,30 @@ struct OzWork {
     OzMaps maps[4];
 };
 
-// Row-sharded projection of one large instance over G ranks:
-// rank k owns the 128-row blocks [k NB/G, (k+1) NB/G) of every iterate. Its
-// tiles are the lower tiles of those row blocks plus the lower tiles whose
-// mirror lands in them, so its rows are complete after its GEMM; an
-// in-place NCCL all-gather of the row blocks of every digit plane then gives
-// every rank the whole iterate. The same kernel computes every tile, so the
-// result is bitwise the single-GPU one. (The final FP64 product is
-// replicated.)
-// Sharded runs store each matrix's planes row-chunk-major,
-// [mat][chunk][slice][rc rows][ld] with rc = ld / G (rc = ld is the plain
-// [mat][slice][ld][ld] layout), so a rank's rows of all planes are one
-// contiguous block: one all-gather per matrix. Tiles never straddle chunks.
-// The S (even matrices) and T (odd) chains of the sign iteration are
-// independent, so each product runs as two launches and one chain's
-// all-gather (comm stream) overlaps the other chain's GEMM.
+// Sharded projection of one large instance over G ranks of one NVLink /
+// NVSwitch domain. The lower tiles of every product are dealt
+// round-robin to the ranks; each rank's GEMM epilogue stores its tiles'
+// digit planes (direct and mirrored rows) into every rank's copy of the
+// output buffer through peer pointers (CUDA IPC), so the all-gather is fused
+// into the product: NVLink traffic overlaps the remaining tiles' math. Per
+// product each rank's last CTA publishes its product counter into every
+// peer's flag array (system-scope release), and the next product's CTAs wait
+// until every peer has published (acquire) before reading operands; the same
+// kernel computes every tile, so the iterate is bitwise the single-GPU one.
+// NCCL is used once, to exchange the IPC handles.
 struct OzShard {
     int rank = 0, nranks = 1;
-    void* comm = nullptr;    // ncclComm_t
-    int* tiles = nullptr;    // device: this rank's tile indices
+    void* comm = nullptr;     // ncclComm_t (setup only)
+    int* tiles = nullptr;     // device: this rank's tile indices
     int ntiles = 0;
-    cudaStream_t cs = nullptr;                    // all-gathers
-    cudaEvent_t gemm_done[2] = {nullptr, nullptr};  // per chain
-    cudaEvent_t ag_done[2] = {nullptr, nullptr};
+    int8_t* peer_d[4][kOzMaxRanks] = {};          // every rank's digit buffer q
+    unsigned long long* flags = nullptr;          // local flag array (peers write their slots)
+    unsigned long long* peer_flags[kOzMaxRanks] = {};
+    int* done = nullptr;
+    int* err = nullptr;
+    unsigned long long epoch = 0;                 // products launched so far (same on every rank)
 };
-// Host tile list of `rank` for an ld x ld iterate (ld % 128 == 0, ld/128 % nranks == 0).
+// Host tile list of `rank`: the lower tiles t with t % nranks == rank.
 std::vector<int> oz_shard_tiles(int ld, int nranks, int rank);
 
 struct SignSchedule;
@@ -107,7 +117,7 @@ struct SignSchedule;
 // on the int8 tensor cores; P_nsd / P_psd written to C.
 void enqueue_cone_ozaki(const double* A, const OzWork& oz, int ld, int n, const double* scale, double* C,
                         long long c_stride_b, long long c_stride_w, const int* ictl, int nmat,
-                        const SignSchedule& sch, cudaStream_t st, const OzShard* shard = nullptr);
+                        const SignSchedule& sch, cudaStream_t st, OzShard* shard = nullptr);
 
 // Digit planes of s * A (s = scale[mat] or 1) with exponent e (layout rc as in OzGemm).
 void launch_oz_split(const double* A, long long mstride, int ld, int nmat, const double* scale,

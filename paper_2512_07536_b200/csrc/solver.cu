@@ -6,6 +6,8 @@
 // streams: cone projections (s0) || top-r selection (s1) -> trace SLEM (s2).
 #include "solver.cuh"
 
+#include "nccl_shim.hpp"
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -222,14 +224,7 @@ Solver::~Solver() {
     cudaStreamSynchronize(s0_);
     phase_mark("free");
     if (h_ctl_) pinned_give(h_ctl_, (size_t)B_ * 8 * sizeof(int));
-    if (shard_.cs) {
-        cudaStreamSynchronize(shard_.cs);
-        for (int q = 0; q < 2; ++q) {
-            cudaEventDestroy(shard_.gemm_done[q]);
-            cudaEventDestroy(shard_.ag_done[q]);
-        }
-        cudaStreamDestroy(shard_.cs);
-    }
+    release_shard();
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_sel_) cudaEventDestroy(ev_sel_);
     if (ev_slem_) cudaEventDestroy(ev_slem_);
@@ -307,6 +302,7 @@ void Solver::alloc() {
         // digit planes of the cone-projection iterates
         for (int q = 0; q < 4; ++q) {
             oz_.d[q] = dalloc<int8_t>(s0_, allocs_, (size_t)B * 2 * kOzSlices * ld2);
+            pool_planes_[q] = oz_.d[q];
             TPB_CUDA(cudaMemsetAsync(oz_.d[q], 0, (size_t)B * 2 * kOzSlices * ld2, s0_));
             make_oz_maps(oz_.d[q], ld_, 2 * B, &oz_.maps[q]);
         }
@@ -561,32 +557,91 @@ void Solver::enqueue_projection() {
     }
 }
 
+void Solver::release_shard() {
+    TPB_CUDA(cudaDeviceSynchronize());
+    for (int r = 0; r < kOzMaxRanks; ++r) {
+        if (r == shard_.rank) continue;
+        for (int q = 0; q < 4; ++q)
+            if (shard_.peer_d[q][r]) cudaIpcCloseMemHandle(shard_.peer_d[q][r]);
+        if (shard_.peer_flags[r]) cudaIpcCloseMemHandle(shard_.peer_flags[r]);
+    }
+    for (void* p : shard_mem_) cudaFree(p);
+    shard_mem_.clear();
+    shard_ = OzShard{};
+}
+
+// Sharded projection over the ranks of `comm`: the digit
+// buffers (plain cudaMalloc, IPC-exportable) and a flag array per rank are
+// mapped into every rank through CUDA IPC handles exchanged with one NCCL
+// all-gather; the GEMM epilogues then store each tile into every rank's
+// buffer over NVLink (ozaki_kernels.cuh, OzShard).
 void Solver::set_shard(void* comm, int nranks, int rank) {
-    if (nranks <= 1) {
-        shard_.nranks = 1;
-        shard_.rank = 0;
-        shard_.comm = nullptr;
-    } else {
+    if (sharded() || !shard_mem_.empty()) {
+        // back to the pool-allocated planes of alloc()
+        for (int q = 0; q < 4; ++q) oz_.d[q] = pool_planes_[q];
+        for (int q = 0; q < 4 && ozaki_; ++q) make_oz_maps(oz_.d[q], ld_, 2 * B_, &oz_.maps[q]);
+        release_shard();
+    }
+    if (nranks > 1) {
         if (!ozaki_) throw Error(kInvalidArgument, "sharded projection: needs the tiled Ozaki path (n > 64)");
+        if (B_ != 1) throw Error(kInvalidArgument, "sharded projection: one instance per solver");
+        if (nranks > kOzMaxRanks) throw Error(kInvalidArgument, "sharded projection: at most 8 ranks");
         const std::vector<int> t = oz_shard_tiles(ld_, nranks, rank);
+        TPB_CUDA(cudaStreamSynchronize(s0_));
+        const size_t pbytes = (size_t)2 * kOzSlices * ld_ * ld_;
+        auto raw = [&](size_t bytes) {
+            void* p = nullptr;
+            TPB_CUDA(cudaMalloc(&p, bytes));
+            TPB_CUDA(cudaMemset(p, 0, bytes));
+            shard_mem_.push_back(p);
+            return p;
+        };
+        for (int q = 0; q < 4; ++q) {
+            oz_.d[q] = static_cast<int8_t*>(raw(pbytes));
+            make_oz_maps(oz_.d[q], ld_, 2, &oz_.maps[q]);
+        }
+        shard_.flags = static_cast<unsigned long long*>(raw(kOzMaxRanks * sizeof(unsigned long long)));
+        shard_.done = static_cast<int*>(raw(sizeof(int)));
+        shard_.err = static_cast<int*>(raw(sizeof(int)));
+        int* dtiles = static_cast<int*>(raw(t.size() * sizeof(int)));
+        h2d(dtiles, t.data(), t.size() * sizeof(int));
+        // IPC handles of the 4 digit buffers and the flag array, all-gathered
+        constexpr int NH = 5;
+        std::vector<cudaIpcMemHandle_t> mine(NH), all((size_t)NH * nranks);
+        for (int q = 0; q < 4; ++q) TPB_CUDA(cudaIpcGetMemHandle(&mine[q], oz_.d[q]));
+        TPB_CUDA(cudaIpcGetMemHandle(&mine[4], shard_.flags));
+        const size_t hb = NH * sizeof(cudaIpcMemHandle_t);
+        void* dh = raw(hb * nranks);
+        h2d(static_cast<char*>(dh) + hb * rank, mine.data(), hb);
+        TPB_NCCL(nccl().all_gather(static_cast<char*>(dh) + hb * rank, dh, hb, ncclInt8,
+                                   static_cast<ncclComm_t>(comm), s0_));
+        TPB_CUDA(cudaStreamSynchronize(s0_));
+        TPB_CUDA(cudaMemcpy(all.data(), dh, hb * nranks, cudaMemcpyDeviceToHost));
         shard_.rank = rank;
         shard_.nranks = nranks;
         shard_.comm = comm;
+        shard_.tiles = dtiles;
         shard_.ntiles = (int)t.size();
-        if (!shard_.cs) {
-            // highest priority: as GEMM CTAs retire, the SMs go to the
-            // all-gather's CTAs first, so it overlaps the other chain's GEMM
-            int lo = 0, hi = 0;
-            TPB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-            TPB_CUDA(cudaStreamCreateWithPriority(&shard_.cs, cudaStreamNonBlocking, hi));
-            for (int q = 0; q < 2; ++q) {
-                TPB_CUDA(cudaEventCreateWithFlags(&shard_.gemm_done[q], cudaEventDisableTiming));
-                TPB_CUDA(cudaEventCreateWithFlags(&shard_.ag_done[q], cudaEventDisableTiming));
+        shard_.epoch = 0;
+        for (int r = 0; r < nranks; ++r) {
+            if (r == rank) {
+                for (int q = 0; q < 4; ++q) shard_.peer_d[q][r] = oz_.d[q];
+                shard_.peer_flags[r] = shard_.flags;
+                continue;
             }
+            for (int q = 0; q < 4; ++q) {
+                void* p = nullptr;
+                TPB_CUDA(cudaIpcOpenMemHandle(&p, all[(size_t)r * NH + q], cudaIpcMemLazyEnablePeerAccess));
+                shard_.peer_d[q][r] = static_cast<int8_t*>(p);
+            }
+            void* f = nullptr;
+            TPB_CUDA(cudaIpcOpenMemHandle(&f, all[(size_t)r * NH + 4], cudaIpcMemLazyEnablePeerAccess));
+            shard_.peer_flags[r] = static_cast<unsigned long long*>(f);
         }
-        shard_.tiles = dalloc<int>(s0_, allocs_, t.size());
+        // every rank's buffers exist and are zeroed before anyone stores
+        TPB_NCCL(nccl().all_gather(static_cast<char*>(dh) + hb * rank, dh, hb, ncclInt8,
+                                   static_cast<ncclComm_t>(comm), s0_));
         TPB_CUDA(cudaStreamSynchronize(s0_));
-        h2d(shard_.tiles, t.data(), t.size() * sizeof(int));
     }
     // graphs captured before hold the old projection
     if (g_chunk_) cudaGraphExecDestroy(g_chunk_);
@@ -595,6 +650,13 @@ void Solver::set_shard(void* comm, int nranks, int rank) {
         g1 = nullptr;
     }
     g_chunk_ = nullptr;
+}
+
+void Solver::check_shard() {
+    if (!sharded()) return;
+    int e = 0;
+    TPB_CUDA(cudaMemcpy(&e, shard_.err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (e) throw Error(kCuda, "sharded projection: a peer did not publish its product (timeout)");
 }
 
 // One ADMM iteration on three streams: prep on s0, then the
@@ -712,6 +774,7 @@ void Solver::iterate_async(int k) {
 bool Solver::all_done() {
     TPB_CUDA(cudaMemcpyAsync(h_ctl_, d_.ictl, (size_t)B_ * 8 * sizeof(int), cudaMemcpyDeviceToHost, s0_));
     TPB_CUDA(cudaStreamSynchronize(s0_));
+    check_shard();
     for (int b = 0; b < B_; ++b)
         if (d_.cg && h_ctl_[b * 8 + kCgFail])
             throw Error(kLinearSolve, "update_X: CG relative residual above 1e-8 (solve " + std::to_string(b) +

@@ -151,6 +151,10 @@ class Solver {
     int *cap_idx_ = nullptr, *cap_load_ = nullptr;
     OzWork oz_;
     OzShard shard_;
+    std::vector<void*> shard_mem_;        // cudaMalloc'd buffers of the sharded mode
+    int8_t* pool_planes_[4] = {};         // the solver's own digit buffers (unsharded)
+    void release_shard();
+    void check_shard();
     int *list_ = nullptr, *list_count_ = nullptr;
     // Per-iteration selection output for the trace SLEM in kSets buffer sets
     // (iteration k uses set k % kSets; set 0 aliases list_/list_count_). The

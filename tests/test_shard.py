@@ -1,9 +1,11 @@
-"""CPU: host logic of the row-sharded single-instance projection (SURVEY §8e,
-ozaki_kernels.cuh OzShard). Each rank's tile list must make its 128-row
-blocks of every iterate complete, given the kernel's store rule (lower tiles
-(I, J), J < 2(I+1), of 128 x 64; direct rows from 64 t in the diagonal block,
-mirror rows from 64 (t+1)); the GPU check (bitwise equality with the
-single-GPU solve at 2 ranks) is tests/test_gpu_shard.py."""
+"""CPU: host logic of the sharded single-instance projection (SURVEY §8e,
+ozaki_kernels.cuh OzShard). The ranks' tile lists partition the lower tiles
+(round-robin, balanced), and since every rank's epilogue stores its tiles
+into every rank's buffer, the union of their footprints under the kernel's
+store rule (lower tiles (I, J), J < 2(I+1), of 128 x 64; direct rows from
+64 t in the diagonal block, mirror rows from 64 (t+1)) writes every entry of
+the iterate exactly once; the GPU check (bitwise equality with the
+single-GPU solve at 2 ranks) is tests/test_gpu_shard.py.""",
 import numpy as np
 import pytest
 
@@ -31,21 +33,28 @@ def footprint(ld, tiles):
     return W
 
 
-@pytest.mark.parametrize("ld,G", [(256, 2), (512, 2), (512, 4), (1024, 2), (1024, 8), (2048, 4)])
-def test_shard_tiles_complete_rows(T, ld, G):
+@pytest.mark.parametrize("ld,G", [(256, 2), (512, 2), (512, 4), (1024, 2), (1024, 8), (2048, 4), (384, 2)])
+def test_shard_tiles_partition_the_iterate(T, ld, G):
     all_lower = R * (ld // BM) * (ld // BM + 1) // 2
     single = footprint(ld, range(all_lower))
     assert (single == 1).all()                               # unsharded: every entry once
-    rows = ld // G
+    union = np.zeros_like(single)
+    seen = set()
+    sizes = []
     for k in range(G):
         t = T.shard_tiles(ld, G, k)
         assert len(t) == len(set(t.tolist())) and t.min() >= 0 and t.max() < all_lower
-        per, NB = ld // BM // G, ld // BM
-        assert 2 * len(t) == R * per * (2 * NB - per + 1)   # the same work on every rank
-        W = footprint(ld, t)
-        assert (W[k * rows:(k + 1) * rows] >= 1).all()       # own rows complete
+        assert not (seen & set(t.tolist()))                  # disjoint
+        seen |= set(t.tolist())
+        sizes.append(len(t))
+        union += footprint(ld, t)
+    assert len(seen) == all_lower                            # every tile on some rank
+    assert max(sizes) - min(sizes) <= 1                      # balanced
+    assert (union == 1).all()                                # every entry written once
 
 
-def test_shard_tiles_rejects_uneven(T):
-    with pytest.raises(T.InvalidArgument if hasattr(T, "InvalidArgument") else Exception):
-        T.shard_tiles(384, 2, 0)                             # 3 row blocks over 2 ranks
+def test_shard_tiles_rejects_bad_ranks(T):
+    with pytest.raises(Exception):
+        T.shard_tiles(512, 9, 0)                             # more than 8 ranks
+    with pytest.raises(Exception):
+        T.shard_tiles(500, 2, 0)                             # ld not a multiple of 128
