@@ -264,23 +264,41 @@ __global__ void __launch_bounds__(TB* TY, 4) prep_kernel(Dev d, XConst c) {
         const int off = which == 0 ? lo.off_s : lo.off_t;
         double* A = d.A + ((long long)b * 2 + which) * ld2;
         __shared__ double Vs[TB][TB + 1];  // Vs[jl][il] = v(i0+il, j0+jl)
-        // orientation 1: entries (i, j), column-major (r=i, c=j) at j*n + i
-        for (int cc = ty; cc < TB; cc += TY) {
+        // both orientations' X and D loads are issued before any use (their
+        // HBM latencies overlap): orientation 1 = entries (i, j) at j*n + i,
+        // orientation 2 = entries (j, i) at i*n + j
+        constexpr int NE = TB / TY;
+        double x1[NE], d1[NE], x2[NE], d2[NE];
+#pragma unroll
+        for (int k = 0; k < NE; ++k) {
+            const int cc = ty + k * TY;
             const int i = i0 + tx, j = j0 + cc;
-            double v = 0.0;
             if (i < n && j < n) {
                 const long long p = off + (long long)j * n + i;
-                v = X[p] + D[p] * c.inv_rho;
+                x1[k] = X[p];
+                d1[k] = D[p];
             }
-            Vs[cc][tx] = v;
+            const int j2 = j0 + tx, i2 = i0 + cc;
+            if (i2 < n && j2 < n) {
+                const long long p = off + (long long)i2 * n + j2;
+                x2[k] = X[p];
+                d2[k] = D[p];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < NE; ++k) {
+            const int cc = ty + k * TY;
+            const int i = i0 + tx, j = j0 + cc;
+            Vs[cc][tx] = (i < n && j < n) ? x1[k] + d1[k] * c.inv_rho : 0.0;
         }
         __syncthreads();
-        // orientation 2: entries (j, i) at i*n + j; symmetrize with (i, j)
-        for (int cc = ty; cc < TB; cc += TY) {
+        // orientation 2: symmetrize with (i, j)
+#pragma unroll
+        for (int k = 0; k < NE; ++k) {
+            const int cc = ty + k * TY;
             const int j = j0 + tx, i = i0 + cc;  // entry (row j, col i)
             if (i < n && j < n) {
-                const long long p = off + (long long)i * n + j;
-                const double vji = X[p] + D[p] * c.inv_rho;
+                const double vji = x2[k] + d2[k] * c.inv_rho;
                 const double vij = Vs[tx][cc];
                 const double a = 0.5 * (vij + vji);  // symmetrize (proj/src/eig.cpp:157)
                 // A is symmetric; write (j, i) here (row-major j*ld + i)
@@ -316,13 +334,34 @@ __global__ void __launch_bounds__(TB* TY, 4) prep_kernel(Dev d, XConst c) {
         __syncthreads();
     }
     // packed edge blocks for pairs (i, j), i < j, i in block bi, j in block bj
-    for (int il = ty; il < TB; il += TY) {
+    // (the g loads of the thread's rows in flight together)
+    {
+        constexpr int NE = TB / TY;
+        double xg[NE], dg[NE];
+        long long lg[NE];
+        bool okg[NE];
+#pragma unroll
+        for (int k = 0; k < NE; ++k) {
+            const int i = i0 + ty + k * TY, j = j0 + tx;
+            okg[k] = i < n && j < n && j > i;
+            lg[k] = okg[k] ? edge_idx(n, i, j) : 0;
+            if (okg[k]) {
+                xg[k] = X[lg[k]];
+                dg[k] = D[lg[k]];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < NE; ++k) {
+            if (!okg[k]) continue;
+            const double vg = xg[k] + dg[k] * c.inv_rho;
+            Y[lg[k]] = (0.0 < vg) ? vg : 0.0;  // std::max(0.0, v) (proj/src/admm.cpp:273)
+        }
+    }
+    for (int il = ty; il < TB && d.het; il += TY) {
         const int i = i0 + il, j = j0 + tx;
         if (i >= n || j >= n || j <= i) continue;
         const long long l = edge_idx(n, i, j);
-        const double vg = X[l] + D[l] * c.inv_rho;
-        Y[l] = (0.0 < vg) ? vg : 0.0;  // std::max(0.0, v) (proj/src/admm.cpp:273)
-        if (d.het) {
+        {
             const long long lz = lo.off_z + l, lv = lo.off_nu + l;
             Y[lz] = X[lz] + D[lz] * c.inv_rho;  // z-score; binary projection follows
             const double vn = X[lv] + D[lv] * c.inv_rho;
