@@ -245,9 +245,28 @@ constexpr int kGThreads = 256;
 constexpr int kGBins = 2048;
 constexpr int kGRounds = 6;
 constexpr int kTopRCacheBytes = 32 * 1024;
+constexpr int kGWarps = kGThreads / 32;
+constexpr int kGCand = 2048;  // compacted candidates after the first round (cached ranges)
 __device__ __forceinline__ int g_shift(int round) { return round < 5 ? 53 - 11 * round : 0; }
 __device__ __forceinline__ int g_bits(int round) { return round < 5 ? 11 : 9; }
 }  // namespace
+
+#ifdef OZ_STAMPS
+// instrumentation build only (make STAMPS=1): globaltimer stamps per CTA
+__device__ long long* g_topr_stamps = nullptr;
+__device__ __forceinline__ void topr_stamp(int slot) {
+    if (!g_topr_stamps || threadIdx.x) return;
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_topr_stamps[16LL * blockIdx.x + slot] = t;
+}
+extern "C" int tp_topr_set_stamps(void* dev_ptr) {
+    return cudaMemcpyToSymbol(g_topr_stamps, &dev_ptr, sizeof(void*)) == cudaSuccess ? 0 : 7;
+}
+#define TOPR_STAMP(slot) topr_stamp(slot)
+#else
+#define TOPR_STAMP(slot) do {} while (0)
+#endif
 
 __global__ void __launch_bounds__(kGThreads, 8) topr_grid_kernel(SelectArgs a, int* gh, int* cnt) {
     cg::grid_group grid = cg::this_grid();
@@ -255,6 +274,7 @@ __global__ void __launch_bounds__(kGThreads, 8) topr_grid_kernel(SelectArgs a, i
         if (a.it_snap && blockIdx.x == 0 && threadIdx.x == 0) a.it_snap[0] = -1;
         return;
     }
+    TOPR_STAMP(0);
     if (a.it_snap && blockIdx.x == 0 && threadIdx.x == 0) a.it_snap[0] = a.done ? a.done[0] : 0;
     const long long m = a.m;
     double* v = a.base;
@@ -265,6 +285,10 @@ __global__ void __launch_bounds__(kGThreads, 8) topr_grid_kernel(SelectArgs a, i
     __shared__ int sh[kGBins];
     __shared__ int scan_scratch[32];
     __shared__ int s_sel[4];  // digit, need after, bucket population, count above
+    __shared__ unsigned short cand[kGCand];  // offsets into sv of the keys matching the prefix
+    __shared__ int s_ncand;
+    __shared__ int s_tw[kGWarps], s_kw[kGWarps];  // per-warp ties / kept nonzero (cached final passes)
+    const int lane = tid & 31, wid = tid >> 5;
     // the CTA's range of values, read from HBM once and kept in shared
     // memory for every later pass when the launch reserved room for it
     extern __shared__ double sv[];
@@ -287,9 +311,10 @@ __global__ void __launch_bounds__(kGThreads, 8) topr_grid_kernel(SelectArgs a, i
         }
     }
     auto val = [&](long long k) { return cached ? sv[k - lo] : v[k]; };
+    TOPR_STAMP(1);
 
-    // zero the global histograms (grid-strided), then the first barrier
-    for (int k = g * kGThreads + tid; k < kGRounds * kGBins; k += G * kGThreads) gh[k] = 0;
+    // the global histograms are zero on entry (zeroed at allocation and by
+    // the previous launch after its last barrier)
     int mode;  // 0 keep all, 1 key >= thresh, 2 key > thresh + first need ties, 3 keep none
     unsigned long long prefix = 0, pmask = 0;
     long long need = r;
@@ -299,35 +324,66 @@ __global__ void __launch_bounds__(kGThreads, 8) topr_grid_kernel(SelectArgs a, i
         mode = 3;
     } else {
         mode = 2;
-        grid.sync();
+        int ncand = -1;  // >= 0: the rounds scan only cand[0, ncand)
         for (int round = 0; round < kGRounds; ++round) {
             const int shift = g_shift(round), nb = 1 << g_bits(round);
             for (int k = tid; k < nb; k += kGThreads) sh[k] = 0;
             __syncthreads();
-            for (long long k = lo + tid; k < hi; k += kGThreads) {
-                const unsigned long long key = (unsigned long long)__double_as_longlong(val(k) + 0.0);
-                if ((key & pmask) == prefix) atomicAdd(&sh[(key >> shift) & (nb - 1)], 1);
+            if (ncand >= 0) {
+                for (int c = tid; c < ncand; c += kGThreads) {
+                    const unsigned long long key = (unsigned long long)__double_as_longlong(sv[cand[c]] + 0.0);
+                    if ((key & pmask) == prefix) atomicAdd(&sh[(key >> shift) & (nb - 1)], 1);
+                }
+            } else {
+                // warp-aggregated: the early rounds put most keys of a warp
+                // in one bin (same exponent), so one atomic per distinct bin;
+                // four keys per thread loaded before the first atomic
+                constexpr int U = 4;
+                for (long long base = lo; base < hi; base += U * kGThreads) {
+                    unsigned bin[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const long long k = base + u * kGThreads + tid;
+                        bin[u] = 0xffffffffu;
+                        if (k < hi) {
+                            const unsigned long long key = (unsigned long long)__double_as_longlong(val(k) + 0.0);
+                            if ((key & pmask) == prefix) bin[u] = (unsigned)((key >> shift) & (nb - 1));
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const unsigned peers = __match_any_sync(0xffffffffu, bin[u]);
+                        if (bin[u] != 0xffffffffu && (__ffs(peers) - 1) == lane) atomicAdd(&sh[bin[u]], __popc(peers));
+                    }
+                }
             }
             __syncthreads();
             int* ghr = gh + round * kGBins;
             for (int k = tid; k < nb; k += kGThreads)
                 if (sh[k]) atomicAdd(&ghr[k], sh[k]);
+            TOPR_STAMP(2 + 2 * round);
             grid.sync();
+            TOPR_STAMP(3 + 2 * round);
             // every CTA: bucket of the need-th largest key (suffix scan, 8 bins per thread)
+            // (the bins stay in registers: all loads in flight at once, and
+            // the selecting thread walks its copies, not L2)
             const int per_t = nb / kGThreads;  // 8 (or 2 in the last round)
+            int hb[8];
             int own = 0;
-            for (int q = 0; q < per_t; ++q) {
-                const int bin = nb - 1 - (tid * per_t + q);  // descending order
-                own += __ldcg(&ghr[bin]);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                hb[q] = q < per_t ? __ldcg(&ghr[nb - 1 - (tid * per_t + q)]) : 0;  // descending order
+                own += hb[q];
             }
             int tot;
             const int before = block_exclusive_scan(own, scan_scratch, &tot);
             if (before < need && before + own >= need) {
                 long long cum = before;
-                for (int q = 0; q < per_t; ++q) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
                     const int bin = nb - 1 - (tid * per_t + q);
-                    const int h = __ldcg(&ghr[bin]);
-                    if (cum + h >= need) {
+                    const int h = hb[q];
+                    if (q < per_t && cum + h >= need) {
                         s_sel[0] = bin;
                         s_sel[1] = (int)(need - cum);
                         s_sel[2] = h;
@@ -336,6 +392,7 @@ __global__ void __launch_bounds__(kGThreads, 8) topr_grid_kernel(SelectArgs a, i
                     cum += h;
                 }
             }
+            if (tid == 0) s_ncand = 0;  // every read of the last compaction's count is behind us
             __syncthreads();
             prefix |= (unsigned long long)s_sel[0] << shift;
             pmask |= (unsigned long long)(nb - 1) << shift;
@@ -346,26 +403,84 @@ __global__ void __launch_bounds__(kGThreads, 8) topr_grid_kernel(SelectArgs a, i
                 mode = 1;
                 break;
             }
+            if (cached && ncand < 0 && round + 1 < kGRounds) {
+                // the keys still matching the prefix (a few per CTA once the
+                // exponent is fixed), so later rounds skip the full range
+                for (long long base = lo; base < hi; base += kGThreads) {
+                    const long long k = base + tid;
+                    const bool match = k < hi && (((unsigned long long)__double_as_longlong(sv[k - lo] + 0.0)) & pmask) == prefix;
+                    const unsigned bal = __ballot_sync(0xffffffffu, match);
+                    int off = 0;
+                    if (lane == 0 && bal) off = atomicAdd(&s_ncand, __popc(bal));
+                    off = __shfl_sync(0xffffffffu, off, 0) + __popc(bal & ((1u << lane) - 1u));
+                    if (match && off < kGCand) cand[off] = (unsigned short)(k - lo);
+                }
+                __syncthreads();
+                ncand = s_ncand <= kGCand ? s_ncand : -1;
+            }
         }
     }
     const unsigned long long thresh = prefix;
-    // final pass 1: ties and kept-nonzero keys above the threshold, per CTA
-    int t_own = 0, k_own = 0;
-    for (long long k = lo + tid; k < hi; k += kGThreads) {
-        const double x = val(k);
+    auto classify = [&](double x, bool& keep, bool& tie) {
         const unsigned long long key = (unsigned long long)__double_as_longlong(x + 0.0);
-        bool keep = mode == 0 || (mode == 1 && key >= thresh) || (mode == 2 && key > thresh);
-        if (mode == 2 && key == thresh) ++t_own;
-        k_own += keep && x != 0.0;
+        keep = mode == 0 || (mode == 1 && key >= thresh) || (mode == 2 && key > thresh);
+        tie = mode == 2 && key == thresh;
+    };
+    // cached ranges: warp w owns the contiguous segment [s0, s1) of the CTA's
+    // range, lane l its elements s0 + l + 32j (index order = (j, l)), so tie
+    // ranks and list positions come from ballots and one per-warp prefix
+    const long long segw = (hi - lo + kGThreads - 1) / kGThreads * 32;
+    const long long s0 = lo + wid * segw < hi ? lo + wid * segw : hi, s1 = s0 + segw < hi ? s0 + segw : hi;
+    // final pass 1: ties and kept-nonzero keys above the threshold, per CTA
+    if (cached) {
+        int tw = 0, kw = 0;
+        for (long long base = s0; base < s1; base += 32) {
+            const long long k = base + lane;
+            bool keep = false, tie = false;
+            double x = 0.0;
+            if (k < s1) {
+                x = sv[k - lo];
+                classify(x, keep, tie);
+            }
+            tw += __popc(__ballot_sync(0xffffffffu, tie));
+            kw += __popc(__ballot_sync(0xffffffffu, keep && x != 0.0));
+        }
+        if (lane == 0) {
+            s_tw[wid] = tw;
+            s_kw[wid] = kw;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int tt = 0, kt = 0;
+            for (int w = 0; w < kGWarps; ++w) {
+                tt += s_tw[w];
+                kt += s_kw[w];
+            }
+            cnt[2 * g] = tt;
+            cnt[2 * g + 1] = kt;
+        }
+    } else {
+        int t_own = 0, k_own = 0;
+        for (long long k = lo + tid; k < hi; k += kGThreads) {
+            const double x = val(k);
+            bool keep, tie;
+            classify(x, keep, tie);
+            t_own += tie;
+            k_own += keep && x != 0.0;
+        }
+        int ttot, ktot;
+        block_exclusive_scan(t_own, scan_scratch, &ttot);
+        block_exclusive_scan(k_own, scan_scratch, &ktot);
+        if (tid == 0) {
+            cnt[2 * g] = ttot;
+            cnt[2 * g + 1] = ktot;
+        }
     }
-    int ttot, ktot;
-    block_exclusive_scan(t_own, scan_scratch, &ttot);
-    block_exclusive_scan(k_own, scan_scratch, &ktot);
-    if (tid == 0) {
-        cnt[2 * g] = ttot;
-        cnt[2 * g + 1] = ktot;
-    }
+    TOPR_STAMP(14);
     grid.sync();
+    TOPR_STAMP(15);
+    // every CTA is past its histogram reads: zero them for the next launch
+    for (int k = g * kGThreads + tid; k < kGRounds * kGBins; k += G * kGThreads) gh[k] = 0;
     // exclusive prefixes over the lower CTAs (index order)
     long long tie_off = 0, list_off = 0;
     for (int q = tid; q < g; q += kGThreads) {
@@ -399,56 +514,45 @@ __global__ void __launch_bounds__(kGThreads, 8) topr_grid_kernel(SelectArgs a, i
         if (tie_nonzero) list_off += kept_before;
     }
     if (cached) {
-        // final pass 2 over the shared-memory copy: each thread a contiguous
-        // run of the CTA's range (index order), two block scans in all
-        const long long L = (hi - lo + kGThreads - 1) / kGThreads;
-        const long long r0 = lo + tid * L < hi ? lo + tid * L : hi, r1 = r0 + L < hi ? r0 + L : hi;
-        auto classify = [&](long long k, bool& keep, bool& tie, double& x) {
-            x = sv[k - lo];
-            const unsigned long long key = (unsigned long long)__double_as_longlong(x + 0.0);
-            keep = mode == 0 || (mode == 1 && key >= thresh) || (mode == 2 && key > thresh);
-            tie = mode == 2 && key == thresh;
-        };
-        int nt = 0;
-        for (long long k = r0; k < r1; ++k) {
-            bool keep, tie;
-            double x;
-            classify(k, keep, tie, x);
-            nt += tie;
+        // final pass 2: the warp's offsets from the per-warp counts, then
+        // ballots per 32 elements; values already +0 are not rewritten
+        long long tie_run = tie_off, pos_run = list_off;
+        int tb_before = 0;
+        for (int w = 0; w < wid; ++w) {
+            tb_before += s_tw[w];
+            pos_run += s_kw[w];
         }
-        int tt;
-        const long long tie0 = tie_off + block_exclusive_scan(nt, scan_scratch, &tt);
-        int nk = 0;
-        {
-            long long tr = tie0;
-            for (long long k = r0; k < r1; ++k) {
-                bool keep, tie;
-                double x;
-                classify(k, keep, tie, x);
-                if (tie) keep = tr++ < need_eq;
-                nk += keep && x != 0.0;
+        tie_run += tb_before;
+        if (tie_nonzero) {
+            const long long room = need_eq - tie_off > 0 ? need_eq - tie_off : 0;
+            pos_run += room < tb_before ? room : tb_before;  // ties kept by lower warps
+        }
+        const unsigned lt = (1u << lane) - 1u;
+        for (long long base = s0; base < s1; base += 32) {
+            const long long k = base + lane;
+            bool keep = false, tie = false;
+            double x = 0.0;
+            if (k < s1) {
+                x = sv[k - lo];
+                classify(x, keep, tie);
             }
-        }
-        int kt;
-        const long long pos0 = list_off + block_exclusive_scan(nk, scan_scratch, &kt);
-        {
-            long long tr = tie0, pos = pos0;
-            for (long long k = r0; k < r1; ++k) {
-                bool keep, tie;
-                double x;
-                classify(k, keep, tie, x);
-                if (tie) keep = tr++ < need_eq;
-                if (!keep) v[k] = 0.0;
-                if (keep && x != 0.0) {
-                    if (a.list && pos < a.list_cap) {
-                        a.list[pos] = (int)k;
-                        if (a.list_w) a.list_w[pos] = x;
-                    }
-                    ++pos;
+            const unsigned tb = __ballot_sync(0xffffffffu, tie);
+            if (tie) keep = tie_run + __popc(tb & lt) < need_eq;
+            const bool nz = keep && x != 0.0;
+            const unsigned kb = __ballot_sync(0xffffffffu, nz);
+            if (k < s1 && !keep && __double_as_longlong(x) != 0) v[k] = 0.0;
+            if (nz && a.list) {
+                const long long pos = pos_run + __popc(kb & lt);
+                if (pos < a.list_cap) {
+                    a.list[pos] = (int)k;
+                    if (a.list_w) a.list_w[pos] = x;
                 }
             }
+            tie_run += __popc(tb);
+            pos_run += __popc(kb);
         }
-        if (a.list && g == G - 1 && tid == 0) a.list_count[0] = (int)(list_off + kt);
+        if (a.list && g == G - 1 && wid == kGWarps - 1 && lane == 0) a.list_count[0] = (int)pos_run;
+        TOPR_STAMP(13);
         return;
     }
     // final pass 2: in index order, chunks of kGThreads with block scans

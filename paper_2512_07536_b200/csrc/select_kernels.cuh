@@ -22,7 +22,8 @@ struct SelectArgs {
 
 void launch_topr(const SelectArgs& a, int B, cudaStream_t st);
 // keep_top_r of one large solve (B = 1, hom) over a cooperative grid:
-// gh >= kTopRGridHist ints, cnt >= 2 x topr_grid_ctas(m) ints (scratch).
+// gh >= kTopRGridHist ints, zero before the first launch (each launch leaves
+// it zero), cnt >= 2 x topr_grid_ctas(m) ints (scratch).
 constexpr int kTopRGridHist = 6 * 2048;
 int topr_grid_ctas(long long m);
 void launch_topr_grid(const SelectArgs& a, int* gh, int* cnt, cudaStream_t st);

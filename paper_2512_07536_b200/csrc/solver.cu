@@ -329,6 +329,7 @@ void Solver::alloc() {
     }
     if (!het_ && !cap_ && B == 1 && m >= kTopRGridMin) {
         topr_gh_ = dalloc<int>(s0_, allocs_, kTopRGridHist);
+        TPB_CUDA(cudaMemsetAsync(topr_gh_, 0, kTopRGridHist * sizeof(int), s0_));  // kept zero by each launch
         topr_cnt_ = dalloc<int>(s0_, allocs_, 2 * (size_t)topr_grid_ctas(m));
     }
     list_ = dalloc<int>(s0_, allocs_,(size_t)B * list_cap_);
