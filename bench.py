@@ -429,7 +429,7 @@ def run_ours(args):
                            "frac": bytes_b / t_xb / 1e9 / pk.get("hbm_gbs", 6538.9)},
                 "whole_xstep": {"bytes": xbytes, "ms": t_x * 1e3, "achieved": xbytes / t_x / 1e9,
                                 "frac": xbytes / t_x / 1e9 / pk.get("hbm_gbs", 6538.9),
-                                "note": "incl. the single-CTA node and diag passes"}},
+                                "note": "pass A + pass B (node-space prologue, diagonal entries in the diagonal tiles, solve-level arrival tail)"}},
             "time_to_topology": ttt,
             "cg_xstep": cgm,
             "e2e": {"value": e2e, "unit": "iter/s", "h2d_bytes_per_step": h2d / K,

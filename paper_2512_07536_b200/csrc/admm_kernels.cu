@@ -1139,8 +1139,9 @@ void launch_xstep_cg(const Dev& d, const XConst& c, cudaStream_t st) {
 //   het: rhs = G21(Q) u_g + G22(Q) u_z - e with Q = (n-2) I + J, whose mean
 //        is g12(2n-2) ubar + g22(2n-2) zbar - mean(e), so mean(mu_d) =
 //        mean(rhs) / mu_den_1 and u_z'' = u_z - Q mu_d in closed form.
-// Leaves nv[q][0..2][lane] (t_g, t_z, mu_d of block q) and, in thread 0,
-// returns lambda. Ends with a CTA barrier.
+// Leaves nv[q][0..2][lane] (het: t_g, t_z, mu_d of block q; hom: t, u = D h
+// and the total of t) and, in thread 0, returns lambda. Ends with a CTA
+// barrier.
 __device__ double node_space(const Dev& d, const XConst& c, int b, int bi, int bj, double (*nv)[3][TB],
                              double (*sp)[2][4][TB], double (*scr)[2]) {
     const Layout& lo = d.lo;
@@ -1201,6 +1202,8 @@ __device__ double node_space(const Dev& d, const XConst& c, int b, int bi, int b
         const double pg = u - ubar;
         if (!d.het) {
             v0 = c.c1 * pg + c.c2 * ubar;
+            v1 = u;               // (D h)_i and sum_k t_k = c2 n ubar: the closed-form
+            v2 = c.c2 * su;       // node degrees of pass B's diagonal tiles
         } else {
             const double zbar = sz / n;
             double z2bar = zbar, uz2 = uz;
@@ -1254,7 +1257,14 @@ __global__ void __launch_bounds__(TB* TY, 4) xstep_b_kernel(Dev d, XConst c) {
 
     __shared__ double sp[2][2][4][TB];
     __shared__ double scr2[TB * TY / 32][2];
+    __shared__ int s_fin;
+    __shared__ double s_lam;
+    // hom closed form: the node degrees are closed-form too (deg_i = f0 u_i +
+    // (n - 2) t_i + sum_k t_k), so the diagonal tiles write the diagonal
+    // entries and no block finisher is needed; the CG x-step and het keep it
+    const bool closed = !d.het && !d.cg;
     const double lam = node_space(d, c, b, bi, bj, nv, sp, scr2);  // thread 0
+    if (tx == 0 && ty == 0) s_lam = lam;
 
     // edge loads of the thread's rows (hom), batched
     constexpr int NR = TB / TY;
@@ -1324,6 +1334,28 @@ __global__ void __launch_bounds__(TB* TY, 4) xstep_b_kernel(Dev d, XConst c) {
         Gs[il][jl] = g;
     }
     __syncthreads();
+    if (closed && bi == bj && ty == 0 && i0 + tx < n) {
+        // diagonal entries of the tile's nodes (see the tail below for the
+        // formulas), deg_i in closed form
+        const int i = i0 + tx;
+        const long long p = (long long)i * n + i;
+        const long long ps = lo.off_s + p, pt = lo.off_t + p, py = lo.off_y + i;
+        const double ys = Y[ps], yt = Y[pt], yy = Y[py], ds = D[ps], dt = D[pt], dy = D[py];
+        const double deg = c.f0 * nv[0][1][tx] + (n - 2.0) * nv[0][0][tx] + nv[0][2][tx];
+        const double rs = ys - ds * c.inv_rho, rt = yt - dt * c.inv_rho, ry = yy - dy * c.inv_rho;
+        const double xs = c.s * (c.delta * rs - c.alpha_over_n - deg + s_lam);
+        const double xt = c.s * (c.delta * rt + 2.0 - deg - s_lam);
+        const double xy = c.s * (c.delta * ry + 1.0 - deg);
+        X[ps] = xs;
+        X[pt] = xt;
+        X[py] = xy;
+        if (d.upd_duals) {
+            D[ps] = ds + c.rho * (xs - ys);
+            D[pt] = dt + c.rho * (xt - yt);
+            D[py] = dy + c.rho * (xy - yy);
+        }
+        res += (xs - ys) * (xs - ys) + (xt - yt) * (xt - yt) + (xy - yy) * (xy - yy);
+    }
     // off-diagonal S/T entries: L_ij = -g, so
     //   S_ij = s (delta r_S,ij - alpha/n + g),  T_ij = s (delta r_T,ij + g)
     // The TB/TY entries a thread owns per orientation are handled as one
@@ -1389,7 +1421,8 @@ __global__ void __launch_bounds__(TB* TY, 4) xstep_b_kernel(Dev d, XConst c) {
     // node partials of g (deg = L_ii)
     const int t = ty * TB + tx;
     double* PG = d.PG + (long long)b * d.nb * n;
-    if (t < TB) {
+    if (closed) {
+    } else if (t < TB) {
         const int il = t, i = i0 + il;
         if (i < n) {
             double s = 0.0;
@@ -1425,8 +1458,9 @@ __global__ void __launch_bounds__(TB* TY, 4) xstep_b_kernel(Dev d, XConst c) {
         }
     }
 
-    // ---- tail: the last tile of a node block writes the block's diagonal
-    // entries (deg_i = L_ii = node sums of g):
+    // ---- tail (CG and het; the hom closed form wrote these in its diagonal
+    // tiles and only needs the solve-level arrival): the last tile of a node
+    // block writes the block's diagonal entries (deg_i = L_ii = node sums of g):
     //   S_ii = s (delta r_S,ii - alpha/n - deg_i + lambda)
     //   T_ii = s (delta r_T,ii + 2 - deg_i - lambda)
     //   y_i  = s (delta r_y,i + 1 - deg_i)
@@ -1434,13 +1468,14 @@ __global__ void __launch_bounds__(TB* TY, 4) xstep_b_kernel(Dev d, XConst c) {
     // reduction tree of a node_threads(n)-thread pass: node terms, then the
     // tile partials), the trace row, the best iterate and the stop flags.
     int* cnt = d.cnt + (long long)b * d.cnt_stride;
-    __shared__ int s_fin;
-    __shared__ double s_lam;
-    if (t == 0) s_lam = lam;
-    const int fin = arrive_blocks(cnt + kCntB * d.nb, d.nb, bi, bj, &s_fin);
-    if (!fin) return;
     double* rnode = d.res_node + (long long)b * n;
     bool last = false;
+    if (closed) {
+        // every tile arrives at the solve counter; the last one finishes
+        last = arrive_solve(cnt + 2 * d.nb + kCntB, d.ntile, &s_fin);
+    } else {
+    const int fin = arrive_blocks(cnt + kCntB * d.nb, d.nb, bi, bj, &s_fin);
+    if (!fin) return;
     for (int q = 0; q < 2; ++q) {
         if (!(fin >> q & 1)) continue;
         const int k = q == 0 ? bi : bj;
@@ -1478,6 +1513,7 @@ __global__ void __launch_bounds__(TB* TY, 4) xstep_b_kernel(Dev d, XConst c) {
         }
         last |= arrive_solve(cnt + 2 * d.nb + kCntB, d.nb, &s_fin);
     }
+    }
     if (!last) return;
     int* ctl = d.ictl + b * 8;
     double yl = 0.0, dl = 0.0, best = 0.0;
@@ -1491,7 +1527,8 @@ __global__ void __launch_bounds__(TB* TY, 4) xstep_b_kernel(Dev d, XConst c) {
     double rsum = 0.0, dummy = 0.0;
     {
         const double* rp = d.res_part + (long long)b * d.ntile;
-        for (int k = t; k < n; k += TB * TY) rsum += __ldcg(rnode + k);
+        if (!closed)
+            for (int k = t; k < n; k += TB * TY) rsum += __ldcg(rnode + k);
         for (int k = t; k < d.ntile; k += TB * TY) rsum += __ldcg(rp + k);
     }
     block_sum2_2d(rsum, dummy, scr2);

@@ -1,15 +1,26 @@
-# A/B of two library builds on one box: the grid top-r tests, then the bench
-# (phases_ms.topr) alternating ab_old/ and the working tree, then ncu of the
-# new top-r kernel.
+# A/B of two library builds on one box (ab_old/ = the build before the
+# change, the working tree = after): GPU suite on the new build, bitwise
+# solve dumps of both, then the bench alternating old/new (x-step passes,
+# top-r and iteration rate from each line).
 set -u
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_large.py tests/test_gpu_lockstep.py tests/test_gpu_substeps.py -q -x > gpurun_out/ab_tests.log 2>&1; echo "rc=$?" >> gpurun_out/ab_tests.log
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/ab_tests.log 2>&1; echo "rc=$?" >> gpurun_out/ab_tests.log
+TPB_LIB=$PWD/ab_old/libtopoopt_b200.so timeout 600 python tools/bitwise_ab.py gpurun_out/ab_old.npz > /dev/null 2>&1
+timeout 600 python tools/bitwise_ab.py gpurun_out/ab_new.npz > /dev/null 2>&1
+python tools/bitwise_ab.py --cmp gpurun_out/ab_old.npz gpurun_out/ab_new.npz > gpurun_out/ab_bitwise.txt 2>&1
 LITE="--steps 30 --warmup 5 --no-cpu-baseline --no-ttt --no-sweep --no-cg"
 for rep in 1 2; do
   TPB_LIB=$PWD/ab_old/libtopoopt_b200.so python bench.py $LITE > gpurun_out/ab_bench_old$rep.log 2>&1
   python bench.py $LITE > gpurun_out/ab_bench_new$rep.log 2>&1
 done
-LITE2="--steps 2 --warmup 3 --no-cpu-baseline --no-ttt --no-cg --no-sweep"
-ncu --set full --clock-control none --import-source on -k regex:topr -s 5 -c 1 -o gpurun_out/ab_topr -f python bench.py $LITE2 > gpurun_out/ab_ncu_topr.log 2>&1
-TPB_LIB=paper_2512_07536_b200/libtopoopt_b200_stamps.so python tools/topr_stamps.py > gpurun_out/topr_stamps.txt 2>&1
+for f in gpurun_out/ab_bench_old1.log gpurun_out/ab_bench_new1.log gpurun_out/ab_bench_old2.log gpurun_out/ab_bench_new2.log; do
+  python - "$f" >> gpurun_out/ab_summary.txt <<'PY'
+import json, sys
+l = [x for x in open(sys.argv[1]) if x.startswith("{")][-1]
+d = json.loads(l); x = d["xstep_roofline"]
+print(sys.argv[1].split("/")[-1], "iter/s %.1f" % d["value"], "passA %.2f us" % (x["pass_a"]["ms"] * 1e3),
+      "passB %.2f us" % (x["pass_b"]["ms"] * 1e3), "xstep %.2f us frac %.3f" % (x["whole_xstep"]["ms"] * 1e3, x["whole_xstep"]["frac"]),
+      "topr %.2f us" % (d["phases_ms"]["topr"] * 1e3), "prep %.2f us" % (d["phases_ms"]["prep"] * 1e3))
+PY
+done
 echo done
