@@ -1,3 +1,5 @@
+"""Per-phase device time of the config-2 solve (n=64 node-level het) at
+trace strides 1 and 32 (GPU box), via BatchSolver.bench_phase."""
 import json, os, sys, time
 sys.path.insert(0, ".")
 import numpy as np
