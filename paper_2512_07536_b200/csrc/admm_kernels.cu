@@ -301,9 +301,10 @@ __global__ void __launch_bounds__(TB* TY, 4) prep_kernel(Dev d, XConst c) {
                 const double vji = x2[k] + d2[k] * c.inv_rho;
                 const double vij = Vs[tx][cc];
                 const double a = 0.5 * (vij + vji);  // symmetrize (proj/src/eig.cpp:157)
-                // A is symmetric; write (j, i) here (row-major j*ld + i)
-                A[(long long)j * d.ld + i] = a;
-                Vs[tx][cc] = a;  // hand (i, j) to the transposed write below
+                // A is symmetric: entry (i, j) of the row-major buffer, lanes
+                // along the row (coalesced)
+                A[(long long)i * d.ld + j] = a;
+                Vs[tx][cc] = a;  // hand (i, j) to the mirrored write below
                 const double w = (bi == bj) ? (i == j ? 1.0 : (j > i ? 2.0 : 0.0)) : 2.0;
                 fro[which] += w * a * a;
             }
@@ -326,9 +327,10 @@ __global__ void __launch_bounds__(TB* TY, 4) prep_kernel(Dev d, XConst c) {
         }
         __syncthreads();
         if (bi != bj) {
+            // the mirror (j, i), j in block bj: rows j0 + cc, lanes along them
             for (int cc = ty; cc < TB; cc += TY) {
                 const int i = i0 + tx, j = j0 + cc;
-                if (i < n && j < n) A[(long long)i * d.ld + j] = Vs[cc][tx];
+                if (i < n && j < n) A[(long long)j * d.ld + i] = Vs[cc][tx];
             }
         }
         __syncthreads();
