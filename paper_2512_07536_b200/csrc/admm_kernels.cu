@@ -241,11 +241,34 @@ XConst make_xconst(int n, double alpha, double rho) {
 }
 
 // ---------------------------------------------------------------- prep
+#ifdef OZ_STAMPS
+// instrumentation build only (make STAMPS=1): globaltimer stamps per CTA of
+// the tile kernels (prep, passes A and B), 16 slots
+__device__ long long* g_tile_stamps = nullptr;
+__device__ __forceinline__ void tile_stamp(int slot) {
+    if (!g_tile_stamps || threadIdx.x || threadIdx.y) return;
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_tile_stamps[16LL * (blockIdx.y * gridDim.x + blockIdx.x) + slot] = t;
+}
+extern "C" int tp_tile_set_stamps(void* dev_ptr) {
+    return cudaMemcpyToSymbol(g_tile_stamps, &dev_ptr, sizeof(void*)) == cudaSuccess ? 0 : 7;
+}
+#define TILE_STAMP(slot) tile_stamp(slot)
+#else
+#define TILE_STAMP(slot) do {} while (0)
+#endif
+
 // Block (bi <= bj) of node pairs. Writes A_S/A_T = sym(v) in both triangles of
 // the ld-padded buffers, clamps the packed edge blocks for pairs in the tile,
 // and the per-node blocks (lambda, y) from tile 0.
 __global__ void __launch_bounds__(TB* TY, 4) prep_kernel(Dev d, XConst c) {
+    // programmatic dependent of the best-iterate copy (the launch overlaps
+    // its tail), which has read the improved flag: cleared here for every
+    // solve, done or not
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int b = blockIdx.y;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0) d.ictl[b * 8 + kImproved] = 0;
     if (solve_done(d, b)) return;
     int bi, bj;
     tile_of(blockIdx.x, bi, bj);
@@ -259,6 +282,7 @@ __global__ void __launch_bounds__(TB* TY, 4) prep_kernel(Dev d, XConst c) {
     const int i0 = bi * TB, j0 = bj * TB;
     __shared__ double red[TB * TY / 32];
     double fro[2] = {0.0, 0.0};
+    TILE_STAMP(0);
 
     for (int which = 0; which < 2; ++which) {
         const int off = which == 0 ? lo.off_s : lo.off_t;
@@ -334,6 +358,7 @@ __global__ void __launch_bounds__(TB* TY, 4) prep_kernel(Dev d, XConst c) {
             }
         }
         __syncthreads();
+        TILE_STAMP(1 + which);
     }
     // packed edge blocks for pairs (i, j), i < j, i in block bi, j in block bj
     // (the g loads of the thread's rows in flight together)
@@ -370,6 +395,7 @@ __global__ void __launch_bounds__(TB* TY, 4) prep_kernel(Dev d, XConst c) {
             Y[lv] = (0.0 < vn) ? vn : 0.0;
         }
     }
+    TILE_STAMP(3);
     if (blockIdx.x == 0) {
         const int t = ty * TB + tx;
         if (t == 0) {
@@ -403,7 +429,9 @@ __global__ void __launch_bounds__(TB* TY, 4) prep_kernel(Dev d, XConst c) {
     __shared__ int s_fin;
     __shared__ double sm8[2][TY][TB + 1];
     int* cnt = d.cnt + (long long)b * d.cnt_stride;
+    TILE_STAMP(4);
     const int fin = arrive_blocks(cnt + kCntP * d.nb, d.nb, bi, bj, &s_fin);
+    TILE_STAMP(5);
     if (!fin) return;
     bool last = false;
     for (int q = 0; q < 2; ++q) {
@@ -422,6 +450,7 @@ __global__ void __launch_bounds__(TB* TY, 4) prep_kernel(Dev d, XConst c) {
         }
         last |= arrive_solve(cnt + 2 * d.nb + kCntP, d.nb, &s_fin);
     }
+    TILE_STAMP(6);
     if (!last) return;
     const int t = ty * TB + tx;
     double f0 = 0.0, f1 = 0.0, inf = 0.0;
@@ -442,12 +471,27 @@ __global__ void __launch_bounds__(TB* TY, 4) prep_kernel(Dev d, XConst c) {
         const double cc = fmin(sqrt(ty == 0 ? f0 : f1), inf);
         d.inv_scale[b * 2 + ty] = cc > 0.0 ? 1.0 / cc : 0.0;
     }
+    TILE_STAMP(7);
+}
+
+// launch as a programmatic dependent of the previous kernel in the stream
+// (the kernel calls griddepcontrol.wait before touching memory)
+template <class K, class... Args>
+void launch_dependent(K kernel, dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    TPB_CUDA(cudaLaunchKernelEx(&cfg, kernel, args...));
 }
 
 void launch_prep(const Dev& d, const XConst& c, cudaStream_t st) {
-    dim3 grid(d.ntile, d.B), block(TB, TY);
-    prep_kernel<<<grid, block, 0, st>>>(d, c);
-    TPB_CHECK_LAUNCH();
+    launch_dependent(prep_kernel, dim3(d.ntile, d.B), dim3(TB, TY), st, d, c);
 }
 
 
@@ -455,6 +499,9 @@ void launch_prep(const Dev& d, const XConst& c, cudaStream_t st) {
 // h_g(i,j) = r_g + s (4 - R_ii - R_jj + R_ij + R_ji + v2_i + v2_j) [- s r_nu]
 // with r = Y - (D + c)/rho, R = r_S + r_T, v2 = 1 - r_y.
 __global__ void __launch_bounds__(TB* TY, 4) xstep_a_kernel(Dev d, XConst c) {
+    // pass B (launched as a programmatic dependent) may be scheduled now; it
+    // waits for this grid's completion before it touches memory
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int b = blockIdx.y;
     if (solve_done(d, b)) return;
     int bi, bj;
@@ -469,6 +516,7 @@ __global__ void __launch_bounds__(TB* TY, 4) xstep_a_kernel(Dev d, XConst c) {
     __shared__ double Hs[TB][TB + 1];  // Hs[il][jl] = h(i,j) (valid for pairs)
     __shared__ double Zs[TB][TB + 1];  // het: h_z'(i,j)
     __shared__ double rd_i[TB], rd_j[TB], v2_i[TB], v2_j[TB];
+    TILE_STAMP(8);
 
     auto rS = [&](long long p) { return Y[lo.off_s + p] - D[lo.off_s + p] * c.inv_rho; };
     auto rT = [&](long long p) { return Y[lo.off_t + p] - D[lo.off_t + p] * c.inv_rho; };
@@ -667,6 +715,7 @@ __global__ void __launch_bounds__(TB* TY, 4) xstep_a_kernel(Dev d, XConst c) {
         ta[1] = s_tot[0][1] + s_tot[1][1];
         if (bi == bj) reinterpret_cast<double4*>(d.blk)[(long long)b * d.nb + bi] = bk;
     }
+    TILE_STAMP(9);
 }
 
 void launch_xstep_a(const Dev& d, const XConst& c, cudaStream_t st) {
@@ -1241,6 +1290,10 @@ __device__ double node_space(const Dev& d, const XConst& c, int b, int bi, int b
 }
 
 __global__ void __launch_bounds__(TB* TY, 4) xstep_b_kernel(Dev d, XConst c) {
+    // programmatic dependent of pass A (or the CG kernel): the launch overlaps
+    // their tail; everything below reads their results
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the best-iterate copy
     const int b = blockIdx.y;
     if (solve_done(d, b)) return;
     int bi, bj;
@@ -1265,8 +1318,10 @@ __global__ void __launch_bounds__(TB* TY, 4) xstep_b_kernel(Dev d, XConst c) {
     // (n - 2) t_i + sum_k t_k), so the diagonal tiles write the diagonal
     // entries and no block finisher is needed; the CG x-step and het keep it
     const bool closed = !d.het && !d.cg;
+    TILE_STAMP(10);
     const double lam = node_space(d, c, b, bi, bj, nv, sp, scr2);  // thread 0
     if (tx == 0 && ty == 0) s_lam = lam;
+    TILE_STAMP(11);
 
     // edge loads of the thread's rows (hom), batched
     constexpr int NR = TB / TY;
@@ -1472,6 +1527,7 @@ __global__ void __launch_bounds__(TB* TY, 4) xstep_b_kernel(Dev d, XConst c) {
     int* cnt = d.cnt + (long long)b * d.cnt_stride;
     double* rnode = d.res_node + (long long)b * n;
     bool last = false;
+    TILE_STAMP(12);
     if (closed) {
         // every tile arrives at the solve counter; the last one finishes
         last = arrive_solve(cnt + 2 * d.nb + kCntB, d.ntile, &s_fin);
@@ -1516,6 +1572,7 @@ __global__ void __launch_bounds__(TB* TY, 4) xstep_b_kernel(Dev d, XConst c) {
         last |= arrive_solve(cnt + 2 * d.nb + kCntB, d.nb, &s_fin);
     }
     }
+    TILE_STAMP(13);
     if (!last) return;
     int* ctl = d.ictl + b * 8;
     double yl = 0.0, dl = 0.0, best = 0.0;
@@ -1538,6 +1595,7 @@ __global__ void __launch_bounds__(TB* TY, 4) xstep_b_kernel(Dev d, XConst c) {
     const double lamv = s_lam;
     d.scal[b * 8 + kLambda] = lamv;
     X[lo.lambda_ix] = lamv;
+    TILE_STAMP(14);
     if (!d.upd_duals) return;
     D[lo.lambda_ix] = dl + c.rho * (lamv - yl);
     rsum += (lamv - yl) * (lamv - yl);
@@ -1561,13 +1619,13 @@ __global__ void __launch_bounds__(TB* TY, 4) xstep_b_kernel(Dev d, XConst c) {
 }
 
 void launch_xstep_b(const Dev& d, const XConst& c, cudaStream_t st) {
-    dim3 grid(d.ntile, d.B), block(TB, TY);
-    xstep_b_kernel<<<grid, block, 0, st>>>(d, c);
-    TPB_CHECK_LAUNCH();
+    launch_dependent(xstep_b_kernel, dim3(d.ntile, d.B), dim3(TB, TY), st, d, c);
 }
 
 // ---------------------------------------------------------------- best copy
 __global__ void best_copy_kernel(Dev d, XConst c) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // pass B set the flag
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the next prep
     const int b = blockIdx.y;
     int* ctl = d.ictl + b * 8;
     if (!ctl[kImproved]) return;
@@ -1586,17 +1644,10 @@ __global__ void best_copy_kernel(Dev d, XConst c) {
     }
 }
 
-__global__ void clear_improved_kernel(Dev d) {
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b < d.B) d.ictl[b * 8 + kImproved] = 0;
-}
-
+// (the improved flag is cleared by the next prep)
 void launch_best_copy(const Dev& d, const XConst& c, cudaStream_t st) {
     const int blocks = (int)std::min<long long>((d.nx + 255) / 256, 512);
-    best_copy_kernel<<<dim3(blocks, d.B), 256, 0, st>>>(d, c);
-    TPB_CHECK_LAUNCH();
-    clear_improved_kernel<<<(d.B + 127) / 128, 128, 0, st>>>(d);
-    TPB_CHECK_LAUNCH();
+    launch_dependent(best_copy_kernel, dim3(blocks, d.B), dim3(256), st, d, c);
 }
 
 void init_attrs_admm() {}

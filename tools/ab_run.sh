@@ -23,4 +23,5 @@ print(sys.argv[1].split("/")[-1], "iter/s %.1f" % d["value"], "passA %.2f us" % 
       "topr %.2f us" % (d["phases_ms"]["topr"] * 1e3), "prep %.2f us" % (d["phases_ms"]["prep"] * 1e3))
 PY
 done
+TPB_LIB=paper_2512_07536_b200/libtopoopt_b200_stamps.so python tools/tile_stamps.py > gpurun_out/tile_stamps.txt 2>&1
 echo done
