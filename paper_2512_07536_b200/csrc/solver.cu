@@ -1062,7 +1062,9 @@ void Solver::xstep_only(bool update_duals) {
 
 int Solver::launches_per_iteration() const {
     const int cone = small_ ? 1 : sch_.gemms();
-    return 1 + 1 + 1 + cone + 2 + 2 + (d_.cg ? 1 : 0);
+    // prep, top-r, trace SLEM, the cone chain, x-step passes A and B, the
+    // best-iterate copy (+ the CG solve)
+    return 1 + 1 + 1 + cone + 2 + 1 + (d_.cg ? 1 : 0);
 }
 
 int Solver::bench_phase(int phase, int reps) {
