@@ -107,7 +107,17 @@ def test_top_r_large_with_ties(T, O, n):
     lo = T.hom_layout(n)
     cases = [rng.choice([0.1, 0.2, 0.3, 0.25, -1.0], size=lo.m),            # heavy ties
              np.where(rng.random(lo.m) < 0.3, rng.random(lo.m), -rng.random(lo.m)),  # ties at 0 after the clamp
-             np.round(rng.random(lo.m), 3)]                                   # ~1000 tied values
+             np.round(rng.random(lo.m), 3),                                   # ~1000 tied values
+             # one exponent for every value: the grid select's candidate
+             # compaction overflows in every CTA (full-range rounds), with
+             # ties and without
+             0.5 + np.round(rng.random(lo.m), 4) / 2,
+             0.5 + rng.random(lo.m) / 2,
+             # 10 % of the values 1 + k 2^-40 (k < 64: the same top 44 bits),
+             # the rest below 0.1: the rounds after the first run on the
+             # compacted candidates down to the ties
+             np.where(rng.random(lo.m) < 0.1, 1.0 + np.floor(rng.random(lo.m) * 64) * 2.0 ** -40,
+                      rng.random(lo.m) * 0.1)]
     for vals in cases:
         x = np.zeros(lo.nx)
         x[:lo.m] = vals
