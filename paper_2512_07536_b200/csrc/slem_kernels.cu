@@ -846,26 +846,34 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
                     }
                 }
             }
-            double alpha = allreduce1(pa, red1);
+            // this CTA's slice of w goes to the other CTAs before the alpha
+            // reduction, whose cluster barrier orders it: ONE cluster barrier
+            // per step. Receive buffers alternate with the step parity (w on
+            // even steps, the foreign part of qp, unused otherwise, on odd
+            // ones), so a CTA one step ahead never overwrites entries another
+            // CTA still reads.
+            double* wsrc = (C > 1 && (k & 1)) ? qp : w;
+            double alpha = allreduce1(pa, red1);  // its CTA barrier: the slice is complete
+            if (C > 1)
+                for (int v = v_lo + tid; v < v_hi; v += nthr) {
+                    const double wv = w[v];
+                    for (int r = 0; r < C; ++r)
+                        if (r != rank) *cl.map_shared_rank(wsrc + v, r) = wv;
+                }
             {
                 double dummy = 0.0;
-                cluster_sum2(alpha, dummy, 0);
+                cluster_sum2(alpha, dummy, k & 1);
             }
-            // x = w - alpha q on this CTA's nodes, pushed with the partial sums
-            // to the other CTAs: one cluster barrier, then every CTA forms the
-            // whole next q itself
+            // every CTA now holds the whole w: x = w - alpha q over all nodes
+            // (kept implicit), its sums in block order, identical in every CTA
+            auto w_at = [&](int v) { return (v >= v_lo && v < v_hi) ? w[v] : wsrc[v]; };
             double s = 0.0, s2 = 0.0;
-            for (int v = v_lo + tid; v < v_hi; v += nthr) {
-                const double x = w[v] - alpha * q[v];
-                w[v] = x;
-                qp[v] = q[v];
-                for (int r = 0; r < C; ++r)
-                    if (r != rank) *cl.map_shared_rank(w + v, r) = x;
+            for (int v = tid; v < n; v += nthr) {
+                const double x = w_at(v) - alpha * q[v];
                 s += x;
                 s2 += x * x;
             }
             allreduce2(s, s2, red2);
-            cluster_sum2(s, s2, 1);  // (C = 1: allreduce2's barrier orders w)
             const double mean = s / n;
             const double beta = sqrt(fmax(s2 - n * mean * mean, 0.0));
             if (tid == 0) {
@@ -923,7 +931,11 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
                 }
             }
             const double inv = beta > 0.0 ? 1.0 / beta : 0.0;
-            for (int v = tid; v < n; v += nthr) q[v] = (w[v] - mean) * inv;
+            for (int v = tid; v < n; v += nthr) {
+                const double qo = q[v];
+                if (v >= v_lo && v < v_hi) qp[v] = qo;  // q_{k-1} of this CTA's nodes
+                q[v] = (w_at(v) - alpha * qo - mean) * inv;
+            }
             beta_prev = beta;
             __syncthreads();
         }

@@ -130,6 +130,7 @@ def test_cg_batched_global_equals_single_register(T, n, r, B):
             assert np.array_equal(got.trace, one.trace)
             assert got.edges.tolist() == one.edges.tolist()
             assert np.array_equal(got.weights, one.weights)
+            assert got.acf_value == one.acf_value  # the final report (8-CTA cluster per solve)
     finally:
         bs.close()
 

@@ -76,6 +76,32 @@ def test_batched_equals_single(T):
         assert got.acf_value == one.acf_value
 
 
+def test_batched_oneoff_reports_equal_single(T):
+    """n = 400: the one-off SLEM reports (feasible start, final) run the plain
+    Lanczos recurrence as an 8-CTA cluster per solve, the incidence from
+    global memory in a batch and from shared memory alone; both give the
+    single solve's report bit for bit, for every solve of the batch."""
+    n, rs = 400, [1200, 1000, 1400]
+    cfg = dict(rho=10.0, epsilon=1e-8, max_iter=6)
+    warms = [T.default_warm_start(n, r, 0) for r in rs]
+    bs = T.BatchSolver(n, r=rs, **cfg)
+    try:
+        for b, w in enumerate(warms):
+            bs.set_warm(b, w)
+        bs.start()
+        bs.run()
+        bs.finish()
+        for b, r in enumerate(rs):
+            got = bs.result(b)
+            one = T.solve(n, r, warm_start=warms[b], **cfg)
+            assert 0.0 < got.acf_value < 1.0
+            assert got.acf_value == one.acf_value
+            assert np.array_equal(got.trace, one.trace)
+            assert got.edges.tolist() == one.edges.tolist()
+    finally:
+        bs.close()
+
+
 def test_batched_het_equals_single(T):
     n = 16
     degs = [[3] * 8 + [1] * 8, [6] * 8 + [2] * 8, [4] * 16]
