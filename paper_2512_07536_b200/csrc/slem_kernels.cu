@@ -259,11 +259,14 @@ __device__ inline void cgs2(const double* Q, int n, int ldq, int k, double* w, d
 #ifdef OZ_STAMPS
 // instrumentation build only (make STAMPS=1): per-kernel {calls, steps} of the
 // Lanczos SLEM kernels, slot 0 trace reports, slot 1 one-off reports
-__device__ unsigned long long g_slem_stats[8];
+// slots 8..13: clocks of the check parts (Gershgorin, multisection, inverse
+// iteration) in warp 0 / lane 0, trace (8..10) and one-off (11..13); 14, 15:
+// number of checks (trace, one-off)
+__device__ unsigned long long g_slem_stats[16];
 extern "C" int tp_slem_stats(unsigned long long* out, int reset) {
     if (cudaMemcpyFromSymbol(out, g_slem_stats, sizeof(g_slem_stats)) != cudaSuccess) return 7;
     if (reset) {
-        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        unsigned long long z[16] = {};
         cudaMemcpyToSymbol(g_slem_stats, z, sizeof(z));
     }
     return 0;
@@ -895,12 +898,30 @@ __global__ void __launch_bounds__(kTraceThreads) slem_trace_kernel(SlemArgs a) {
                 // warp 0: smallest Ritz pair, warp 1: largest, concurrently
                 if (wid < 2) {
                     double lo, hi;
+#ifdef OZ_STAMPS
+                    const long long c0 = clock64();
+#endif
                     gershgorin(al, be, kk, lo, hi);
+#ifdef OZ_STAMPS
+                    const long long c1 = clock64();
+#endif
                     const double t = tri_eig(al, be, kk, wid == 0 ? 0 : kk - 1, lo, hi);
+#ifdef OZ_STAMPS
+                    const long long c2 = clock64();
+#endif
                     if ((tid & 31) == 0) {
                         s_th[wid] = t;
                         s_res[wid] = beta * tri_vec(al, be, kk, t, wk + 2 * kcap * wid, wid == 0 ? smin : smax);
                     }
+#ifdef OZ_STAMPS
+                    if (tid == 0 && rank == 0) {
+                        const int o = a.out ? 11 : 8;
+                        atomicAdd(&g_slem_stats[o], (unsigned long long)(c1 - c0));
+                        atomicAdd(&g_slem_stats[o + 1], (unsigned long long)(c2 - c1));
+                        atomicAdd(&g_slem_stats[o + 2], (unsigned long long)(clock64() - c2));
+                        atomicAdd(&g_slem_stats[a.out ? 15 : 14], 1ull);  // checks
+                    }
+#endif
                 }
                 __syncthreads();
                 if (tid == 0) {
