@@ -42,7 +42,11 @@ __device__ int sturm_count(const double* al, const double* be, int k, double x) 
     for (int i = 0; i < k; ++i) {
         const double b2 = i > 0 ? be[i - 1] * be[i - 1] : 0.0;
         const double pn = fma(al[i] - x, p, -b2 * pm);
-        const bool neg = pn < 0.0 || (pn == 0.0 && !prev_neg);
+        // sign and zero tests on the bits (integer pipe; the FP64 pipe keeps
+        // only the recurrence): pn < 0 <=> sign set and nonzero (no NaN here)
+        const long long pb = __double_as_longlong(pn);
+        const bool zero = (pb & 0x7fffffffffffffffLL) == 0;
+        const bool neg = zero ? !prev_neg : pb < 0;
         cnt += neg != prev_neg;
         prev_neg = neg;
         pm = p;
