@@ -218,7 +218,9 @@ void slem_edges(int n, const std::vector<int>& packed, const std::vector<double>
     a.plain = exact ? 0 : 1;  // as the solver's one-off reports (Solver::final_slem)
     a.cluster = kOneOffCluster;
     a.max_restarts = 200;
-    a.min_steps = 64;
+    // first residual check: the plain recurrence at n ~ 1000 needs ~380
+    // steps to 1e-10, so a check at 128 is wasted (a check at k costs ~k us)
+    a.min_steps = std::min(std::max(64, n / 4), 256);
     a.check_every = 128;
     a.tol = 1e-10;
     a.out = out.p;

@@ -454,7 +454,9 @@ void Solver::final_slem(const double* packed, const int* list, const int* count,
         a.ritz_ok = ritz_ok_[0];
     }
     a.max_restarts = 200;
-    a.min_steps = 64;
+    // first residual check: the plain recurrence at n ~ 1000 needs ~380
+    // steps to 1e-10, so a check at 128 is wasted (a check at k costs ~k us)
+    a.min_steps = std::min(std::max(64, lo_.n / 4), 256);
     a.check_every = 128;
     a.tol = 1e-10;
     a.out = out;
