@@ -101,8 +101,13 @@ __global__ void __launch_bounds__(kThreads) topr_kernel(SelectArgs a) {
             __syncthreads();
             pmask |= (255ull << shift);
             if (s_fin) break;
-            // compact the surviving bucket into shared memory once it fits
-            if (s_ncand < 0 && s_mode <= kCap && shift > 0) {
+            // compact the surviving bucket into shared memory once it fits;
+            // every thread reads the condition before thread 0 resets the
+            // count (a thread reading the reset count would skip the block
+            // and its barrier)
+            const bool compact = s_ncand < 0 && s_mode <= kCap && shift > 0;
+            __syncthreads();
+            if (compact) {
                 if (tid == 0) s_ncand = 0;
                 __syncthreads();
                 const unsigned long long pf = s_prefix;
